@@ -1,0 +1,621 @@
+"""CPU oracle for the periodic FMM + HI electrostatics path.
+
+TEST INFRASTRUCTURE — NOT PART OF THE PRODUCT.  Only ``tests/``,
+``__graft_entry__.smoke()`` and ``bench.py``'s ``cpu_baseline`` / reference
+arm may import this module, and only as the checker or as the timed CPU
+baseline; the GPU path never calls it.
+
+It restates, in complex128 numpy, the algorithm of the reference package
+``lambdafmm`` 0.1.0 (paths relative to /root/reference/pkg/src/lambdafmm):
+solid harmonics and translation operators (fmm/harmonics.py), the uniform
+periodic octree (fmm/octree.py), the lattice operator and surface term
+(fmm/lattice.py), the solve / spatial-force pipeline (fmm/solver.py) and
+the HI correction + assembly (corrections.py, weights.py, system.py).
+The vectorisation is its own (padded leaf blocks for P2P, particle-batched
+P2M/L2P, parity-grouped M2L) but every formula follows the cited lines.
+
+Parity pin: ``tests/golden/*.npz`` were produced by running the reference
+itself (tests/golden/make_golden.py); tests/test_oracle.py checks this
+oracle against them and against the reference's known-answer values.
+"""
+
+import math
+from functools import lru_cache
+
+import numpy as np
+
+DIPOLE_ETA = -1.0  # lattice.py:41
+
+
+# ----------------------------------------------------------- harmonics ----
+def ncoef(p):
+    return (p + 1) ** 2
+
+
+def cidx(l, m):
+    return l * l + l + m  # harmonics.py:37
+
+
+@lru_cache(maxsize=None)
+def lm_tables(p):
+    ls = np.repeat(np.arange(p + 1), 2 * np.arange(p + 1) + 1)
+    ms = np.concatenate([np.arange(-l, l + 1) for l in range(p + 1)])
+    return ls, ms
+
+
+def regular(xyz, p):
+    """R_l^m(r) = P_l^m r^l e^{im phi}/(l+m)!  by recurrence (harmonics.py:58-77)."""
+    xyz = np.atleast_2d(np.asarray(xyz, dtype=np.float64))
+    x, y, z = xyz[:, 0], xyz[:, 1], xyz[:, 2]
+    u = x + 1j * y
+    rr = x * x + y * y + z * z
+    out = np.zeros((xyz.shape[0], ncoef(p)), np.complex128)
+    diag = np.ones(xyz.shape[0], np.complex128)
+    for m in range(p + 1):
+        if m:
+            diag = diag * u / (2.0 * m)
+        out[:, cidx(m, m)] = diag
+        if m < p:
+            out[:, cidx(m + 1, m)] = z * diag
+        for l in range(m + 2, p + 1):
+            out[:, cidx(l, m)] = ((2 * l - 1) * z * out[:, cidx(l - 1, m)]
+                                  - rr * out[:, cidx(l - 2, m)]) / ((l + m) * (l - m))
+    _fill_negative(out, p)
+    return out
+
+
+def irregular(xyz, p):
+    """I_l^m(r) = (l-m)! P_l^m e^{im phi}/r^(l+1)  (harmonics.py:80-103)."""
+    xyz = np.atleast_2d(np.asarray(xyz, dtype=np.float64))
+    x, y, z = xyz[:, 0], xyz[:, 1], xyz[:, 2]
+    u = x + 1j * y
+    inv2 = 1.0 / (x * x + y * y + z * z)
+    out = np.zeros((xyz.shape[0], ncoef(p)), np.complex128)
+    diag = np.sqrt(inv2).astype(np.complex128)
+    for m in range(p + 1):
+        if m:
+            diag = (2 * m - 1) * diag * u * inv2
+        out[:, cidx(m, m)] = diag
+        if m < p:
+            out[:, cidx(m + 1, m)] = (2 * m + 1) * z * diag * inv2
+        for l in range(m + 2, p + 1):
+            out[:, cidx(l, m)] = ((2 * l - 1) * z * out[:, cidx(l - 1, m)]
+                                  - ((l - 1) ** 2 - m * m) * out[:, cidx(l - 2, m)]) * inv2
+    _fill_negative(out, p)
+    return out
+
+
+def _fill_negative(out, p):
+    # X_l^{-m} = (-1)^m conj(X_l^m)  (harmonics.py:3-8)
+    for l in range(1, p + 1):
+        for m in range(1, l + 1):
+            out[:, cidx(l, -m)] = (-1) ** m * np.conj(out[:, cidx(l, m)])
+
+
+def regular_grad(xyz, p):
+    """Cartesian gradient of R_l^m via the R_{l-1} ladder (harmonics.py:106-130)."""
+    r = regular(xyz, p)
+    ls, ms = lm_tables(p)
+    g = np.zeros(r.shape + (3,), np.complex128)
+    for dm, col in ((-1, "a"), (1, "b"), (0, "c")):
+        lt, mt = ls - 1, ms + dm
+        ok = (lt >= 0) & (np.abs(mt) <= lt)
+        src = np.where(ok, lt * lt + lt + mt, 0)
+        v = np.where(ok[None, :], r[:, src], 0.0)
+        if col == "a":
+            g[..., 0] += 0.5 * v
+            g[..., 1] += 0.5j * v
+        elif col == "b":
+            g[..., 0] -= 0.5 * v
+            g[..., 1] += 0.5j * v
+        else:
+            g[..., 2] = v
+    return g
+
+
+@lru_cache(maxsize=None)
+def _shift_map(p):
+    ls, ms = lm_tables(p)
+    dl = ls[:, None] - ls[None, :]
+    dm = ms[:, None] - ms[None, :]
+    ok = (dl >= 0) & (np.abs(dm) <= dl)
+    return np.where(ok, dl * dl + dl + dm, 0), ok
+
+
+@lru_cache(maxsize=None)
+def _m2l_gather(p):
+    ls, ms = lm_tables(p)
+    L = ls[:, None] + ls[None, :]
+    M = -(ms[:, None] + ms[None, :])
+    sign = np.where((ls[None, :] + ms[:, None] + ms[None, :]) % 2 == 0, 1.0, -1.0)
+    return L * L + L + M, sign
+
+
+def m2m_op(d, p):
+    """M_new = A M_old for c_new = c_old + d (harmonics.py:155-159)."""
+    src, ok = _shift_map(p)
+    rv = regular(-np.asarray(d, float)[None, :], p)[0]
+    return np.where(ok, rv[src], 0.0)
+
+
+def l2l_op(d, p):
+    """L_new = C L_old for c_new = c_old + d (harmonics.py:162-166)."""
+    src, ok = _shift_map(p)
+    rv = regular(np.asarray(d, float)[None, :], p)[0]
+    return np.where(ok, rv[src], 0.0).T
+
+
+def m2l_from_iv(iv, p):
+    """B from I(-d) at order 2p (harmonics.py:196-203)."""
+    src, sign = _m2l_gather(p)
+    return sign * iv[..., src]
+
+
+# -------------------------------------------------------------- octree ----
+NB_OFF = np.array([(a, b, c) for a in (-1, 0, 1) for b in (-1, 0, 1) for c in (-1, 0, 1)], np.int64)
+_C3 = np.array([(a, b, c) for a in range(-3, 4) for b in range(-3, 4) for c in range(-3, 4)], np.int64)
+M2L_OFF = _C3[np.abs(_C3).max(1) >= 2]  # (316,3) octree.py:31
+OCT = np.array([(a, b, c) for a in (0, 1) for b in (0, 1) for c in (0, 1)], np.int64)
+
+
+def grid_of(n):
+    i = np.arange(n ** 3, dtype=np.int64)
+    return np.stack([i // (n * n), (i // n) % n, i % n], 1)
+
+
+def flat(g, n):
+    return (g[..., 0] * n + g[..., 1]) * n + g[..., 2]
+
+
+def wrap(pos, box):
+    """np.mod wrap, exact box multiples -> 0 (system.py:103-108)."""
+    w = np.mod(np.asarray(pos, np.float64), box)
+    w[w >= box] = 0.0
+    return w
+
+
+def m2l_pairs(level):
+    """Per M2L_OFFSETS row: targets whose parity admits the offset and their
+    wrapped sources (octree.py:35-38, :96-111)."""
+    n = 2 ** level
+    g = grid_of(n)
+    par = g & 1
+    out = []
+    for row, o in enumerate(M2L_OFF):
+        ok = np.all((-2 - par <= o) & (o <= 3 - par), axis=1)
+        t = np.flatnonzero(ok)
+        if t.size:
+            out.append((row, t, flat(np.mod(g[t] + o, n), n)))
+    return out
+
+
+def build_tree(pos, box, depth):
+    """Canonical order + CSR + periodic neighbours (octree.py:114-163)."""
+    pos = np.atleast_2d(np.asarray(pos, np.float64))
+    n = 2 ** depth
+    size = box / n
+    cell = np.clip((pos / size).astype(np.int64), 0, n - 1)
+    leaf = flat(cell, n)
+    perm = np.lexsort((pos[:, 2], pos[:, 1], pos[:, 0], leaf))
+    inv = np.empty_like(perm)
+    inv[perm] = np.arange(perm.size)
+    start = np.zeros(n ** 3 + 1, np.int64)
+    np.cumsum(np.bincount(leaf, minlength=n ** 3), out=start[1:])
+    raw = grid_of(n)[:, None, :] + NB_OFF[None]
+    shift = np.floor_divide(raw, n)
+    nb = flat(raw - shift * n, n)
+    return dict(perm=perm, inv_perm=inv, positions=pos[perm], leaf_of_particle=leaf[perm], leaf_start=start,
+                nb_box=nb, nb_shift=shift, depth=depth, box=float(box), size=size)
+
+
+# ------------------------------------------------------------- lattice ----
+def image_vectors(smin, smax):
+    a = np.arange(-smax, smax + 1)
+    g = np.stack(np.meshgrid(a, a, a, indexing="ij"), -1).reshape(-1, 3)
+    nrm = np.abs(g).max(1)
+    return g[(nrm >= smin) & (nrm <= smax)].astype(np.float64)
+
+
+def _symmetrise(t):
+    return 0.5 * (t + t.T)
+
+
+@lru_cache(maxsize=8)
+def lattice_shells(p, cap):
+    """Exact finite-shell far-image operator (lattice.py:109-121)."""
+    v = image_vectors(2, cap)
+    iv = np.zeros(ncoef(2 * p), np.complex128)
+    for lo in range(0, v.shape[0], 4096):
+        iv += irregular(v[lo:lo + 4096], 2 * p).sum(0)
+    return _symmetrise(m2l_from_iv(iv, p))
+
+
+@lru_cache(maxsize=8)
+def lattice_converged(p, steps=24):
+    """Factor-3 telescoped infinite lattice (lattice.py:124-155)."""
+    ls, _ = lm_tables(p)
+    t_ring = m2l_from_iv(irregular(image_vectors(2, 4), 2 * p).sum(0), p)
+    src, ok = _shift_map(p)
+    rv = regular(image_vectors(0, 1), p).sum(0)
+    s_hat = (3.0 ** -ls)[:, None] * np.where(ok, rv[src], 0.0)
+    acc = np.zeros((ncoef(p), ncoef(p)), np.complex128)
+    b = np.eye(ncoef(p), dtype=np.complex128)
+    for k in range(steps):
+        acc += (3.0 ** (-k * (ls + 1.0)))[:, None] * (t_ring @ b)
+        if k + 1 < steps:
+            b = s_hat @ b
+    acc[(ls[:, None] + ls[None, :]) < 4] = 0.0
+    return _symmetrise(acc)
+
+
+def lattice_scaled(unit, p, box):
+    ls, _ = lm_tables(p)
+    return (box ** -(ls + 1.0))[:, None] * unit * (box ** -ls.astype(float))[None, :]
+
+
+def lattice_matrix(cfg, box):
+    if cfg["lattice_mode"] == "converged":
+        return lattice_scaled(lattice_converged(cfg["p"]), cfg["p"], box)
+    if cfg["lattice_mode"] == "shells":
+        return lattice_scaled(lattice_shells(cfg["p"], cfg["shell_cap"]), cfg["p"], box)
+    return None
+
+
+# ------------------------------------------------------------ near field ----
+def _padded_leaves(tree):
+    start = tree["leaf_start"]
+    cnt = np.diff(start)
+    nleaf = cnt.size
+    width = max(1, int(cnt.max()) if cnt.size else 1)
+    slot = np.arange(width)[None, :]
+    idx = start[:-1, None] + slot
+    valid = slot < cnt[:, None]
+    return np.where(valid, idx, 0), valid, nleaf
+
+
+def near_field(tree, q, periodic=True, grad=False, leaves=None):
+    """27-image direct sums (solver.py:126-224): V_near (N,K) and optionally
+    grad V_near (N,3) for column 0, canonical order.  `leaves` restricts the
+    targets (timing samples only)."""
+    pos = tree["positions"]
+    box = tree["box"]
+    idx, valid, nleaf = _padded_leaves(tree)
+    tl = np.arange(nleaf) if leaves is None else np.asarray(leaves)
+    nk = q.shape[1]
+    v = np.zeros((pos.shape[0], nk))
+    g = np.zeros((pos.shape[0], 3)) if grad else None
+    rows = range(27) if periodic else (13,)
+    for c0 in range(0, tl.size, 2048):
+        tb = tl[c0:c0 + 2048]
+        ti, tv = idx[tb], valid[tb]
+        tp = pos[ti]  # (B,W,3)
+        acc = np.zeros(ti.shape + (nk,))
+        gacc = np.zeros(ti.shape + (3,)) if grad else None
+        for t in rows:
+            sb = tree["nb_box"][tb, t]
+            si, sv = idx[sb], valid[sb]
+            sp = pos[si] + (tree["nb_shift"][tb, t] * box)[:, None, :]
+            d = tp[:, :, None, :] - sp[:, None, :, :]
+            r2 = (d * d).sum(-1)
+            mask = tv[:, :, None] & sv[:, None, :]
+            if t == 13:
+                mask = mask & (ti[:, :, None] != si[:, None, :])
+            with np.errstate(divide="ignore", invalid="ignore"):
+                inv = np.where(mask, 1.0 / np.sqrt(np.where(mask, r2, 1.0)), 0.0)
+            qs = q[si] * sv[:, :, None]
+            acc += np.einsum("bts,bsk->btk", inv, qs)
+            if grad:
+                gacc += np.einsum("btsd,bts,bs->btd", d, -inv ** 3, qs[:, :, 0])
+        v[ti[tv]] = acc[tv]
+        if grad:
+            g[ti[tv]] = gacc[tv]
+    return v, g
+
+
+# ------------------------------------------------------------- far field ----
+def leaf_centers(tree):
+    n = 2 ** tree["depth"]
+    return (grid_of(n) + 0.5) * tree["size"]
+
+
+def upward(tree, q, p, leaves=None):
+    """Leaf P2M then M2M to the root (solver.py:227-259); list over levels of
+    (nc, nbox, K) complex."""
+    d = tree["depth"]
+    nc = ncoef(p)
+    nk = q.shape[1]
+    start = tree["leaf_start"]
+    lof = tree["leaf_of_particle"]
+    cen = leaf_centers(tree)
+    mult = [None] * (d + 1)
+    m = np.zeros((nc, 8 ** d, nk), np.complex128)
+    sel = np.arange(tree["positions"].shape[0])
+    if leaves is not None:
+        sel = np.concatenate([np.arange(start[b], start[b + 1]) for b in leaves])
+    for c0 in range(0, sel.size, 65536):
+        ii = sel[c0:c0 + 65536]
+        r = regular(tree["positions"][ii] - cen[lof[ii]], p)  # (n, nc)
+        contrib = r[:, :, None] * q[ii][:, None, :]
+        # particles are leaf-sorted: segment sums per leaf
+        lv = lof[ii]
+        cut = np.flatnonzero(np.diff(lv)) + 1
+        seg = np.add.reduceat(contrib, np.concatenate([[0], cut]), axis=0)
+        m[:, lv[np.concatenate([[0], cut])], :] += np.transpose(seg, (1, 0, 2))
+    mult[d] = m
+    for l in range(d - 1, -1, -1):
+        child_size = tree["box"] / 2 ** (l + 1)
+        n = 2 ** l
+        g = grid_of(n)
+        mp = np.zeros((nc, n ** 3, nk), np.complex128)
+        for o in range(8):
+            op = m2m_op((0.5 - OCT[o]) * child_size, p)
+            ci = flat(2 * g + OCT[o], 2 * n)
+            mp += (op @ mult[l + 1][:, ci, :].reshape(nc, -1)).reshape(mp.shape)
+        mult[l] = mp
+    return mult
+
+
+def downward(tree, mult, p, root_local, boxes_fraction=None):
+    """L2L + parity-grouped M2L per level (solver.py:262-291)."""
+    d = tree["depth"]
+    nc = ncoef(p)
+    nk = mult[0].shape[2]
+    loc = [None] * (d + 1)
+    loc[0] = np.zeros((nc, 1, nk), np.complex128) if root_local is None else root_local.reshape(nc, 1, nk)
+    for l in range(1, d + 1):
+        n = 2 ** l
+        size = tree["box"] / n
+        g = grid_of(n)
+        cur = np.zeros((nc, n ** 3, nk), np.complex128)
+        pg = grid_of(n // 2)
+        for o in range(8):
+            op = l2l_op((OCT[o] - 0.5) * size, p)
+            ci = flat(2 * pg + OCT[o], n)
+            cur[:, ci, :] = (op @ loc[l - 1].reshape(nc, -1)).reshape(nc, -1, nk)
+        iv = irregular(M2L_OFF * size, 2 * p)
+        lim = None if boxes_fraction is None else max(1, int(math.ceil(boxes_fraction * n ** 3)))
+        for row, t, s in m2l_pairs(l):
+            if lim is not None:
+                keep = t < lim
+                t, s = t[keep], s[keep]
+                if t.size == 0:
+                    continue
+            op = m2l_from_iv(iv[row], p)
+            cur[:, t, :] += (op @ mult[l][:, s, :].reshape(nc, -1)).reshape(nc, t.size, nk)
+        loc[l] = cur
+    return loc
+
+
+def evaluate(tree, loc, p, grad=False, leaves=None):
+    """L2P (+gradient) at the particles (solver.py:294-324)."""
+    d = tree["depth"]
+    cen = leaf_centers(tree)
+    lof = tree["leaf_of_particle"]
+    start = tree["leaf_start"]
+    npart = tree["positions"].shape[0]
+    nk = loc[d].shape[2]
+    v = np.zeros((npart, nk))
+    g = np.zeros((npart, 3)) if grad else None
+    sel = np.arange(npart)
+    if leaves is not None:
+        sel = np.concatenate([np.arange(start[b], start[b + 1]) for b in leaves])
+    for c0 in range(0, sel.size, 65536):
+        ii = sel[c0:c0 + 65536]
+        disp = tree["positions"][ii] - cen[lof[ii]]
+        coeff = loc[d][:, lof[ii], :]  # (nc, n, K)
+        r = regular(disp, p)
+        v[ii] = np.real(np.einsum("nc,cnk->nk", r, coeff))
+        if grad:
+            gr = regular_grad(disp, p)
+            g[ii] = np.real(np.einsum("ncd,cn->nd", gr, coeff[:, :, 0]))
+    return v, g
+
+
+# -------------------------------------------------------------- solve ----
+def default_config(**kw):
+    cfg = dict(p=8, depth=2, lattice_mode="converged", shell_cap=8, dipole=True, periodic_near=True,
+               intra_site_images="full")
+    cfg.update(kw)
+    return cfg
+
+
+def solve(positions, charges, box, cfg, forces=False):
+    """PeriodicSolver(...).solve(q) (+ spatial_forces) in one function
+    (solver.py:330-427).  Returns a dict of input-order arrays."""
+    pos = wrap(np.atleast_2d(positions), box)
+    tree = build_tree(pos, box, cfg["depth"])
+    q = np.asarray(charges, np.float64)
+    single = q.ndim == 1
+    q2 = q[:, None] if single else q
+    qs = q2[tree["perm"]]
+    p = cfg["p"]
+    vn, gn = near_field(tree, qs, cfg["periodic_near"], grad=forces)
+    mult = upward(tree, qs, p)
+    lat = lattice_matrix(cfg, box)
+    root_local = None if lat is None else lat @ mult[0][:, 0, :]
+    loc = downward(tree, mult, p, root_local)
+    vf, gf = evaluate(tree, loc, p, grad=forces)
+    disp = tree["positions"] - 0.5 * box
+    dvec = disp.T @ qs
+    gam = 2.0 * math.pi / (3.0 * box ** 3)
+    if cfg["dipole"]:
+        vd = 2.0 * DIPOLE_ETA * gam * (disp @ dvec)
+        ed = DIPOLE_ETA * gam * (dvec * dvec).sum(0)
+    else:
+        vd = np.zeros_like(vn)
+        ed = np.zeros(qs.shape[1])
+    en = 0.5 * np.array([math.fsum((qs[:, k] * vn[:, k]).tolist()) for k in range(qs.shape[1])])
+    ef = 0.5 * np.array([math.fsum((qs[:, k] * vf[:, k]).tolist()) for k in range(qs.shape[1])])
+    inv = tree["inv_perm"]
+
+    def back(a):
+        a = a[inv]
+        return a[:, 0] if single else a
+
+    def sc(a):
+        return a[0] if single else a
+
+    out = dict(potentials=back(vn + vf + vd), near=back(vn), far=back(vf), dip=back(vd),
+               energy=sc(en + ef + ed), near_energy=sc(en), far_energy=sc(ef), dipole_energy=sc(ed),
+               root_multipole=mult[0][:, 0, 0] if single else mult[0][:, 0, :],
+               dipole_vector=dvec[:, 0] if single else dvec,
+               total_charge=sc(np.array([math.fsum(qs[:, k].tolist()) for k in range(qs.shape[1])])),
+               tree=tree, lattice=lat)
+    if forces:
+        f = -qs[:, :1] * (gn + gf)
+        if cfg["dipole"]:
+            f += -2.0 * DIPOLE_ETA * gam * qs[:, :1] * dvec[None, :, 0]
+        out["forces"] = f[inv]
+    return out
+
+
+# ------------------------------------------------------------------ HI ----
+def weights(lams):
+    """expand_weights (weights.py:54-60): lambda_0 on the LSB."""
+    w = np.ones(1)
+    for lam in lams:
+        w = np.concatenate([w * (1.0 - lam), w * lam])
+    return w
+
+
+def weight_grads(lams):
+    """weight_gradient_matrix (weights.py:63-85)."""
+    rows = []
+    for k in range(len(lams)):
+        g = np.ones(1)
+        for i, lam in enumerate(lams):
+            g = np.concatenate([-g, g]) if i == k else np.concatenate([g * (1.0 - lam), g * lam])
+        rows.append(g)
+    return np.stack(rows)
+
+
+def near_kernel(sp, box, images="full"):
+    """corrections.near_kernel (corrections.py:46-70)."""
+    disp = sp[:, None, :] - sp[None, :, :]
+    if images == "minimum":
+        d = disp - box * np.round(disp / box)
+        r = np.sqrt((d * d).sum(-1))
+        np.fill_diagonal(r, np.inf)
+        return 1.0 / r
+    k = np.zeros((sp.shape[0],) * 2)
+    for nvec in image_vectors(0, 1):
+        d = disp + nvec * box
+        r = np.sqrt((d * d).sum(-1))
+        if not nvec.any():
+            np.fill_diagonal(r, np.inf)
+        k += 1.0 / r
+    return k
+
+
+def lattice_kernel(sp, box, lat, p):
+    """corrections.lattice_kernel (corrections.py:73-77)."""
+    rv = regular(sp - 0.5 * box, p)
+    return np.real(rv @ lat @ rv.T)
+
+
+def hi(positions, charges, box, sites, lam_values, cfg, mode="hi", potentials=None, solve_out=None):
+    """hi_energy_and_forces (corrections.py:252-274) on plain arrays.
+
+    sites: list of (indices, form_charges (nf, ns)).  Returns dict with
+    energy, forces (list), per-site c_p2p / c_lattice / c_dipole / blend."""
+    q = np.array(charges, np.float64, copy=True)
+    for (idx, forms), lams in zip(sites, lam_values):
+        q[idx] = weights(lams) @ forms  # scale_charges (system.py:185-197)
+    res = solve_out if solve_out is not None else solve(positions, q, box, cfg)
+    v = res["potentials"] if potentials is None else potentials
+    lat = res["lattice"]
+    gam = 2.0 * math.pi / (3.0 * box ** 3)
+    out = dict(forces=[], c_p2p=[], c_lattice=[], c_dipole=[], blend=[], offset=[], solve=res, q_tilde=q)
+    for (idx, forms), lams in zip(sites, lam_values):
+        w = weights(lams)
+        gmat = weight_grads(lams)
+        sp = np.asarray(positions, np.float64)[idx]
+        qt = w @ forms
+        half = qt[None, :] - 0.5 * forms
+        dev = qt[None, :] - forms
+        s_rho = forms @ v[idx]
+        if mode == "qi":
+            out["forces"].append(-(gmat @ s_rho))
+            continue
+        full = cfg["intra_site_images"] == "full"
+        kern = near_kernel(sp, box, "full" if full else "minimum")
+        cp = np.einsum("fs,st,ft->f", forms, kern, half)
+        eb = 0.5 * float(qt @ kern @ qt)
+        if full and lat is not None:
+            gk = lattice_kernel(sp, box, lat, cfg["p"])
+            cl = np.einsum("fs,st,ft->f", forms, gk, half)
+            eb += 0.5 * float(qt @ gk @ qt)
+        else:
+            cl = np.zeros(forms.shape[0])
+        if full and cfg["dipole"]:
+            dd = dev @ (sp - 0.5 * box)
+            cd = -DIPOLE_ETA * gam * (dd * dd).sum(1)
+        else:
+            cd = np.zeros(forms.shape[0])
+        ct = cp + cl + cd
+        out["forces"].append(-(gmat @ (s_rho - ct)))
+        out["c_p2p"].append(cp)
+        out["c_lattice"].append(cl)
+        out["c_dipole"].append(cd)
+        out["blend"].append(eb)
+        out["offset"].append(eb - float(w @ ct))
+    e = float(res["energy"])
+    out["energy"] = e if mode == "qi" else e + math.fsum(out["offset"])
+    return out
+
+
+# ------------------------------------------------------ direct sums ----
+def direct_potentials(positions, charges, box, shell_cap=0):
+    """Brute-force image sum |n|_inf <= shell_cap (oracle.py:33-51)."""
+    pos = np.asarray(positions, np.float64)
+    q = np.asarray(charges, np.float64)
+    disp = pos[:, None, :] - pos[None, :, :]
+    v = np.zeros(pos.shape[0])
+    for nvec in image_vectors(0, shell_cap):
+        d = disp + nvec * box
+        r = np.sqrt((d * d).sum(-1))
+        if not nvec.any():
+            np.fill_diagonal(r, np.inf)
+        v += (1.0 / r) @ q
+    return v
+
+
+# --------------------------------------------------- timed CPU sample ----
+def timed_step_sample(positions, charges, box, sites, lam_values, cfg, fraction, clock):
+    """Time one full step (tree + scale + solve + forces + HI) with the
+    per-target stages (P2P, P2M, L2P, M2L/L2L) restricted to the first
+    `fraction` of leaves / boxes; returns (extrapolated seconds, parts).
+    Whole-system stages (tree, M2M, lattice, HI) run in full."""
+    parts = {}
+    t0 = clock()
+    pos = wrap(np.atleast_2d(positions), box)
+    tree = build_tree(pos, box, cfg["depth"])
+    q = np.array(charges, np.float64, copy=True)
+    for (idx, forms), lams in zip(sites, lam_values):
+        q[idx] = weights(lams) @ forms
+    parts["tree+scale"] = (clock() - t0, 1.0)
+    qs = q[tree["perm"]][:, None]
+    nleaf = 8 ** cfg["depth"]
+    leaves = np.arange(max(1, int(math.ceil(fraction * nleaf))))
+    f_eff = leaves.size / nleaf
+    t0 = clock()
+    near_field(tree, qs, cfg["periodic_near"], grad=True, leaves=leaves)
+    parts["p2p"] = (clock() - t0, f_eff)
+    t0 = clock()
+    mult = upward(tree, qs, cfg["p"], leaves=leaves)
+    parts["p2m+m2m"] = (clock() - t0, f_eff)
+    t0 = clock()
+    lat = lattice_matrix(cfg, box)
+    root_local = None if lat is None else lat @ mult[0][:, 0, :]
+    loc = downward(tree, mult, cfg["p"], root_local, boxes_fraction=fraction)
+    parts["m2l+l2l"] = (clock() - t0, max(fraction, 1.0 / nleaf))
+    t0 = clock()
+    evaluate(tree, loc, cfg["p"], grad=True, leaves=leaves)
+    parts["l2p"] = (clock() - t0, f_eff)
+    t0 = clock()
+    v = np.zeros(pos.shape[0])
+    res = dict(potentials=v, energy=0.0, lattice=lat)
+    hi(positions, charges, box, sites, lam_values, cfg, solve_out=res)
+    parts["hi"] = (clock() - t0, 1.0)
+    total = sum(t / f for t, f in parts.values())
+    return total, parts

@@ -1,0 +1,1384 @@
+// lfmm_api.cu — the C-ABI (include/lfmm.h) over the B200 kernels.
+//
+// One plan = one PeriodicSolver (fmm/solver.py:327-427): it owns every device
+// buffer (tree, expansions, operators, outputs) and runs on one CUDA stream.
+// All work is issued asynchronously on that stream; host<->device copies
+// happen only at the API edges (host pointers) or not at all (device
+// pointers, io_on_device != 0).
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <array>
+#include <cmath>
+#include <cstring>
+#include <map>
+#include <memory>
+#include <mutex>
+#include <string>
+#include <tuple>
+#include <vector>
+
+#include "lfmm_common.cuh"
+#include "lfmm_expansions.cuh"
+#include "lfmm_hi.cuh"
+#include "lfmm_p2p.cuh"
+#include "lfmm_setup.cuh"
+#include "lfmm_tree.cuh"
+
+using namespace lfmm;
+
+namespace {
+
+thread_local std::string g_last_error;
+
+enum Stage {
+  ST_TREE = 0,
+  ST_STAGE,
+  ST_P2P,
+  ST_P2M,
+  ST_M2M,
+  ST_ROOT,
+  ST_DOWN,
+  ST_L2P,
+  ST_FINAL,
+  ST_HI,
+  ST_SCALE,
+  ST_SETUP,
+  ST_COUNT
+};
+const char* kStageNames[ST_COUNT] = {"tree",  "stage_q", "p2p",      "p2m", "m2m",   "lattice",
+                                     "m2l_l2l", "l2p",   "finalize", "hi",  "scale", "setup"};
+
+// ------------------------------------------------------------ kernels ----
+template <class T>
+__global__ void k_stage_q(const double* __restrict__ q, int K, int c, const int* __restrict__ perm,
+                          const double* __restrict__ pos_sorted, int64_t n, double box,
+                          vec4_t<T>* __restrict__ xq, double* __restrict__ qs, dd* __restrict__ part) {
+  const int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  dd v[4] = {dd{0, 0}, dd{0, 0}, dd{0, 0}, dd{0, 0}};
+  if (k < n) {
+    const int i = perm[k];
+    const double qv = q[(size_t)i * K + c];
+    xq[k].w = (T)qv;
+    qs[k] = qv;
+    const double h = 0.5 * box;
+    v[0] = dd_from((pos_sorted[3 * k] - h) * qv);
+    v[1] = dd_from((pos_sorted[3 * k + 1] - h) * qv);
+    v[2] = dd_from((pos_sorted[3 * k + 2] - h) * qv);
+    v[3] = dd_from(qv);
+  }
+  block_reduce_dd<4>(v, part + (size_t)blockIdx.x * 4);
+}
+
+template <int NQ>
+__global__ void k_reduce_parts(const dd* __restrict__ part, int nb, double* __restrict__ out) {
+  dd v[NQ];
+#pragma unroll
+  for (int q = 0; q < NQ; ++q) v[q] = dd{0, 0};
+  // contiguous chunks per thread keep the order fixed
+  const int per = (nb + blockDim.x - 1) / blockDim.x;
+  const int b0 = min(nb, (int)threadIdx.x * per), b1 = min(nb, b0 + per);
+  for (int b = b0; b < b1; ++b)
+#pragma unroll
+    for (int q = 0; q < NQ; ++q) v[q] = dd_add(v[q], part[(size_t)b * NQ + q]);
+  __shared__ dd res[NQ];
+  block_reduce_dd<NQ>(v, res);
+  if (threadIdx.x == 0)
+#pragma unroll
+    for (int q = 0; q < NQ; ++q) out[q] = res[q].hi + res[q].lo;
+}
+
+template <class T, bool GRAD>
+__global__ void k_finalize(int64_t n, int K, int c, const int* __restrict__ perm,
+                           const double* __restrict__ pos_sorted, const double* __restrict__ qs,
+                           const T* __restrict__ vnear, const T* __restrict__ vfar,
+                           const T* __restrict__ gnear, const T* __restrict__ gfar,
+                           const double* __restrict__ scal /* Dx,Dy,Dz,Q */, int dipole, double box,
+                           double* __restrict__ out_pot, double* __restrict__ out_near,
+                           double* __restrict__ out_far, double* __restrict__ out_dip,
+                           double* __restrict__ out_forces, dd* __restrict__ part) {
+  const int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  dd v[2] = {dd{0, 0}, dd{0, 0}};
+  if (k < n) {
+    const int i = perm[k];
+    const double q = qs[k];
+    const double vn = (double)vnear[k], vf = (double)vfar[k];
+    const double gam = 2.0 * 3.14159265358979323846 / (3.0 * box * box * box);
+    const double h = 0.5 * box;
+    double vd = 0.0;
+    if (dipole)
+      vd = 2.0 * DIPOLE_ETA * gam *
+           ((pos_sorted[3 * k] - h) * scal[0] + (pos_sorted[3 * k + 1] - h) * scal[1] +
+            (pos_sorted[3 * k + 2] - h) * scal[2]);
+    const size_t o = (size_t)i * K + c;
+    if (out_pot) out_pot[o] = vn + vf + vd;
+    if (out_near) out_near[o] = vn;
+    if (out_far) out_far[o] = vf;
+    if (out_dip) out_dip[o] = vd;
+    if (GRAD && out_forces) {
+#pragma unroll
+      for (int a = 0; a < 3; ++a) {
+        double f = -q * ((double)gnear[3 * k + a] + (double)gfar[3 * k + a]);
+        if (dipole) f += -2.0 * DIPOLE_ETA * gam * q * scal[a];
+        out_forces[3 * (size_t)i + a] = f;
+      }
+    }
+    v[0] = dd_from(q * vn);
+    v[1] = dd_from(q * vf);
+  }
+  block_reduce_dd<2>(v, part + (size_t)blockIdx.x * 2);
+}
+
+// energies (4,K) rows total/near/far/dip; dipole (3,K); qtot (K)
+__global__ void k_energies(const double* __restrict__ scal, const double* __restrict__ epart, int K, int c,
+                           int dipole, double box, double* __restrict__ energies,
+                           double* __restrict__ dvec, double* __restrict__ qtot) {
+  const double gam = 2.0 * 3.14159265358979323846 / (3.0 * box * box * box);
+  const double en = 0.5 * epart[0], ef = 0.5 * epart[1];
+  const double ed = dipole ? DIPOLE_ETA * gam * (scal[0] * scal[0] + scal[1] * scal[1] + scal[2] * scal[2]) : 0.0;
+  energies[0 * K + c] = en + ef + ed;
+  energies[1 * K + c] = en;
+  energies[2 * K + c] = ef;
+  energies[3 * K + c] = ed;
+  dvec[0 * K + c] = scal[0];
+  dvec[1 * K + c] = scal[1];
+  dvec[2 * K + c] = scal[2];
+  qtot[c] = scal[3];
+}
+
+// warp per site: S_rho and lambda forces from given potentials and C_rho
+__global__ void k_assemble(int S, const int* __restrict__ atom_off, const int* __restrict__ atom_idx,
+                           const int* __restrict__ nforms, const int* __restrict__ form_off,
+                           const int* __restrict__ fslot_off, const double* __restrict__ form_q,
+                           const double* __restrict__ lambdas, const int* __restrict__ nlam,
+                           const double* __restrict__ c_total, const double* __restrict__ pot,
+                           double* __restrict__ out) {
+  const int s = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  const int lane = threadIdx.x & 31;
+  if (s >= S) return;
+  const int a0 = atom_off[s], ns = atom_off[s + 1] - a0, nf = nforms[s], nl = nlam[s];
+  const double* Q = form_q + form_off[s];
+  const double* lam = lambdas + 4 * s;
+  double f[4] = {0, 0, 0, 0};
+  for (int r = 0; r < nf; ++r) {
+    double sv = 0.0;
+    for (int i = lane; i < ns; i += 32) sv += Q[r * ns + i] * pot[atom_idx[a0 + i]];
+    for (int off = 16; off > 0; off >>= 1) sv += __shfl_down_sync(0xffffffffu, sv, off);
+    if (c_total) sv -= c_total[fslot_off[s] + r];
+    for (int k = 0; k < nl; ++k) f[k] += hi_wgrad(lam, nl, k, r) * sv;
+  }
+  if (lane == 0)
+    for (int k = 0; k < 4; ++k) out[4 * s + k] = k < nl ? -f[k] : 0.0;
+}
+
+__global__ void k_step_energy(const double* __restrict__ energies, const double* __restrict__ off, int add,
+                              double* __restrict__ out) {
+  *out = energies[0] + (add ? off[0] : 0.0);
+}
+
+__global__ void k_i32_to_i64(const int* __restrict__ in, int64_t n, int64_t* __restrict__ out) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i < n) out[i] = in[i];
+}
+
+__global__ void k_check_finite(const double* __restrict__ v, int64_t n, int* __restrict__ flag) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i < n && !isfinite(v[i])) atomicOr(flag, 1);
+}
+
+// ------------------------------------------------------ host helpers ----
+struct DevBuf {
+  void* p = nullptr;
+  size_t bytes = 0;
+  void ensure(size_t b) {
+    if (b <= bytes) return;
+    if (p) cudaFree(p);
+    p = nullptr;
+    bytes = 0;
+    if (b == 0) return;
+    LFMM_CUDA(cudaMalloc(&p, b));
+    bytes = b;
+  }
+  void release() {
+    if (p) cudaFree(p);
+    p = nullptr;
+    bytes = 0;
+  }
+  template <class U>
+  U* as() const {
+    return reinterpret_cast<U*>(p);
+  }
+};
+
+std::once_flag g_const_once;
+std::vector<std::array<int, 3>> g_m2l_offsets;  // 316 rows (octree.py:31)
+
+void init_constants() {
+  // 1/((l+m)(l-m)) and 1/(2m)
+  std::vector<double> inv_lm((PMAX + 2) * (PMAX + 2), 0.0);
+  std::vector<float> inv_lm_f((PMAX + 2) * (PMAX + 2), 0.0f);
+  std::vector<double> inv2m(PMAX + 2, 0.0);
+  std::vector<float> inv2m_f(PMAX + 2, 0.0f);
+  for (int l = 0; l <= PMAX + 1; ++l)
+    for (int m = 0; m < l; ++m) {
+      inv_lm[l * (PMAX + 2) + m] = 1.0 / double((l + m) * (l - m));
+      inv_lm_f[l * (PMAX + 2) + m] = (float)inv_lm[l * (PMAX + 2) + m];
+    }
+  for (int m = 1; m <= PMAX + 1; ++m) {
+    inv2m[m] = 1.0 / (2.0 * m);
+    inv2m_f[m] = (float)inv2m[m];
+  }
+  LFMM_CUDA(cudaMemcpyToSymbol(c_inv_lm_d, inv_lm.data(), inv_lm.size() * sizeof(double)));
+  LFMM_CUDA(cudaMemcpyToSymbol(c_inv_lm_f, inv_lm_f.data(), inv_lm_f.size() * sizeof(float)));
+  LFMM_CUDA(cudaMemcpyToSymbol(c_inv_2m_d, inv2m.data(), inv2m.size() * sizeof(double)));
+  LFMM_CUDA(cudaMemcpyToSymbol(c_inv_2m_f, inv2m_f.data(), inv2m_f.size() * sizeof(float)));
+  // M2L offsets in lexicographic order over [-3,3]^3 with Chebyshev norm >= 2,
+  // and per parity the valid rows (-2-par <= o <= 3-par per axis)
+  g_m2l_offsets.clear();
+  for (int x = -3; x <= 3; ++x)
+    for (int y = -3; y <= 3; ++y)
+      for (int z = -3; z <= 3; ++z)
+        if (std::max(std::abs(x), std::max(std::abs(y), std::abs(z))) >= 2) g_m2l_offsets.push_back({x, y, z});
+  std::vector<char4> off(8 * NM2L);
+  std::vector<short> rows(8 * NM2L);
+  for (int par = 0; par < 8; ++par) {
+    const int pb[3] = {(par >> 2) & 1, (par >> 1) & 1, par & 1};
+    int s = 0;
+    for (int r = 0; r < (int)g_m2l_offsets.size(); ++r) {
+      bool ok = true;
+      for (int a = 0; a < 3; ++a) ok = ok && (-2 - pb[a] <= g_m2l_offsets[r][a]) && (g_m2l_offsets[r][a] <= 3 - pb[a]);
+      if (!ok) continue;
+      if (s >= NM2L) throw Error{LFMM_ECUDA, "M2L list overflow"};
+      off[par * NM2L + s] = make_char4((char)g_m2l_offsets[r][0], (char)g_m2l_offsets[r][1],
+                                       (char)g_m2l_offsets[r][2], 0);
+      rows[par * NM2L + s] = (short)r;
+      ++s;
+    }
+    if (s != NM2L) throw Error{LFMM_ECUDA, "M2L list size mismatch"};
+  }
+  LFMM_CUDA(cudaMemcpyToSymbol(c_m2l_off, off.data(), off.size() * sizeof(char4)));
+  LFMM_CUDA(cudaMemcpyToSymbol(c_m2l_row, rows.data(), rows.size() * sizeof(short)));
+}
+
+// process-level cache of unit-box lattice operators, like lru_cache on
+// converged_operator / shell_sum_operator (lattice.py:108, :123)
+std::mutex g_lat_mu;
+std::map<std::tuple<int, int, int>, std::vector<double2>> g_lat_cache;
+
+inline unsigned nblk(int64_t n, int t) { return (unsigned)((n + t - 1) / t); }
+
+}  // namespace
+
+// ----------------------------------------------------------------- plan ----
+struct lfmm_plan {
+  int64_t N = 0;
+  double L = 0.0;
+  int p = 0, depth = 0, lattice_mode = 0, shell_cap = 0, flags = 0;
+  bool fp32 = false;
+  int nc = 0, ncp = 0, nleaf = 0;
+  double size = 0.0;  // leaf edge
+  int64_t level_off[DMAX + 2] = {0};
+  int64_t nbox_total = 0;
+  cudaStream_t stream = nullptr, own_stream = nullptr;
+  int64_t launches = 0;
+  bool profiling = false;
+  struct Ev {
+    int stage;
+    cudaEvent_t a, b;
+  };
+  std::vector<Ev> pending;
+  std::vector<cudaEvent_t> free_events;
+  double stage_ms[ST_COUNT] = {0};
+  int64_t stage_launch[ST_COUNT] = {0};
+
+  // tree
+  DevBuf pos_in, pos_wrap, leaf_of, counts, cursor, leaf_start, bucket, perm, inv_perm, pos_sorted, leaf_sorted, xq;
+  // expansions / operators
+  DevBuf mult, loc, ops_m2l, ops_m2m, ops_l2l, ops_lat, lat64t;
+  std::vector<double2> lat_unit;  // unit-box complex lattice operator (nc x nc)
+  // solve work
+  DevBuf q_in, qs, vnear, vfar, gnear, gfar, part, scal, epart, roots;
+  DevBuf out_pot, out_near, out_far, out_dip, out_forces, energies, dvec, qtot;
+  int64_t last_k = 0;
+  bool last_valid = false;
+  // sites
+  int64_t n_sites = 0, n_site_atoms = 0, n_form_slots = 0;
+  int ns_max = 0;
+  std::vector<int> h_atom_off, h_atom_idx, h_nforms, h_fslot_off;
+  DevBuf atom_off, atom_idx, nforms, form_off, fslot_off, form_q, site_pos, lambdas, nlam, rscr, uscr;
+  DevBuf c_p2p, c_lat, c_dip, blend, lam_forces, offsets, offset_total, pot_tmp, q_tmp;
+  DevBuf finite_flag;
+
+  size_t tsz() const { return fp32 ? sizeof(float) : sizeof(double); }
+
+  // --- launch bookkeeping ---
+  cudaEvent_t get_event() {
+    if (!free_events.empty()) {
+      cudaEvent_t e = free_events.back();
+      free_events.pop_back();
+      return e;
+    }
+    cudaEvent_t e;
+    LFMM_CUDA(cudaEventCreate(&e));
+    return e;
+  }
+  template <class F>
+  void launch(int stage, F&& f) {
+    cudaEvent_t a = nullptr, b = nullptr;
+    if (profiling) {
+      a = get_event();
+      b = get_event();
+      LFMM_CUDA(cudaEventRecord(a, stream));
+    }
+    f();
+    LFMM_CUDA(cudaGetLastError());
+    ++launches;
+    stage_launch[stage]++;
+    if (profiling) {
+      LFMM_CUDA(cudaEventRecord(b, stream));
+      pending.push_back({stage, a, b});
+    }
+  }
+  void harvest() {
+    if (pending.empty()) return;
+    LFMM_CUDA(cudaStreamSynchronize(stream));
+    for (auto& e : pending) {
+      float ms = 0.f;
+      LFMM_CUDA(cudaEventElapsedTime(&ms, e.a, e.b));
+      stage_ms[e.stage] += ms;
+      free_events.push_back(e.a);
+      free_events.push_back(e.b);
+    }
+    pending.clear();
+  }
+  ~lfmm_plan() {
+    if (stream) cudaStreamSynchronize(stream);
+    for (auto& e : pending) {
+      cudaEventDestroy(e.a);
+      cudaEventDestroy(e.b);
+    }
+    for (auto e : free_events) cudaEventDestroy(e);
+    DevBuf* bufs[] = {&pos_in, &pos_wrap, &leaf_of, &counts, &cursor, &leaf_start, &bucket, &perm,
+                      &inv_perm, &pos_sorted, &leaf_sorted, &xq, &mult, &loc, &ops_m2l, &ops_m2m,
+                      &ops_l2l, &ops_lat, &lat64t, &q_in, &qs, &vnear, &vfar, &gnear, &gfar, &part,
+                      &scal, &epart, &roots, &out_pot, &out_near, &out_far, &out_dip, &out_forces, &energies,
+                      &dvec, &qtot, &atom_off, &atom_idx, &nforms, &form_off, &fslot_off, &form_q,
+                      &site_pos, &lambdas, &nlam, &rscr, &uscr, &c_p2p, &c_lat, &c_dip, &blend,
+                      &lam_forces, &offsets, &offset_total, &pot_tmp, &q_tmp, &finite_flag};
+    for (auto* b : bufs) b->release();
+    if (own_stream) cudaStreamDestroy(own_stream);
+  }
+
+  // ------------------------------------------------ operator setup ----
+  template <class T>
+  void realify(int kind, int nmat, const double2* data, int64_t stride, double out_pow, int out_add,
+               double in_pow, T* out) {
+    const int64_t total = (int64_t)ncp * ncp * nmat;
+    launch(ST_SETUP, [&] {
+      k_realify<T><<<nblk(total, 256), 256, 0, stream>>>(kind, p, nmat, data, stride, out_pow, out_add, in_pow,
+                                                         out, ncp);
+    });
+  }
+
+  std::vector<double2> build_lattice_unit() {
+    const int nco = ncoef(p), P2 = 2 * p, nc2 = ncoef(P2);
+    auto key = std::make_tuple(p, lattice_mode, lattice_mode == LFMM_LATTICE_SHELLS ? shell_cap : 0);
+    {
+      std::lock_guard<std::mutex> lk(g_lat_mu);
+      auto it = g_lat_cache.find(key);
+      if (it != g_lat_cache.end()) return it->second;
+    }
+    // image vectors
+    auto shell = [](int smin, int smax) {
+      std::vector<double> v;
+      for (int x = -smax; x <= smax; ++x)
+        for (int y = -smax; y <= smax; ++y)
+          for (int z = -smax; z <= smax; ++z) {
+            const int nrm = std::max(std::abs(x), std::max(std::abs(y), std::abs(z)));
+            if (nrm >= smin && nrm <= smax) {
+              v.push_back(x);
+              v.push_back(y);
+              v.push_back(z);
+            }
+          }
+      return v;
+    };
+    DevBuf vecs, vals, ivsum, rvsum, t_ring, s_hat, bmat, tmp, total, fin;
+    ivsum.ensure(sizeof(double2) * nc2);
+    LFMM_CUDA(cudaMemsetAsync(ivsum.p, 0, ivsum.bytes, stream));
+    auto sum_harmonics = [&](const std::vector<double>& v, int order, int irregular, DevBuf& acc) {
+      const int nv = (int)v.size() / 3, ncoefs = ncoef(order);
+      const int chunk = 1024;
+      vecs.ensure(sizeof(double) * 3 * chunk);
+      vals.ensure(sizeof(double2) * (size_t)ncoefs * chunk);
+      for (int lo = 0; lo < nv; lo += chunk) {
+        const int cnt = std::min(chunk, nv - lo);
+        LFMM_CUDA(cudaMemcpyAsync(vecs.p, v.data() + 3 * lo, sizeof(double) * 3 * cnt, cudaMemcpyHostToDevice,
+                                  stream));
+        launch(ST_SETUP, [&] {
+          k_harmonics_full<<<nblk(cnt, 64), 64, 0, stream>>>(vecs.as<double>(), cnt, order, irregular,
+                                                              vals.as<double2>());
+        });
+        launch(ST_SETUP, [&] {
+          k_sum_vectors<<<nblk(ncoefs, 128), 128, 0, stream>>>(vals.as<double2>(), cnt, ncoefs,
+                                                                acc.as<double2>());
+        });
+        LFMM_CUDA(cudaStreamSynchronize(stream));  // host vector chunk reuse
+      }
+    };
+    const int64_t nn = (int64_t)nco * nco;
+    total.ensure(sizeof(double2) * nn);
+    fin.ensure(sizeof(double2) * nn);
+    if (lattice_mode == LFMM_LATTICE_SHELLS) {
+      auto v = shell(2, shell_cap);
+      if (!v.empty()) sum_harmonics(v, P2, 1, ivsum);
+      launch(ST_SETUP, [&] {
+        k_dense_from_vector<<<nblk(nn, 256), 256, 0, stream>>>(OP_M2L, ivsum.as<double2>(), p, 1.0,
+                                                               total.as<double2>());
+      });
+      launch(ST_SETUP, [&] {
+        k_lattice_finish<<<nblk(nn, 256), 256, 0, stream>>>(total.as<double2>(), fin.as<double2>(), p, 0);
+      });
+    } else {
+      // converged_operator: factor-3 telescoping, 24 steps (lattice.py:124-155)
+      auto ring = shell(2, 4);
+      sum_harmonics(ring, P2, 1, ivsum);
+      auto w27 = shell(0, 1);
+      rvsum.ensure(sizeof(double2) * nco);
+      LFMM_CUDA(cudaMemsetAsync(rvsum.p, 0, rvsum.bytes, stream));
+      sum_harmonics(w27, p, 0, rvsum);
+      t_ring.ensure(sizeof(double2) * nn);
+      s_hat.ensure(sizeof(double2) * nn);
+      bmat.ensure(sizeof(double2) * nn);
+      tmp.ensure(sizeof(double2) * nn);
+      launch(ST_SETUP, [&] {
+        k_dense_from_vector<<<nblk(nn, 256), 256, 0, stream>>>(OP_M2L, ivsum.as<double2>(), p, 1.0,
+                                                               t_ring.as<double2>());
+      });
+      launch(ST_SETUP, [&] {
+        k_dense_from_vector<<<nblk(nn, 256), 256, 0, stream>>>(OP_M2M, rvsum.as<double2>(), p, 1.0 / 3.0,
+                                                               s_hat.as<double2>());
+      });
+      launch(ST_SETUP, [&] { k_identity<<<nblk(nn, 256), 256, 0, stream>>>(bmat.as<double2>(), nco); });
+      LFMM_CUDA(cudaMemsetAsync(total.p, 0, total.bytes, stream));
+      dim3 zb(16, 16), zg((nco + 15) / 16, (nco + 15) / 16);
+      const int steps = 24;
+      for (int k = 0; k < steps; ++k) {
+        launch(ST_SETUP, [&] {
+          k_zgemm<<<zg, zb, 0, stream>>>(t_ring.as<double2>(), bmat.as<double2>(), tmp.as<double2>(), nco);
+        });
+        launch(ST_SETUP, [&] {
+          k_lattice_accum<<<nblk(nn, 256), 256, 0, stream>>>(total.as<double2>(), tmp.as<double2>(), p, k);
+        });
+        if (k + 1 < steps) {
+          launch(ST_SETUP, [&] {
+            k_zgemm<<<zg, zb, 0, stream>>>(s_hat.as<double2>(), bmat.as<double2>(), tmp.as<double2>(), nco);
+          });
+          std::swap(bmat, tmp);
+        }
+      }
+      launch(ST_SETUP, [&] {
+        k_lattice_finish<<<nblk(nn, 256), 256, 0, stream>>>(total.as<double2>(), fin.as<double2>(), p, 4);
+      });
+    }
+    std::vector<double2> host(nn);
+    LFMM_CUDA(cudaMemcpyAsync(host.data(), fin.p, sizeof(double2) * nn, cudaMemcpyDeviceToHost, stream));
+    LFMM_CUDA(cudaStreamSynchronize(stream));
+    DevBuf* tmpbufs[] = {&vecs, &vals, &ivsum, &rvsum, &t_ring, &s_hat, &bmat, &tmp, &total, &fin};
+    for (auto* b : tmpbufs) b->release();
+    std::lock_guard<std::mutex> lk(g_lat_mu);
+    g_lat_cache[key] = host;
+    return host;
+  }
+
+  template <class T>
+  void build_operators() {
+    const size_t opb = (size_t)ncp * ncp * sizeof(T);
+    ops_m2l.ensure(opb * NOFF);
+    ops_m2m.ensure(opb * 8);
+    ops_l2l.ensure(opb * 8);
+    DevBuf vecs, vals;
+    // M2L: irregular(o, 2p) of the 316 unit offsets
+    {
+      std::vector<double> v;
+      for (auto& o : g_m2l_offsets) {
+        v.push_back(o[0]);
+        v.push_back(o[1]);
+        v.push_back(o[2]);
+      }
+      const int nc2 = ncoef(2 * p);
+      vecs.ensure(sizeof(double) * v.size());
+      vals.ensure(sizeof(double2) * (size_t)nc2 * NOFF);
+      LFMM_CUDA(cudaMemcpyAsync(vecs.p, v.data(), sizeof(double) * v.size(), cudaMemcpyHostToDevice, stream));
+      launch(ST_SETUP, [&] {
+        k_harmonics_full<<<nblk(NOFF, 64), 64, 0, stream>>>(vecs.as<double>(), NOFF, 2 * p, 1,
+                                                             vals.as<double2>());
+      });
+      realify<T>(OP_M2L, NOFF, vals.as<double2>(), nc2, 1.0, 0, 1.0, ops_m2l.as<T>());
+      LFMM_CUDA(cudaStreamSynchronize(stream));
+    }
+    // M2M (parent edge 1, child 1/2): A(d) = gather R(-d), d = (0.5-oct)/2;
+    // normalised by child^j; L2L: C = gather R(d)^T, d = (oct-0.5)/2,
+    // normalised by child^(j+1)
+    for (int which = 0; which < 2; ++which) {
+      std::vector<double> v;
+      for (int oct = 0; oct < 8; ++oct) {
+        const int ob[3] = {(oct >> 2) & 1, (oct >> 1) & 1, oct & 1};
+        for (int a = 0; a < 3; ++a) {
+          const double d = which == 0 ? (0.5 - ob[a]) * 0.5 : (ob[a] - 0.5) * 0.5;
+          v.push_back(which == 0 ? -d : d);
+        }
+      }
+      const int ncr = ncoef(p);
+      vecs.ensure(sizeof(double) * v.size());
+      vals.ensure(sizeof(double2) * (size_t)ncr * 8);
+      LFMM_CUDA(cudaMemcpyAsync(vecs.p, v.data(), sizeof(double) * v.size(), cudaMemcpyHostToDevice, stream));
+      launch(ST_SETUP, [&] {
+        k_harmonics_full<<<1, 64, 0, stream>>>(vecs.as<double>(), 8, p, 0, vals.as<double2>());
+      });
+      if (which == 0)
+        realify<T>(OP_M2M, 8, vals.as<double2>(), ncr, 1.0, 0, 0.5, ops_m2m.as<T>());
+      else
+        realify<T>(OP_L2L, 8, vals.as<double2>(), ncr, 0.5, 1, 1.0, ops_l2l.as<T>());
+      LFMM_CUDA(cudaStreamSynchronize(stream));
+    }
+    if (lattice_mode != LFMM_LATTICE_OFF) {
+      lat_unit = build_lattice_unit();
+      const int64_t nn = (int64_t)nc * nc;
+      vals.ensure(sizeof(double2) * nn);
+      LFMM_CUDA(cudaMemcpyAsync(vals.p, lat_unit.data(), sizeof(double2) * nn, cudaMemcpyHostToDevice, stream));
+      ops_lat.ensure(opb);
+      realify<T>(OP_DENSE, 1, vals.as<double2>(), nn, 1.0, 0, 1.0, ops_lat.as<T>());
+      // fp64 transposed copy for the HI lattice kernel
+      DevBuf l64;
+      l64.ensure(sizeof(double) * ncp * ncp);
+      realify<double>(OP_DENSE, 1, vals.as<double2>(), nn, 1.0, 0, 1.0, l64.as<double>());
+      std::vector<double> h(ncp * (size_t)ncp), ht(ncp * (size_t)ncp);
+      LFMM_CUDA(cudaMemcpyAsync(h.data(), l64.p, sizeof(double) * h.size(), cudaMemcpyDeviceToHost, stream));
+      LFMM_CUDA(cudaStreamSynchronize(stream));
+      for (int a = 0; a < ncp; ++a)
+        for (int b = 0; b < ncp; ++b) ht[(size_t)b * ncp + a] = h[(size_t)a * ncp + b];
+      lat64t.ensure(sizeof(double) * ht.size());
+      LFMM_CUDA(cudaMemcpyAsync(lat64t.p, ht.data(), sizeof(double) * ht.size(), cudaMemcpyHostToDevice, stream));
+      LFMM_CUDA(cudaStreamSynchronize(stream));
+      l64.release();
+    }
+    LFMM_CUDA(cudaStreamSynchronize(stream));
+    vecs.release();
+    vals.release();
+  }
+
+  // ----------------------------------------------------------- tree ----
+  template <class T>
+  void build_tree(const double* positions, bool on_device) {
+    if (on_device)
+      LFMM_CUDA(cudaMemcpyAsync(pos_in.p, positions, sizeof(double) * 3 * N, cudaMemcpyDeviceToDevice, stream));
+    else
+      LFMM_CUDA(cudaMemcpyAsync(pos_in.p, positions, sizeof(double) * 3 * N, cudaMemcpyHostToDevice, stream));
+    LFMM_CUDA(cudaMemsetAsync(counts.p, 0, sizeof(int) * nleaf, stream));
+    LFMM_CUDA(cudaMemsetAsync(cursor.p, 0, sizeof(int) * nleaf, stream));
+    if (N > 0) {
+      launch(ST_TREE, [&] {
+        k_wrap_cell<<<nblk(N, 256), 256, 0, stream>>>(pos_in.as<double>(), N, L, size, depth,
+                                                       pos_wrap.as<double>(), leaf_of.as<int>(), counts.as<int>());
+      });
+    }
+    launch(ST_TREE, [&] { k_scan_counts<<<1, 1024, 0, stream>>>(counts.as<int>(), nleaf, leaf_start.as<int>()); });
+    if (N > 0) {
+      launch(ST_TREE, [&] {
+        k_scatter_leaf<<<nblk(N, 256), 256, 0, stream>>>(leaf_of.as<int>(), N, leaf_start.as<int>(),
+                                                          cursor.as<int>(), bucket.as<int>());
+      });
+      launch(ST_TREE, [&] {
+        k_leaf_rank<<<nblk((int64_t)nleaf * 32, 128), 128, 0, stream>>>(
+            pos_wrap.as<double>(), leaf_start.as<int>(), bucket.as<int>(), nleaf, perm.as<int>(), inv_perm.as<int>());
+      });
+      launch(ST_TREE, [&] {
+        k_sorted_arrays<T><<<nblk(N, 256), 256, 0, stream>>>(pos_wrap.as<double>(), perm.as<int>(),
+                                                              leaf_of.as<int>(), N, depth, size,
+                                                              pos_sorted.as<double>(), xq.as<vec4_t<T>>(),
+                                                              leaf_sorted.as<int>());
+      });
+    }
+    last_valid = false;
+  }
+
+  // ---------------------------------------------------------- solve ----
+  template <class T>
+  void solve_column(int K, int c, bool grad) {
+    const int64_t nb = nblk(N, 256);
+    const T tsize = (T)size;
+    launch(ST_STAGE, [&] {
+      k_stage_q<T><<<(unsigned)nb, 256, 0, stream>>>(q_in.as<double>(), K, c, perm.as<int>(), pos_sorted.as<double>(),
+                                                     N, L, xq.as<vec4_t<T>>(), qs.as<double>(), part.as<dd>());
+    });
+    launch(ST_STAGE, [&] { k_reduce_parts<4><<<1, 256, 0, stream>>>(part.as<dd>(), (int)nb, scal.as<double>()); });
+    const int periodic = (flags & LFMM_F_PERIODIC_NEAR) ? 1 : 0;
+    const unsigned lb = nblk(nleaf, P2P_WARPS);
+    launch(ST_P2P, [&] {
+      if (grad)
+        k_p2p<T, true><<<lb, P2P_WARPS * 32, 0, stream>>>(xq.as<vec4_t<T>>(), leaf_start.as<int>(), depth, tsize,
+                                                           periodic, vnear.as<T>(), gnear.as<T>());
+      else
+        k_p2p<T, false><<<lb, P2P_WARPS * 32, 0, stream>>>(xq.as<vec4_t<T>>(), leaf_start.as<int>(), depth, tsize,
+                                                            periodic, vnear.as<T>(), gnear.as<T>());
+    });
+    T* M = mult.as<T>();
+    T* Lc = loc.as<T>();
+    launch(ST_P2M, [&] {
+      k_p2m<T><<<nblk(nleaf, EXP_WARPS), EXP_WARPS * 32, 0, stream>>>(
+          xq.as<vec4_t<T>>(), leaf_start.as<int>(), depth, p, (T)(1.0 / size), ncp, M + level_off[depth] * ncp);
+    });
+    const unsigned rowb = (unsigned)((ncp + GB_M - 1) / GB_M);
+    for (int l = depth - 1; l >= 0; --l) {
+      GemmArgs ga{};
+      ga.mode = GEMM_UP;
+      ga.level = l;
+      ga.ncp = ncp;
+      ga.src_aux = M + level_off[l + 1] * ncp;
+      ga.dst = M + level_off[l] * ncp;
+      ga.ops_main = ops_m2m.p;
+      dim3 grid(gemm_tiles_per_class(GEMM_UP, l), rowb);
+      launch(ST_M2M, [&] { k_gemm_gather<T><<<grid, G_THREADS, 0, stream>>>(ga); });
+    }
+    if (lattice_mode != LFMM_LATTICE_OFF) {
+      GemmArgs ga{};
+      ga.mode = GEMM_ROOT;
+      ga.level = 0;
+      ga.ncp = ncp;
+      ga.src_aux = M;
+      ga.dst = Lc;
+      ga.ops_main = ops_lat.p;
+      dim3 grid(1, rowb);
+      launch(ST_ROOT, [&] { k_gemm_gather<T><<<grid, G_THREADS, 0, stream>>>(ga); });
+    } else {
+      LFMM_CUDA(cudaMemsetAsync(Lc, 0, sizeof(T) * ncp, stream));
+    }
+    for (int l = 1; l <= depth; ++l) {
+      GemmArgs ga{};
+      ga.mode = GEMM_DOWN;
+      ga.level = l;
+      ga.ncp = ncp;
+      ga.src_m2l = M + level_off[l] * ncp;
+      ga.src_aux = Lc + level_off[l - 1] * ncp;
+      ga.dst = Lc + level_off[l] * ncp;
+      ga.ops_main = ops_m2l.p;
+      ga.ops_l2l = ops_l2l.p;
+      ga.use_m2l = 1;
+      dim3 grid(8 * gemm_tiles_per_class(GEMM_DOWN, l), rowb);
+      launch(ST_DOWN, [&] { k_gemm_gather<T><<<grid, G_THREADS, 0, stream>>>(ga); });
+    }
+    {
+      const int per_warp = ncoef(p) + 3 * p * p;
+      int warps = EXP_WARPS;
+      while (warps > 1 && (size_t)warps * per_warp * sizeof(T) > 48 * 1024) warps >>= 1;
+      const size_t smem = (size_t)warps * per_warp * sizeof(T);
+      launch(ST_L2P, [&] {
+        if (grad)
+          k_l2p<T, true><<<nblk(nleaf, warps), warps * 32, smem, stream>>>(
+              xq.as<vec4_t<T>>(), leaf_start.as<int>(), depth, p, tsize, ncp, Lc + level_off[depth] * ncp,
+              vfar.as<T>(), gfar.as<T>());
+        else
+          k_l2p<T, false><<<nblk(nleaf, warps), warps * 32, smem, stream>>>(
+              xq.as<vec4_t<T>>(), leaf_start.as<int>(), depth, p, tsize, ncp, Lc + level_off[depth] * ncp,
+              vfar.as<T>(), gfar.as<T>());
+      });
+    }
+    const int dip = (flags & LFMM_F_DIPOLE) ? 1 : 0;
+    launch(ST_FINAL, [&] {
+      if (grad)
+        k_finalize<T, true><<<(unsigned)nb, 256, 0, stream>>>(
+            N, K, c, perm.as<int>(), pos_sorted.as<double>(), qs.as<double>(), vnear.as<T>(), vfar.as<T>(),
+            gnear.as<T>(), gfar.as<T>(), scal.as<double>(), dip, L, out_pot.as<double>(), out_near.as<double>(),
+            out_far.as<double>(), out_dip.as<double>(), out_forces.as<double>(), part.as<dd>());
+      else
+        k_finalize<T, false><<<(unsigned)nb, 256, 0, stream>>>(
+            N, K, c, perm.as<int>(), pos_sorted.as<double>(), qs.as<double>(), vnear.as<T>(), vfar.as<T>(),
+            gnear.as<T>(), gfar.as<T>(), scal.as<double>(), dip, L, out_pot.as<double>(), out_near.as<double>(),
+            out_far.as<double>(), out_dip.as<double>(), nullptr, part.as<dd>());
+    });
+    launch(ST_FINAL, [&] { k_reduce_parts<2><<<1, 256, 0, stream>>>(part.as<dd>(), (int)nb, epart.as<double>()); });
+    launch(ST_FINAL, [&] {
+      k_energies<<<1, 1, 0, stream>>>(scal.as<double>(), epart.as<double>(), K, c, dip, L, energies.as<double>(),
+                                      dvec.as<double>(), qtot.as<double>());
+    });
+  }
+
+  void ensure_solve_buffers(int64_t K, bool grad) {
+    const size_t t = tsz();
+    q_in.ensure(sizeof(double) * N * K + 8);
+    qs.ensure(sizeof(double) * N + 8);
+    vnear.ensure(t * N + 16);
+    vfar.ensure(t * N + 16);
+    if (grad) {
+      gnear.ensure(t * 3 * N + 16);
+      gfar.ensure(t * 3 * N + 16);
+      out_forces.ensure(sizeof(double) * 3 * N + 8);
+    }
+    part.ensure(sizeof(dd) * 4 * (nblk(N, 256) + 1));
+    out_pot.ensure(sizeof(double) * N * K + 8);
+    out_near.ensure(sizeof(double) * N * K + 8);
+    out_far.ensure(sizeof(double) * N * K + 8);
+    out_dip.ensure(sizeof(double) * N * K + 8);
+    energies.ensure(sizeof(double) * 4 * K);
+    dvec.ensure(sizeof(double) * 3 * K);
+    qtot.ensure(sizeof(double) * K);
+  }
+
+  void run_solve(int64_t K, bool grad) {
+    roots.ensure(tsz() * ncp * K);
+    for (int64_t c = 0; c < K; ++c) {
+      if (fp32)
+        solve_column<float>((int)K, (int)c, grad);
+      else
+        solve_column<double>((int)K, (int)c, grad);
+      // keep this column's root multipole (level 0 of the upward pass)
+      LFMM_CUDA(cudaMemcpyAsync(static_cast<char*>(roots.p) + tsz() * ncp * c, mult.p, tsz() * ncp,
+                                cudaMemcpyDeviceToDevice, stream));
+    }
+    last_k = K;
+    last_valid = true;
+  }
+
+  void root_multipole_host(int64_t K, int64_t c, double* out /* nc x K complex interleaved */) {
+    // leaf-level normalisation: M_l = M^_l * L^l at the root (edge L)
+    std::vector<double> hv(ncp);
+    const char* src = static_cast<const char*>(roots.p) + tsz() * ncp * c;
+    if (fp32) {
+      std::vector<float> hf(ncp);
+      LFMM_CUDA(cudaMemcpyAsync(hf.data(), src, sizeof(float) * ncp, cudaMemcpyDeviceToHost, stream));
+      LFMM_CUDA(cudaStreamSynchronize(stream));
+      for (int i = 0; i < ncp; ++i) hv[i] = hf[i];
+    } else {
+      LFMM_CUDA(cudaMemcpyAsync(hv.data(), src, sizeof(double) * ncp, cudaMemcpyDeviceToHost, stream));
+      LFMM_CUDA(cudaStreamSynchronize(stream));
+    }
+    for (int l = 0; l <= p; ++l) {
+      const double sc = std::pow(L, l);
+      for (int m = -l; m <= l; ++m) {
+        double re, im;
+        const int mm = std::abs(m);
+        if (mm == 0) {
+          re = hv[pk_index(p, l, 0, 0)];
+          im = 0.0;
+        } else {
+          re = hv[pk_index(p, l, mm, 0)];
+          im = hv[pk_index(p, l, mm, 1)];
+          if (m < 0) {
+            const double s = (mm & 1) ? -1.0 : 1.0;
+            re *= s;
+            im *= -s;
+          }
+        }
+        const size_t o = ((size_t)cidx(l, m) * K + c) * 2;
+        out[o] = re * sc;
+        out[o + 1] = im * sc;
+      }
+    }
+  }
+};
+
+namespace {
+
+int fail(const Error& e) {
+  g_last_error = e.msg;
+  return e.code;
+}
+
+template <class F>
+int guarded(F&& f) {
+  try {
+    f();
+    return LFMM_OK;
+  } catch (const Error& e) {
+    return fail(e);
+  } catch (const std::exception& e) {
+    return fail(Error{LFMM_ECUDA, e.what()});
+  }
+}
+
+void copy_out(lfmm_plan* pl, double* dst, const DevBuf& src, size_t bytes, int on_device) {
+  if (!dst) return;
+  LFMM_CUDA(cudaMemcpyAsync(dst, src.p, bytes, on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost,
+                            pl->stream));
+}
+
+void check_finite(lfmm_plan* pl, const DevBuf& buf, int64_t n, const char* what) {
+  pl->finite_flag.ensure(sizeof(int));
+  LFMM_CUDA(cudaMemsetAsync(pl->finite_flag.p, 0, sizeof(int), pl->stream));
+  if (n > 0) k_check_finite<<<nblk(n, 256), 256, 0, pl->stream>>>(buf.as<double>(), n, pl->finite_flag.as<int>());
+  int h = 0;
+  LFMM_CUDA(cudaMemcpyAsync(&h, pl->finite_flag.p, sizeof(int), cudaMemcpyDeviceToHost, pl->stream));
+  LFMM_CUDA(cudaStreamSynchronize(pl->stream));
+  if (h) throw Error{LFMM_ENONFINITE, std::string("non-finite values in ") + what};
+}
+
+void hi_args(lfmm_plan* pl, HiArgs& g) {
+  g.n_sites = (int)pl->n_sites;
+  g.atom_off = pl->atom_off.as<int>();
+  g.atom_idx = pl->atom_idx.as<int>();
+  g.nforms = pl->nforms.as<int>();
+  g.form_off = pl->form_off.as<int>();
+  g.fslot_off = pl->fslot_off.as<int>();
+  g.form_q = pl->form_q.as<double>();
+  g.lambdas = pl->lambdas.as<double>();
+  g.nlam = pl->nlam.as<int>();
+  g.site_pos = pl->site_pos.as<double>();
+  g.box = pl->L;
+  g.p = pl->p;
+  g.ncp = pl->ncp;
+  g.lat_t = pl->lattice_mode != LFMM_LATTICE_OFF ? pl->lat64t.as<double>() : nullptr;
+  g.rscratch = pl->rscr.as<double>();
+  g.uscratch = pl->uscr.as<double>();
+  g.images_full = (pl->flags & LFMM_F_INTRA_MINIMUM) ? 0 : 1;
+  g.dipole = (pl->flags & LFMM_F_DIPOLE) ? 1 : 0;
+}
+
+void upload_lambdas(lfmm_plan* pl, const double* lambdas, const int32_t* n_lambda, int on_device) {
+  LFMM_REQUIRE(pl->n_sites > 0 || true, "");
+  const size_t S = (size_t)pl->n_sites;
+  if (S == 0) return;
+  LFMM_REQUIRE(lambdas && n_lambda, "lambdas and n_lambda are required");
+  if (!on_device) {
+    for (size_t s = 0; s < S; ++s) {
+      const int nl = n_lambda[s];
+      LFMM_REQUIRE(nl >= 1 && nl <= 4, "need between 1 and 4 lambda values per site");
+      LFMM_REQUIRE((1 << nl) == pl->h_nforms[s], std::to_string(nl) + " lambdas give " + std::to_string(1 << nl) +
+                                                      " weights, site has " + std::to_string(pl->h_nforms[s]) +
+                                                      " forms");
+    }
+  }
+  const auto kind = on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice;
+  LFMM_CUDA(cudaMemcpyAsync(pl->lambdas.p, lambdas, sizeof(double) * 4 * S, kind, pl->stream));
+  LFMM_CUDA(cudaMemcpyAsync(pl->nlam.p, n_lambda, sizeof(int32_t) * S, kind, pl->stream));
+}
+
+void run_hi(lfmm_plan* pl, int mode, const double* pot_dev) {
+  if (pl->n_sites == 0) {
+    LFMM_CUDA(cudaMemsetAsync(pl->offset_total.p, 0, sizeof(double), pl->stream));
+    return;
+  }
+  HiArgs g{};
+  hi_args(pl, g);
+  g.pot = pot_dev;
+  g.mode = mode;
+  g.c_p2p = pl->c_p2p.as<double>();
+  g.c_lat = pl->c_lat.as<double>();
+  g.c_dip = pl->c_dip.as<double>();
+  g.blend = pl->blend.as<double>();
+  g.forces = pl->lam_forces.as<double>();
+  g.offset = pl->offsets.as<double>();
+  const int ns = pl->ns_max;
+  const size_t smem = sizeof(double) * ((size_t)ns + 2 * (size_t)ns * ns + 3 * (size_t)ns);
+  if (smem > 48 * 1024) {
+    LFMM_CUDA(cudaFuncSetAttribute(k_hi_site, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  }
+  pl->launch(ST_HI, [&] { k_hi_site<<<(unsigned)pl->n_sites, HI_THREADS, smem, pl->stream>>>(g); });
+  pl->launch(ST_HI, [&] {
+    k_sum_offsets<<<1, 256, 0, pl->stream>>>(pl->offsets.as<double>(), (int)pl->n_sites,
+                                             pl->offset_total.as<double>());
+  });
+}
+
+void gather_site_positions(lfmm_plan* pl, const double* site_positions, int on_device) {
+  if (pl->n_site_atoms == 0) return;
+  if (site_positions) {
+    LFMM_CUDA(cudaMemcpyAsync(pl->site_pos.p, site_positions, sizeof(double) * 3 * pl->n_site_atoms,
+                              on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, pl->stream));
+  } else {
+    pl->launch(ST_HI, [&] {
+      k_gather_site_pos<<<nblk(pl->n_site_atoms, 128), 128, 0, pl->stream>>>(
+          pl->pos_in.as<double>(), pl->atom_idx.as<int>(), (int)pl->n_site_atoms, pl->site_pos.as<double>());
+    });
+  }
+}
+
+void run_scale(lfmm_plan* pl, const double* q_dev, double* out_dev) {
+  pl->launch(ST_SCALE, [&] { k_scale_charges<<<nblk(pl->N, 256), 256, 0, pl->stream>>>(q_dev, pl->N, out_dev); });
+  if (pl->n_sites == 0) return;
+  HiArgs g{};
+  hi_args(pl, g);
+  pl->launch(ST_SCALE, [&] { k_blend_sites<<<(unsigned)pl->n_sites, 32, 0, pl->stream>>>(g, out_dev); });
+}
+
+}  // namespace
+
+// ============================================================ C-ABI ====
+extern "C" {
+
+const char* lfmm_version(void) { return "lfmm-b200 0.1.0 sm_100a"; }
+
+int lfmm_last_error(char* buf, int64_t len) {
+  if (!buf || len <= 0) return LFMM_EINVAL;
+  std::strncpy(buf, g_last_error.c_str(), (size_t)len - 1);
+  buf[len - 1] = '\0';
+  return LFMM_OK;
+}
+
+int lfmm_plan_create(const double* positions, int64_t n, double box_length, int p, int depth, int lattice_mode,
+                     int shell_cap, int flags, lfmm_plan** out) {
+  if (!out) return fail(Error{LFMM_EINVAL, "out is NULL"});
+  *out = nullptr;
+  std::unique_ptr<lfmm_plan> pl(new lfmm_plan());
+  int rc = guarded([&] {
+    // SolverConfig.validated (solver.py:60-75)
+    LFMM_REQUIRE(p >= 1 && p <= PMAX, "expansion order p=" + std::to_string(p) + " outside [1, 40]");
+    LFMM_REQUIRE(depth >= 0 && depth <= DMAX, "tree depth " + std::to_string(depth) + " outside [0, 6]");
+    LFMM_REQUIRE(lattice_mode >= 0 && lattice_mode <= 2, "unknown lattice_mode");
+    LFMM_REQUIRE(lattice_mode != LFMM_LATTICE_SHELLS || shell_cap >= 2, "shells mode needs shell_cap >= 2");
+    LFMM_REQUIRE((flags & LFMM_F_PERIODIC_NEAR) || (depth == 0 && lattice_mode == LFMM_LATTICE_OFF),
+                 "periodic_near=False requires depth=0 and lattice_mode='off'");
+    LFMM_REQUIRE(box_length > 0 && std::isfinite(box_length), "box_length must be positive");
+    LFMM_REQUIRE(n >= 0 && n < (1LL << 31), "particle count out of range");
+    LFMM_REQUIRE(n == 0 || positions, "positions is NULL");
+    for (int64_t i = 0; i < 3 * n; ++i)
+      LFMM_REQUIRE(std::isfinite(positions[i]), "positions contain non-finite values");
+    int dev = 0;
+    LFMM_CUDA(cudaGetDevice(&dev));
+    std::call_once(g_const_once, init_constants);
+    pl->N = n;
+    pl->L = box_length;
+    pl->p = p;
+    pl->depth = depth;
+    pl->lattice_mode = lattice_mode;
+    pl->shell_cap = shell_cap;
+    pl->flags = flags;
+    pl->fp32 = (flags & LFMM_F_FP32) != 0;
+    pl->nc = ncoef(p);
+    pl->ncp = ncpad(p);
+    pl->nleaf = 1 << (3 * depth);
+    pl->size = box_length / double(1 << depth);
+    LFMM_CUDA(cudaStreamCreateWithFlags(&pl->own_stream, cudaStreamNonBlocking));
+    pl->stream = pl->own_stream;
+    int64_t off = 0;
+    for (int l = 0; l <= depth; ++l) {
+      pl->level_off[l] = off;
+      off += 1LL << (3 * l);
+    }
+    pl->nbox_total = off;
+    const size_t t = pl->tsz();
+    const int64_t nn = std::max<int64_t>(n, 1);
+    pl->pos_in.ensure(sizeof(double) * 3 * nn);
+    pl->pos_wrap.ensure(sizeof(double) * 3 * nn);
+    pl->leaf_of.ensure(sizeof(int) * nn);
+    pl->counts.ensure(sizeof(int) * pl->nleaf);
+    pl->cursor.ensure(sizeof(int) * pl->nleaf);
+    pl->leaf_start.ensure(sizeof(int) * (pl->nleaf + 1));
+    pl->bucket.ensure(sizeof(int) * nn);
+    pl->perm.ensure(sizeof(int) * nn);
+    pl->inv_perm.ensure(sizeof(int) * nn);
+    pl->pos_sorted.ensure(sizeof(double) * 3 * nn);
+    pl->leaf_sorted.ensure(sizeof(int) * nn);
+    pl->xq.ensure(4 * t * nn);
+    pl->mult.ensure(t * pl->ncp * off);
+    pl->loc.ensure(t * pl->ncp * off);
+    LFMM_CUDA(cudaMemsetAsync(pl->mult.p, 0, pl->mult.bytes, pl->stream));
+    LFMM_CUDA(cudaMemsetAsync(pl->loc.p, 0, pl->loc.bytes, pl->stream));
+    pl->scal.ensure(sizeof(double) * 8);
+    pl->epart.ensure(sizeof(double) * 4);
+    pl->offset_total.ensure(sizeof(double));
+    if (pl->fp32)
+      pl->build_operators<float>();
+    else
+      pl->build_operators<double>();
+    if (pl->fp32)
+      pl->build_tree<float>(positions, false);
+    else
+      pl->build_tree<double>(positions, false);
+    LFMM_CUDA(cudaStreamSynchronize(pl->stream));
+  });
+  if (rc != LFMM_OK) return rc;
+  *out = pl.release();
+  return LFMM_OK;
+}
+
+int lfmm_plan_destroy(lfmm_plan* plan) {
+  delete plan;
+  return LFMM_OK;
+}
+
+int lfmm_plan_set_stream(lfmm_plan* plan, void* stream) {
+  if (!plan) return fail(Error{LFMM_EINVAL, "plan is NULL"});
+  return guarded([&] {
+    LFMM_CUDA(cudaStreamSynchronize(plan->stream));
+    plan->stream = stream ? reinterpret_cast<cudaStream_t>(stream) : plan->own_stream;
+  });
+}
+
+int lfmm_plan_set_positions(lfmm_plan* plan, const double* positions, int on_device) {
+  if (!plan) return fail(Error{LFMM_EINVAL, "plan is NULL"});
+  return guarded([&] {
+    LFMM_REQUIRE(plan->N == 0 || positions, "positions is NULL");
+    if (plan->fp32)
+      plan->build_tree<float>(positions, on_device != 0);
+    else
+      plan->build_tree<double>(positions, on_device != 0);
+  });
+}
+
+int lfmm_plan_info(const lfmm_plan* plan, int64_t* out6) {
+  if (!plan || !out6) return fail(Error{LFMM_EINVAL, "NULL argument"});
+  out6[0] = plan->N;
+  out6[1] = plan->p;
+  out6[2] = plan->depth;
+  out6[3] = plan->nc;
+  out6[4] = plan->nleaf;
+  out6[5] = plan->flags;
+  return LFMM_OK;
+}
+
+int lfmm_export_tree(const lfmm_plan* cplan, int64_t* perm, int64_t* inv_perm, int64_t* leaf_of_particle,
+                     int64_t* leaf_start, double* positions_sorted) {
+  if (!cplan) return fail(Error{LFMM_EINVAL, "plan is NULL"});
+  lfmm_plan* plan = const_cast<lfmm_plan*>(cplan);
+  return guarded([&] {
+    DevBuf tmp;
+    const int64_t n = plan->N;
+    tmp.ensure(sizeof(int64_t) * (std::max<int64_t>(n, plan->nleaf + 1) + 1));
+    auto conv = [&](const DevBuf& src, int64_t cnt, int64_t* dst) {
+      if (!dst || cnt == 0) return;
+      k_i32_to_i64<<<nblk(cnt, 256), 256, 0, plan->stream>>>(src.as<int>(), cnt, tmp.as<int64_t>());
+      LFMM_CUDA(cudaGetLastError());
+      LFMM_CUDA(cudaMemcpyAsync(dst, tmp.p, sizeof(int64_t) * cnt, cudaMemcpyDeviceToHost, plan->stream));
+      LFMM_CUDA(cudaStreamSynchronize(plan->stream));
+    };
+    conv(plan->perm, n, perm);
+    conv(plan->inv_perm, n, inv_perm);
+    conv(plan->leaf_sorted, n, leaf_of_particle);
+    conv(plan->leaf_start, plan->nleaf + 1, leaf_start);
+    if (positions_sorted && n > 0) {
+      LFMM_CUDA(cudaMemcpyAsync(positions_sorted, plan->pos_sorted.p, sizeof(double) * 3 * n,
+                                cudaMemcpyDeviceToHost, plan->stream));
+      LFMM_CUDA(cudaStreamSynchronize(plan->stream));
+    }
+    tmp.release();
+  });
+}
+
+int lfmm_export_lists(const lfmm_plan* cplan, int level, int64_t* nb_box, int64_t* nb_shift, int64_t* m2l_src,
+                      int64_t* m2l_row) {
+  if (!cplan) return fail(Error{LFMM_EINVAL, "plan is NULL"});
+  lfmm_plan* plan = const_cast<lfmm_plan*>(cplan);
+  return guarded([&] {
+    LFMM_REQUIRE(level >= 0 && level <= plan->depth, "level out of range");
+    DevBuf a, b;
+    if (nb_box || nb_shift) {
+      const int64_t cnt = (int64_t)plan->nleaf * 27;
+      a.ensure(sizeof(int64_t) * cnt);
+      b.ensure(sizeof(int64_t) * cnt * 3);
+      k_export_nb<<<nblk(cnt, 256), 256, 0, plan->stream>>>(plan->depth, a.as<int64_t>(), b.as<int64_t>());
+      LFMM_CUDA(cudaGetLastError());
+      if (nb_box)
+        LFMM_CUDA(cudaMemcpyAsync(nb_box, a.p, sizeof(int64_t) * cnt, cudaMemcpyDeviceToHost, plan->stream));
+      if (nb_shift)
+        LFMM_CUDA(cudaMemcpyAsync(nb_shift, b.p, sizeof(int64_t) * cnt * 3, cudaMemcpyDeviceToHost, plan->stream));
+      LFMM_CUDA(cudaStreamSynchronize(plan->stream));
+    }
+    if ((m2l_src || m2l_row) && level >= 1) {
+      const int64_t cnt = (1LL << (3 * level)) * NM2L;
+      a.ensure(sizeof(int64_t) * cnt);
+      b.ensure(sizeof(int64_t) * cnt);
+      k_export_m2l<<<nblk(cnt, 256), 256, 0, plan->stream>>>(level, a.as<int64_t>(), b.as<int64_t>());
+      LFMM_CUDA(cudaGetLastError());
+      if (m2l_src)
+        LFMM_CUDA(cudaMemcpyAsync(m2l_src, a.p, sizeof(int64_t) * cnt, cudaMemcpyDeviceToHost, plan->stream));
+      if (m2l_row)
+        LFMM_CUDA(cudaMemcpyAsync(m2l_row, b.p, sizeof(int64_t) * cnt, cudaMemcpyDeviceToHost, plan->stream));
+      LFMM_CUDA(cudaStreamSynchronize(plan->stream));
+    }
+    a.release();
+    b.release();
+  });
+}
+
+int lfmm_lattice_matrix(const lfmm_plan* plan, double* out) {
+  if (!plan || !out) return fail(Error{LFMM_EINVAL, "NULL argument"});
+  if (plan->lattice_mode == LFMM_LATTICE_OFF) return fail(Error{LFMM_EINVAL, "lattice is off"});
+  const int nc = plan->nc;
+  // T_L = diag(L^-(n+1)) T_1 diag(L^-j)   (lattice.py:95-100)
+  for (int r = 0; r < nc; ++r) {
+    const int lr = (int)std::sqrt((double)r);
+    const double sr = std::pow(plan->L, -(lr + 1.0));
+    for (int c = 0; c < nc; ++c) {
+      const int lc = (int)std::sqrt((double)c);
+      const double sc = std::pow(plan->L, -(double)lc);
+      const double2 v = plan->lat_unit[(size_t)r * nc + c];
+      out[2 * ((size_t)r * nc + c)] = sr * v.x * sc;
+      out[2 * ((size_t)r * nc + c) + 1] = sr * v.y * sc;
+    }
+  }
+  return LFMM_OK;
+}
+
+int lfmm_solve(lfmm_plan* plan, const double* charges, int64_t k, int io_on_device, double* potentials,
+               double* near_pot, double* far_pot, double* dip_pot, double* energies, double* root_multipole,
+               double* dipole_vector, double* total_charge, double* forces) {
+  if (!plan) return fail(Error{LFMM_EINVAL, "plan is NULL"});
+  return guarded([&] {
+    LFMM_REQUIRE(k >= 1, "need at least one charge column");
+    LFMM_REQUIRE(!forces || k == 1, "forces need a single charge column");
+    LFMM_REQUIRE(plan->N == 0 || charges, "charges is NULL");
+    const int64_t N = plan->N;
+    const bool grad = forces != nullptr;
+    plan->ensure_solve_buffers(k, grad);
+    if (N > 0)
+      LFMM_CUDA(cudaMemcpyAsync(plan->q_in.p, charges, sizeof(double) * N * k,
+                                io_on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, plan->stream));
+    plan->run_solve(k, grad);
+    const size_t nk = sizeof(double) * N * k;
+    copy_out(plan, potentials, plan->out_pot, nk, io_on_device);
+    copy_out(plan, near_pot, plan->out_near, nk, io_on_device);
+    copy_out(plan, far_pot, plan->out_far, nk, io_on_device);
+    copy_out(plan, dip_pot, plan->out_dip, nk, io_on_device);
+    copy_out(plan, energies, plan->energies, sizeof(double) * 4 * k, io_on_device);
+    copy_out(plan, dipole_vector, plan->dvec, sizeof(double) * 3 * k, io_on_device);
+    copy_out(plan, total_charge, plan->qtot, sizeof(double) * k, io_on_device);
+    if (grad) copy_out(plan, forces, plan->out_forces, sizeof(double) * 3 * N, io_on_device);
+    if (root_multipole) {
+      LFMM_REQUIRE(!io_on_device, "root_multipole is returned to host memory only");
+      for (int64_t c = 0; c < k; ++c) plan->root_multipole_host(k, c, root_multipole);
+    }
+    if (!io_on_device) LFMM_CUDA(cudaStreamSynchronize(plan->stream));
+  });
+}
+
+int lfmm_sites_set(lfmm_plan* plan, int64_t n_sites, const int64_t* atom_offsets, const int64_t* atom_index,
+                   const int32_t* n_forms, const int64_t* form_offsets, const double* form_charges) {
+  if (!plan) return fail(Error{LFMM_EINVAL, "plan is NULL"});
+  return guarded([&] {
+    LFMM_REQUIRE(n_sites >= 0, "n_sites < 0");
+    const int64_t S = n_sites;
+    std::vector<int> aoff(S + 1), aidx, nf(S), foff(S + 1), fsl(S + 1);
+    int ns_max = 0;
+    for (int64_t s = 0; s <= S; ++s) {
+      aoff[s] = (int)atom_offsets[s];
+      foff[s] = (int)form_offsets[s];
+    }
+    const int64_t A = atom_offsets[S];
+    aidx.resize(A);
+    for (int64_t a = 0; a < A; ++a) {
+      LFMM_REQUIRE(atom_index[a] >= 0 && atom_index[a] < plan->N, "site particle index out of range");
+      aidx[a] = (int)atom_index[a];
+    }
+    fsl[0] = 0;
+    for (int64_t s = 0; s < S; ++s) {
+      const int ns = aoff[s + 1] - aoff[s];
+      LFMM_REQUIRE(ns >= 1, "site " + std::to_string(s) + ": empty particle list");
+      nf[s] = n_forms[s];
+      LFMM_REQUIRE(nf[s] >= 1 && nf[s] <= HI_MAXF, "site " + std::to_string(s) + ": bad form count");
+      LFMM_REQUIRE(foff[s + 1] - foff[s] == nf[s] * ns, "site " + std::to_string(s) + ": form table size");
+      fsl[s + 1] = fsl[s] + nf[s];
+      ns_max = std::max(ns_max, ns);
+    }
+    plan->n_sites = S;
+    plan->n_site_atoms = A;
+    plan->n_form_slots = fsl[S];
+    plan->ns_max = ns_max;
+    plan->h_atom_off = aoff;
+    plan->h_atom_idx = aidx;
+    plan->h_nforms = nf;
+    plan->h_fslot_off = fsl;
+    auto up = [&](DevBuf& d, const void* h, size_t bytes) {
+      d.ensure(std::max<size_t>(bytes, 8));
+      if (bytes) LFMM_CUDA(cudaMemcpyAsync(d.p, h, bytes, cudaMemcpyHostToDevice, plan->stream));
+    };
+    up(plan->atom_off, aoff.data(), sizeof(int) * (S + 1));
+    up(plan->atom_idx, aidx.data(), sizeof(int) * A);
+    up(plan->nforms, nf.data(), sizeof(int) * S);
+    up(plan->form_off, foff.data(), sizeof(int) * (S + 1));
+    up(plan->fslot_off, fsl.data(), sizeof(int) * (S + 1));
+    up(plan->form_q, form_charges, sizeof(double) * foff[S]);
+    plan->site_pos.ensure(sizeof(double) * 3 * std::max<int64_t>(A, 1));
+    plan->lambdas.ensure(sizeof(double) * 4 * std::max<int64_t>(S, 1));
+    plan->nlam.ensure(sizeof(int) * std::max<int64_t>(S, 1));
+    plan->rscr.ensure(sizeof(double) * plan->ncp * std::max<int64_t>(A, 1));
+    plan->uscr.ensure(sizeof(double) * plan->ncp * std::max<int64_t>(A, 1));
+    const size_t fs = sizeof(double) * std::max<int64_t>(fsl[S], 1);
+    plan->c_p2p.ensure(fs);
+    plan->c_lat.ensure(fs);
+    plan->c_dip.ensure(fs);
+    plan->blend.ensure(sizeof(double) * std::max<int64_t>(S, 1));
+    plan->lam_forces.ensure(sizeof(double) * 4 * std::max<int64_t>(S, 1));
+    plan->offsets.ensure(sizeof(double) * std::max<int64_t>(S, 1));
+    LFMM_CUDA(cudaStreamSynchronize(plan->stream));
+  });
+}
+
+int lfmm_hi(lfmm_plan* plan, const double* lambdas, const int32_t* n_lambda, int mode, const double* site_positions,
+            const double* potentials, int io_on_device, double* c_p2p, double* c_lattice, double* c_dipole,
+            double* blend_energy, double* lambda_forces, double* energy_offset) {
+  if (!plan) return fail(Error{LFMM_EINVAL, "plan is NULL"});
+  return guarded([&] {
+    LFMM_REQUIRE(mode == LFMM_MODE_HI || mode == LFMM_MODE_QI, "unknown mode");
+    upload_lambdas(plan, lambdas, n_lambda, io_on_device);
+    gather_site_positions(plan, site_positions, io_on_device);
+    const double* pot = nullptr;
+    if (potentials) {
+      plan->pot_tmp.ensure(sizeof(double) * std::max<int64_t>(plan->N, 1));
+      LFMM_CUDA(cudaMemcpyAsync(plan->pot_tmp.p, potentials, sizeof(double) * plan->N,
+                                io_on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, plan->stream));
+      pot = plan->pot_tmp.as<double>();
+    } else if (lambda_forces) {
+      LFMM_REQUIRE(plan->last_valid && plan->last_k == 1, "no single-column solve to take potentials from");
+      pot = plan->out_pot.as<double>();
+    }
+    run_hi(plan, mode, pot);
+    const size_t S = (size_t)plan->n_sites, F = (size_t)plan->n_form_slots;
+    copy_out(plan, c_p2p, plan->c_p2p, sizeof(double) * F, io_on_device);
+    copy_out(plan, c_lattice, plan->c_lat, sizeof(double) * F, io_on_device);
+    copy_out(plan, c_dipole, plan->c_dip, sizeof(double) * F, io_on_device);
+    copy_out(plan, blend_energy, plan->blend, sizeof(double) * S, io_on_device);
+    copy_out(plan, lambda_forces, plan->lam_forces, sizeof(double) * 4 * S, io_on_device);
+    copy_out(plan, energy_offset, plan->offset_total, sizeof(double), io_on_device);
+    if (!io_on_device) LFMM_CUDA(cudaStreamSynchronize(plan->stream));
+  });
+}
+
+int lfmm_assemble(int64_t n_sites, const int64_t* atom_offsets, const int64_t* atom_index, const int32_t* n_forms,
+                  const int64_t* form_offsets, const double* form_charges, const double* lambdas,
+                  const int32_t* n_lambda, const double* c_total, const double* potentials, int64_t n_particles,
+                  double* out) {
+  return guarded([&] {
+    const int64_t S = n_sites;
+    LFMM_REQUIRE(S >= 0, "n_sites < 0");
+    if (S == 0) return;
+    std::vector<int> aoff(S + 1), foff(S + 1), fsl(S + 1, 0), nf(S), nl(S);
+    for (int64_t s = 0; s <= S; ++s) {
+      aoff[s] = (int)atom_offsets[s];
+      foff[s] = (int)form_offsets[s];
+    }
+    const int64_t A = atom_offsets[S];
+    std::vector<int> aidx(A);
+    for (int64_t a = 0; a < A; ++a) {
+      LFMM_REQUIRE(atom_index[a] >= 0 && atom_index[a] < n_particles, "site particle index out of range");
+      aidx[a] = (int)atom_index[a];
+    }
+    for (int64_t s = 0; s < S; ++s) {
+      nf[s] = n_forms[s];
+      nl[s] = n_lambda[s];
+      LFMM_REQUIRE(nl[s] >= 1 && nl[s] <= 4 && (1 << nl[s]) == nf[s],
+                   std::to_string(nl[s]) + " lambdas give " + std::to_string(1 << nl[s]) + " weights, site has " +
+                       std::to_string(nf[s]) + " forms");
+      fsl[s + 1] = fsl[s] + nf[s];
+    }
+    DevBuf d_ao, d_ai, d_nf, d_fo, d_fs, d_fq, d_lam, d_nl, d_ct, d_pot, d_out;
+    cudaStream_t st;
+    LFMM_CUDA(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+    auto up = [&](DevBuf& d, const void* h, size_t bytes) {
+      d.ensure(std::max<size_t>(bytes, 8));
+      if (bytes) LFMM_CUDA(cudaMemcpyAsync(d.p, h, bytes, cudaMemcpyHostToDevice, st));
+    };
+    up(d_ao, aoff.data(), sizeof(int) * (S + 1));
+    up(d_ai, aidx.data(), sizeof(int) * A);
+    up(d_nf, nf.data(), sizeof(int) * S);
+    up(d_fo, foff.data(), sizeof(int) * (S + 1));
+    up(d_fs, fsl.data(), sizeof(int) * (S + 1));
+    up(d_fq, form_charges, sizeof(double) * foff[S]);
+    up(d_lam, lambdas, sizeof(double) * 4 * S);
+    up(d_nl, nl.data(), sizeof(int) * S);
+    if (c_total) up(d_ct, c_total, sizeof(double) * fsl[S]);
+    up(d_pot, potentials, sizeof(double) * n_particles);
+    d_out.ensure(sizeof(double) * 4 * S);
+    k_assemble<<<nblk(S, 4), 128, 0, st>>>((int)S, d_ao.as<int>(), d_ai.as<int>(), d_nf.as<int>(), d_fo.as<int>(),
+                                           d_fs.as<int>(), d_fq.as<double>(), d_lam.as<double>(), d_nl.as<int>(),
+                                           c_total ? d_ct.as<double>() : nullptr, d_pot.as<double>(),
+                                           d_out.as<double>());
+    LFMM_CUDA(cudaGetLastError());
+    LFMM_CUDA(cudaMemcpyAsync(out, d_out.p, sizeof(double) * 4 * S, cudaMemcpyDeviceToHost, st));
+    LFMM_CUDA(cudaStreamSynchronize(st));
+    DevBuf* bufs[] = {&d_ao, &d_ai, &d_nf, &d_fo, &d_fs, &d_fq, &d_lam, &d_nl, &d_ct, &d_pot, &d_out};
+    for (auto* b : bufs) b->release();
+    cudaStreamDestroy(st);
+  });
+}
+
+int lfmm_scale_charges(lfmm_plan* plan, const double* charges, const double* lambdas, const int32_t* n_lambda,
+                       int io_on_device, double* out_charges) {
+  if (!plan) return fail(Error{LFMM_EINVAL, "plan is NULL"});
+  return guarded([&] {
+    const int64_t N = plan->N;
+    upload_lambdas(plan, lambdas, n_lambda, io_on_device);
+    plan->q_tmp.ensure(sizeof(double) * std::max<int64_t>(N, 1));
+    plan->pot_tmp.ensure(sizeof(double) * std::max<int64_t>(N, 1));
+    LFMM_CUDA(cudaMemcpyAsync(plan->pot_tmp.p, charges, sizeof(double) * N,
+                              io_on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, plan->stream));
+    run_scale(plan, plan->pot_tmp.as<double>(), plan->q_tmp.as<double>());
+    copy_out(plan, out_charges, plan->q_tmp, sizeof(double) * N, io_on_device);
+    if (!io_on_device) LFMM_CUDA(cudaStreamSynchronize(plan->stream));
+  });
+}
+
+int lfmm_step(lfmm_plan* plan, const double* positions, const double* charges, const double* lambdas,
+              const int32_t* n_lambda, int mode, int plain, int io_on_device, double* energy, double* forces,
+              double* lambda_forces, double* potentials) {
+  if (!plan) return fail(Error{LFMM_EINVAL, "plan is NULL"});
+  return guarded([&] {
+    const int64_t N = plan->N;
+    LFMM_REQUIRE(mode == LFMM_MODE_HI || mode == LFMM_MODE_QI, "unknown mode");
+    if (positions) {
+      if (plan->fp32)
+        plan->build_tree<float>(positions, io_on_device != 0);
+      else
+        plan->build_tree<double>(positions, io_on_device != 0);
+    }
+    plan->ensure_solve_buffers(1, true);
+    plan->q_tmp.ensure(sizeof(double) * std::max<int64_t>(N, 1));
+    const auto kind = io_on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice;
+    if (plain || plan->n_sites == 0) {
+      LFMM_CUDA(cudaMemcpyAsync(plan->q_in.p, charges, sizeof(double) * N, kind, plan->stream));
+    } else {
+      upload_lambdas(plan, lambdas, n_lambda, io_on_device);
+      LFMM_CUDA(cudaMemcpyAsync(plan->q_tmp.p, charges, sizeof(double) * N, kind, plan->stream));
+      run_scale(plan, plan->q_tmp.as<double>(), plan->q_in.as<double>());
+    }
+    plan->run_solve(1, true);
+    if (!plain && plan->n_sites > 0) {
+      gather_site_positions(plan, nullptr, 0);
+      run_hi(plan, mode, plan->out_pot.as<double>());
+    }
+    // energy = E_solve + sum of site offsets (hi_energy_and_forces :273)
+    const bool add_off = !plain && plan->n_sites > 0 && mode == LFMM_MODE_HI;
+    plan->launch(ST_FINAL, [&] {
+      k_step_energy<<<1, 1, 0, plan->stream>>>(plan->energies.as<double>(), plan->offset_total.as<double>(),
+                                               add_off ? 1 : 0, plan->scal.as<double>() + 6);
+    });
+    if (energy)
+      LFMM_CUDA(cudaMemcpyAsync(energy, plan->scal.as<double>() + 6, sizeof(double),
+                                io_on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost, plan->stream));
+    copy_out(plan, forces, plan->out_forces, sizeof(double) * 3 * N, io_on_device);
+    if (!plain) copy_out(plan, lambda_forces, plan->lam_forces, sizeof(double) * 4 * plan->n_sites, io_on_device);
+    copy_out(plan, potentials, plan->out_pot, sizeof(double) * N, io_on_device);
+    if (!io_on_device) LFMM_CUDA(cudaStreamSynchronize(plan->stream));
+  });
+}
+
+int lfmm_profile_enable(lfmm_plan* plan, int enable) {
+  if (!plan) return fail(Error{LFMM_EINVAL, "plan is NULL"});
+  return guarded([&] {
+    plan->harvest();
+    plan->profiling = enable != 0;
+    for (int i = 0; i < ST_COUNT; ++i) {
+      plan->stage_ms[i] = 0.0;
+      plan->stage_launch[i] = 0;
+    }
+  });
+}
+
+int lfmm_stage_count(void) { return ST_COUNT; }
+
+const char* lfmm_stage_name(int i) { return (i >= 0 && i < ST_COUNT) ? kStageNames[i] : ""; }
+
+int lfmm_stage_times(lfmm_plan* plan, double* ms, int64_t* launches, int n) {
+  if (!plan) return fail(Error{LFMM_EINVAL, "plan is NULL"});
+  return guarded([&] {
+    plan->harvest();
+    for (int i = 0; i < n && i < ST_COUNT; ++i) {
+      if (ms) ms[i] = plan->stage_ms[i];
+      if (launches) launches[i] = plan->stage_launch[i];
+    }
+  });
+}
+
+int64_t lfmm_launch_count(const lfmm_plan* plan) { return plan ? plan->launches : -1; }
+
+}  // extern "C"

@@ -1,0 +1,253 @@
+// lfmm_common.cuh — shared definitions for the B200 FMM + HI kernels.
+//
+// Expansion storage ("packed, m-major"): an order-p expansion X_l^m with
+// conjugate symmetry X_l^{-m} = (-1)^m conj(X_l^m) (fmm/harmonics.py:3-8) is
+// kept as (p+1)^2 reals:
+//     m = 0       : Re X_l^0                    l = 0..p        (p+1 reals)
+//     m = 1..p    : Re X_l^m, Im X_l^m          l = m..p        (2(p+1-m))
+// in exactly the order the regular-harmonic recurrence (harmonics.py:58-77)
+// produces them, so P2M/L2P stream coefficients without index tables.
+// Rows are padded to ncp = round_up((p+1)^2, 16) with zeros.
+//
+// Box-size normalisation: multipoles are stored as M^_l = M_l / s^l and locals
+// as L^_l = L_l * s^(l+1) (s = box edge of the level).  Every translation
+// operator is then level independent (one table of 316 M2L operators serves
+// all levels) and values stay O(1), which keeps fp32 well inside its range.
+#pragma once
+#include <cuda_runtime.h>
+#include <cstdint>
+#include <cstdio>
+#include <string>
+
+#include "../../include/lfmm.h"
+
+namespace lfmm {
+
+constexpr int PMAX = 40;           // SolverConfig.validated p <= 40 (solver.py:62)
+constexpr int DMAX = 6;            // depth <= 6 (solver.py:64)
+constexpr int NM2L = 189;          // partners per box at every level >= 1
+constexpr int NOFF = 316;          // M2L_OFFSETS rows (octree.py:31)
+constexpr double DIPOLE_ETA = -1.0;  // lattice.py:41
+
+struct Error {
+  int code;
+  std::string msg;
+};
+
+#define LFMM_CUDA(expr)                                                              \
+  do {                                                                               \
+    cudaError_t _e = (expr);                                                         \
+    if (_e != cudaSuccess)                                                           \
+      throw ::lfmm::Error{LFMM_ECUDA, std::string(#expr) + ": " + cudaGetErrorString(_e)}; \
+  } while (0)
+
+#define LFMM_REQUIRE(cond, msg)                                   \
+  do {                                                            \
+    if (!(cond)) throw ::lfmm::Error{LFMM_EINVAL, std::string(msg)}; \
+  } while (0)
+
+__host__ __device__ inline int ncoef(int p) { return (p + 1) * (p + 1); }
+__host__ __device__ inline int ncpad(int p) { return (ncoef(p) + 15) & ~15; }
+// full complex index (harmonics.py:37)
+__host__ __device__ inline int cidx(int l, int m) { return l * l + l + m; }
+// packed m-major layout
+__host__ __device__ inline int pk_base(int p, int m) {
+  return m == 0 ? 0 : (p + 1) + 2 * ((m - 1) * (p + 1) - ((m - 1) * m) / 2);
+}
+__host__ __device__ inline int pk_index(int p, int l, int m, int part) {
+  return m == 0 ? l : pk_base(p, m) + 2 * (l - m) + part;
+}
+__host__ __device__ inline void pk_decode(int p, int a, int& l, int& m, int& part) {
+  if (a <= p) {
+    l = a;
+    m = 0;
+    part = 0;
+    return;
+  }
+  int mm = 1;
+  while (mm < p && a >= pk_base(p, mm + 1)) ++mm;
+  int r = a - pk_base(p, mm);
+  m = mm;
+  l = mm + (r >> 1);
+  part = r & 1;
+}
+
+// recurrence constants, broadcast from constant memory
+__constant__ double c_inv_lm_d[(PMAX + 2) * (PMAX + 2)];  // 1/((l+m)(l-m)), l>m
+__constant__ float c_inv_lm_f[(PMAX + 2) * (PMAX + 2)];
+__constant__ double c_inv_2m_d[PMAX + 2];  // 1/(2m)
+__constant__ float c_inv_2m_f[PMAX + 2];
+// M2L partner tables per target parity (octree.py:35-38, :96-111):
+// offsets (ox,oy,oz) packed into int8x4 and the M2L_OFFSETS row index.
+__constant__ char4 c_m2l_off[8 * NM2L];
+__constant__ short c_m2l_row[8 * NM2L];
+
+template <class T>
+__device__ __forceinline__ T inv_lm(int l, int m);
+template <>
+__device__ __forceinline__ double inv_lm<double>(int l, int m) { return c_inv_lm_d[l * (PMAX + 2) + m]; }
+template <>
+__device__ __forceinline__ float inv_lm<float>(int l, int m) { return c_inv_lm_f[l * (PMAX + 2) + m]; }
+template <class T>
+__device__ __forceinline__ T inv_2m(int m);
+template <>
+__device__ __forceinline__ double inv_2m<double>(int m) { return c_inv_2m_d[m]; }
+template <>
+__device__ __forceinline__ float inv_2m<float>(int m) { return c_inv_2m_f[m]; }
+
+template <class T>
+struct Vec4;
+template <>
+struct Vec4<float> {
+  using type = float4;
+};
+template <>
+struct Vec4<double> {
+  using type = double4;
+};
+template <class T>
+using vec4_t = typename Vec4<T>::type;
+
+__device__ __forceinline__ float rsqrt_t(float x) { return rsqrtf(x); }
+__device__ __forceinline__ double rsqrt_t(double x) { return rsqrt(x); }
+
+// Streams the packed regular harmonics R_l^m(x,y,z), m-major (see top), to
+// f(m, l, re, im).  Same recurrence as harmonics.regular (harmonics.py:58-77)
+// with the divisions turned into multiplications by table reciprocals.
+template <class T, class F>
+__device__ __forceinline__ void regular_stream(T x, T y, T z, int p, F&& f) {
+  const T r2 = x * x + y * y + z * z;
+  T mr = T(1), mi = T(0);
+  for (int m = 0; m <= p; ++m) {
+    if (m > 0) {
+      const T c = inv_2m<T>(m);
+      const T nr = (mr * x - mi * y) * c;
+      const T ni = (mr * y + mi * x) * c;
+      mr = nr;
+      mi = ni;
+    }
+    f(m, m, mr, mi);
+    if (m + 1 <= p) {
+      T p2r = mr, p2i = mi;
+      T p1r = z * mr, p1i = z * mi;
+      f(m, m + 1, p1r, p1i);
+      for (int l = m + 2; l <= p; ++l) {
+        const T c = inv_lm<T>(l, m);
+        const T a = T(2 * l - 1) * z;
+        const T nr = (a * p1r - r2 * p2r) * c;
+        const T ni = (a * p1i - r2 * p2i) * c;
+        p2r = p1r;
+        p2i = p1i;
+        p1r = nr;
+        p1i = ni;
+        f(m, l, nr, ni);
+      }
+    }
+  }
+}
+
+// Full complex solid harmonics (setup only, fp64): harmonics.regular /
+// harmonics.irregular (harmonics.py:58-103), out has (p+1)^2 entries.
+__host__ __device__ inline void regular_full(double x, double y, double z, int p, double2* out) {
+  const double r2 = x * x + y * y + z * z;
+  double mr = 1.0, mi = 0.0;
+  for (int m = 0; m <= p; ++m) {
+    if (m > 0) {
+      const double nr = (mr * x - mi * y) / (2.0 * m);
+      const double ni = (mr * y + mi * x) / (2.0 * m);
+      mr = nr;
+      mi = ni;
+    }
+    out[cidx(m, m)] = make_double2(mr, mi);
+    if (m + 1 <= p) out[cidx(m + 1, m)] = make_double2(z * mr, z * mi);
+    for (int l = m + 2; l <= p; ++l) {
+      const double2 a = out[cidx(l - 1, m)], b = out[cidx(l - 2, m)];
+      const double den = double((l + m) * (l - m));
+      out[cidx(l, m)] = make_double2(((2 * l - 1) * z * a.x - r2 * b.x) / den,
+                                     ((2 * l - 1) * z * a.y - r2 * b.y) / den);
+    }
+  }
+  for (int l = 1; l <= p; ++l)
+    for (int m = 1; m <= l; ++m) {
+      const double2 v = out[cidx(l, m)];
+      const double s = (m & 1) ? -1.0 : 1.0;
+      out[cidx(l, -m)] = make_double2(s * v.x, -s * v.y);
+    }
+}
+
+__host__ __device__ inline void irregular_full(double x, double y, double z, int p, double2* out) {
+  const double r2 = x * x + y * y + z * z;
+  const double ir2 = 1.0 / r2;
+  double mr = sqrt(ir2), mi = 0.0;
+  for (int m = 0; m <= p; ++m) {
+    if (m > 0) {
+      const double c = (2 * m - 1) * ir2;
+      const double nr = (mr * x - mi * y) * c;
+      const double ni = (mr * y + mi * x) * c;
+      mr = nr;
+      mi = ni;
+    }
+    out[cidx(m, m)] = make_double2(mr, mi);
+    if (m + 1 <= p) {
+      const double c = (2 * m + 1) * z * ir2;
+      out[cidx(m + 1, m)] = make_double2(c * mr, c * mi);
+    }
+    for (int l = m + 2; l <= p; ++l) {
+      const double2 a = out[cidx(l - 1, m)], b = out[cidx(l - 2, m)];
+      const double k2 = double((l - 1) * (l - 1) - m * m);
+      out[cidx(l, m)] = make_double2(((2 * l - 1) * z * a.x - k2 * b.x) * ir2,
+                                     ((2 * l - 1) * z * a.y - k2 * b.y) * ir2);
+    }
+  }
+  for (int l = 1; l <= p; ++l)
+    for (int m = 1; m <= l; ++m) {
+      const double2 v = out[cidx(l, m)];
+      const double s = (m & 1) ? -1.0 : 1.0;
+      out[cidx(l, -m)] = make_double2(s * v.x, -s * v.y);
+    }
+}
+
+// ---- deterministic double-double accumulation (stands in for math.fsum,
+// solver.py:105-107) ----
+struct dd {
+  double hi, lo;
+};
+__host__ __device__ inline dd dd_from(double a) { return dd{a, 0.0}; }
+__host__ __device__ inline dd dd_add(dd a, dd b) {
+  double s = a.hi + b.hi;
+  double bb = s - a.hi;
+  double err = (a.hi - (s - bb)) + (b.hi - bb);
+  err += a.lo + b.lo;
+  double hi = s + err;
+  double lo = err - (hi - s);
+  return dd{hi, lo};
+}
+
+__device__ __forceinline__ dd dd_shfl_down(dd v, int off) {
+  return dd{__shfl_down_sync(0xffffffffu, v.hi, off), __shfl_down_sync(0xffffffffu, v.lo, off)};
+}
+
+// Block reduction of NQ double-double quantities, fixed order (deterministic).
+template <int NQ>
+__device__ inline void block_reduce_dd(dd (&v)[NQ], dd* out /* NQ */) {
+  __shared__ dd sh[32][NQ];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+#pragma unroll
+  for (int q = 0; q < NQ; ++q)
+    for (int off = 16; off > 0; off >>= 1) v[q] = dd_add(v[q], dd_shfl_down(v[q], off));
+  if (lane == 0)
+#pragma unroll
+    for (int q = 0; q < NQ; ++q) sh[w][q] = v[q];
+  __syncthreads();
+  if (w == 0) {
+    const int nw = blockDim.x >> 5;
+#pragma unroll
+    for (int q = 0; q < NQ; ++q) {
+      dd x = lane < nw ? sh[lane][q] : dd{0.0, 0.0};
+      for (int off = 16; off > 0; off >>= 1) x = dd_add(x, dd_shfl_down(x, off));
+      if (lane == 0) out[q] = x;
+    }
+  }
+}
+
+}  // namespace lfmm

@@ -1,0 +1,420 @@
+// lfmm_expansions.cuh — P2M, L2P(+gradient) and the gathered-GEMM kernel that
+// runs every dense translation (M2M, L2L, M2L, lattice).
+//
+//   P2M  harmonics.particle_multipole (harmonics.py:206-216), upward_pass
+//        leaf loop (solver.py:237-247)
+//   L2P  harmonics.eval_local / eval_local_grad (harmonics.py:219-234),
+//        evaluate / evaluate_gradient (solver.py:294-324)
+//   GEMM upward_pass M2M (solver.py:248-258), lattice root (:364-367),
+//        downward_pass L2L + offset-grouped M2L (:262-291)
+#pragma once
+#include "lfmm_common.cuh"
+#include "lfmm_tree.cuh"
+
+namespace lfmm {
+
+constexpr int EXP_WARPS = 4;
+
+// ---------------------------------------------------------------- P2M ----
+// One warp per leaf, one lane per atom.  Each lane streams q*R^(a/s) into a
+// per-warp 32x33 transpose tile; every 32 coefficients the lanes sum one
+// column each (fixed order) and accumulate into the leaf's multipole.
+template <class T>
+__global__ void __launch_bounds__(EXP_WARPS * 32) k_p2m(const vec4_t<T>* __restrict__ xq,
+                                                        const int* __restrict__ leaf_start, int depth,
+                                                        int p, T inv_size, int ncp,
+                                                        T* __restrict__ mult) {
+  __shared__ T buf[EXP_WARPS][32][33];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int b = blockIdx.x * EXP_WARPS + w;
+  const int nleaf = 1 << (3 * depth);
+  if (b >= nleaf) return;
+  T* out = mult + (size_t)b * ncp;
+  const int t0 = leaf_start[b], t1 = leaf_start[b + 1];
+  const int nc = ncoef(p);
+  if (t1 == t0) {
+    for (int c = lane; c < nc; c += 32) out[c] = T(0);
+    return;
+  }
+  T(*tb)[33] = buf[w];
+  for (int tc = t0; tc < t1; tc += 32) {
+    const int i = tc + lane;
+    T x = 0, y = 0, z = 0, q = 0;
+    if (i < t1) {
+      const vec4_t<T> v = xq[i];
+      x = v.x * inv_size;
+      y = v.y * inv_size;
+      z = v.z * inv_size;
+      q = v.w;
+    }
+    const bool first = (tc == t0);
+    int col = 0, sbase = 0;
+    auto flush = [&]() {
+      __syncwarp();
+      if (lane < col) {
+        T s = T(0);
+#pragma unroll 8
+        for (int k = 0; k < 32; ++k) s += tb[lane][k];
+        const int g = sbase + lane;
+        out[g] = first ? s : out[g] + s;
+      }
+      __syncwarp();
+      sbase += col;
+      col = 0;
+    };
+    regular_stream<T>(x, y, z, p, [&](int m, int l, T re, T im) {
+      tb[col][lane] = q * re;
+      ++col;
+      if (col == 32) flush();
+      if (m > 0) {
+        tb[col][lane] = q * im;
+        ++col;
+        if (col == 32) flush();
+      }
+    });
+    if (col > 0) flush();
+  }
+}
+
+// ---------------------------------------------------------------- L2P ----
+// Warp per leaf.  The leaf local L^ and its three gradient coefficient
+// vectors (order p-1, G_x = (L_{j+1}^{k+1} - L_{j+1}^{k-1})/2,
+// G_y = i(L_{j+1}^{k+1} + L_{j+1}^{k-1})/2, G_z = L_{j+1}^k — the
+// harmonics.regular_grad ladder, harmonics.py:106-130, moved onto the
+// coefficients) are staged in shared memory; each lane streams R^(a/s) of
+// its atom and contracts.  V = Re sum L R / s, grad V = Re sum G R / s^2.
+template <class T>
+__device__ __forceinline__ void ld_full(const T* Lh, int p, int l, int m, T& re, T& im) {
+  // full-index read of a conj-symmetric packed vector
+  if (m == 0) {
+    re = Lh[l];
+    im = T(0);
+  } else if (m > 0) {
+    const int a = pk_base(p, m) + 2 * (l - m);
+    re = Lh[a];
+    im = Lh[a + 1];
+  } else {
+    const int mm = -m;
+    const int a = pk_base(p, mm) + 2 * (l - mm);
+    const T s = (mm & 1) ? T(-1) : T(1);
+    re = s * Lh[a];
+    im = -s * Lh[a + 1];
+  }
+}
+
+template <class T, bool GRAD>
+__global__ void __launch_bounds__(EXP_WARPS * 32) k_l2p(const vec4_t<T>* __restrict__ xq,
+                                                        const int* __restrict__ leaf_start, int depth,
+                                                        int p, T size, int ncp,
+                                                        const T* __restrict__ loc,
+                                                        T* __restrict__ vout, T* __restrict__ gout) {
+  extern __shared__ unsigned char smem_raw[];
+  const int nc = ncoef(p), ng = p * p;
+  const int per_warp = nc + 3 * ng;
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  T* Lh = reinterpret_cast<T*>(smem_raw) + w * per_warp;
+  T* Gx = Lh + nc;
+  T* Gy = Gx + ng;
+  T* Gz = Gy + ng;
+  const int b = blockIdx.x * (blockDim.x >> 5) + w;
+  const int nleaf = 1 << (3 * depth);
+  if (b >= nleaf) return;
+  const int t0 = leaf_start[b], t1 = leaf_start[b + 1];
+  if (t1 == t0) return;
+  const T* src = loc + (size_t)b * ncp;
+  for (int c = lane; c < nc; c += 32) Lh[c] = src[c];
+  __syncwarp();
+  if (GRAD) {
+    const int q = p - 1;
+    for (int a = lane; a < ng; a += 32) {
+      int j, k, part;
+      pk_decode(q, a, j, k, part);
+      T ar, ai, br, bi, cr, ci;
+      ld_full(Lh, p, j + 1, k + 1, ar, ai);
+      ld_full(Lh, p, j + 1, k - 1, br, bi);
+      ld_full(Lh, p, j + 1, k, cr, ci);
+      const T gxr = T(0.5) * (ar - br), gxi = T(0.5) * (ai - bi);
+      const T gyr = T(-0.5) * (ai + bi), gyi = T(0.5) * (ar + br);
+      Gx[a] = part ? gxi : gxr;
+      Gy[a] = part ? gyi : gyr;
+      Gz[a] = part ? ci : cr;
+    }
+    __syncwarp();
+  }
+  const T inv_s = T(1) / size;
+  for (int tc = t0; tc < t1; tc += 32) {
+    const int i = tc + lane;
+    const bool act = i < t1;
+    T x = 0, y = 0, z = 0;
+    if (act) {
+      const vec4_t<T> v = xq[i];
+      x = v.x * inv_s;
+      y = v.y * inv_s;
+      z = v.z * inv_s;
+    }
+    T V = 0, dx = 0, dy = 0, dz = 0;
+    int a = 0, g = 0;
+    regular_stream<T>(x, y, z, p, [&](int m, int l, T re, T im) {
+      if (m == 0) {
+        V = fma(Lh[a], re, V);
+        ++a;
+        if (GRAD && l < p) {
+          dx = fma(Gx[g], re, dx);
+          dy = fma(Gy[g], re, dy);
+          dz = fma(Gz[g], re, dz);
+          ++g;
+        }
+      } else {
+        V += T(2) * (Lh[a] * re - Lh[a + 1] * im);
+        a += 2;
+        if (GRAD && l < p) {
+          dx += T(2) * (Gx[g] * re - Gx[g + 1] * im);
+          dy += T(2) * (Gy[g] * re - Gy[g + 1] * im);
+          dz += T(2) * (Gz[g] * re - Gz[g + 1] * im);
+          g += 2;
+        }
+      }
+    });
+    if (act) {
+      vout[i] = V * inv_s;
+      if (GRAD) {
+        const T s2 = inv_s * inv_s;
+        gout[3 * (size_t)i] = dx * s2;
+        gout[3 * (size_t)i + 1] = dy * s2;
+        gout[3 * (size_t)i + 2] = dz * s2;
+      }
+    }
+  }
+}
+
+// ------------------------------------------------------- gathered GEMM ----
+// dst[:, tile] = sum_terms Op_term (ncp x ncp) * src_term[:, gather(tile)]
+// Tiles hold BN targets of one level.  For the downward mode all targets of
+// a tile share one parity (= octant within the parent), hence one L2L
+// operator and one list of 189 M2L offsets (octree.py:35-38): term 0 is the
+// L2L from the parent local, terms 1..189 the M2L partners in M2L_OFFSETS
+// row order.  Upward mode: terms are the 8 children (M2M).  Root mode: one
+// term, the lattice operator on the root multipole.
+enum GemmMode { GEMM_UP = 0, GEMM_DOWN = 1, GEMM_ROOT = 2 };
+
+struct GemmArgs {
+  int mode;
+  int level;            // target level
+  int ncp;
+  const void* src_m2l;  // DOWN: multipoles of this level
+  const void* src_aux;  // UP: children multipoles (level+1); DOWN: parent locals; ROOT: root multipole
+  void* dst;
+  const void* ops_main;  // UP: M2M[8]; DOWN: M2L[316]; ROOT: lattice
+  const void* ops_l2l;   // DOWN: L2L[8]
+  int use_m2l;           // DOWN: 0 -> only the L2L term (never for level>=1 here)
+};
+
+constexpr int GB_M = 128, GB_N = 64, G_THREADS = 256;
+template <class T>
+struct GemmTile {
+  static constexpr int BK = sizeof(T) == 4 ? 16 : 8;  // keeps smem double buffer < 48 KB
+  static constexpr int AK = BK / 2;                    // A elements per thread per stage
+  static constexpr int BKT = BK / 4;                   // B elements per thread per stage
+};
+
+__host__ __device__ inline int gemm_tiles_per_class(int mode, int level) {
+  if (mode == GEMM_DOWN) {
+    const int sub = 1 << (level - 1);
+    return (sub * sub * sub + GB_N - 1) / GB_N;
+  }
+  if (mode == GEMM_UP) return ((1 << (3 * level)) + GB_N - 1) / GB_N;
+  return 1;
+}
+
+// vector load of N consecutive T (16-B aligned)
+template <class T, int N>
+__device__ __forceinline__ void ldv(const T* __restrict__ p, T (&r)[N]) {
+  constexpr int VW = 16 / sizeof(T);
+  static_assert(N % VW == 0, "vector width");
+#pragma unroll
+  for (int u = 0; u < N / VW; ++u) {
+    if constexpr (sizeof(T) == 4) {
+      const float4 v = reinterpret_cast<const float4*>(p)[u];
+      r[4 * u] = v.x;
+      r[4 * u + 1] = v.y;
+      r[4 * u + 2] = v.z;
+      r[4 * u + 3] = v.w;
+    } else {
+      const double2 v = reinterpret_cast<const double2*>(p)[u];
+      r[2 * u] = v.x;
+      r[2 * u + 1] = v.y;
+    }
+  }
+}
+
+template <class T>
+__global__ void __launch_bounds__(G_THREADS) k_gemm_gather(GemmArgs g) {
+  constexpr int BK = GemmTile<T>::BK, AK = GemmTile<T>::AK, BKT = GemmTile<T>::BKT;
+  __shared__ __align__(16) T As[2][BK][GB_M];
+  __shared__ __align__(16) T Bs[2][BK][GB_N];
+  __shared__ int col_dst[GB_N];
+  const int tid = threadIdx.x;
+  const int ncp = g.ncp;
+  const int row0 = blockIdx.y * GB_M;
+  const int level = g.level;
+  const int nside = 1 << level, msk = nside - 1;
+
+  // ---- which targets does this tile hold, and how many terms? ----
+  int par = 0, nterm = 1;
+  if (g.mode == GEMM_DOWN) {
+    const int tpc = gemm_tiles_per_class(GEMM_DOWN, level);
+    par = blockIdx.x / tpc;
+    const int q0 = (blockIdx.x % tpc) * GB_N;
+    const int sub = nside >> 1;
+    const int ntarget = min(GB_N, sub * sub * sub - q0);
+    nterm = 1 + (g.use_m2l ? NM2L : 0);
+    if (tid < GB_N) {
+      int box = -1;
+      if (tid < ntarget) {
+        const int q = q0 + tid;
+        const int lsub = level - 1;
+        const int qx = q >> (2 * lsub), qy = (q >> lsub) & (sub - 1), qz = q & (sub - 1);
+        const int gx = 2 * qx + ((par >> 2) & 1), gy = 2 * qy + ((par >> 1) & 1), gz = 2 * qz + (par & 1);
+        box = (gx << (2 * level)) | (gy << level) | gz;
+      }
+      col_dst[tid] = box;
+    }
+  } else if (g.mode == GEMM_UP) {
+    const int q0 = blockIdx.x * GB_N;
+    const int ntarget = min(GB_N, (1 << (3 * level)) - q0);
+    nterm = 8;
+    if (tid < GB_N) col_dst[tid] = tid < ntarget ? q0 + tid : -1;
+  } else {
+    nterm = 1;
+    if (tid < GB_N) col_dst[tid] = tid == 0 ? 0 : -1;
+  }
+  __syncthreads();
+
+  const int nk = ncp / BK;
+  const int niter = nterm * nk;
+
+  // loader mapping: A tile GB_M rows x BK k, B tile BK k x GB_N columns
+  const int a_row = tid >> 1, a_k = (tid & 1) * AK;
+  const int b_col = tid >> 2, b_k = (tid & 3) * BKT;
+  // compute mapping: 16 x 16 threads, 8 rows (two groups of 4) x 4 columns
+  const int ty = tid >> 4, tx = tid & 15;
+
+  T acc[8][4];
+#pragma unroll
+  for (int i = 0; i < 8; ++i)
+#pragma unroll
+    for (int j = 0; j < 4; ++j) acc[i][j] = T(0);
+
+  T ra[AK], rb[BKT];
+  const T* Ab = nullptr;
+  const T* Bb = nullptr;
+  int cur_term = -1, my_src = -1;
+  const int tgt = col_dst[b_col];
+
+  auto term_setup = [&](int term) {
+    int src_box = -1;
+    if (g.mode == GEMM_DOWN) {
+      if (term == 0) {  // L2L from the parent (same octant for the whole tile)
+        Ab = reinterpret_cast<const T*>(g.ops_l2l) + (size_t)par * ncp * ncp;
+        Bb = reinterpret_cast<const T*>(g.src_aux);
+        if (tgt >= 0) {
+          const int pl = level - 1;
+          const int gx = (tgt >> (2 * level)) >> 1, gy = ((tgt >> level) & msk) >> 1, gz = (tgt & msk) >> 1;
+          src_box = (gx << (2 * pl)) | (gy << pl) | gz;
+        }
+      } else {  // M2L partner term-1 of this parity class
+        const int s = term - 1;
+        const char4 o = c_m2l_off[par * NM2L + s];
+        const int row = c_m2l_row[par * NM2L + s];
+        Ab = reinterpret_cast<const T*>(g.ops_main) + (size_t)row * ncp * ncp;
+        Bb = reinterpret_cast<const T*>(g.src_m2l);
+        if (tgt >= 0) {
+          const int gx = tgt >> (2 * level), gy = (tgt >> level) & msk, gz = tgt & msk;
+          src_box = ((((gx + o.x) & msk) << level | ((gy + o.y) & msk)) << level) | ((gz + o.z) & msk);
+        }
+      }
+    } else if (g.mode == GEMM_UP) {  // M2M from child octant `term`
+      Ab = reinterpret_cast<const T*>(g.ops_main) + (size_t)term * ncp * ncp;
+      Bb = reinterpret_cast<const T*>(g.src_aux);
+      if (tgt >= 0) {
+        const int cl = level + 1;
+        const int gx = tgt >> (2 * level), gy = (tgt >> level) & msk, gz = tgt & msk;
+        const int cx = 2 * gx + ((term >> 2) & 1), cy = 2 * gy + ((term >> 1) & 1), cz = 2 * gz + (term & 1);
+        src_box = (cx << (2 * cl)) | (cy << cl) | cz;
+      }
+    } else {  // lattice operator on the root multipole
+      Ab = reinterpret_cast<const T*>(g.ops_main);
+      Bb = reinterpret_cast<const T*>(g.src_aux);
+      if (tgt >= 0) src_box = 0;
+    }
+    return src_box;
+  };
+
+  auto load_regs = [&](int it) {
+    const int term = it / nk, kc = it - term * nk;
+    if (term != cur_term) {
+      my_src = term_setup(term);
+      cur_term = term;
+    }
+    const int k0 = kc * BK;
+    const int r = row0 + a_row;
+    if (r < ncp) {
+      ldv<T, AK>(Ab + (size_t)r * ncp + k0 + a_k, ra);
+    } else {
+#pragma unroll
+      for (int u = 0; u < AK; ++u) ra[u] = T(0);
+    }
+    if (my_src >= 0) {
+      ldv<T, BKT>(Bb + (size_t)my_src * ncp + k0 + b_k, rb);
+    } else {
+#pragma unroll
+      for (int u = 0; u < BKT; ++u) rb[u] = T(0);
+    }
+  };
+  auto store_smem = [&](int buf) {
+#pragma unroll
+    for (int u = 0; u < AK; ++u) As[buf][a_k + u][a_row] = ra[u];
+#pragma unroll
+    for (int u = 0; u < BKT; ++u) Bs[buf][b_k + u][b_col] = rb[u];
+  };
+
+  load_regs(0);
+  store_smem(0);
+  __syncthreads();
+  for (int it = 0; it < niter; ++it) {
+    const int buf = it & 1;
+    if (it + 1 < niter) load_regs(it + 1);
+#pragma unroll
+    for (int k = 0; k < BK; ++k) {
+      T a[8], bv[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        a[u] = As[buf][k][ty * 4 + u];
+        a[4 + u] = As[buf][k][64 + ty * 4 + u];
+        bv[u] = Bs[buf][k][tx * 4 + u];
+      }
+#pragma unroll
+      for (int i = 0; i < 8; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) acc[i][j] = fma(a[i], bv[j], acc[i][j]);
+    }
+    if (it + 1 < niter) store_smem(buf ^ 1);
+    __syncthreads();
+  }
+
+  // ---- epilogue: overwrite the target coefficients ----
+  T* dst = reinterpret_cast<T*>(g.dst);
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+    const int col = tx * 4 + j;
+    const int box = col_dst[col];
+    if (box < 0) continue;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      const int r = row0 + (i < 4 ? ty * 4 + i : 64 + ty * 4 + (i - 4));
+      if (r < ncp) dst[(size_t)box * ncp + r] = acc[i][j];
+    }
+  }
+}
+
+}  // namespace lfmm

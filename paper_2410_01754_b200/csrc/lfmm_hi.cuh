@@ -1,0 +1,287 @@
+// lfmm_hi.cuh — Hamiltonian-interpolation (MAHI) correction, one CTA per
+// titratable site, fp64 throughout (the per-site work is tiny; the
+// potentials it consumes come from the fp32 or fp64 solve).
+//
+// Per site with lambda weights w (weights.expand_weights, weights.py:54-60),
+// forms Q (nf x ns) and blended charges q~ = w Q (system.scale_charges,
+// system.py:179-197):
+//   K_st  27-image pair kernel, self-image sum on the diagonal, or the
+//         minimum-image kernel          (corrections.near_kernel :46-70)
+//   G_st  = Re(R(r_s - L/2) T_L R(r_t - L/2)^T)   (lattice_kernel :73-77),
+//         evaluated as the lattice operator applied to the unit-charge
+//         multipole of atom t and contracted with R of atom s
+//   C_rho = Q_rho K h_rho + Q_rho G h_rho + c_dip,  h_rho = q~ - Q_rho/2
+//   c_dip = -eta*gamma*|(q~ - Q_rho).(r - L/2)|^2   (c_dipole :112-124)
+//   e(q~) = 1/2 q~ (K+G) q~                          (build_corrections :179-183)
+//   S_rho = Q_rho . V[site]                          (s_values :196-198)
+//   F_k   = -sum_rho dw_rho/dlambda_k (S_rho - C_rho) (assemble :221-238)
+// QI mode: F_k = -sum_rho dw_rho/dlambda_k S_rho, no offset.
+#pragma once
+#include "lfmm_common.cuh"
+
+namespace lfmm {
+
+constexpr int HI_THREADS = 128;
+constexpr int HI_MAXF = 16;  // weights.MAX_BRANCHES = 4 -> 16 forms
+
+struct HiArgs {
+  int n_sites;
+  const int* atom_off;     // S+1
+  const int* atom_idx;     // A, input-order particle index
+  const int* nforms;       // S
+  const int* form_off;     // S+1, offsets into form_q (nf*ns per site)
+  const int* fslot_off;    // S+1, offsets of per-form outputs (sum nf)
+  const double* form_q;
+  const double* lambdas;   // S x 4
+  const int* nlam;         // S
+  const double* site_pos;  // A x 3 (caller-supplied site positions)
+  const double* pot;       // input-order potentials (N), may be null (corrections only)
+  double box;
+  int p, ncp;
+  const double* lat_t;     // packed lattice operator, transposed [in][out], fp64, or null
+  double* rscratch;        // A x ncp
+  double* uscratch;        // A x ncp
+  int images_full;         // intra_site_images == "full"
+  int dipole;
+  int mode;                // 0 hi, 1 qi
+  // outputs
+  double* c_p2p;
+  double* c_lat;
+  double* c_dip;
+  double* blend;       // S
+  double* forces;      // S x 4
+  double* offset;      // S
+};
+
+__device__ inline double hi_weight(const double* lam, int nl, int rho) {
+  double w = 1.0;
+  for (int k = 0; k < nl; ++k) w *= ((rho >> k) & 1) ? lam[k] : (1.0 - lam[k]);
+  return w;
+}
+__device__ inline double hi_wgrad(const double* lam, int nl, int k, int rho) {
+  double g = 1.0;
+  for (int i = 0; i < nl; ++i) {
+    if (i == k)
+      g *= ((rho >> i) & 1) ? 1.0 : -1.0;
+    else
+      g *= ((rho >> i) & 1) ? lam[i] : (1.0 - lam[i]);
+  }
+  return g;
+}
+
+// Packed weighted dot Re sum_full a b for conj-symmetric packed vectors.
+__device__ inline double packed_pair(const double* a, const double* b, int p, int lane_lo, int stride) {
+  const int nc = ncoef(p);
+  double s = 0.0;
+  for (int c = lane_lo; c < nc; c += stride) {
+    if (c <= p) {
+      s += a[c] * b[c];
+    } else {
+      const int r = c - (p + 1);
+      // entries after the m=0 block come in (re, im) pairs
+      s += (r & 1) ? -2.0 * a[c] * b[c] : 2.0 * a[c] * b[c];
+    }
+  }
+  return s;
+}
+
+__global__ void __launch_bounds__(HI_THREADS) k_hi_site(HiArgs g) {
+  const int s = blockIdx.x;
+  if (s >= g.n_sites) return;
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  const int a0 = g.atom_off[s], ns = g.atom_off[s + 1] - a0;
+  const int nf = g.nforms[s], nl = g.nlam[s];
+  const double* Q = g.form_q + g.form_off[s];
+  const double L = g.box;
+  const int p = g.p, ncp = g.ncp, nc = ncoef(p);
+
+  extern __shared__ double sm[];
+  double* qt = sm;               // ns
+  double* KG = qt + ns;          // ns*ns (K)
+  double* GG = KG + ns * ns;     // ns*ns (G)
+  double* pos = GG + ns * ns;    // ns*3
+  __shared__ double lam[4], w[HI_MAXF], Cv[HI_MAXF], Sv[HI_MAXF];
+
+  if (tid < 4) lam[tid] = g.lambdas[4 * s + tid];
+  for (int i = tid; i < 3 * ns; i += blockDim.x) pos[i] = g.site_pos[3 * a0 + i];
+  __syncthreads();
+  if (tid < nf) w[tid] = hi_weight(lam, nl, tid);
+  __syncthreads();
+  for (int t = tid; t < ns; t += blockDim.x) {
+    double acc = 0.0;
+    for (int r = 0; r < nf; ++r) acc += w[r] * Q[r * ns + t];
+    qt[t] = acc;
+  }
+  const bool qi = g.mode == 1;
+  const bool lattice = !qi && g.images_full && g.lat_t != nullptr;
+  if (!qi) {
+    // ---- near kernel K ----
+    for (int e = tid; e < ns * ns; e += blockDim.x) {
+      const int i = e / ns, j = e % ns;
+      const double dx = pos[3 * i] - pos[3 * j], dy = pos[3 * i + 1] - pos[3 * j + 1],
+                   dz = pos[3 * i + 2] - pos[3 * j + 2];
+      double k = 0.0;
+      if (g.images_full) {
+        for (int n = 0; n < 27; ++n) {
+          const int nx = n / 9 - 1, ny = (n / 3) % 3 - 1, nz = n % 3 - 1;
+          if (i == j && n == 13) continue;
+          const double ex = dx + nx * L, ey = dy + ny * L, ez = dz + nz * L;
+          k += 1.0 / sqrt(ex * ex + ey * ey + ez * ez);
+        }
+      } else if (i != j) {
+        const double ex = dx - L * rint(dx / L), ey = dy - L * rint(dy / L), ez = dz - L * rint(dz / L);
+        k = 1.0 / sqrt(ex * ex + ey * ey + ez * ez);
+      }
+      KG[e] = k;
+    }
+    // ---- lattice kernel G ----
+    if (lattice) {
+      double* R = g.rscratch + (size_t)a0 * ncp;
+      double* U = g.uscratch + (size_t)a0 * ncp;
+      const double invL = 1.0 / L;
+      for (int t = tid; t < ns; t += blockDim.x) {
+        double* Rt = R + (size_t)t * ncp;
+        const double x = (pos[3 * t] - 0.5 * L) * invL, y = (pos[3 * t + 1] - 0.5 * L) * invL,
+                     z = (pos[3 * t + 2] - 0.5 * L) * invL;
+        int a = 0;
+        regular_stream<double>(x, y, z, p, [&](int m, int l, double re, double im) {
+          Rt[a++] = re;
+          if (m > 0) Rt[a++] = im;
+        });
+      }
+      __syncthreads();
+      // U_t = T1 R_t  (lat_t stored transposed: [in b][out a])
+      for (int t0 = 0; t0 < ns; t0 += 8) {
+        const int tn = min(8, ns - t0);
+        for (int a = tid; a < nc; a += blockDim.x) {
+          double acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+          for (int b = 0; b < nc; ++b) {
+            const double tv = g.lat_t[(size_t)b * ncp + a];
+#pragma unroll
+            for (int u = 0; u < 8; ++u)
+              if (u < tn) acc[u] = fma(tv, R[(size_t)(t0 + u) * ncp + b], acc[u]);
+          }
+          for (int u = 0; u < tn; ++u) U[(size_t)(t0 + u) * ncp + a] = acc[u];
+        }
+      }
+      __syncthreads();
+      // G_st = (1/L) <R_s, U_t>, one warp per pair
+      for (int e = wid; e < ns * ns; e += blockDim.x / 32) {
+        const int i = e / ns, j = e % ns;
+        double v = packed_pair(R + (size_t)i * ncp, U + (size_t)j * ncp, p, lane, 32);
+        for (int off = 16; off > 0; off >>= 1) v += __shfl_down_sync(0xffffffffu, v, off);
+        if (lane == 0) GG[e] = v * invL;
+      }
+    }
+  }
+  __syncthreads();
+
+  // ---- per-form scalars (warp per form) ----
+  const double gamma = 2.0 * 3.14159265358979323846 / (3.0 * L * L * L);
+  for (int r = wid; r < nf; r += blockDim.x / 32) {
+    const double* Qr = Q + r * ns;
+    double cp = 0.0, cl = 0.0, sv = 0.0, ddx = 0.0, ddy = 0.0, ddz = 0.0;
+    for (int i = lane; i < ns; i += 32) {
+      if (!qi) {
+        double kh = 0.0, gh = 0.0;
+        for (int j = 0; j < ns; ++j) {
+          const double h = qt[j] - 0.5 * Qr[j];
+          kh += KG[i * ns + j] * h;
+          if (lattice) gh += GG[i * ns + j] * h;
+        }
+        cp += Qr[i] * kh;
+        cl += Qr[i] * gh;
+        const double dev = qt[i] - Qr[i];
+        ddx += dev * (pos[3 * i] - 0.5 * L);
+        ddy += dev * (pos[3 * i + 1] - 0.5 * L);
+        ddz += dev * (pos[3 * i + 2] - 0.5 * L);
+      }
+      if (g.pot) sv += Qr[i] * g.pot[g.atom_idx[a0 + i]];
+    }
+    for (int off = 16; off > 0; off >>= 1) {
+      cp += __shfl_down_sync(0xffffffffu, cp, off);
+      cl += __shfl_down_sync(0xffffffffu, cl, off);
+      sv += __shfl_down_sync(0xffffffffu, sv, off);
+      ddx += __shfl_down_sync(0xffffffffu, ddx, off);
+      ddy += __shfl_down_sync(0xffffffffu, ddy, off);
+      ddz += __shfl_down_sync(0xffffffffu, ddz, off);
+    }
+    if (lane == 0) {
+      const double cd = (!qi && g.images_full && g.dipole) ? -DIPOLE_ETA * gamma * (ddx * ddx + ddy * ddy + ddz * ddz) : 0.0;
+      const int slot = g.fslot_off[s] + r;
+      if (g.c_p2p) g.c_p2p[slot] = cp;
+      if (g.c_lat) g.c_lat[slot] = cl;
+      if (g.c_dip) g.c_dip[slot] = cd;
+      Cv[r] = cp + cl + cd;
+      Sv[r] = sv;
+    }
+  }
+  __syncthreads();
+  // ---- blend energy, offset, lambda forces (warp 0) ----
+  if (wid == 0) {
+    double eb = 0.0;
+    if (!qi) {
+      for (int e = lane; e < ns * ns; e += 32) {
+        const int i = e / ns, j = e % ns;
+        eb += qt[i] * (KG[e] + (lattice ? GG[e] : 0.0)) * qt[j];
+      }
+      for (int off = 16; off > 0; off >>= 1) eb += __shfl_down_sync(0xffffffffu, eb, off);
+      eb *= 0.5;
+    }
+    if (lane == 0) {
+      double wc = 0.0;
+      for (int r = 0; r < nf; ++r) wc += w[r] * (qi ? 0.0 : Cv[r]);
+      if (g.blend) g.blend[s] = eb;
+      if (g.offset) g.offset[s] = qi ? 0.0 : eb - wc;
+      if (g.forces) {
+        for (int k = 0; k < 4; ++k) {
+          double f = 0.0;
+          if (k < nl && g.pot)
+            for (int r = 0; r < nf; ++r) f += hi_wgrad(lam, nl, k, r) * (Sv[r] - (qi ? 0.0 : Cv[r]));
+          g.forces[4 * s + k] = k < nl ? -f : 0.0;
+        }
+      }
+    }
+  }
+}
+
+// fixed-order sum of per-site offsets (CorrectionSet.energy_offset, :153-154)
+__global__ void k_sum_offsets(const double* __restrict__ v, int n, double* __restrict__ out) {
+  dd acc[1] = {dd{0.0, 0.0}};
+  for (int i = threadIdx.x; i < n; i += blockDim.x) acc[0] = dd_add(acc[0], dd_from(v[i]));
+  __shared__ dd res[1];
+  block_reduce_dd<1>(acc, res);
+  if (threadIdx.x == 0) *out = res[0].hi + res[0].lo;
+}
+
+// gather caller positions of site atoms from the raw input positions
+__global__ void k_gather_site_pos(const double* __restrict__ pos_in, const int* __restrict__ idx, int n,
+                                  double* __restrict__ out) {
+  const int a = blockIdx.x * blockDim.x + threadIdx.x;
+  if (a >= n) return;
+  const int i = idx[a];
+  out[3 * a] = pos_in[3 * i];
+  out[3 * a + 1] = pos_in[3 * i + 1];
+  out[3 * a + 2] = pos_in[3 * i + 2];
+}
+
+// scale_charges (system.py:179-197): copy, then blend site entries
+__global__ void k_scale_charges(const double* __restrict__ q_in, int64_t n, double* __restrict__ q_out) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i < n) q_out[i] = q_in[i];
+}
+__global__ void k_blend_sites(HiArgs g, double* __restrict__ q_out) {
+  const int s = blockIdx.x;
+  if (s >= g.n_sites) return;
+  const int a0 = g.atom_off[s], ns = g.atom_off[s + 1] - a0;
+  const int nf = g.nforms[s], nl = g.nlam[s];
+  const double* Q = g.form_q + g.form_off[s];
+  const double* lam = g.lambdas + 4 * s;
+  for (int t = threadIdx.x; t < ns; t += blockDim.x) {
+    double acc = 0.0;
+    for (int r = 0; r < nf; ++r) acc += hi_weight(lam, nl, r) * Q[r * ns + t];
+    q_out[g.atom_idx[a0 + t]] = acc;
+  }
+}
+
+}  // namespace lfmm

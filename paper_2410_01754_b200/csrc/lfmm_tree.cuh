@@ -1,0 +1,189 @@
+// lfmm_tree.cuh — uniform periodic octree on the device, bit-exact with
+// octree.build_octree (fmm/octree.py:114-163):
+//   wrap    : np.mod(x, L), then x >= L -> 0          (system.py:103-108)
+//   cell    : clip(int64(x / (L / 2^d)), 0, 2^d - 1)    (octree.py:121-123)
+//   leaf    : (ix*n + iy)*n + iz                        (octree.py:48-49)
+//   order   : lexsort((z, y, x, leaf)) — leaf, x, y, z, then input index
+//             (numpy's lexsort is stable)               (octree.py:125)
+// Counting sort into leaf buckets (integer atomics only: the histogram is
+// order independent), then a per-leaf rank sort on the full fp64 key makes
+// the canonical permutation independent of scheduling.
+#pragma once
+#include "lfmm_common.cuh"
+
+namespace lfmm {
+
+// numpy float remainder (npy_divmod): fmod, shifted into the divisor's sign,
+// and +0.0 for an exact zero.
+__device__ __forceinline__ double np_mod(double a, double b) {
+  double m = fmod(a, b);
+  if (m != 0.0) {
+    if ((b < 0.0) != (m < 0.0)) m += b;
+  } else {
+    m = copysign(0.0, b);
+  }
+  return m;
+}
+
+__global__ void k_wrap_cell(const double* __restrict__ pos_in, int64_t n, double box, double size,
+                            int depth, double* __restrict__ pos_wrap, int* __restrict__ leaf_of,
+                            int* __restrict__ counts) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const int nside = 1 << depth;
+  int cell[3];
+#pragma unroll
+  for (int a = 0; a < 3; ++a) {
+    double w = np_mod(pos_in[3 * i + a], box);
+    if (w >= box) w = 0.0;
+    pos_wrap[3 * i + a] = w;
+    double t = w / size;  // IEEE division, like positions / size
+    long long c = (long long)t;  // astype(int64): truncation
+    c = c < 0 ? 0 : (c > nside - 1 ? nside - 1 : c);
+    cell[a] = (int)c;
+  }
+  const int leaf = (cell[0] * nside + cell[1]) * nside + cell[2];
+  leaf_of[i] = leaf;
+  atomicAdd(&counts[leaf], 1);
+}
+
+// Exclusive scan of counts[0..n) into start[0..n]; one block of 1024 threads.
+__global__ void k_scan_counts(const int* __restrict__ counts, int n, int* __restrict__ start) {
+  __shared__ int part[1024];
+  const int t = threadIdx.x;
+  const int per = (n + blockDim.x - 1) / blockDim.x;
+  const int b0 = min(n, t * per), b1 = min(n, b0 + per);
+  int s = 0;
+  for (int i = b0; i < b1; ++i) s += counts[i];
+  part[t] = s;
+  __syncthreads();
+  for (int off = 1; off < blockDim.x; off <<= 1) {
+    int v = t >= off ? part[t - off] : 0;
+    __syncthreads();
+    part[t] += v;
+    __syncthreads();
+  }
+  int run = part[t] - s;  // exclusive prefix of this segment
+  for (int i = b0; i < b1; ++i) {
+    start[i] = run;
+    run += counts[i];
+  }
+  if (t == blockDim.x - 1) start[n] = part[t];
+}
+
+__global__ void k_scatter_leaf(const int* __restrict__ leaf_of, int64_t n, const int* __restrict__ start,
+                               int* __restrict__ cursor, int* __restrict__ bucket) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const int leaf = leaf_of[i];
+  const int slot = atomicAdd(&cursor[leaf], 1);
+  bucket[start[leaf] + slot] = (int)i;
+}
+
+__device__ __forceinline__ bool key_less(double ax, double ay, double az, int ai, double bx, double by,
+                                         double bz, int bi) {
+  if (ax != bx) return ax < bx;
+  if (ay != by) return ay < by;
+  if (az != bz) return az < bz;
+  return ai < bi;
+}
+
+// One warp per leaf: rank of every bucket entry under (x, y, z, index).
+__global__ void k_leaf_rank(const double* __restrict__ pos_wrap, const int* __restrict__ start,
+                            const int* __restrict__ bucket, int nleaf, int* __restrict__ perm,
+                            int* __restrict__ inv_perm) {
+  const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (warp >= nleaf) return;
+  const int s0 = start[warp], s1 = start[warp + 1];
+  for (int e = s0 + lane; e < s1; e += 32) {
+    const int i = bucket[e];
+    const double x = pos_wrap[3 * i], y = pos_wrap[3 * i + 1], z = pos_wrap[3 * i + 2];
+    int rank = 0;
+    for (int f = s0; f < s1; ++f) {
+      const int j = bucket[f];
+      rank += key_less(pos_wrap[3 * j], pos_wrap[3 * j + 1], pos_wrap[3 * j + 2], j, x, y, z, i);
+    }
+    perm[s0 + rank] = i;
+    inv_perm[i] = s0 + rank;
+  }
+}
+
+// Canonical-order arrays: fp64 sorted positions and leaf-relative coordinates
+// (x - c_leaf with c_leaf = (grid + 0.5) * size, octree.py:65-66) in T.
+template <class T>
+__global__ void k_sorted_arrays(const double* __restrict__ pos_wrap, const int* __restrict__ perm,
+                                const int* __restrict__ leaf_of, int64_t n, int depth, double size,
+                                double* __restrict__ pos_sorted, vec4_t<T>* __restrict__ xq,
+                                int* __restrict__ leaf_sorted) {
+  const int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (k >= n) return;
+  const int i = perm[k];
+  const int leaf = leaf_of[i];
+  const int nside = 1 << depth, msk = nside - 1;
+  const int g[3] = {leaf >> (2 * depth), (leaf >> depth) & msk, leaf & msk};
+  double r[3];
+#pragma unroll
+  for (int a = 0; a < 3; ++a) {
+    r[a] = pos_wrap[3 * i + a];
+    pos_sorted[3 * k + a] = r[a];
+  }
+  vec4_t<T> v;
+  v.x = (T)(r[0] - (g[0] + 0.5) * size);
+  v.y = (T)(r[1] - (g[1] + 0.5) * size);
+  v.z = (T)(r[2] - (g[2] + 0.5) * size);
+  v.w = T(0);
+  xq[k] = v;
+  leaf_sorted[k] = leaf;
+}
+
+// Neighbour enumeration shared by P2P and the list export (octree.py:136-139):
+// row t of NEIGHBOR_OFFSETS is ((t/9)-1, (t/3)%3-1, t%3-1).
+__host__ __device__ inline void neighbor(int b, int t, int depth, int& nb, int& shx, int& shy, int& shz) {
+  const int nside = 1 << depth, msk = nside - 1;
+  const int bx = b >> (2 * depth), by = (b >> depth) & msk, bz = b & msk;
+  const int rx = bx + t / 9 - 1, ry = by + (t / 3) % 3 - 1, rz = bz + t % 3 - 1;
+  // floor_divide by a power of two == arithmetic shift
+  shx = rx >> depth;
+  shy = ry >> depth;
+  shz = rz >> depth;
+  nb = (((rx & msk) << depth | (ry & msk)) << depth) | (rz & msk);
+}
+
+__global__ void k_export_nb(int depth, int64_t* __restrict__ nb_box, int64_t* __restrict__ nb_shift) {
+  const int nleaf = 1 << (3 * depth);
+  const int idx = blockIdx.x * blockDim.x + threadIdx.x;
+  if (idx >= nleaf * 27) return;
+  const int b = idx / 27, t = idx % 27;
+  int nb, sx, sy, sz;
+  neighbor(b, t, depth, nb, sx, sy, sz);
+  if (nb_box) nb_box[idx] = nb;
+  if (nb_shift) {
+    nb_shift[3 * idx] = sx;
+    nb_shift[3 * idx + 1] = sy;
+    nb_shift[3 * idx + 2] = sz;
+  }
+}
+
+// M2L partner of target box b at level l, slot s (0..188), as the M2L
+// kernels gather it: sources = wrap(grid + offset) (octree.py:109).
+__device__ __forceinline__ int m2l_source(int b, int s, int level, int& row) {
+  const int nside = 1 << level, msk = nside - 1;
+  const int gx = b >> (2 * level), gy = (b >> level) & msk, gz = b & msk;
+  const int par = ((gx & 1) << 2) | ((gy & 1) << 1) | (gz & 1);
+  const char4 o = c_m2l_off[par * NM2L + s];
+  row = c_m2l_row[par * NM2L + s];
+  return ((((gx + o.x) & msk) << level | ((gy + o.y) & msk)) << level) | ((gz + o.z) & msk);
+}
+
+__global__ void k_export_m2l(int level, int64_t* __restrict__ src, int64_t* __restrict__ rows) {
+  const int nbox = 1 << (3 * level);
+  const int idx = blockIdx.x * blockDim.x + threadIdx.x;
+  if (idx >= nbox * NM2L) return;
+  int row;
+  const int s = m2l_source(idx / NM2L, idx % NM2L, level, row);
+  if (src) src[idx] = s;
+  if (rows) rows[idx] = row;
+}
+
+}  // namespace lfmm
