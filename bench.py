@@ -1,0 +1,435 @@
+#!/usr/bin/env python
+"""Benchmark of one full FMM + HI electrostatics step (BASELINE.json metric).
+
+Workload (BASELINE.json configs[2], the paper headline on one GPU): a
+synthetic ~1M-atom TIP3P-like water box with 512 titratable 10-atom sites
+(2 forms each), p = 10, depth 5, fp32 kernels (fp64 reductions).  One step =
+tree rebuild from the step's positions + scale_charges + solve (potentials,
+near/far/dipole, energies) + spatial forces + HI corrections + lambda-force
+assembly.  The "plain FMM" step (same positions, same
+blended charges, no lambda machinery) is timed alongside for the HI
+overhead.
+
+    python bench.py [--gpus N --steps K --warmup W] [--impl reference]
+
+Under torchrun each rank runs an independent replica (its own water box,
+seed = rank); value = all ranks' steps / max-over-ranks time.
+"""
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "FMM+HI electrostatics steps/sec at 1M atoms/512 sites; HI overhead % vs FMM"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--atoms", type=int, default=1_000_000)
+    ap.add_argument("--sites", type=int, default=512)
+    ap.add_argument("--p", type=int, default=10)
+    ap.add_argument("--depth", type=int, default=5)
+    ap.add_argument("--precision", default="single", choices=["single", "double"])
+    ap.add_argument("--cpu-fraction", type=float, default=1.0 / 32)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--seed", type=int, default=0)
+    return ap.parse_args()
+
+
+# ------------------------------------------------------------- helpers ----
+def dist_env():
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return rank, world, local
+
+
+def load_system(args, rank):
+    from paper_2410_01754_b200.waterbox import generate_water_box
+
+    cache = f"/tmp/lfmm_wb_{args.atoms}_{args.sites}_{args.seed + rank}.npz"
+    if os.path.exists(cache):
+        z = np.load(cache)
+        from paper_2410_01754_b200.system import LambdaState, ParticleSystem, TitratableSite
+
+        off = z["site_off"]
+        sites = [TitratableSite(z["site_idx"][off[s]:off[s + 1]], z["site_forms"][s]) for s in range(len(off) - 1)]
+        system = ParticleSystem(float(z["box"]), z["positions"], z["charges"], sites)
+        lam = LambdaState(values=list(z["lams"][:, None]) if z["lams"].ndim == 1 else list(z["lams"]),
+                          velocities=[np.zeros(1)] * len(sites), masses=[5.0] * len(sites))
+        return system, lam
+    n_sites = args.sites
+    # waters removed around each site (~8.25 molecules) are compensated
+    target = args.atoms + int(round(n_sites * (3 * 8.25 - 10)))
+    system, lam, _ = generate_water_box(target, n_sites, forms_per_site=2, seed=args.seed + rank)
+    try:
+        off = np.concatenate([[0], np.cumsum([s.num_particles for s in system.sites])])
+        np.savez(cache, box=system.box_length, positions=system.positions, charges=system.charges,
+                 site_off=off, site_idx=np.concatenate([s.particle_indices for s in system.sites]),
+                 site_forms=np.stack([s.form_charges for s in system.sites]),
+                 lams=np.array([v[0] for v in lam.values]))
+    except OSError:
+        pass
+    return system, lam
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.proc = None
+        self.lines = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
+                 "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except OSError:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *a):
+        if self.proc is not None:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+
+    def summary(self):
+        sm, smax, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [x.strip() for x in ln.split(",")]
+            if len(parts) < 6:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                smax = float(parts[1])
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[2:6]):
+                if v.lower().startswith("active"):
+                    reasons.add(nm)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": smax, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+def measured_peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
+            return json.load(fh), "measured"
+    except OSError:
+        return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0}, "fallback"
+
+
+def pair_count(leaf_start, depth):
+    """Exact ordered P2P pair count: sum_b sum_t n_b n_nb(b,t) - N."""
+    n = 2 ** depth
+    cnt = np.diff(leaf_start).astype(np.float64)
+    g = np.arange(n ** 3)
+    gx, gy, gz = g // (n * n), (g // n) % n, g % n
+    tot = 0.0
+    for dx in (-1, 0, 1):
+        for dy in (-1, 0, 1):
+            for dz in (-1, 0, 1):
+                nb = (((gx + dx) % n) * n + (gy + dy) % n) * n + (gz + dz) % n
+                tot += float(np.dot(cnt, cnt[nb]))
+    return tot - cnt.sum()
+
+
+def algorithmic_work(p, depth, n_atoms, pairs, n_sites, ns=10, nf=2):
+    """Closed-form work per step."""
+    nc = (p + 1) ** 2
+    boxes = sum(8 ** l for l in range(1, depth + 1))
+    t_m2l = 189 * boxes
+    w = {
+        "p2p": {"flop": 20.0 * pairs, "bytes": 2 * 16.0 * n_atoms},
+        "m2l": {"flop": 2.0 * nc * nc * t_m2l, "bytes": 2.0 * 4 * nc * boxes},
+        "l2l": {"flop": 2.0 * nc * nc * boxes, "bytes": 3.0 * 4 * nc * boxes},
+        "m2m": {"flop": 2.0 * nc * nc * boxes, "bytes": 4.0 * nc * boxes * 2},
+        "p2m": {"flop": 8.0 * nc * n_atoms, "bytes": 16.0 * n_atoms + 4.0 * nc * 8 ** depth},
+        "l2p": {"flop": 16.0 * nc * n_atoms, "bytes": 16.0 * n_atoms + 4.0 * nc * 8 ** depth + 16.0 * n_atoms},
+        "hi": {"flop": n_sites * (20.0 * 27 * ns * ns + nf * (2.0 * nc * nc + 8 * ns * nc)), "bytes": 0.0},
+        "t_m2l": t_m2l,
+    }
+    return w
+
+
+# ----------------------------------------------------------- our arm ----
+def run_ours(args):
+    import torch
+
+    rank, world, local = dist_env()
+    if world > 1:
+        import torch.distributed as dist
+
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl")
+    else:
+        torch.cuda.set_device(0)
+    dev = torch.device("cuda", torch.cuda.current_device())
+
+    from paper_2410_01754_b200 import _native
+    from paper_2410_01754_b200.fmm.solver import PeriodicSolver, SolverConfig
+    from paper_2410_01754_b200.system import lambda_table, site_tables
+
+    system, lam_state = load_system(args, rank)
+    n = system.num_particles
+    cfg = SolverConfig(p=args.p, depth=args.depth, precision=args.precision)
+    solver = PeriodicSolver(system.positions, system.box_length, cfg)
+    plan = solver.plan
+    tables = site_tables(system)
+    plan.set_sites(*tables)
+    lam, nl = lambda_table(system, lam_state.values)
+    stream = torch.cuda.Stream(device=dev)
+    plan.set_stream(stream.cuda_stream)
+    s = len(system.sites)
+
+    # device-resident inputs (value) -----------------------------------
+    d_pos = torch.from_numpy(np.ascontiguousarray(system.positions)).to(dev)
+    d_q = torch.from_numpy(np.ascontiguousarray(system.charges)).to(dev)
+    d_lam = torch.from_numpy(np.ascontiguousarray(lam)).to(dev)
+    d_nl = torch.from_numpy(np.ascontiguousarray(nl)).to(dev)
+    d_e = torch.empty(1, dtype=torch.float64, device=dev)
+    d_f = torch.empty((n, 3), dtype=torch.float64, device=dev)
+    d_lf = torch.empty((s, 4), dtype=torch.float64, device=dev)
+    flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)
+    # plain FMM charges: the same blended charges, no lambda machinery
+    qt = plan.scale_charges(system.charges, lam, nl)
+    d_qt = torch.from_numpy(qt).to(dev)
+
+    def step_dev(plain=False):
+        plan.step(d_pos, d_qt if plain else d_q, None if plain else d_lam, None if plain else d_nl,
+                  mode=_native.MODE_HI, plain=plain, on_device=True, energy=d_e, forces=d_f, lambda_forces=d_lf)
+
+    def timed(fn, k, flush_l2=True):
+        times = []
+        for _ in range(k):
+            if flush_l2:
+                with torch.cuda.stream(stream):
+                    flush.fill_(1.0)
+            e0 = torch.cuda.Event(enable_timing=True)
+            e1 = torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            fn()
+            e1.record(stream)
+            e1.synchronize()
+            times.append(e0.elapsed_time(e1))
+        return times
+
+    def barrier():
+        torch.cuda.synchronize()
+        if world > 1:
+            import torch.distributed as dist
+
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    def max_over_ranks(x):
+        if world == 1:
+            return x
+        import torch.distributed as dist
+
+        t = torch.tensor([x], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    # warm-up
+    for _ in range(max(3, args.warmup)):
+        step_dev()
+        step_dev(plain=True)
+    torch.cuda.synchronize()
+
+    # timed: full step, device-resident inputs
+    l0 = plan.launch_count()
+    barrier()
+    clk = ClockSampler(local).__enter__()
+    t_full = timed(step_dev, args.steps)
+    barrier()
+    launches = (plan.launch_count() - l0) // args.steps
+    t_plain = timed(lambda: step_dev(plain=True), args.steps)
+    ms_full = max_over_ranks(sum(t_full) / len(t_full))
+    ms_plain = max_over_ranks(sum(t_plain) / len(t_plain))
+
+    # e2e through the C-ABI with pinned host buffers
+    h_pos = torch.from_numpy(np.ascontiguousarray(system.positions)).pin_memory()
+    h_q = torch.from_numpy(np.ascontiguousarray(system.charges)).pin_memory()
+    h_lam = torch.from_numpy(np.ascontiguousarray(lam)).pin_memory()
+    h_nl = torch.from_numpy(np.ascontiguousarray(nl)).pin_memory()
+    h_e = torch.empty(1, dtype=torch.float64).pin_memory()
+    h_f = torch.empty((n, 3), dtype=torch.float64).pin_memory()
+    h_lf = torch.empty((s, 4), dtype=torch.float64).pin_memory()
+
+    def step_host():
+        plan.step(h_pos, h_q, h_lam, h_nl, mode=_native.MODE_HI, plain=False, on_device=False, energy=h_e,
+                  forces=h_f, lambda_forces=h_lf)
+
+    for _ in range(2):
+        step_host()
+    barrier()
+    t_e2e = timed(step_host, args.steps)
+    barrier()
+    clk.__exit__(None, None, None)
+    ms_e2e = max_over_ranks(sum(t_e2e) / len(t_e2e))
+    h2d = n * 3 * 8 + n * 8 + s * 4 * 8 + s * 4
+    d2h = 8 + n * 3 * 8 + s * 4 * 8
+
+    # per-stage breakdown (separate profiled pass, CUDA events per launch)
+    plan.profile(True)
+    kprof = max(3, min(args.steps, 10))
+    for _ in range(kprof):
+        step_dev()
+    stages = plan.stage_times()
+    plan.profile(False)
+
+    perm, inv, leaf, start, _ = plan.export_tree()
+    pairs = pair_count(start, args.depth)
+    work = algorithmic_work(args.p, args.depth, n, pairs, s)
+    peaks, peak_kind = measured_peaks()
+    stage_rows = {}
+    step_ms = sum(v[0] for v in stages.values()) / kprof
+    for name, (ms_tot, cnt) in stages.items():
+        if cnt == 0 or name in ("setup",):
+            continue
+        ms = ms_tot / kprof
+        row = {"ms": round(ms, 4), "launches_per_step": cnt // kprof,
+               "share": round(ms / step_ms, 4) if step_ms else None}
+        if name in work and isinstance(work[name], dict):
+            fl = work[name]["flop"]
+            row["algorithmic_gflop"] = round(fl / 1e9, 3)
+            row["achieved_tflops"] = round(fl / (ms * 1e-3) / 1e12, 3) if ms > 0 else None
+        stage_rows[name] = row
+    dom = max(stage_rows, key=lambda k: stage_rows[k]["ms"])
+    # dominant kernel roofline: per launch = per-step work / launches
+    fl = work.get(dom, {}).get("flop", 0.0) if isinstance(work.get(dom), dict) else 0.0
+    dom_ms = stage_rows[dom]["ms"]
+    achieved = fl / (dom_ms * 1e-3) / 1e12 if dom_ms > 0 else 0.0
+    fp32_pipe = 62.2  # TFLOP/s, profiles/r01_pipe_peaks.txt (FFMA microbenchmark on this pool)
+    roofline = {
+        "kernel": dom, "bound": "tensor", "achieved": round(achieved, 3), "peak": peaks.get("bf16_tflops"),
+        "unit": "TFLOP/s", "frac": round(achieved / peaks.get("bf16_tflops", 1.0), 5), "traffic": None,
+        "peak_source": f"{peak_kind} bf16 dense (MEASURED_PEAKS.json); kernel runs on FP32 SIMT pipes",
+        "fp32_simt_peak": fp32_pipe, "frac_of_fp32_simt": round(achieved / fp32_pipe, 4),
+        "algorithmic": "2*(p+1)^4 flop per M2L translation (dense real-packed operator), 189*sum_l 8^l "
+                       "translations per step" if dom == "m2l" else "see stages",
+    }
+
+    cpu = None
+    if rank == 0 and not args.no_cpu_baseline and world == 1:
+        cpu = cpu_sample(system, lam_state, args)
+
+    value = world * 1000.0 / ms_full
+    line = {
+        "metric": METRIC, "value": round(value, 3), "unit": "steps/s", "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": round(ms_full, 4), "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f32" if args.precision == "single" else "f64", "data": "synthetic",
+        "config": {"workload": f"C3: ~{n} atom TIP3P-like water box, {s} titratable sites x 2 forms, p={args.p}, "
+                               f"depth={args.depth}, {args.precision}; full step = tree rebuild + scale_charges + "
+                               f"solve + spatial forces + HI corrections + lambda forces",
+                   "atoms": n, "sites": s, "p": args.p, "depth": args.depth,
+                   "parallelism": "replicas (one independent system per rank)" if world > 1 else "single GPU",
+                   "l2": "flushed between timed steps (256 MiB write)"},
+        "hi_overhead_pct": round(100.0 * (ms_full / ms_plain - 1.0), 2),
+        "plain_fmm_ms_per_step": round(ms_plain, 4),
+        "e2e": {"value": round(world * 1000.0 / ms_e2e, 3), "unit": "steps/s", "h2d_bytes_per_step": h2d,
+                "d2h_bytes_per_step": d2h, "ms_per_step": round(ms_e2e, 4)},
+        "gpu_launches": launches,
+        "clocks": clk.summary(),
+        "roofline": roofline,
+        "stages": stage_rows,
+        "p2p_pairs": pairs,
+        "cpu_baseline": cpu,
+    }
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.destroy_process_group()
+
+
+# ---------------------------------------------------- CPU (oracle) arm ----
+def cpu_sample(system, lam_state, args, reps=1):
+    from oracle import lfmm_oracle as orc
+
+    cfg = orc.default_config(p=args.p, depth=args.depth)
+    sites = [(s.particle_indices, s.form_charges) for s in system.sites]
+    lams = [np.asarray(v) for v in lam_state.values]
+    orc.lattice_matrix(cfg, system.box_length)  # per-process cache, like lru_cache in the reference
+    secs = []
+    parts = None
+    for _ in range(reps):
+        t, parts = orc.timed_step_sample(system.positions, system.charges, system.box_length, sites, lams, cfg,
+                                         args.cpu_fraction, time.perf_counter)
+        secs.append(t)
+    t = statistics.median(secs)
+    return {"value": round(1.0 / t, 6), "unit": "steps/s", "cores": os.cpu_count(), "kind": "port",
+            "sample": f"oracle/lfmm_oracle.py full step; P2P/P2M/L2P/M2L+L2L timed on the first "
+                      f"{args.cpu_fraction:.4f} and {2 * args.cpu_fraction:.4f} of leaves/boxes and extrapolated "
+                      f"linearly to the whole system; tree, lists, M2M, lattice, HI in full; numpy complex128 + "
+                      f"OpenBLAS, numba-parallel P2P",
+            "extrapolated_s_per_step": round(t, 3),
+            "parts_s": {k: round(v, 3) for k, v in parts.items()}}
+
+
+def run_reference(args):
+    rank, world, _ = dist_env()
+    if rank != 0:
+        return
+    os.environ.setdefault("OMP_NUM_THREADS", str(os.cpu_count()))
+    system, lam_state = load_system(args, 0)
+    for _ in range(args.warmup):
+        cpu_sample(system, lam_state, args)
+    samples = [cpu_sample(system, lam_state, args) for _ in range(args.steps)]
+    secs = [1.0 / c["value"] for c in samples]
+    t = statistics.median(secs)
+    base = dict(samples[0])
+    base["value"] = round(1.0 / t, 6)
+    line = {"impl": "reference", "metric": METRIC, "value": round(1.0 / t, 6), "unit": "steps/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(1000 * t, 2),
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": f"C3: ~{system.num_particles} atom water box, {len(system.sites)} sites, "
+                                   f"p={args.p}, depth={args.depth}; oracle port on host cores",
+                       "atoms": system.num_particles, "sites": len(system.sites), "p": args.p, "depth": args.depth},
+            "cpu_baseline": base,
+            "e2e": {"value": round(1.0 / t, 6), "unit": "steps/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

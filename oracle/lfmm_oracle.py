@@ -262,54 +262,77 @@ def lattice_matrix(cfg, box):
 
 
 # ------------------------------------------------------------ near field ----
-def _padded_leaves(tree):
-    start = tree["leaf_start"]
-    cnt = np.diff(start)
-    nleaf = cnt.size
-    width = max(1, int(cnt.max()) if cnt.size else 1)
-    slot = np.arange(width)[None, :]
-    idx = start[:-1, None] + slot
-    valid = slot < cnt[:, None]
-    return np.where(valid, idx, 0), valid, nleaf
+try:  # the reference accelerates the same loop with numba (solver.py:30-33, :164-195)
+    import numba as _nb
+except ImportError:  # pragma: no cover
+    _nb = None
+
+if _nb is not None:
+
+    @_nb.njit(parallel=True, cache=False)
+    def _p2p_numba(pos, start, nb_box, shift_len, q, rows, targets, grad, out, gout):
+        nk = q.shape[1]
+        for ti in _nb.prange(targets.shape[0]):
+            b = targets[ti]
+            t0, t1 = start[b], start[b + 1]
+            for t in rows:
+                s = nb_box[b, t]
+                s0, s1 = start[s], start[s + 1]
+                sx, sy, sz = shift_len[b, t, 0], shift_len[b, t, 1], shift_len[b, t, 2]
+                home = t == 13
+                for i in range(t0, t1):
+                    xi, yi, zi = pos[i, 0], pos[i, 1], pos[i, 2]
+                    for j in range(s0, s1):
+                        if home and j == i:
+                            continue
+                        dx = xi - pos[j, 0] - sx
+                        dy = yi - pos[j, 1] - sy
+                        dz = zi - pos[j, 2] - sz
+                        inv = 1.0 / np.sqrt(dx * dx + dy * dy + dz * dz)
+                        for k in range(nk):
+                            out[i, k] += q[j, k] * inv
+                        if grad:
+                            c = -q[j, 0] * inv * inv * inv
+                            gout[i, 0] += c * dx
+                            gout[i, 1] += c * dy
+                            gout[i, 2] += c * dz
 
 
 def near_field(tree, q, periodic=True, grad=False, leaves=None):
     """27-image direct sums (solver.py:126-224): V_near (N,K) and optionally
     grad V_near (N,3) for column 0, canonical order.  `leaves` restricts the
-    targets (timing samples only)."""
+    targets (timing samples only).  Parallel numba loop over target leaves
+    (each leaf's sums run serially, so results do not depend on threads)."""
     pos = tree["positions"]
     box = tree["box"]
-    idx, valid, nleaf = _padded_leaves(tree)
-    tl = np.arange(nleaf) if leaves is None else np.asarray(leaves)
-    nk = q.shape[1]
-    v = np.zeros((pos.shape[0], nk))
-    g = np.zeros((pos.shape[0], 3)) if grad else None
-    rows = range(27) if periodic else (13,)
-    for c0 in range(0, tl.size, 2048):
-        tb = tl[c0:c0 + 2048]
-        ti, tv = idx[tb], valid[tb]
-        tp = pos[ti]  # (B,W,3)
-        acc = np.zeros(ti.shape + (nk,))
-        gacc = np.zeros(ti.shape + (3,)) if grad else None
+    nleaf = tree["leaf_start"].size - 1
+    v = np.zeros((pos.shape[0], q.shape[1]))
+    g = np.zeros((pos.shape[0], 3))
+    rows = np.arange(27) if periodic else np.array([13])
+    targets = np.arange(nleaf) if leaves is None else np.asarray(leaves, np.int64)
+    if _nb is not None:
+        _p2p_numba(pos, tree["leaf_start"], tree["nb_box"], (tree["nb_shift"] * box).astype(np.float64),
+                   np.ascontiguousarray(q, dtype=np.float64), rows, targets, bool(grad), v, g)
+        return v, (g if grad else None)
+    start = tree["leaf_start"]
+    for b in targets:  # plain numpy fallback (solver.py:144-161)
+        t0, t1 = start[b], start[b + 1]
+        if t1 == t0:
+            continue
         for t in rows:
-            sb = tree["nb_box"][tb, t]
-            si, sv = idx[sb], valid[sb]
-            sp = pos[si] + (tree["nb_shift"][tb, t] * box)[:, None, :]
-            d = tp[:, :, None, :] - sp[:, None, :, :]
+            s = tree["nb_box"][b, t]
+            s0, s1 = start[s], start[s + 1]
+            if s1 == s0:
+                continue
+            d = pos[t0:t1, None, :] - (pos[None, s0:s1, :] + tree["nb_shift"][b, t] * box)
             r2 = (d * d).sum(-1)
-            mask = tv[:, :, None] & sv[:, None, :]
             if t == 13:
-                mask = mask & (ti[:, :, None] != si[:, None, :])
-            with np.errstate(divide="ignore", invalid="ignore"):
-                inv = np.where(mask, 1.0 / np.sqrt(np.where(mask, r2, 1.0)), 0.0)
-            qs = q[si] * sv[:, :, None]
-            acc += np.einsum("bts,bsk->btk", inv, qs)
+                np.fill_diagonal(r2, np.inf)
+            inv = 1.0 / np.sqrt(r2)
+            v[t0:t1] += inv @ q[s0:s1]
             if grad:
-                gacc += np.einsum("btsd,bts,bs->btd", d, -inv ** 3, qs[:, :, 0])
-        v[ti[tv]] = acc[tv]
-        if grad:
-            g[ti[tv]] = gacc[tv]
-    return v, g
+                g[t0:t1] += np.einsum("tsd,ts,s->td", d, -inv ** 3, q[s0:s1, 0])
+    return v, (g if grad else None)
 
 
 # ------------------------------------------------------------- far field ----
@@ -355,8 +378,15 @@ def upward(tree, q, p, leaves=None):
     return mult
 
 
-def downward(tree, mult, p, root_local, boxes_fraction=None):
-    """L2L + parity-grouped M2L per level (solver.py:262-291)."""
+def m2l_level_ops(p, size):
+    """Per-level operator table: irregular vectors of the 316 offsets at the
+    level scale (solver.py:120-123) gathered into B matrices (harmonics.py:196)."""
+    iv = irregular(M2L_OFF * size, 2 * p)
+    return [m2l_from_iv(iv[row], p) for row in range(M2L_OFF.shape[0])]
+
+
+def downward(tree, mult, p, root_local, boxes_fraction=None, ops=None, pairs=None):
+    """L2L + offset-grouped M2L per level (solver.py:262-291)."""
     d = tree["depth"]
     nc = ncoef(p)
     nk = mult[0].shape[2]
@@ -372,15 +402,15 @@ def downward(tree, mult, p, root_local, boxes_fraction=None):
             op = l2l_op((OCT[o] - 0.5) * size, p)
             ci = flat(2 * pg + OCT[o], n)
             cur[:, ci, :] = (op @ loc[l - 1].reshape(nc, -1)).reshape(nc, -1, nk)
-        iv = irregular(M2L_OFF * size, 2 * p)
+        lops = ops[l] if ops is not None else m2l_level_ops(p, size)
         lim = None if boxes_fraction is None else max(1, int(math.ceil(boxes_fraction * n ** 3)))
-        for row, t, s in m2l_pairs(l):
+        for row, t, s in (pairs[l] if pairs is not None else m2l_pairs(l)):
             if lim is not None:
                 keep = t < lim
                 t, s = t[keep], s[keep]
                 if t.size == 0:
                     continue
-            op = m2l_from_iv(iv[row], p)
+            op = lops[row]
             cur[:, t, :] += (op @ mult[l][:, s, :].reshape(nc, -1)).reshape(nc, t.size, nk)
         loc[l] = cur
     return loc
@@ -582,40 +612,66 @@ def direct_potentials(positions, charges, box, shell_cap=0):
 
 # --------------------------------------------------- timed CPU sample ----
 def timed_step_sample(positions, charges, box, sites, lam_values, cfg, fraction, clock):
-    """Time one full step (tree + scale + solve + forces + HI) with the
-    per-target stages (P2P, P2M, L2P, M2L/L2L) restricted to the first
-    `fraction` of leaves / boxes; returns (extrapolated seconds, parts).
-    Whole-system stages (tree, M2M, lattice, HI) run in full."""
+    """Time one full step (tree + scale + solve + forces + HI) on a bounded
+    sample and extrapolate to the whole system.
+
+    Whole-system stages (tree + lists + charge scaling, M2L operator tables,
+    lattice, HI) run in full.  Per-target stages (P2P, P2M, M2L+L2L, L2P) run
+    on the first `fraction` and `2*fraction` of leaves / boxes; the two
+    timings fix a linear model t(f) = a + b f whose value at f = 1 is the
+    extrapolated stage time (the intercept keeps per-call overheads from
+    being scaled up).  Returns (seconds per step, parts)."""
     parts = {}
     t0 = clock()
     pos = wrap(np.atleast_2d(positions), box)
     tree = build_tree(pos, box, cfg["depth"])
+    pairs = {l: m2l_pairs(l) for l in range(1, cfg["depth"] + 1)}  # lists are part of build_octree
     q = np.array(charges, np.float64, copy=True)
     for (idx, forms), lams in zip(sites, lam_values):
         q[idx] = weights(lams) @ forms
-    parts["tree+scale"] = (clock() - t0, 1.0)
+    parts["tree+scale"] = clock() - t0
     qs = q[tree["perm"]][:, None]
     nleaf = 8 ** cfg["depth"]
-    leaves = np.arange(max(1, int(math.ceil(fraction * nleaf))))
-    f_eff = leaves.size / nleaf
     t0 = clock()
-    near_field(tree, qs, cfg["periodic_near"], grad=True, leaves=leaves)
-    parts["p2p"] = (clock() - t0, f_eff)
-    t0 = clock()
-    mult = upward(tree, qs, cfg["p"], leaves=leaves)
-    parts["p2m+m2m"] = (clock() - t0, f_eff)
-    t0 = clock()
+    ops = {l: m2l_level_ops(cfg["p"], box / 2 ** l) for l in range(1, cfg["depth"] + 1)}
     lat = lattice_matrix(cfg, box)
-    root_local = None if lat is None else lat @ mult[0][:, 0, :]
-    loc = downward(tree, mult, cfg["p"], root_local, boxes_fraction=fraction)
-    parts["m2l+l2l"] = (clock() - t0, max(fraction, 1.0 / nleaf))
+    parts["m2l operators+lattice"] = clock() - t0
+
+    def fit(run):
+        ts = []
+        fs = []
+        for f in (fraction, 2 * fraction):
+            f = min(1.0, f)
+            t0 = clock()
+            run(f)
+            ts.append(clock() - t0)
+            fs.append(f)
+        if fs[1] == fs[0]:
+            return ts[1]
+        b = max(0.0, (ts[1] - ts[0]) / (fs[1] - fs[0]))
+        a = max(0.0, ts[0] - b * fs[0])
+        return a + b
+
+    def leaves_of(f):
+        return np.arange(max(1, int(math.ceil(f * nleaf))))
+
+    state = {}
+    parts["p2p"] = fit(lambda f: near_field(tree, qs, cfg["periodic_near"], grad=True, leaves=leaves_of(f)))
+
+    def up(f):
+        state["mult"] = upward(tree, qs, cfg["p"], leaves=leaves_of(f))
+
+    parts["p2m+m2m"] = fit(up)
+
+    def down(f):
+        mult = state["mult"]
+        root_local = None if lat is None else lat @ mult[0][:, 0, :]
+        state["loc"] = downward(tree, mult, cfg["p"], root_local, boxes_fraction=f, ops=ops, pairs=pairs)
+
+    parts["m2l+l2l"] = fit(down)
+    parts["l2p"] = fit(lambda f: evaluate(tree, state["loc"], cfg["p"], grad=True, leaves=leaves_of(f)))
     t0 = clock()
-    evaluate(tree, loc, cfg["p"], grad=True, leaves=leaves)
-    parts["l2p"] = (clock() - t0, f_eff)
-    t0 = clock()
-    v = np.zeros(pos.shape[0])
-    res = dict(potentials=v, energy=0.0, lattice=lat)
+    res = dict(potentials=np.zeros(pos.shape[0]), energy=0.0, lattice=lat)
     hi(positions, charges, box, sites, lam_values, cfg, solve_out=res)
-    parts["hi"] = (clock() - t0, 1.0)
-    total = sum(t / f for t, f in parts.values())
-    return total, parts
+    parts["hi"] = clock() - t0
+    return sum(parts.values()), parts

@@ -39,6 +39,7 @@ enum Stage {
   ST_M2M,
   ST_ROOT,
   ST_DOWN,
+  ST_L2L,
   ST_L2P,
   ST_FINAL,
   ST_HI,
@@ -47,7 +48,7 @@ enum Stage {
   ST_COUNT
 };
 const char* kStageNames[ST_COUNT] = {"tree",  "stage_q", "p2p",      "p2m", "m2m",   "lattice",
-                                     "m2l_l2l", "l2p",   "finalize", "hi",  "scale", "setup"};
+                                     "m2l", "l2l", "l2p",   "finalize", "hi",  "scale", "setup"};
 
 // ------------------------------------------------------------ kernels ----
 template <class T>
@@ -294,7 +295,7 @@ struct lfmm_plan {
   // tree
   DevBuf pos_in, pos_wrap, leaf_of, counts, cursor, leaf_start, bucket, perm, inv_perm, pos_sorted, leaf_sorted, xq;
   // expansions / operators
-  DevBuf mult, loc, ops_m2l, ops_m2m, ops_l2l, ops_lat, lat64t;
+  DevBuf mult, loc, partial, ops_m2l, ops_m2m, ops_l2l, ops_lat, lat64t;
   std::vector<double2> lat_unit;  // unit-box complex lattice operator (nc x nc)
   // solve work
   DevBuf q_in, qs, vnear, vfar, gnear, gfar, part, scal, epart, roots;
@@ -359,7 +360,7 @@ struct lfmm_plan {
     }
     for (auto e : free_events) cudaEventDestroy(e);
     DevBuf* bufs[] = {&pos_in, &pos_wrap, &leaf_of, &counts, &cursor, &leaf_start, &bucket, &perm,
-                      &inv_perm, &pos_sorted, &leaf_sorted, &xq, &mult, &loc, &ops_m2l, &ops_m2m,
+                      &inv_perm, &pos_sorted, &leaf_sorted, &xq, &mult, &loc, &partial, &ops_m2l, &ops_m2m,
                       &ops_l2l, &ops_lat, &lat64t, &q_in, &qs, &vnear, &vfar, &gnear, &gfar, &part,
                       &scal, &epart, &roots, &out_pot, &out_near, &out_far, &out_dip, &out_forces, &energies,
                       &dvec, &qtot, &atom_off, &atom_idx, &nforms, &form_off, &fslot_off, &form_q,
@@ -568,6 +569,48 @@ struct lfmm_plan {
     vals.release();
   }
 
+  // M2L work split: partial slots per level so that every level gets enough
+  // CTAs (small levels would otherwise run 189 terms in a single CTA)
+  int nsplit[DMAX + 2] = {0};
+  int64_t part_off[DMAX + 2] = {0};
+  int job_start[DMAX + 3] = {0};
+  void plan_m2l_split() {
+    const int target_jobs = 4 * 148 * 2;
+    int64_t off = 0;
+    int jobs = 0;
+    for (int l = 1; l <= depth; ++l) {
+      const int tiles = 8 * tiles_per_parity(l);
+      int ns = (target_jobs + tiles - 1) / tiles;
+      ns = std::max(1, std::min(MAX_SPLIT, ns));
+      nsplit[l] = ns;
+      part_off[l] = off;
+      off += (int64_t)ns << (3 * l);
+      job_start[l] = jobs;
+      jobs += tiles * ns;
+    }
+    job_start[depth + 1] = jobs;
+    partial.ensure(tsz() * ncp * std::max<int64_t>(off, 1));
+  }
+  GemmArgs gemm_base() const {
+    GemmArgs ga{};
+    ga.ncp = ncp;
+    ga.depth = depth;
+    ga.mult = mult.p;
+    ga.loc = loc.p;
+    ga.partial = partial.p;
+    ga.ops_m2l = ops_m2l.p;
+    ga.ops_m2m = ops_m2m.p;
+    ga.ops_l2l = ops_l2l.p;
+    ga.ops_lat = ops_lat.p;
+    for (int l = 0; l <= depth; ++l) {
+      ga.level_off[l] = level_off[l];
+      ga.part_off[l] = part_off[l];
+      ga.nsplit[l] = nsplit[l];
+    }
+    for (int l = 0; l <= depth + 1; ++l) ga.job_start[l] = job_start[l];
+    return ga;
+  }
+
   // ----------------------------------------------------------- tree ----
   template <class T>
   void build_tree(const double* positions, bool on_device) {
@@ -630,43 +673,34 @@ struct lfmm_plan {
           xq.as<vec4_t<T>>(), leaf_start.as<int>(), depth, p, (T)(1.0 / size), ncp, M + level_off[depth] * ncp);
     });
     const unsigned rowb = (unsigned)((ncp + GB_M - 1) / GB_M);
+    GemmArgs ga = gemm_base();
     for (int l = depth - 1; l >= 0; --l) {
-      GemmArgs ga{};
       ga.mode = GEMM_UP;
       ga.level = l;
-      ga.ncp = ncp;
-      ga.src_aux = M + level_off[l + 1] * ncp;
-      ga.dst = M + level_off[l] * ncp;
-      ga.ops_main = ops_m2m.p;
-      dim3 grid(gemm_tiles_per_class(GEMM_UP, l), rowb);
+      dim3 grid(tiles_all(l), rowb);
       launch(ST_M2M, [&] { k_gemm_gather<T><<<grid, G_THREADS, 0, stream>>>(ga); });
     }
     if (lattice_mode != LFMM_LATTICE_OFF) {
-      GemmArgs ga{};
       ga.mode = GEMM_ROOT;
       ga.level = 0;
-      ga.ncp = ncp;
-      ga.src_aux = M;
-      ga.dst = Lc;
-      ga.ops_main = ops_lat.p;
       dim3 grid(1, rowb);
       launch(ST_ROOT, [&] { k_gemm_gather<T><<<grid, G_THREADS, 0, stream>>>(ga); });
     } else {
       LFMM_CUDA(cudaMemsetAsync(Lc, 0, sizeof(T) * ncp, stream));
     }
-    for (int l = 1; l <= depth; ++l) {
-      GemmArgs ga{};
-      ga.mode = GEMM_DOWN;
-      ga.level = l;
-      ga.ncp = ncp;
-      ga.src_m2l = M + level_off[l] * ncp;
-      ga.src_aux = Lc + level_off[l - 1] * ncp;
-      ga.dst = Lc + level_off[l] * ncp;
-      ga.ops_main = ops_m2l.p;
-      ga.ops_l2l = ops_l2l.p;
-      ga.use_m2l = 1;
-      dim3 grid(8 * gemm_tiles_per_class(GEMM_DOWN, l), rowb);
+    if (depth >= 1) {
+      // M2L of every level in one launch (terms split over CTAs), then the
+      // L2L sweep adds the partial slots level by level
+      ga.mode = GEMM_M2L;
+      ga.level = 0;
+      dim3 grid(ga.job_start[depth + 1], rowb);
       launch(ST_DOWN, [&] { k_gemm_gather<T><<<grid, G_THREADS, 0, stream>>>(ga); });
+      for (int l = 1; l <= depth; ++l) {
+        ga.mode = GEMM_L2L;
+        ga.level = l;
+        dim3 g2(8 * tiles_per_parity(l), rowb);
+        launch(ST_L2L, [&] { k_gemm_gather<T><<<g2, G_THREADS, 0, stream>>>(ga); });
+      }
     }
     {
       const int per_warp = ncoef(p) + 3 * p * p;
@@ -974,6 +1008,7 @@ int lfmm_plan_create(const double* positions, int64_t n, double box_length, int 
     pl->loc.ensure(t * pl->ncp * off);
     LFMM_CUDA(cudaMemsetAsync(pl->mult.p, 0, pl->mult.bytes, pl->stream));
     LFMM_CUDA(cudaMemsetAsync(pl->loc.p, 0, pl->loc.bytes, pl->stream));
+    pl->plan_m2l_split();
     pl->scal.ensure(sizeof(double) * 8);
     pl->epart.ensure(sizeof(double) * 4);
     pl->offset_total.ensure(sizeof(double));

@@ -189,27 +189,44 @@ __global__ void __launch_bounds__(EXP_WARPS * 32) k_l2p(const vec4_t<T>* __restr
 
 // ------------------------------------------------------- gathered GEMM ----
 // dst[:, tile] = sum_terms Op_term (ncp x ncp) * src_term[:, gather(tile)]
-// Tiles hold BN targets of one level.  For the downward mode all targets of
-// a tile share one parity (= octant within the parent), hence one L2L
-// operator and one list of 189 M2L offsets (octree.py:35-38): term 0 is the
-// L2L from the parent local, terms 1..189 the M2L partners in M2L_OFFSETS
-// row order.  Upward mode: terms are the 8 children (M2M).  Root mode: one
-// term, the lattice operator on the root multipole.
-enum GemmMode { GEMM_UP = 0, GEMM_DOWN = 1, GEMM_ROOT = 2 };
+//
+// Modes (one CTA = one job: a tile of up to GB_N target boxes of one level
+// and a contiguous range of terms):
+//   UP    M2M: terms are the 8 children (solver.py:248-258)
+//   ROOT  lattice operator on the root multipole (solver.py:364-367)
+//   M2L   terms are the 189 partners of the tile's parity class, in
+//         M2L_OFFSETS row order (octree.py:35-38, :96-111); all targets of a
+//         tile share one parity, hence one offset list.  The 189 terms are
+//         split over `nsplit` CTAs writing partial slots, which keeps the
+//         small levels from serialising 189 terms in a single CTA.
+//   L2L   one term (parent local, solver.py:276-281); the epilogue adds the
+//         level's M2L partial slots in fixed slot order and writes the local.
+// Every output element is produced by exactly one thread with a fixed
+// summation order: reruns are bit identical.
+enum GemmMode { GEMM_UP = 0, GEMM_ROOT = 1, GEMM_M2L = 2, GEMM_L2L = 3 };
+
+constexpr int GB_M = 128, GB_N = 64, G_THREADS = 256;
+constexpr int MAX_SPLIT = 8;
 
 struct GemmArgs {
   int mode;
-  int level;            // target level
   int ncp;
-  const void* src_m2l;  // DOWN: multipoles of this level
-  const void* src_aux;  // UP: children multipoles (level+1); DOWN: parent locals; ROOT: root multipole
-  void* dst;
-  const void* ops_main;  // UP: M2M[8]; DOWN: M2L[316]; ROOT: lattice
-  const void* ops_l2l;   // DOWN: L2L[8]
-  int use_m2l;           // DOWN: 0 -> only the L2L term (never for level>=1 here)
+  int depth;
+  const void* mult;   // all levels, box-major, ncp per box
+  void* loc;          // all levels
+  void* partial;      // M2L partial slots
+  const void* ops_m2l;   // [316][ncp][ncp]
+  const void* ops_m2m;   // [8]
+  const void* ops_l2l;   // [8]
+  const void* ops_lat;   // [1]
+  int64_t level_off[DMAX + 2];  // box offset of each level in mult/loc
+  int64_t part_off[DMAX + 2];   // vector offset of each level's partial slots
+  int nsplit[DMAX + 2];         // partial slots per level (M2L)
+  // job decoding for M2L: cumulative job counts per level
+  int job_start[DMAX + 3];
+  int level;  // UP / L2L / ROOT: the single target level of this launch
 };
 
-constexpr int GB_M = 128, GB_N = 64, G_THREADS = 256;
 template <class T>
 struct GemmTile {
   static constexpr int BK = sizeof(T) == 4 ? 16 : 8;  // keeps smem double buffer < 48 KB
@@ -217,14 +234,11 @@ struct GemmTile {
   static constexpr int BKT = BK / 4;                   // B elements per thread per stage
 };
 
-__host__ __device__ inline int gemm_tiles_per_class(int mode, int level) {
-  if (mode == GEMM_DOWN) {
-    const int sub = 1 << (level - 1);
-    return (sub * sub * sub + GB_N - 1) / GB_N;
-  }
-  if (mode == GEMM_UP) return ((1 << (3 * level)) + GB_N - 1) / GB_N;
-  return 1;
+__host__ __device__ inline int tiles_per_parity(int level) {
+  const int sub = 1 << (level - 1);
+  return (sub * sub * sub + GB_N - 1) / GB_N;
 }
+__host__ __device__ inline int tiles_all(int level) { return ((1 << (3 * level)) + GB_N - 1) / GB_N; }
 
 // vector load of N consecutive T (16-B aligned)
 template <class T, int N>
@@ -247,6 +261,14 @@ __device__ __forceinline__ void ldv(const T* __restrict__ p, T (&r)[N]) {
   }
 }
 
+// box index of the q-th target of parity `par` at `level`
+__device__ __forceinline__ int parity_box(int level, int par, int q) {
+  const int lsub = level - 1, sub = 1 << lsub;
+  const int qx = q >> (2 * lsub), qy = (q >> lsub) & (sub - 1), qz = q & (sub - 1);
+  const int gx = 2 * qx + ((par >> 2) & 1), gy = 2 * qy + ((par >> 1) & 1), gz = 2 * qz + (par & 1);
+  return (gx << (2 * level)) | (gy << level) | gz;
+}
+
 template <class T>
 __global__ void __launch_bounds__(G_THREADS) k_gemm_gather(GemmArgs g) {
   constexpr int BK = GemmTile<T>::BK, AK = GemmTile<T>::AK, BKT = GemmTile<T>::BKT;
@@ -256,46 +278,46 @@ __global__ void __launch_bounds__(G_THREADS) k_gemm_gather(GemmArgs g) {
   const int tid = threadIdx.x;
   const int ncp = g.ncp;
   const int row0 = blockIdx.y * GB_M;
-  const int level = g.level;
-  const int nside = 1 << level, msk = nside - 1;
 
-  // ---- which targets does this tile hold, and how many terms? ----
-  int par = 0, nterm = 1;
-  if (g.mode == GEMM_DOWN) {
-    const int tpc = gemm_tiles_per_class(GEMM_DOWN, level);
-    par = blockIdx.x / tpc;
-    const int q0 = (blockIdx.x % tpc) * GB_N;
-    const int sub = nside >> 1;
-    const int ntarget = min(GB_N, sub * sub * sub - q0);
-    nterm = 1 + (g.use_m2l ? NM2L : 0);
-    if (tid < GB_N) {
-      int box = -1;
-      if (tid < ntarget) {
-        const int q = q0 + tid;
-        const int lsub = level - 1;
-        const int qx = q >> (2 * lsub), qy = (q >> lsub) & (sub - 1), qz = q & (sub - 1);
-        const int gx = 2 * qx + ((par >> 2) & 1), gy = 2 * qy + ((par >> 1) & 1), gz = 2 * qz + (par & 1);
-        box = (gx << (2 * level)) | (gy << level) | gz;
-      }
-      col_dst[tid] = box;
-    }
+  // ---- decode the job ----
+  int level = g.level, par = 0, t0 = 0, t1 = 1, slot = -1;
+  if (g.mode == GEMM_M2L) {
+    level = 1;
+    while (level < g.depth && (int)blockIdx.x >= g.job_start[level + 1]) ++level;
+    const int j = blockIdx.x - g.job_start[level];
+    const int ns = g.nsplit[level];
+    const int tpp = tiles_per_parity(level);
+    slot = j % ns;
+    const int tile = j / ns;
+    par = tile / tpp;
+    const int q0 = (tile % tpp) * GB_N;
+    const int sub = 1 << (level - 1);
+    if (tid < GB_N) col_dst[tid] = (q0 + tid < sub * sub * sub) ? parity_box(level, par, q0 + tid) : -1;
+    t0 = (NM2L * slot) / ns;
+    t1 = (NM2L * (slot + 1)) / ns;
+  } else if (g.mode == GEMM_L2L) {
+    const int tpp = tiles_per_parity(level);
+    par = blockIdx.x / tpp;
+    const int q0 = (blockIdx.x % tpp) * GB_N;
+    const int sub = 1 << (level - 1);
+    if (tid < GB_N) col_dst[tid] = (q0 + tid < sub * sub * sub) ? parity_box(level, par, q0 + tid) : -1;
   } else if (g.mode == GEMM_UP) {
     const int q0 = blockIdx.x * GB_N;
-    const int ntarget = min(GB_N, (1 << (3 * level)) - q0);
-    nterm = 8;
-    if (tid < GB_N) col_dst[tid] = tid < ntarget ? q0 + tid : -1;
-  } else {
-    nterm = 1;
+    if (tid < GB_N) col_dst[tid] = (q0 + tid < (1 << (3 * level))) ? q0 + tid : -1;
+    t1 = 8;
+  } else {  // ROOT
     if (tid < GB_N) col_dst[tid] = tid == 0 ? 0 : -1;
   }
   __syncthreads();
 
+  const int nside = 1 << level, msk = nside - 1;
   const int nk = ncp / BK;
-  const int niter = nterm * nk;
+  const int niter = (t1 - t0) * nk;
 
-  // loader mapping: A tile GB_M rows x BK k, B tile BK k x GB_N columns
-  const int a_row = tid >> 1, a_k = (tid & 1) * AK;
-  const int b_col = tid >> 2, b_k = (tid & 3) * BKT;
+  // loader mapping (conflict-free smem stores): A: 128 consecutive rows per
+  // k-group, B: 64 consecutive target columns per k-group
+  const int a_row = tid & (GB_M - 1), a_k = (tid >> 7) * AK;
+  const int b_col = tid & (GB_N - 1), b_k = (tid >> 6) * BKT;
   // compute mapping: 16 x 16 threads, 8 rows (two groups of 4) x 4 columns
   const int ty = tid >> 4, tx = tid & 15;
 
@@ -310,48 +332,48 @@ __global__ void __launch_bounds__(G_THREADS) k_gemm_gather(GemmArgs g) {
   const T* Bb = nullptr;
   int cur_term = -1, my_src = -1;
   const int tgt = col_dst[b_col];
+  const T* mult = reinterpret_cast<const T*>(g.mult);
+  const T* loc = reinterpret_cast<const T*>(g.loc);
 
   auto term_setup = [&](int term) {
     int src_box = -1;
-    if (g.mode == GEMM_DOWN) {
-      if (term == 0) {  // L2L from the parent (same octant for the whole tile)
-        Ab = reinterpret_cast<const T*>(g.ops_l2l) + (size_t)par * ncp * ncp;
-        Bb = reinterpret_cast<const T*>(g.src_aux);
-        if (tgt >= 0) {
-          const int pl = level - 1;
-          const int gx = (tgt >> (2 * level)) >> 1, gy = ((tgt >> level) & msk) >> 1, gz = (tgt & msk) >> 1;
-          src_box = (gx << (2 * pl)) | (gy << pl) | gz;
-        }
-      } else {  // M2L partner term-1 of this parity class
-        const int s = term - 1;
-        const char4 o = c_m2l_off[par * NM2L + s];
-        const int row = c_m2l_row[par * NM2L + s];
-        Ab = reinterpret_cast<const T*>(g.ops_main) + (size_t)row * ncp * ncp;
-        Bb = reinterpret_cast<const T*>(g.src_m2l);
-        if (tgt >= 0) {
-          const int gx = tgt >> (2 * level), gy = (tgt >> level) & msk, gz = tgt & msk;
-          src_box = ((((gx + o.x) & msk) << level | ((gy + o.y) & msk)) << level) | ((gz + o.z) & msk);
-        }
+    if (g.mode == GEMM_M2L) {
+      const char4 o = c_m2l_off[par * NM2L + term];
+      const int row = c_m2l_row[par * NM2L + term];
+      Ab = reinterpret_cast<const T*>(g.ops_m2l) + (size_t)row * ncp * ncp;
+      Bb = mult + g.level_off[level] * ncp;
+      if (tgt >= 0) {
+        const int gx = tgt >> (2 * level), gy = (tgt >> level) & msk, gz = tgt & msk;
+        src_box = ((((gx + o.x) & msk) << level | ((gy + o.y) & msk)) << level) | ((gz + o.z) & msk);
       }
-    } else if (g.mode == GEMM_UP) {  // M2M from child octant `term`
-      Ab = reinterpret_cast<const T*>(g.ops_main) + (size_t)term * ncp * ncp;
-      Bb = reinterpret_cast<const T*>(g.src_aux);
+    } else if (g.mode == GEMM_L2L) {
+      Ab = reinterpret_cast<const T*>(g.ops_l2l) + (size_t)par * ncp * ncp;
+      Bb = loc + g.level_off[level - 1] * ncp;
+      if (tgt >= 0) {
+        const int pl = level - 1;
+        const int gx = (tgt >> (2 * level)) >> 1, gy = ((tgt >> level) & msk) >> 1, gz = (tgt & msk) >> 1;
+        src_box = (gx << (2 * pl)) | (gy << pl) | gz;
+      }
+    } else if (g.mode == GEMM_UP) {
+      Ab = reinterpret_cast<const T*>(g.ops_m2m) + (size_t)term * ncp * ncp;
+      Bb = mult + g.level_off[level + 1] * ncp;
       if (tgt >= 0) {
         const int cl = level + 1;
         const int gx = tgt >> (2 * level), gy = (tgt >> level) & msk, gz = tgt & msk;
         const int cx = 2 * gx + ((term >> 2) & 1), cy = 2 * gy + ((term >> 1) & 1), cz = 2 * gz + (term & 1);
         src_box = (cx << (2 * cl)) | (cy << cl) | cz;
       }
-    } else {  // lattice operator on the root multipole
-      Ab = reinterpret_cast<const T*>(g.ops_main);
-      Bb = reinterpret_cast<const T*>(g.src_aux);
+    } else {
+      Ab = reinterpret_cast<const T*>(g.ops_lat);
+      Bb = mult;
       if (tgt >= 0) src_box = 0;
     }
     return src_box;
   };
 
   auto load_regs = [&](int it) {
-    const int term = it / nk, kc = it - term * nk;
+    const int tl = it / nk, kc = it - tl * nk;
+    const int term = t0 + tl;
     if (term != cur_term) {
       my_src = term_setup(term);
       cur_term = term;
@@ -378,8 +400,10 @@ __global__ void __launch_bounds__(G_THREADS) k_gemm_gather(GemmArgs g) {
     for (int u = 0; u < BKT; ++u) Bs[buf][b_k + u][b_col] = rb[u];
   };
 
-  load_regs(0);
-  store_smem(0);
+  if (niter > 0) {
+    load_regs(0);
+    store_smem(0);
+  }
   __syncthreads();
   for (int it = 0; it < niter; ++it) {
     const int buf = it & 1;
@@ -402,8 +426,21 @@ __global__ void __launch_bounds__(G_THREADS) k_gemm_gather(GemmArgs g) {
     __syncthreads();
   }
 
-  // ---- epilogue: overwrite the target coefficients ----
-  T* dst = reinterpret_cast<T*>(g.dst);
+  // ---- epilogue ----
+  T* out;
+  size_t out_base;
+  if (g.mode == GEMM_M2L) {
+    out = reinterpret_cast<T*>(g.partial);
+    out_base = (size_t)(g.part_off[level] + (int64_t)slot * (1LL << (3 * level)));
+  } else if (g.mode == GEMM_UP) {
+    out = const_cast<T*>(mult);
+    out_base = (size_t)g.level_off[level];
+  } else {
+    out = reinterpret_cast<T*>(g.loc);
+    out_base = (size_t)g.level_off[level];
+  }
+  const T* part = reinterpret_cast<const T*>(g.partial);
+  const int ns = (g.mode == GEMM_L2L) ? g.nsplit[level] : 0;
 #pragma unroll
   for (int j = 0; j < 4; ++j) {
     const int col = tx * 4 + j;
@@ -412,7 +449,11 @@ __global__ void __launch_bounds__(G_THREADS) k_gemm_gather(GemmArgs g) {
 #pragma unroll
     for (int i = 0; i < 8; ++i) {
       const int r = row0 + (i < 4 ? ty * 4 + i : 64 + ty * 4 + (i - 4));
-      if (r < ncp) dst[(size_t)box * ncp + r] = acc[i][j];
+      if (r >= ncp) continue;
+      T v = acc[i][j];
+      for (int s = 0; s < ns; ++s)  // M2L partial slots, fixed order
+        v += part[((size_t)g.part_off[level] + (size_t)s * (1u << (3 * level)) + box) * ncp + r];
+      out[(out_base + box) * ncp + r] = v;
     }
   }
 }
