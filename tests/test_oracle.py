@@ -1,0 +1,148 @@
+"""The CPU oracle pinned against the reference: golden fixtures produced by
+running the reference itself (tests/golden/make_golden.py) and the
+reference tests' known-answer values (pkg/tests/test_{oracle,lattice,weights}.py)."""
+
+import math
+
+import numpy as np
+import pytest
+
+from conftest import relerr
+from oracle import lfmm_oracle as orc
+
+
+def cfg_of(g):
+    return orc.default_config(p=int(g["p"]), depth=int(g["depth"]), lattice_mode=str(g["lattice_mode"]),
+                              shell_cap=int(g["shell_cap"]), dipole=bool(g["dipole"]),
+                              periodic_near=bool(g["periodic_near"]) if "periodic_near" in g else True)
+
+
+@pytest.mark.parametrize("name", ["tree_d1.npz", "tree_d3.npz"])
+def test_oracle_tree_bit_exact(golden, name):
+    g = golden(name)
+    t = orc.build_tree(orc.wrap(g["positions"], float(g["box"])), float(g["box"]), int(g["depth"]))
+    for key in ("perm", "inv_perm", "leaf_start", "leaf_of_particle", "nb_box", "nb_shift"):
+        assert np.array_equal(t[key], g[key]), key
+    assert t["positions"].tobytes() == g["positions_sorted"].tobytes()
+    for l in range(1, int(g["depth"]) + 1):
+        pairs = orc.m2l_pairs(l)
+        assert np.array_equal([r for r, _, _ in pairs], g[f"m2l{l}_rows"])
+        assert np.array_equal(np.concatenate([t_ for _, t_, _ in pairs]), g[f"m2l{l}_targets"])
+        assert np.array_equal(np.concatenate([s for _, _, s in pairs]), g[f"m2l{l}_sources"])
+
+
+@pytest.mark.parametrize("name", ["solve_d0_off.npz", "solve_d2_conv_p9.npz", "solve_d1_shells_p16.npz",
+                                  "solve_d0_conv_p14.npz", "solve_multi_rhs.npz", "solve_c1_water.npz"])
+def test_oracle_solve_matches_reference(golden, name):
+    g = golden(name)
+    forces = "forces" in g
+    r = orc.solve(g["positions"], g["charges"], float(g["box"]), cfg_of(g), forces=forces)
+    tol = 1e-11
+    for a, b in (("potentials", "potentials"), ("near", "near"), ("far", "far"), ("dip", "dip"),
+                 ("energy", "energy"), ("near_energy", "near_energy"), ("far_energy", "far_energy"),
+                 ("dipole_energy", "dipole_energy"), ("root_multipole", "root_multipole"),
+                 ("dipole_vector", "dipole_vector"), ("total_charge", "total_charge")):
+        assert relerr(r[a], g[b]) <= tol, a
+    if "lattice_matrix" in g:
+        assert relerr(r["lattice"], g["lattice_matrix"]) <= 1e-12
+    if forces:
+        assert relerr(r["forces"], g["forces"]) <= tol
+
+
+def _sites(g):
+    off, nf, forms = g["site_atom_offsets"], g["site_nforms"], g["site_forms"]
+    out, fo = [], 0
+    for s in range(len(nf)):
+        ns = int(off[s + 1] - off[s])
+        out.append((g["site_atoms"][off[s]:off[s + 1]], forms[fo:fo + nf[s] * ns].reshape(nf[s], ns)))
+        fo += nf[s] * ns
+    lam, lo = [], 0
+    for n in g["n_lambda"]:
+        lam.append(g["lambdas"][lo:lo + n])
+        lo += n
+    return out, lam
+
+
+@pytest.mark.parametrize("name", ["hi_c1_water.npz", "hi_small_conv.npz", "hi_small_minimum.npz",
+                                  "hi_small_nodip_shells.npz"])
+def test_oracle_hi_matches_reference(golden, name):
+    g = golden(name)
+    sites, lam = _sites(g)
+    cfg = orc.default_config(p=int(g["p"]), depth=int(g["depth"]), lattice_mode=str(g["lattice_mode"]),
+                             shell_cap=int(g["shell_cap"]), dipole=bool(g["dipole"]),
+                             intra_site_images=str(g["intra"]))
+    r = orc.hi(g["positions"], g["charges"], float(g["box"]), sites, lam, cfg)
+    assert relerr(r["energy"], g["hi_energy"]) <= 1e-11
+    assert relerr(np.concatenate(r["forces"]), g["hi_forces"]) <= 1e-10
+    assert relerr(np.concatenate(r["c_p2p"]), g["c_p2p"]) <= 1e-12
+    assert relerr(np.array(r["blend"]), g["blend"]) <= 1e-12
+    rq = orc.hi(g["positions"], g["charges"], float(g["box"]), sites, lam, cfg, mode="qi")
+    assert relerr(np.concatenate(rq["forces"]), g["qi_forces"]) <= 1e-10
+
+
+# ---- known answers from the reference's own tests ----
+def test_direct_pair():
+    # pkg/tests/test_oracle.py:19-24
+    pos = np.array([[0.0, 0.0, 0.0], [0.5, 0.0, 0.0]])
+    v = orc.direct_potentials(pos, np.array([1.0, -1.0]), 100.0, shell_cap=0)
+    assert abs(0.5 * (1.0 * v[0] - 1.0 * v[1]) - (-2.0)) < 1e-14
+
+
+def test_unit_box_pair_shell10():
+    # pkg/tests/test_oracle.py:27-32
+    pos = np.array([[0.25, 0.5, 0.5], [0.75, 0.5, 0.5]])
+    q = np.array([1.0, -1.0])
+    v = orc.direct_potentials(pos, q, 1.0, shell_cap=10)
+    e = 0.5 * math.fsum((q * v).tolist())
+    assert abs(e - (-2.217620929771452)) < 1e-12
+
+
+def test_self_image_sum():
+    # pkg/tests/test_corrections.py:84-91
+    pos = np.random.default_rng(0).uniform(0, 3.0, (4, 3))
+    k = orc.near_kernel(pos, 3.0)
+    assert np.allclose(np.diag(k), (6.0 + 12.0 / np.sqrt(2.0) + 8.0 / np.sqrt(3.0)) / 3.0, rtol=1e-13)
+
+
+def test_weights_known_values():
+    # pkg/tests/test_weights.py:18-32
+    assert np.allclose(orc.weights([0.345]), [0.655, 0.345], rtol=0, atol=1e-15)
+    assert np.allclose(orc.weights([0.345, 0.721]), [0.182745, 0.096255, 0.472255, 0.248745], rtol=0, atol=1e-15)
+    assert np.allclose(orc.weight_grads([0.345, 0.721])[0], [-0.279, 0.279, -0.721, 0.721], atol=1e-15)
+
+
+def test_harmonics_closed_forms():
+    # pkg/tests/test_harmonics.py:28-39 (p = 2 closed forms)
+    x, y, z = 0.3, -0.2, 0.7
+    r = orc.regular([[x, y, z]], 2)[0]
+    assert np.isclose(r[orc.cidx(1, 0)], z)
+    assert np.isclose(r[orc.cidx(1, 1)], 0.5 * (x + 1j * y))
+    assert np.isclose(r[orc.cidx(2, 0)], (3 * z * z - (x * x + y * y + z * z)) / 4.0, rtol=1e-12)
+    assert np.isclose(r[orc.cidx(2, 2)], (x + 1j * y) ** 2 / 8.0, rtol=1e-12)
+    irr = orc.irregular([[x, y, z]], 2)[0]
+    rr = math.sqrt(x * x + y * y + z * z)
+    assert np.isclose(irr[0], 1.0 / rr)
+    assert np.isclose(irr[orc.cidx(1, 0)], z / rr ** 3)
+
+
+def test_p2m_far_potential_matches_direct():
+    # pkg/tests/test_harmonics.py:42-51: multipole far field vs direct sum
+    g = np.random.default_rng(3)
+    src = g.uniform(-0.3, 0.3, (12, 3))
+    q = g.uniform(-1, 1, 12)
+    m = (orc.regular(src, 20) * q[:, None]).sum(0)
+    tgt = np.array([[2.0, 1.5, -1.0]])
+    far = np.real(np.conj(orc.irregular(tgt, 20)[0]) @ m)
+    direct = np.sum(q / np.linalg.norm(tgt - src, axis=1))
+    assert abs(far - direct) <= 1e-12 * abs(direct)
+
+
+@pytest.mark.slow
+def test_oracle_madelung():
+    # pkg/tests/test_lattice.py:76-91
+    box = 2.0
+    grid = np.stack(np.meshgrid([0, 1], [0, 1], [0, 1], indexing="ij"), axis=-1).reshape(-1, 3)
+    pos = (grid + 0.25) * (box / 2)
+    q = np.where(grid.sum(axis=1) % 2 == 0, 1.0, -1.0)
+    r = orc.solve(pos, q, box, orc.default_config(p=22, depth=0))
+    assert abs(r["energy"] - (-8.0 * 1.7475645946331822 / box)) <= 1e-10 * 8 * 1.7475645946331822 / box
