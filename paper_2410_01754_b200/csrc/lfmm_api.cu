@@ -10,6 +10,7 @@
 #include <algorithm>
 #include <array>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <map>
 #include <memory>
@@ -21,6 +22,7 @@
 #include "lfmm_common.cuh"
 #include "lfmm_expansions.cuh"
 #include "lfmm_hi.cuh"
+#include "lfmm_m2l_tc.cuh"
 #include "lfmm_p2p.cuh"
 #include "lfmm_setup.cuh"
 #include "lfmm_tree.cuh"
@@ -295,6 +297,8 @@ struct lfmm_plan {
   // tree
   DevBuf pos_in, pos_wrap, leaf_of, counts, cursor, leaf_start, bucket, perm, inv_perm, pos_sorted, leaf_sorted, xq;
   // expansions / operators
+  bool use_tc = false;  // M2L on tcgen05 (fp32, (p+1)^2 <= 128)
+  DevBuf ops_tc;
   DevBuf mult, loc, partial, ops_m2l, ops_m2m, ops_l2l, ops_lat, lat64t;
   std::vector<double2> lat_unit;  // unit-box complex lattice operator (nc x nc)
   // solve work
@@ -360,7 +364,7 @@ struct lfmm_plan {
     }
     for (auto e : free_events) cudaEventDestroy(e);
     DevBuf* bufs[] = {&pos_in, &pos_wrap, &leaf_of, &counts, &cursor, &leaf_start, &bucket, &perm,
-                      &inv_perm, &pos_sorted, &leaf_sorted, &xq, &mult, &loc, &partial, &ops_m2l, &ops_m2m,
+                      &inv_perm, &pos_sorted, &leaf_sorted, &xq, &mult, &loc, &partial, &ops_tc, &ops_m2l, &ops_m2m,
                       &ops_l2l, &ops_lat, &lat64t, &q_in, &qs, &vnear, &vfar, &gnear, &gfar, &part,
                       &scal, &epart, &roots, &out_pot, &out_near, &out_far, &out_dip, &out_forces, &energies,
                       &dvec, &qtot, &atom_off, &atom_idx, &nforms, &form_off, &fslot_off, &form_q,
@@ -564,6 +568,14 @@ struct lfmm_plan {
       LFMM_CUDA(cudaStreamSynchronize(stream));
       l64.release();
     }
+    if (use_tc) {
+      ops_tc.ensure((size_t)NOFF * TC_NCHUNK * TC_STAGE);
+      const int64_t total = (int64_t)NOFF * TC_M * TC_M;
+      launch(ST_SETUP, [&] {
+        k_tc_arrange_ops<<<nblk(total, 256), 256, 0, stream>>>(ops_m2l.as<float>(), ops_tc.as<float>(), NOFF);
+      });
+      LFMM_CUDA(cudaFuncSetAttribute(k_m2l_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, TC_SMEM));
+    }
     LFMM_CUDA(cudaStreamSynchronize(stream));
     vecs.release();
     vals.release();
@@ -575,11 +587,11 @@ struct lfmm_plan {
   int64_t part_off[DMAX + 2] = {0};
   int job_start[DMAX + 3] = {0};
   void plan_m2l_split() {
-    const int target_jobs = 4 * 148 * 2;
+    const int target_jobs = use_tc ? 4 * 148 : 4 * 148 * 2;
     int64_t off = 0;
     int jobs = 0;
     for (int l = 1; l <= depth; ++l) {
-      const int tiles = 8 * tiles_per_parity(l);
+      const int tiles = 8 * (use_tc ? tc_tiles_per_parity(l) : tiles_per_parity(l));
       int ns = (target_jobs + tiles - 1) / tiles;
       ns = std::max(1, std::min(MAX_SPLIT, ns));
       nsplit[l] = ns;
@@ -691,10 +703,25 @@ struct lfmm_plan {
     if (depth >= 1) {
       // M2L of every level in one launch (terms split over CTAs), then the
       // L2L sweep adds the partial slots level by level
-      ga.mode = GEMM_M2L;
-      ga.level = 0;
-      dim3 grid(ga.job_start[depth + 1], rowb);
-      launch(ST_DOWN, [&] { k_gemm_gather<T><<<grid, G_THREADS, 0, stream>>>(ga); });
+      if (use_tc && sizeof(T) == 4) {
+        TcArgs ta{};
+        ta.mult = reinterpret_cast<const float*>(mult.p);
+        ta.partial = reinterpret_cast<float*>(partial.p);
+        ta.ops_tc = ops_tc.as<float>();
+        ta.depth = depth;
+        for (int l = 0; l <= depth; ++l) {
+          ta.level_off[l] = level_off[l];
+          ta.part_off[l] = part_off[l];
+          ta.nsplit[l] = nsplit[l];
+        }
+        for (int l = 0; l <= depth + 1; ++l) ta.job_start[l] = job_start[l];
+        launch(ST_DOWN, [&] { k_m2l_tc<<<job_start[depth + 1], 128, TC_SMEM, stream>>>(ta); });
+      } else {
+        ga.mode = GEMM_M2L;
+        ga.level = 0;
+        dim3 grid(ga.job_start[depth + 1], rowb);
+        launch(ST_DOWN, [&] { k_gemm_gather<T><<<grid, G_THREADS, 0, stream>>>(ga); });
+      }
       for (int l = 1; l <= depth; ++l) {
         ga.mode = GEMM_L2L;
         ga.level = l;
@@ -980,6 +1007,12 @@ int lfmm_plan_create(const double* positions, int64_t n, double box_length, int 
     pl->fp32 = (flags & LFMM_F_FP32) != 0;
     pl->nc = ncoef(p);
     pl->ncp = ncpad(p);
+    {
+      const char* env = std::getenv("LFMM_M2L");
+      const bool force_simt = env && std::string(env) == "simt";
+      pl->use_tc = pl->fp32 && depth >= 1 && pl->nc > 64 && pl->nc <= 128 && !force_simt;
+      if (pl->use_tc) pl->ncp = 128;
+    }
     pl->nleaf = 1 << (3 * depth);
     pl->size = box_length / double(1 << depth);
     LFMM_CUDA(cudaStreamCreateWithFlags(&pl->own_stream, cudaStreamNonBlocking));

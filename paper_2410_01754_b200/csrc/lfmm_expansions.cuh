@@ -206,7 +206,7 @@ __global__ void __launch_bounds__(EXP_WARPS * 32) k_l2p(const vec4_t<T>* __restr
 enum GemmMode { GEMM_UP = 0, GEMM_ROOT = 1, GEMM_M2L = 2, GEMM_L2L = 3 };
 
 constexpr int GB_M = 128, GB_N = 64, G_THREADS = 256;
-constexpr int MAX_SPLIT = 8;
+constexpr int MAX_SPLIT = 16;
 
 struct GemmArgs {
   int mode;
