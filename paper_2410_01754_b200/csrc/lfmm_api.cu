@@ -53,10 +53,50 @@ const char* kStageNames[ST_COUNT] = {"tree",  "stage_q", "p2p",      "p2m", "m2m
                                      "m2l", "l2l", "l2p",   "finalize", "hi",  "scale", "setup"};
 
 // ------------------------------------------------------------ kernels ----
+// Fixed-order reduction of NQ double-double block partials by one block.
+template <int NQ>
+__device__ void reduce_parts_dev(const dd* __restrict__ part, int nb, double* __restrict__ out) {
+  dd v[NQ];
+#pragma unroll
+  for (int q = 0; q < NQ; ++q) v[q] = dd{0, 0};
+  const int per = (nb + blockDim.x - 1) / blockDim.x;
+  const int b0 = min(nb, (int)threadIdx.x * per), b1 = min(nb, b0 + per);
+  for (int b = b0; b < b1; ++b)
+#pragma unroll
+    for (int q = 0; q < NQ; ++q) {
+      dd x;
+      x.hi = __ldcg(&part[(size_t)b * NQ + q].hi);
+      x.lo = __ldcg(&part[(size_t)b * NQ + q].lo);
+      v[q] = dd_add(v[q], x);
+    }
+  __shared__ dd res[NQ];
+  block_reduce_dd<NQ>(v, res);
+  __syncthreads();
+  if (threadIdx.x == 0)
+#pragma unroll
+    for (int q = 0; q < NQ; ++q) out[q] = res[q].hi + res[q].lo;
+}
+
+// true in exactly one block: the last to finish its partial (counter reset)
+__device__ bool last_block(int* cnt) {
+  __shared__ int is_last;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    const int old = atomicAdd(cnt, 1);
+    is_last = (old == (int)gridDim.x - 1);
+    if (is_last) *cnt = 0;
+  }
+  __syncthreads();
+  if (is_last) __threadfence();
+  return is_last != 0;
+}
+
 template <class T>
 __global__ void k_stage_q(const double* __restrict__ q, int K, int c, const int* __restrict__ perm,
                           const double* __restrict__ pos_sorted, int64_t n, double box,
-                          vec4_t<T>* __restrict__ xq, double* __restrict__ qs, dd* __restrict__ part) {
+                          vec4_t<T>* __restrict__ xq, double* __restrict__ qs, dd* __restrict__ part,
+                          int* __restrict__ cnt, double* __restrict__ scal) {
   const int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   dd v[4] = {dd{0, 0}, dd{0, 0}, dd{0, 0}, dd{0, 0}};
   if (k < n) {
@@ -71,6 +111,7 @@ __global__ void k_stage_q(const double* __restrict__ q, int K, int c, const int*
     v[3] = dd_from(qv);
   }
   block_reduce_dd<4>(v, part + (size_t)blockIdx.x * 4);
+  if (last_block(cnt)) reduce_parts_dev<4>(part, gridDim.x, scal);
 }
 
 template <int NQ>
@@ -99,7 +140,9 @@ __global__ void k_finalize(int64_t n, int K, int c, const int* __restrict__ perm
                            const double* __restrict__ scal /* Dx,Dy,Dz,Q */, int dipole, double box,
                            double* __restrict__ out_pot, double* __restrict__ out_near,
                            double* __restrict__ out_far, double* __restrict__ out_dip,
-                           double* __restrict__ out_forces, dd* __restrict__ part) {
+                           double* __restrict__ out_forces, dd* __restrict__ part, int* __restrict__ cnt,
+                           double* __restrict__ epart, double* __restrict__ energies, double* __restrict__ dvec,
+                           double* __restrict__ qtot) {
   const int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   dd v[2] = {dd{0, 0}, dd{0, 0}};
   if (k < n) {
@@ -130,6 +173,24 @@ __global__ void k_finalize(int64_t n, int K, int c, const int* __restrict__ perm
     v[1] = dd_from(q * vf);
   }
   block_reduce_dd<2>(v, part + (size_t)blockIdx.x * 2);
+  if (last_block(cnt)) {
+    reduce_parts_dev<2>(part, gridDim.x, epart);
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      const double gam = 2.0 * 3.14159265358979323846 / (3.0 * box * box * box);
+      const double en = 0.5 * epart[0], ef = 0.5 * epart[1];
+      const double ed =
+          dipole ? DIPOLE_ETA * gam * (scal[0] * scal[0] + scal[1] * scal[1] + scal[2] * scal[2]) : 0.0;
+      energies[0 * K + c] = en + ef + ed;
+      energies[1 * K + c] = en;
+      energies[2 * K + c] = ef;
+      energies[3 * K + c] = ed;
+      dvec[0 * K + c] = scal[0];
+      dvec[1 * K + c] = scal[1];
+      dvec[2 * K + c] = scal[2];
+      qtot[c] = scal[3];
+    }
+  }
 }
 
 // energies (4,K) rows total/near/far/dip; dipole (3,K); qtot (K)
@@ -298,7 +359,7 @@ struct lfmm_plan {
   DevBuf pos_in, pos_wrap, leaf_of, counts, cursor, leaf_start, bucket, perm, inv_perm, pos_sorted, leaf_sorted, xq;
   // expansions / operators
   bool use_tc = false;  // M2L on tcgen05 (fp32, (p+1)^2 <= 128)
-  DevBuf ops_tc;
+  DevBuf ops_tc, up_part, up_cnt, counters;
   DevBuf mult, loc, partial, ops_m2l, ops_m2m, ops_l2l, ops_lat, lat64t;
   std::vector<double2> lat_unit;  // unit-box complex lattice operator (nc x nc)
   // solve work
@@ -364,7 +425,7 @@ struct lfmm_plan {
     }
     for (auto e : free_events) cudaEventDestroy(e);
     DevBuf* bufs[] = {&pos_in, &pos_wrap, &leaf_of, &counts, &cursor, &leaf_start, &bucket, &perm,
-                      &inv_perm, &pos_sorted, &leaf_sorted, &xq, &mult, &loc, &partial, &ops_tc, &ops_m2l, &ops_m2m,
+                      &inv_perm, &pos_sorted, &leaf_sorted, &xq, &mult, &loc, &partial, &ops_tc, &up_part, &up_cnt, &counters, &ops_m2l, &ops_m2m,
                       &ops_l2l, &ops_lat, &lat64t, &q_in, &qs, &vnear, &vfar, &gnear, &gfar, &part,
                       &scal, &epart, &roots, &out_pot, &out_near, &out_far, &out_dip, &out_forces, &energies,
                       &dvec, &qtot, &atom_off, &atom_idx, &nforms, &form_off, &fslot_off, &form_q,
@@ -602,6 +663,12 @@ struct lfmm_plan {
     }
     job_start[depth + 1] = jobs;
     partial.ensure(tsz() * ncp * std::max<int64_t>(off, 1));
+    // M2M child split: 8 partial slots of the largest parent level
+    const int64_t top = depth >= 1 ? (1LL << (3 * (depth - 1))) : 1;
+    up_part.ensure(tsz() * ncp * 8 * top);
+    const int64_t ncnt = (int64_t)tiles_all(std::max(depth - 1, 0)) * ((ncp + GB_M - 1) / GB_M) + 8;
+    up_cnt.ensure(sizeof(int) * ncnt);
+    LFMM_CUDA(cudaMemsetAsync(up_cnt.p, 0, up_cnt.bytes, stream));
   }
   GemmArgs gemm_base() const {
     GemmArgs ga{};
@@ -614,6 +681,9 @@ struct lfmm_plan {
     ga.ops_m2m = ops_m2m.p;
     ga.ops_l2l = ops_l2l.p;
     ga.ops_lat = ops_lat.p;
+    ga.up_split = 8;
+    ga.up_part = up_part.p;
+    ga.up_cnt = up_cnt.as<int>();
     for (int l = 0; l <= depth; ++l) {
       ga.level_off[l] = level_off[l];
       ga.part_off[l] = part_off[l];
@@ -638,7 +708,16 @@ struct lfmm_plan {
                                                        pos_wrap.as<double>(), leaf_of.as<int>(), counts.as<int>());
       });
     }
-    launch(ST_TREE, [&] { k_scan_counts<<<1, 1024, 0, stream>>>(counts.as<int>(), nleaf, leaf_start.as<int>()); });
+    {
+      const int nb = (nleaf + 1023) / 1024;
+      int* bt = cursor.as<int>() + nleaf;  // scratch after the cursors
+      launch(ST_TREE, [&] {
+        k_scan_blocks<<<nb, 1024, 0, stream>>>(counts.as<int>(), nleaf, leaf_start.as<int>(), bt);
+      });
+      launch(ST_TREE, [&] { k_scan_totals<<<1, 1024, 0, stream>>>(bt, nb, leaf_start.as<int>(), nleaf); });
+      if (nb > 1)
+        launch(ST_TREE, [&] { k_scan_add<<<nb, 1024, 0, stream>>>(leaf_start.as<int>(), nleaf, bt); });
+    }
     if (N > 0) {
       launch(ST_TREE, [&] {
         k_scatter_leaf<<<nblk(N, 256), 256, 0, stream>>>(leaf_of.as<int>(), N, leaf_start.as<int>(),
@@ -665,9 +744,9 @@ struct lfmm_plan {
     const T tsize = (T)size;
     launch(ST_STAGE, [&] {
       k_stage_q<T><<<(unsigned)nb, 256, 0, stream>>>(q_in.as<double>(), K, c, perm.as<int>(), pos_sorted.as<double>(),
-                                                     N, L, xq.as<vec4_t<T>>(), qs.as<double>(), part.as<dd>());
+                                                     N, L, xq.as<vec4_t<T>>(), qs.as<double>(), part.as<dd>(),
+                                                     counters.as<int>(), scal.as<double>());
     });
-    launch(ST_STAGE, [&] { k_reduce_parts<4><<<1, 256, 0, stream>>>(part.as<dd>(), (int)nb, scal.as<double>()); });
     const int periodic = (flags & LFMM_F_PERIODIC_NEAR) ? 1 : 0;
     const unsigned lb = nblk(nleaf, P2P_WARPS);
     launch(ST_P2P, [&] {
@@ -689,7 +768,7 @@ struct lfmm_plan {
     for (int l = depth - 1; l >= 0; --l) {
       ga.mode = GEMM_UP;
       ga.level = l;
-      dim3 grid(tiles_all(l), rowb);
+      dim3 grid(tiles_all(l) * ga.up_split, rowb);
       launch(ST_M2M, [&] { k_gemm_gather<T><<<grid, G_THREADS, 0, stream>>>(ga); });
     }
     if (lattice_mode != LFMM_LATTICE_OFF) {
@@ -751,17 +830,14 @@ struct lfmm_plan {
         k_finalize<T, true><<<(unsigned)nb, 256, 0, stream>>>(
             N, K, c, perm.as<int>(), pos_sorted.as<double>(), qs.as<double>(), vnear.as<T>(), vfar.as<T>(),
             gnear.as<T>(), gfar.as<T>(), scal.as<double>(), dip, L, out_pot.as<double>(), out_near.as<double>(),
-            out_far.as<double>(), out_dip.as<double>(), out_forces.as<double>(), part.as<dd>());
+            out_far.as<double>(), out_dip.as<double>(), out_forces.as<double>(), part.as<dd>(), counters.as<int>() + 1,
+            epart.as<double>(), energies.as<double>(), dvec.as<double>(), qtot.as<double>());
       else
         k_finalize<T, false><<<(unsigned)nb, 256, 0, stream>>>(
             N, K, c, perm.as<int>(), pos_sorted.as<double>(), qs.as<double>(), vnear.as<T>(), vfar.as<T>(),
             gnear.as<T>(), gfar.as<T>(), scal.as<double>(), dip, L, out_pot.as<double>(), out_near.as<double>(),
-            out_far.as<double>(), out_dip.as<double>(), nullptr, part.as<dd>());
-    });
-    launch(ST_FINAL, [&] { k_reduce_parts<2><<<1, 256, 0, stream>>>(part.as<dd>(), (int)nb, epart.as<double>()); });
-    launch(ST_FINAL, [&] {
-      k_energies<<<1, 1, 0, stream>>>(scal.as<double>(), epart.as<double>(), K, c, dip, L, energies.as<double>(),
-                                      dvec.as<double>(), qtot.as<double>());
+            out_far.as<double>(), out_dip.as<double>(), nullptr, part.as<dd>(), counters.as<int>() + 1,
+            epart.as<double>(), energies.as<double>(), dvec.as<double>(), qtot.as<double>());
     });
   }
 
@@ -1029,7 +1105,7 @@ int lfmm_plan_create(const double* positions, int64_t n, double box_length, int 
     pl->pos_wrap.ensure(sizeof(double) * 3 * nn);
     pl->leaf_of.ensure(sizeof(int) * nn);
     pl->counts.ensure(sizeof(int) * pl->nleaf);
-    pl->cursor.ensure(sizeof(int) * pl->nleaf);
+    pl->cursor.ensure(sizeof(int) * (pl->nleaf + pl->nleaf / 1024 + 2));
     pl->leaf_start.ensure(sizeof(int) * (pl->nleaf + 1));
     pl->bucket.ensure(sizeof(int) * nn);
     pl->perm.ensure(sizeof(int) * nn);
@@ -1043,6 +1119,8 @@ int lfmm_plan_create(const double* positions, int64_t n, double box_length, int 
     LFMM_CUDA(cudaMemsetAsync(pl->loc.p, 0, pl->loc.bytes, pl->stream));
     pl->plan_m2l_split();
     pl->scal.ensure(sizeof(double) * 8);
+    pl->counters.ensure(sizeof(int) * 16);
+    LFMM_CUDA(cudaMemsetAsync(pl->counters.p, 0, pl->counters.bytes, pl->stream));
     pl->epart.ensure(sizeof(double) * 4);
     pl->offset_total.ensure(sizeof(double));
     if (pl->fp32)

@@ -225,6 +225,12 @@ struct GemmArgs {
   // job decoding for M2L: cumulative job counts per level
   int job_start[DMAX + 3];
   int level;  // UP / L2L / ROOT: the single target level of this launch
+  // UP split: the 8 children over `up_split` CTAs writing partial slots
+  // (up_part[slot][box]); the last CTA of a tile to finish reduces the slots
+  // in fixed order (counter up_cnt[tile], reset by that CTA)
+  int up_split;
+  void* up_part;
+  int* up_cnt;
 };
 
 template <class T>
@@ -302,9 +308,12 @@ __global__ void __launch_bounds__(G_THREADS) k_gemm_gather(GemmArgs g) {
     const int sub = 1 << (level - 1);
     if (tid < GB_N) col_dst[tid] = (q0 + tid < sub * sub * sub) ? parity_box(level, par, q0 + tid) : -1;
   } else if (g.mode == GEMM_UP) {
-    const int q0 = blockIdx.x * GB_N;
+    const int ns = g.up_split;
+    slot = blockIdx.x % ns;
+    const int q0 = (blockIdx.x / ns) * GB_N;
     if (tid < GB_N) col_dst[tid] = (q0 + tid < (1 << (3 * level))) ? q0 + tid : -1;
-    t1 = 8;
+    t0 = (8 * slot) / ns;
+    t1 = (8 * (slot + 1)) / ns;
   } else {  // ROOT
     if (tid < GB_N) col_dst[tid] = tid == 0 ? 0 : -1;
   }
@@ -426,12 +435,17 @@ __global__ void __launch_bounds__(G_THREADS) k_gemm_gather(GemmArgs g) {
     __syncthreads();
   }
 
-  // ---- epilogue ----
+  // ---- epilogue, staged through shared memory so that every global
+  // access (partial slots, outputs) is a coalesced run along the coefficients
   T* out;
   size_t out_base;
+  const size_t nbox_l = (size_t)1 << (3 * level);
   if (g.mode == GEMM_M2L) {
     out = reinterpret_cast<T*>(g.partial);
-    out_base = (size_t)(g.part_off[level] + (int64_t)slot * (1LL << (3 * level)));
+    out_base = (size_t)(g.part_off[level] + (int64_t)slot * nbox_l);
+  } else if (g.mode == GEMM_UP && g.up_split > 1) {
+    out = reinterpret_cast<T*>(g.up_part);
+    out_base = (size_t)slot * nbox_l;
   } else if (g.mode == GEMM_UP) {
     out = const_cast<T*>(mult);
     out_base = (size_t)g.level_off[level];
@@ -440,20 +454,56 @@ __global__ void __launch_bounds__(G_THREADS) k_gemm_gather(GemmArgs g) {
     out_base = (size_t)g.level_off[level];
   }
   const T* part = reinterpret_cast<const T*>(g.partial);
-  const int ns = (g.mode == GEMM_L2L) ? g.nsplit[level] : 0;
+  const int nsl = (g.mode == GEMM_L2L) ? g.nsplit[level] : 0;
+  T* stage = &As[0][0][0];
+  constexpr int CC = (2 * BK * GB_M) / GB_M;  // columns per pass
+#pragma unroll 1
+  for (int c0 = 0; c0 < GB_N; c0 += CC) {
 #pragma unroll
-  for (int j = 0; j < 4; ++j) {
-    const int col = tx * 4 + j;
-    const int box = col_dst[col];
-    if (box < 0) continue;
+    for (int j = 0; j < 4; ++j) {
+      const int col = tx * 4 + j - c0;
+      if (col < 0 || col >= CC) continue;
 #pragma unroll
-    for (int i = 0; i < 8; ++i) {
-      const int r = row0 + (i < 4 ? ty * 4 + i : 64 + ty * 4 + (i - 4));
-      if (r >= ncp) continue;
-      T v = acc[i][j];
-      for (int s = 0; s < ns; ++s)  // M2L partial slots, fixed order
-        v += part[((size_t)g.part_off[level] + (size_t)s * (1u << (3 * level)) + box) * ncp + r];
+      for (int i = 0; i < 8; ++i) {
+        const int r = (i < 4 ? ty * 4 + i : 64 + ty * 4 + (i - 4));
+        stage[col * GB_M + r] = acc[i][j];
+      }
+    }
+    __syncthreads();
+    for (int e = tid; e < CC * GB_M; e += G_THREADS) {
+      const int col = e / GB_M, rr = e % GB_M, r = row0 + rr;
+      const int box = col_dst[c0 + col];
+      if (box < 0 || r >= ncp) continue;
+      T v = stage[e];
+      for (int s2 = 0; s2 < nsl; ++s2)  // M2L partial slots, fixed order
+        v += part[((size_t)g.part_off[level] + (size_t)s2 * nbox_l + box) * ncp + r];
       out[(out_base + box) * ncp + r] = v;
+    }
+    __syncthreads();
+  }
+  if (g.mode == GEMM_UP && g.up_split > 1) {
+    __shared__ int last;
+    __threadfence();
+    __syncthreads();
+    const int tile = blockIdx.x / g.up_split;
+    if (tid == 0) {
+      const int old = atomicAdd(&g.up_cnt[tile * gridDim.y + blockIdx.y], 1);
+      last = (old == g.up_split - 1);
+    }
+    __syncthreads();
+    if (last) {
+      __threadfence();
+      const T* up = reinterpret_cast<const T*>(g.up_part);
+      T* dst = const_cast<T*>(mult) + (size_t)g.level_off[level] * ncp;
+      for (int e = tid; e < GB_N * GB_M; e += G_THREADS) {
+        const int col = e / GB_M, r = row0 + e % GB_M;
+        const int box = col_dst[col];
+        if (box < 0 || r >= ncp) continue;
+        T v = T(0);
+        for (int s2 = 0; s2 < g.up_split; ++s2) v += __ldcg(up + ((size_t)s2 * nbox_l + box) * ncp + r);
+        dst[(size_t)box * ncp + r] = v;
+      }
+      if (tid == 0) g.up_cnt[tile * gridDim.y + blockIdx.y] = 0;
     }
   }
 }

@@ -47,28 +47,64 @@ __global__ void k_wrap_cell(const double* __restrict__ pos_in, int64_t n, double
   atomicAdd(&counts[leaf], 1);
 }
 
-// Exclusive scan of counts[0..n) into start[0..n]; one block of 1024 threads.
-__global__ void k_scan_counts(const int* __restrict__ counts, int n, int* __restrict__ start) {
-  __shared__ int part[1024];
-  const int t = threadIdx.x;
-  const int per = (n + blockDim.x - 1) / blockDim.x;
-  const int b0 = min(n, t * per), b1 = min(n, b0 + per);
-  int s = 0;
-  for (int i = b0; i < b1; ++i) s += counts[i];
-  part[t] = s;
+// Exclusive scan of counts[0..n) into start[0..n] in three passes:
+// per-1024 block scans (warp shuffles), a scan of the block totals, and the
+// block-offset add.
+__device__ __forceinline__ int block_scan_excl(int v, int* warp_tot, int& total) {
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  int x = v;
+#pragma unroll
+  for (int off = 1; off < 32; off <<= 1) {
+    const int y = __shfl_up_sync(0xffffffffu, x, off);
+    if (lane >= off) x += y;
+  }
+  if (lane == 31) warp_tot[w] = x;
   __syncthreads();
-  for (int off = 1; off < blockDim.x; off <<= 1) {
-    int v = t >= off ? part[t - off] : 0;
+  if (w == 0) {
+    int t = lane < nw ? warp_tot[lane] : 0;
+#pragma unroll
+    for (int off = 1; off < 32; off <<= 1) {
+      const int y = __shfl_up_sync(0xffffffffu, t, off);
+      if (lane >= off) t += y;
+    }
+    if (lane < nw) warp_tot[lane] = t;
+  }
+  __syncthreads();
+  total = warp_tot[nw - 1];
+  const int base = w > 0 ? warp_tot[w - 1] : 0;
+  return base + x - v;
+}
+
+__global__ void k_scan_blocks(const int* __restrict__ counts, int n, int* __restrict__ start,
+                              int* __restrict__ block_tot) {
+  __shared__ int wt[32];
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  const int v = i < n ? counts[i] : 0;
+  int total;
+  const int ex = block_scan_excl(v, wt, total);
+  if (i < n) start[i] = ex;
+  if (threadIdx.x == 0) block_tot[blockIdx.x] = total;
+}
+
+__global__ void k_scan_totals(int* __restrict__ block_tot, int nb, int* __restrict__ start, int n) {
+  __shared__ int wt[32];
+  int run = 0;
+  for (int b0 = 0; b0 < nb; b0 += blockDim.x) {
+    const int b = b0 + threadIdx.x;
+    const int v = b < nb ? block_tot[b] : 0;
+    int total;
+    const int ex = block_scan_excl(v, wt, total);
     __syncthreads();
-    part[t] += v;
+    if (b < nb) block_tot[b] = run + ex;
+    run += total;
     __syncthreads();
   }
-  int run = part[t] - s;  // exclusive prefix of this segment
-  for (int i = b0; i < b1; ++i) {
-    start[i] = run;
-    run += counts[i];
-  }
-  if (t == blockDim.x - 1) start[n] = part[t];
+  if (threadIdx.x == 0) start[n] = run;
+}
+
+__global__ void k_scan_add(int* __restrict__ start, int n, const int* __restrict__ block_tot) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) start[i] += block_tot[blockIdx.x];
 }
 
 __global__ void k_scatter_leaf(const int* __restrict__ leaf_of, int64_t n, const int* __restrict__ start,
@@ -89,6 +125,8 @@ __device__ __forceinline__ bool key_less(double ax, double ay, double az, int ai
 }
 
 // One warp per leaf: rank of every bucket entry under (x, y, z, index).
+// Keys of 32 entries at a time are held by the lanes and broadcast with
+// shuffles, so the O(n^2) comparison loop touches no memory.
 __global__ void k_leaf_rank(const double* __restrict__ pos_wrap, const int* __restrict__ start,
                             const int* __restrict__ bucket, int nleaf, int* __restrict__ perm,
                             int* __restrict__ inv_perm) {
@@ -96,16 +134,39 @@ __global__ void k_leaf_rank(const double* __restrict__ pos_wrap, const int* __re
   const int lane = threadIdx.x & 31;
   if (warp >= nleaf) return;
   const int s0 = start[warp], s1 = start[warp + 1];
-  for (int e = s0 + lane; e < s1; e += 32) {
-    const int i = bucket[e];
-    const double x = pos_wrap[3 * i], y = pos_wrap[3 * i + 1], z = pos_wrap[3 * i + 2];
-    int rank = 0;
-    for (int f = s0; f < s1; ++f) {
-      const int j = bucket[f];
-      rank += key_less(pos_wrap[3 * j], pos_wrap[3 * j + 1], pos_wrap[3 * j + 2], j, x, y, z, i);
+  for (int e0 = s0; e0 < s1; e0 += 32) {
+    const int e = e0 + lane;
+    int i = -1;
+    double x = 0, y = 0, z = 0;
+    if (e < s1) {
+      i = bucket[e];
+      x = pos_wrap[3 * i];
+      y = pos_wrap[3 * i + 1];
+      z = pos_wrap[3 * i + 2];
     }
-    perm[s0 + rank] = i;
-    inv_perm[i] = s0 + rank;
+    int rank = 0;
+    for (int f0 = s0; f0 < s1; f0 += 32) {
+      const int f = f0 + lane;
+      int jf = -1;
+      double xf = 0, yf = 0, zf = 0;
+      if (f < s1) {
+        jf = bucket[f];
+        xf = pos_wrap[3 * jf];
+        yf = pos_wrap[3 * jf + 1];
+        zf = pos_wrap[3 * jf + 2];
+      }
+      const int cnt = min(32, s1 - f0);
+      for (int k = 0; k < cnt; ++k) {
+        const int j = __shfl_sync(0xffffffffu, jf, k);
+        const double xj = __shfl_sync(0xffffffffu, xf, k), yj = __shfl_sync(0xffffffffu, yf, k),
+                     zj = __shfl_sync(0xffffffffu, zf, k);
+        rank += key_less(xj, yj, zj, j, x, y, z, i);
+      }
+    }
+    if (e < s1) {
+      perm[s0 + rank] = i;
+      inv_perm[i] = s0 + rank;
+    }
   }
 }
 
