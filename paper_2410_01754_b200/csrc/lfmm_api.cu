@@ -635,7 +635,7 @@ struct lfmm_plan {
       launch(ST_SETUP, [&] {
         k_tc_arrange_ops<<<nblk(total, 256), 256, 0, stream>>>(ops_m2l.as<float>(), ops_tc.as<float>(), NOFF);
       });
-      LFMM_CUDA(cudaFuncSetAttribute(k_m2l_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, TC_SMEM));
+      LFMM_CUDA(cudaFuncSetAttribute(k_m2l_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, TC_SMEM_WS));
     }
     LFMM_CUDA(cudaStreamSynchronize(stream));
     vecs.release();
@@ -794,7 +794,7 @@ struct lfmm_plan {
           ta.nsplit[l] = nsplit[l];
         }
         for (int l = 0; l <= depth + 1; ++l) ta.job_start[l] = job_start[l];
-        launch(ST_DOWN, [&] { k_m2l_tc<<<job_start[depth + 1], 128, TC_SMEM, stream>>>(ta); });
+        launch(ST_DOWN, [&] { k_m2l_tc<<<job_start[depth + 1], TC_THREADS, TC_SMEM_WS, stream>>>(ta); });
       } else {
         ga.mode = GEMM_M2L;
         ga.level = 0;

@@ -130,14 +130,26 @@ __global__ void k_tc_arrange_ops(const float* __restrict__ ops, float* __restric
   *reinterpret_cast<float*>(base + TC_TILE + tc_core_off(r, kk)) = lo;
 }
 
-__global__ void __launch_bounds__(128, 1) k_m2l_tc(TcArgs g) {
+__device__ __forceinline__ void mbar_arrive(uint32_t bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(bar) : "memory");
+}
+
+// Warp-specialised pipeline over TC_STAGES stages of (A 32 KB | B 32 KB):
+//   warps 0-3  B producers: one target row per thread; register prefetch of
+//              the next chunk, tf32 split, st.shared, fence.proxy.async,
+//              arrive on full_b[s]; afterwards the TMEM epilogue
+//   warp 4     MMA issuer (one lane): waits full_a/full_b, 12 MMAs per
+//              stage, tcgen05.commit -> empty[s]
+//   warp 5     A loader (one lane): waits empty[s], one cp.async.bulk of
+//              the pre-arranged operator chunk -> full_a[s]
+constexpr int TC_STAGES = 3;
+constexpr int TC_SMEM_WS = TC_STAGES * 2 * TC_STAGE + 1024;
+constexpr int TC_THREADS = 192;
+
+__global__ void __launch_bounds__(TC_THREADS, 1) k_m2l_tc(TcArgs g) {
   extern __shared__ __align__(1024) unsigned char tc_smem_raw[];
-  // 1024-B aligned carve-up
   unsigned char* smem = reinterpret_cast<unsigned char*>(((uintptr_t)tc_smem_raw + 1023) & ~(uintptr_t)1023);
-  unsigned char* Abuf = smem;                                // 3 x 32 KB
-  unsigned char* Bbuf = smem + TC_ASTAGES * TC_STAGE;        // 2 x 32 KB
-  __shared__ __align__(8) uint64_t full_bar[TC_ASTAGES];
-  __shared__ __align__(8) uint64_t mma_bar[TC_BSTAGES];
+  __shared__ __align__(8) uint64_t full_a[TC_STAGES], full_b[TC_STAGES], empty_bar[TC_STAGES], done_bar;
   __shared__ uint32_t tmem_base_sh;
   __shared__ int col_dst[TC_N];
 
@@ -155,14 +167,20 @@ __global__ void __launch_bounds__(128, 1) k_m2l_tc(TcArgs g) {
   const int q0 = (tile % tpp) * TC_N;
   const int sub = 1 << (level - 1);
   const int nside = 1 << level, msk = nside - 1;
-  const int my_box = (q0 + tid < sub * sub * sub) ? parity_box(level, par, q0 + tid) : -1;
-  col_dst[tid] = my_box;
   const int t0 = (NM2L * slot) / ns, t1 = (NM2L * (slot + 1)) / ns;
   const int niter = (t1 - t0) * TC_NCHUNK;
-
+  int my_box = -1;
+  if (tid < TC_N) {
+    my_box = (q0 + tid < sub * sub * sub) ? parity_box(level, par, q0 + tid) : -1;
+    col_dst[tid] = my_box;
+  }
   if (tid == 0) {
-    for (int s = 0; s < TC_ASTAGES; ++s) mbar_init(smem_u32(&full_bar[s]), 1);
-    for (int s = 0; s < TC_BSTAGES; ++s) mbar_init(smem_u32(&mma_bar[s]), 1);
+    for (int s = 0; s < TC_STAGES; ++s) {
+      mbar_init(smem_u32(&full_a[s]), 1);
+      mbar_init(smem_u32(&full_b[s]), TC_N);
+      mbar_init(smem_u32(&empty_bar[s]), 1);
+    }
+    mbar_init(smem_u32(&done_bar), 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   if (warp == 0) {
@@ -175,117 +193,127 @@ __global__ void __launch_bounds__(128, 1) k_m2l_tc(TcArgs g) {
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
   const uint32_t tmem = tmem_base_sh;
 
-  const int gx = my_box >= 0 ? my_box >> (2 * level) : 0;
-  const int gy = my_box >= 0 ? (my_box >> level) & msk : 0;
-  const int gz = my_box >= 0 ? my_box & msk : 0;
-  const float* mult_l = g.mult + g.level_off[level] * TC_M;
-
-  auto a_src = [&](int it) {
-    const int term = t0 + it / TC_NCHUNK, chunk = it % TC_NCHUNK;
-    const int row = c_m2l_row[par * NM2L + term];
-    return reinterpret_cast<const char*>(g.ops_tc) + ((size_t)row * TC_NCHUNK + chunk) * TC_STAGE;
-  };
-  auto b_load = [&](int it, float4 (&r)[8]) {
-    if (my_box < 0 || it >= niter) {
+  if (warp < 4) {
+    // ------------------------------------------------ B producers ----
+    const int gx = my_box >= 0 ? my_box >> (2 * level) : 0;
+    const int gy = my_box >= 0 ? (my_box >> level) & msk : 0;
+    const int gz = my_box >= 0 ? my_box & msk : 0;
+    const float* mult_l = g.mult + g.level_off[level] * TC_M;
+    auto b_load = [&](int it, float4 (&r)[8]) {
+      if (my_box < 0 || it >= niter) {
 #pragma unroll
-      for (int u = 0; u < 8; ++u) r[u] = make_float4(0.f, 0.f, 0.f, 0.f);
-      return;
-    }
-    const int term = t0 + it / TC_NCHUNK, chunk = it % TC_NCHUNK;
-    const char4 o = c_m2l_off[par * NM2L + term];
-    const int src = ((((gx + o.x) & msk) << level | ((gy + o.y) & msk)) << level) | ((gz + o.z) & msk);
-    const float4* p = reinterpret_cast<const float4*>(mult_l + (size_t)src * TC_M + chunk * TC_BK);
-#pragma unroll
-    for (int u = 0; u < 8; ++u) r[u] = __ldg(p + u);
-  };
-
-  if (tid == 0 && niter > 0) bulk_load(smem_u32(Abuf), a_src(0), TC_STAGE, smem_u32(&full_bar[0]));
-  float4 rb[8], rn[8];
-  b_load(0, rb);
-
-  for (int it = 0; it < niter; ++it) {
-    const int sa = it % TC_ASTAGES, sb = it & 1;
-    // stage reuse: MMAs of iteration it-2 read B stage sb and A stage (it+1)%3
-    if (it >= 2) mbar_wait(smem_u32(&mma_bar[sb]), ((it - 2) >> 1) & 1);
-    if (tid == 0 && it + 1 < niter)
-      bulk_load(smem_u32(Abuf + ((it + 1) % TC_ASTAGES) * TC_STAGE), a_src(it + 1), TC_STAGE,
-                smem_u32(&full_bar[(it + 1) % TC_ASTAGES]));
-    b_load(it + 1, rn);  // prefetch the next chunk of my target's source
-    // split B(it) into tf32 hi / lo and store in the core-matrix layout
-    unsigned char* bh = Bbuf + sb * TC_STAGE;
-#pragma unroll
-    for (int u = 0; u < 8; ++u) {
-      const float4 v = rb[u];
-      float4 h, l;
-      h.x = tf32_rna(v.x);
-      h.y = tf32_rna(v.y);
-      h.z = tf32_rna(v.z);
-      h.w = tf32_rna(v.w);
-      l.x = v.x - h.x;
-      l.y = v.y - h.y;
-      l.z = v.z - h.z;
-      l.w = v.w - h.w;
-      const uint32_t off = tc_core_off(tid, 4 * u);
-      *reinterpret_cast<float4*>(bh + off) = h;
-      *reinterpret_cast<float4*>(bh + TC_TILE + off) = l;
-    }
-    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-    __syncthreads();
-    if (tid == 0) {
-      mbar_wait(smem_u32(&full_bar[sa]), (it / TC_ASTAGES) & 1);
-      asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-      const uint32_t a0 = smem_u32(Abuf + sa * TC_STAGE), b0 = smem_u32(bh);
-      const int tl = it / TC_NCHUNK;  // term index within this CTA
-      const uint32_t dacc = tmem + (uint32_t)((tl % TC_NACC) * TC_N);
-      const bool fresh = tl < TC_NACC && (it % TC_NCHUNK) == 0;
-#pragma unroll
-      for (int kk = 0; kk < TC_BK / 8; ++kk) {
-        const uint32_t ko = kk * 256;  // 8 k = two 16-B core columns
-        const uint64_t ah = tc_desc(a0 + ko), al = tc_desc(a0 + TC_TILE + ko);
-        const uint64_t bhd = tc_desc(b0 + ko), bld = tc_desc(b0 + TC_TILE + ko);
-        tc_mma(dacc, ah, bhd, (fresh && kk == 0) ? 0u : 1u);
-        tc_mma(dacc, ah, bld, 1u);
-        tc_mma(dacc, al, bhd, 1u);
+        for (int u = 0; u < 8; ++u) r[u] = make_float4(0.f, 0.f, 0.f, 0.f);
+        return;
       }
-      tc_commit(smem_u32(&mma_bar[sb]));
-    }
+      const int term = t0 + it / TC_NCHUNK, chunk = it % TC_NCHUNK;
+      const char4 o = c_m2l_off[par * NM2L + term];
+      const int src = ((((gx + o.x) & msk) << level | ((gy + o.y) & msk)) << level) | ((gz + o.z) & msk);
+      const float4* p = reinterpret_cast<const float4*>(mult_l + (size_t)src * TC_M + chunk * TC_BK);
 #pragma unroll
-    for (int u = 0; u < 8; ++u) rb[u] = rn[u];
-  }
-  if (niter > 0) mbar_wait(smem_u32(&mma_bar[(niter - 1) & 1]), ((niter - 1) >> 1) & 1);
-  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-
-  // ---- epilogue: TMEM lane = output coefficient, column = target ----
-  float* out = g.partial + ((size_t)g.part_off[level] + (size_t)slot * (1u << (3 * level))) * TC_M;
-  const int coef = warp * 32 + lane;
-  const int nterm_cta = t1 - t0;
-  const int nacc = nterm_cta < TC_NACC ? nterm_cta : TC_NACC;
+      for (int u = 0; u < 8; ++u) r[u] = __ldg(p + u);
+    };
+    float4 rb[8], rn[8];
+    b_load(0, rb);
+    for (int it = 0; it < niter; ++it) {
+      const int st = it % TC_STAGES, use = it / TC_STAGES;
+      b_load(it + 1, rn);
+      if (use >= 1) mbar_wait(smem_u32(&empty_bar[st]), (use - 1) & 1);
+      unsigned char* bh = smem + st * 2 * TC_STAGE + TC_STAGE;
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const float4 v = rb[u];
+        float4 h, l;
+        h.x = tf32_rna(v.x);
+        h.y = tf32_rna(v.y);
+        h.z = tf32_rna(v.z);
+        h.w = tf32_rna(v.w);
+        l.x = v.x - h.x;
+        l.y = v.y - h.y;
+        l.z = v.z - h.z;
+        l.w = v.w - h.w;
+        const uint32_t off = tc_core_off(tid, 4 * u);
+        *reinterpret_cast<float4*>(bh + off) = h;
+        *reinterpret_cast<float4*>(bh + TC_TILE + off) = l;
+      }
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      mbar_arrive(smem_u32(&full_b[st]));
+#pragma unroll
+      for (int u = 0; u < 8; ++u) rb[u] = rn[u];
+    }
+    // ------------------------------------------------ epilogue ----
+    if (niter > 0) mbar_wait(smem_u32(&done_bar), 0);
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    float* out = g.partial + ((size_t)g.part_off[level] + (size_t)slot * (1u << (3 * level))) * TC_M;
+    const int coef = warp * 32 + lane;
+    const int nterm_cta = t1 - t0;
+    const int nacc = nterm_cta < TC_NACC ? nterm_cta : TC_NACC;
 #pragma unroll 1
-  for (int c0 = 0; c0 < TC_N; c0 += 32) {
-    float sum[32];
+    for (int c0 = 0; c0 < TC_N; c0 += 32) {
+      float sum[32];
 #pragma unroll
-    for (int jj = 0; jj < 32; ++jj) sum[jj] = 0.f;
+      for (int jj = 0; jj < 32; ++jj) sum[jj] = 0.f;
 #pragma unroll 1
-    for (int a = 0; a < nacc; ++a) {
-    uint32_t v[32];
-    const uint32_t taddr = tmem + ((uint32_t)(warp * 32) << 16) + (uint32_t)(c0 + a * TC_N);
-    asm volatile(
-        "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
-        "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
-        : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]),
-          "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15]),
-          "=r"(v[16]), "=r"(v[17]), "=r"(v[18]), "=r"(v[19]), "=r"(v[20]), "=r"(v[21]), "=r"(v[22]), "=r"(v[23]),
-          "=r"(v[24]), "=r"(v[25]), "=r"(v[26]), "=r"(v[27]), "=r"(v[28]), "=r"(v[29]), "=r"(v[30]), "=r"(v[31])
-        : "r"(taddr));
-    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+      for (int a = 0; a < nacc; ++a) {
+        uint32_t v[32];
+        const uint32_t taddr = tmem + ((uint32_t)(warp * 32) << 16) + (uint32_t)(c0 + a * TC_N);
+        asm volatile(
+            "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+            "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+            : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]),
+              "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]),
+              "=r"(v[15]), "=r"(v[16]), "=r"(v[17]), "=r"(v[18]), "=r"(v[19]), "=r"(v[20]), "=r"(v[21]),
+              "=r"(v[22]), "=r"(v[23]), "=r"(v[24]), "=r"(v[25]), "=r"(v[26]), "=r"(v[27]), "=r"(v[28]),
+              "=r"(v[29]), "=r"(v[30]), "=r"(v[31])
+            : "r"(taddr));
+        asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 #pragma unroll
-    for (int jj = 0; jj < 32; ++jj) sum[jj] += __uint_as_float(v[jj]);
-    }
+        for (int jj = 0; jj < 32; ++jj) sum[jj] += __uint_as_float(v[jj]);
+      }
 #pragma unroll
-    for (int jj = 0; jj < 32; ++jj) {
-      const int box = col_dst[c0 + jj];
-      if (box >= 0) out[(size_t)box * TC_M + coef] = sum[jj];
+      for (int jj = 0; jj < 32; ++jj) {
+        const int box = col_dst[c0 + jj];
+        if (box >= 0) out[(size_t)box * TC_M + coef] = sum[jj];
+      }
     }
+  } else if (warp == 4) {
+    // ------------------------------------------------ MMA issuer ----
+    if (lane == 0) {
+      for (int it = 0; it < niter; ++it) {
+        const int st = it % TC_STAGES, ph = (it / TC_STAGES) & 1;
+        mbar_wait(smem_u32(&full_a[st]), ph);
+        mbar_wait(smem_u32(&full_b[st]), ph);
+        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+        const uint32_t a0 = smem_u32(smem + st * 2 * TC_STAGE), b0 = a0 + TC_STAGE;
+        const int tl = it / TC_NCHUNK;
+        const uint32_t dacc = tmem + (uint32_t)((tl % TC_NACC) * TC_N);
+        const bool fresh = tl < TC_NACC && (it % TC_NCHUNK) == 0;
+#pragma unroll
+        for (int kk = 0; kk < TC_BK / 8; ++kk) {
+          const uint32_t ko = kk * 256;
+          const uint64_t ah = tc_desc(a0 + ko), al = tc_desc(a0 + TC_TILE + ko);
+          const uint64_t bhd = tc_desc(b0 + ko), bld = tc_desc(b0 + TC_TILE + ko);
+          tc_mma(dacc, ah, bhd, (fresh && kk == 0) ? 0u : 1u);
+          tc_mma(dacc, ah, bld, 1u);
+          tc_mma(dacc, al, bhd, 1u);
+        }
+        tc_commit(smem_u32(&empty_bar[st]));
+      }
+      if (niter > 0) tc_commit(smem_u32(&done_bar));
+    }
+    __syncwarp();
+  } else {
+    // ------------------------------------------------ A loader ----
+    if (lane == 0) {
+      for (int it = 0; it < niter; ++it) {
+        const int st = it % TC_STAGES, use = it / TC_STAGES;
+        if (use >= 1) mbar_wait(smem_u32(&empty_bar[st]), (use - 1) & 1);
+        const int term = t0 + it / TC_NCHUNK, chunk = it % TC_NCHUNK;
+        const int row = c_m2l_row[par * NM2L + term];
+        const char* src = reinterpret_cast<const char*>(g.ops_tc) + ((size_t)row * TC_NCHUNK + chunk) * TC_STAGE;
+        bulk_load(smem_u32(smem + st * 2 * TC_STAGE), src, TC_STAGE, smem_u32(&full_a[st]));
+      }
+    }
+    __syncwarp();
   }
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
   __syncthreads();
