@@ -22,6 +22,7 @@
 #include "lfmm_common.cuh"
 #include "lfmm_expansions.cuh"
 #include "lfmm_hi.cuh"
+#include "lfmm_m2l_halo.cuh"
 #include "lfmm_m2l_tc.cuh"
 #include "lfmm_p2p.cuh"
 #include "lfmm_setup.cuh"
@@ -112,6 +113,48 @@ __global__ void k_stage_q(const double* __restrict__ q, int K, int c, const int*
   }
   block_reduce_dd<4>(v, part + (size_t)blockIdx.x * 4);
   if (last_block(cnt)) reduce_parts_dev<4>(part, gridDim.x, scal);
+}
+
+// Exact box charges (the l = 0 multipole) at every level.  The fp32 P2M/M2M
+// sums of the ~30 repeated water charges per leaf round coherently: summed
+// over 32k leaves they leave a fake net charge of ~5e-3 e that the M2L turns
+// into a constant far-potential offset of ~4e-4 of max|V| (tools/
+// diag_precision.py).  Each box's charge is summed here in fp64 (leaf atoms in
+// canonical order, then 8 children per parent, fixed order) and rounded once
+// into coefficient 0; only the l = 0 column is replaced, the higher moments
+// keep the P2M/M2M values.  Multi-block leaf pass; the last block to finish
+// sums the parent levels.
+template <class T>
+__global__ void k_box_charges(const double* __restrict__ qs, const int* __restrict__ leaf_start, int depth,
+                              int64_t leaf_off, int ncp, T* __restrict__ mult, double* __restrict__ boxq,
+                              int* __restrict__ cnt) {
+  const int nleaf = 1 << (3 * depth);
+  const int b = blockIdx.x * blockDim.x + threadIdx.x;
+  if (b < nleaf) {
+    double c = 0.0;
+    for (int i = leaf_start[b]; i < leaf_start[b + 1]; ++i) c += qs[i];
+    boxq[leaf_off + b] = c;
+    mult[(size_t)(leaf_off + b) * ncp] = (T)c;
+  }
+  if (!last_block(cnt)) return;
+  int64_t child_off = leaf_off;
+  for (int l = depth - 1; l >= 0; --l) {
+    const int n = 1 << l, nb = 1 << (3 * l);
+    const int64_t off = child_off - nb;  // level_off[l] (levels are stored consecutively)
+    for (int pb = threadIdx.x; pb < nb; pb += blockDim.x) {
+      const int x = pb >> (2 * l), y = (pb >> l) & (n - 1), z = pb & (n - 1);
+      double c = 0.0;
+      for (int o = 0; o < 8; ++o) {
+        const int cx = 2 * x + ((o >> 2) & 1), cy = 2 * y + ((o >> 1) & 1), cz = 2 * z + (o & 1);
+        c += __ldcg(&boxq[child_off + ((((int64_t)cx << (l + 1)) | (cy)) << (l + 1) | cz)]);
+      }
+      boxq[off + pb] = c;
+      mult[(size_t)(off + pb) * ncp] = (T)c;
+    }
+    __syncthreads();
+    __threadfence_block();
+    child_off = off;
+  }
 }
 
 template <int NQ>
@@ -322,6 +365,32 @@ void init_constants() {
   }
   LFMM_CUDA(cudaMemcpyToSymbol(c_m2l_off, off.data(), off.size() * sizeof(char4)));
   LFMM_CUDA(cudaMemcpyToSymbol(c_m2l_row, rows.data(), rows.size() * sizeof(short)));
+  // halo M2L: per (target class tc, source class sc) the offsets o with
+  // tc + o = 2d + sc, as {operator row, d}
+  std::vector<int> hn(64, 0);
+  std::vector<short> hrow(64 * 27, 0);
+  std::vector<char4> hd(64 * 27, make_char4(0, 0, 0, 0));
+  for (int tc = 0; tc < 8; ++tc)
+    for (int s = 0; s < NM2L; ++s) {
+      const char4 o = off[tc * NM2L + s];
+      const int tcb[3] = {(tc >> 2) & 1, (tc >> 1) & 1, tc & 1};
+      const int oo[3] = {o.x, o.y, o.z};
+      int sc = 0, d[3];
+      for (int a = 0; a < 3; ++a) {
+        const int v = tcb[a] + oo[a];
+        const int par = ((v % 2) + 2) % 2;
+        d[a] = (v - par) / 2;
+        sc = (sc << 1) | par;
+      }
+      const int tab = tc * 8 + sc;
+      if (hn[tab] >= 27) throw Error{LFMM_ECUDA, "halo term table overflow"};
+      hrow[tab * 27 + hn[tab]] = rows[tc * NM2L + s];
+      hd[tab * 27 + hn[tab]] = make_char4((char)d[0], (char)d[1], (char)d[2], 0);
+      hn[tab]++;
+    }
+  LFMM_CUDA(cudaMemcpyToSymbol(c_hterm_n, hn.data(), hn.size() * sizeof(int)));
+  LFMM_CUDA(cudaMemcpyToSymbol(c_hterm_row, hrow.data(), hrow.size() * sizeof(short)));
+  LFMM_CUDA(cudaMemcpyToSymbol(c_hterm_d, hd.data(), hd.size() * sizeof(char4)));
 }
 
 // process-level cache of unit-box lattice operators, like lru_cache on
@@ -358,11 +427,16 @@ struct lfmm_plan {
   // tree
   DevBuf pos_in, pos_wrap, leaf_of, counts, cursor, leaf_start, bucket, perm, inv_perm, pos_sorted, leaf_sorted, xq;
   // expansions / operators
-  bool use_tc = false;  // M2L on tcgen05 (fp32, (p+1)^2 <= 128)
+  bool use_tc = false;    // M2L on tcgen05 (fp32, (p+1)^2 <= 128)
+  bool use_halo = false;  // ... as shifted-window fp16x3 GEMMs (lfmm_m2l_halo.cuh)
   DevBuf ops_tc, up_part, up_cnt, counters;
+  DevBuf ops16, hm_inv_r, hm_inv_c, hm_jobs, hm_level_max, mult16;
+  int64_t m16_off[DMAX + 2] = {0};
+  int hm_njobs = 0, hm_rw_cap = 0;
   DevBuf mult, loc, partial, ops_m2l, ops_m2m, ops_l2l, ops_lat, lat64t;
   std::vector<double2> lat_unit;  // unit-box complex lattice operator (nc x nc)
   // solve work
+  DevBuf boxq;
   DevBuf q_in, qs, vnear, vfar, gnear, gfar, part, scal, epart, roots;
   DevBuf out_pot, out_near, out_far, out_dip, out_forces, energies, dvec, qtot;
   int64_t last_k = 0;
@@ -424,6 +498,8 @@ struct lfmm_plan {
       cudaEventDestroy(e.b);
     }
     for (auto e : free_events) cudaEventDestroy(e);
+    DevBuf* hbufs[] = {&ops16, &hm_inv_r, &hm_inv_c, &hm_jobs, &hm_level_max, &mult16, &boxq};
+    for (auto* b : hbufs) b->release();
     DevBuf* bufs[] = {&pos_in, &pos_wrap, &leaf_of, &counts, &cursor, &leaf_start, &bucket, &perm,
                       &inv_perm, &pos_sorted, &leaf_sorted, &xq, &mult, &loc, &partial, &ops_tc, &up_part, &up_cnt, &counters, &ops_m2l, &ops_m2m,
                       &ops_l2l, &ops_lat, &lat64t, &q_in, &qs, &vnear, &vfar, &gnear, &gfar, &part,
@@ -629,7 +705,8 @@ struct lfmm_plan {
       LFMM_CUDA(cudaStreamSynchronize(stream));
       l64.release();
     }
-    if (use_tc) {
+    if (use_halo) build_halo_operators();
+    if (use_tc && !use_halo) {
       ops_tc.ensure((size_t)NOFF * TC_NCHUNK * TC_STAGE);
       const int64_t total = (int64_t)NOFF * TC_M * TC_M;
       launch(ST_SETUP, [&] {
@@ -640,6 +717,96 @@ struct lfmm_plan {
     LFMM_CUDA(cudaStreamSynchronize(stream));
     vecs.release();
     vals.release();
+  }
+
+  // Halo M2L operators: power-of-two row/column equilibration of the 316
+  // fp32 operators (so fp16 hi/lo pairs keep 22 bits, tools/m2l_fp16_study.py),
+  // then the pre-arranged fp16 chunks.  The scales depend on p only.
+  void build_halo_operators() {
+    const size_t nel = (size_t)NOFF * 128 * 128;
+    std::vector<float> h(nel);
+    LFMM_CUDA(cudaMemcpyAsync(h.data(), ops_m2l.p, nel * sizeof(float), cudaMemcpyDeviceToHost, stream));
+    LFMM_CUDA(cudaStreamSynchronize(stream));
+    std::vector<double> amax(128 * 128, 0.0);
+    for (size_t o = 0; o < (size_t)NOFF; ++o)
+      for (int i = 0; i < 128 * 128; ++i) amax[i] = std::max(amax[i], (double)std::fabs(h[o * 16384 + i]));
+    std::vector<double> r(128, 1.0), c(128, 1.0);
+    for (int iter = 0; iter < 30; ++iter) {
+      for (int a = 0; a < 128; ++a) {
+        double m = 0.0;
+        for (int b = 0; b < 128; ++b) m = std::max(m, r[a] * amax[a * 128 + b] * c[b]);
+        if (m > 0) r[a] /= std::sqrt(m);
+      }
+      for (int b = 0; b < 128; ++b) {
+        double m = 0.0;
+        for (int a = 0; a < 128; ++a) m = std::max(m, r[a] * amax[a * 128 + b] * c[b]);
+        if (m > 0) c[b] /= std::sqrt(m);
+      }
+    }
+    std::vector<float> rs(128), cs(128), ir(128), ic(128);
+    for (int a = 0; a < 128; ++a) {
+      const double pr = std::exp2(std::round(std::log2(r[a]))), pc = std::exp2(std::round(std::log2(c[a])));
+      rs[a] = (float)pr;
+      cs[a] = (float)pc;
+      ir[a] = (float)(1.0 / pr);
+      ic[a] = (float)(1.0 / pc);
+    }
+    DevBuf drs, dcs;
+    drs.ensure(sizeof(float) * 128);
+    dcs.ensure(sizeof(float) * 128);
+    hm_inv_r.ensure(sizeof(float) * 128);
+    hm_inv_c.ensure(sizeof(float) * 128);
+    LFMM_CUDA(cudaMemcpyAsync(drs.p, rs.data(), 512, cudaMemcpyHostToDevice, stream));
+    LFMM_CUDA(cudaMemcpyAsync(dcs.p, cs.data(), 512, cudaMemcpyHostToDevice, stream));
+    LFMM_CUDA(cudaMemcpyAsync(hm_inv_r.p, ir.data(), 512, cudaMemcpyHostToDevice, stream));
+    LFMM_CUDA(cudaMemcpyAsync(hm_inv_c.p, ic.data(), 512, cudaMemcpyHostToDevice, stream));
+    ops16.ensure((size_t)NOFF * HM_NKC * HM_ATILE);
+    launch(ST_SETUP, [&] {
+      k_h16_arrange<<<nblk((int64_t)nel, 256), 256, 0, stream>>>(ops_m2l.as<float>(), drs.as<float>(), dcs.as<float>(),
+                                                                 ops16.as<unsigned char>(), NOFF);
+    });
+    LFMM_CUDA(cudaStreamSynchronize(stream));
+    hm_level_max.ensure(sizeof(unsigned int) * (DMAX + 2));
+    LFMM_CUDA(cudaFuncSetAttribute(k_m2l_halo, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   (int)hm_smem_bytes(hm_rw_cap)));
+  }
+
+  // Halo M2L jobs: (level, target class, 256-row tile of the padded linear
+  // class grid, group of source classes); level d first so the small levels
+  // fill the tail of the single launch.  Groups: 4 per tile (pairs of source
+  // classes with |D| 26+19 / 25+23) at levels >= 4, one source class per job
+  // below.  Each group writes its own partial slot.
+  void plan_halo_jobs() {
+    std::vector<int4> jobs;
+    int64_t off = 0;
+    hm_rw_cap = 0;
+    for (int l = depth; l >= 1; --l) nsplit[l] = (l >= 4) ? 4 : 8;
+    for (int l = 1; l <= depth; ++l) {
+      part_off[l] = off;
+      off += (int64_t)nsplit[l] << (3 * l);
+    }
+    for (int l = depth; l >= 1; --l) {
+      const int h = 1 << (l - 1), Z = h + 2, S = Z * Z + Z + 1, last = h * S;
+      const int G = nsplit[l];
+      for (int t0 = S; t0 <= last; t0 += HM_NMAX) {
+        const int N = std::min(HM_NMAX, ((last + 1 - t0) + 15) / 16 * 16);
+        hm_rw_cap = std::max(hm_rw_cap, hm_rw(N, Z));
+        for (int tc = 0; tc < 8; ++tc)
+          for (int grp = 0; grp < G; ++grp) jobs.push_back(make_int4(l | (tc << 4) | (grp << 8) | (G << 12), t0, N, 0));
+      }
+    }
+    int64_t moff = 0;
+    for (int l = 1; l <= depth; ++l) {
+      m16_off[l] = moff;
+      moff += (int64_t)256 * hm_plane_rows(l) * 16;
+    }
+    mult16.ensure(std::max<int64_t>(moff, 16));
+    hm_njobs = (int)jobs.size();
+    hm_jobs.ensure(sizeof(int4) * std::max<size_t>(jobs.size(), 1));
+    if (!jobs.empty())
+      LFMM_CUDA(cudaMemcpyAsync(hm_jobs.p, jobs.data(), sizeof(int4) * jobs.size(), cudaMemcpyHostToDevice, stream));
+    LFMM_CUDA(cudaStreamSynchronize(stream));
+    partial.ensure(tsz() * ncp * std::max<int64_t>(off, 1));
   }
 
   // M2L work split: partial slots per level so that every level gets enough
@@ -663,6 +830,7 @@ struct lfmm_plan {
     }
     job_start[depth + 1] = jobs;
     partial.ensure(tsz() * ncp * std::max<int64_t>(off, 1));
+    if (use_halo) plan_halo_jobs();
     // M2M child split: 8 partial slots of the largest parent level
     const int64_t top = depth >= 1 ? (1LL << (3 * (depth - 1))) : 1;
     up_part.ensure(tsz() * ncp * 8 * top);
@@ -771,6 +939,11 @@ struct lfmm_plan {
       dim3 grid(tiles_all(l) * ga.up_split, rowb);
       launch(ST_M2M, [&] { k_gemm_gather<T><<<grid, G_THREADS, 0, stream>>>(ga); });
     }
+    launch(ST_M2M, [&] {
+      k_box_charges<T><<<nblk(nleaf, 256), 256, 0, stream>>>(qs.as<double>(), leaf_start.as<int>(), depth,
+                                                             level_off[depth], ncp, M, boxq.as<double>(),
+                                                             counters.as<int>() + 2);
+    });
     if (lattice_mode != LFMM_LATTICE_OFF) {
       ga.mode = GEMM_ROOT;
       ga.level = 0;
@@ -782,7 +955,34 @@ struct lfmm_plan {
     if (depth >= 1) {
       // M2L of every level in one launch (terms split over CTAs), then the
       // L2L sweep adds the partial slots level by level
-      if (use_tc && sizeof(T) == 4) {
+      if (use_halo && sizeof(T) == 4) {
+        HaloArgs ha{};
+        ha.mult = reinterpret_cast<const float*>(mult.p);
+        ha.partial = reinterpret_cast<float*>(partial.p);
+        ha.ops16 = ops16.as<unsigned char>();
+        ha.jobs = hm_jobs.as<int4>();
+        ha.level_max = hm_level_max.as<unsigned int>();
+        ha.inv_r = hm_inv_r.as<float>();
+        ha.inv_c = hm_inv_c.as<float>();
+        ha.rw_cap = hm_rw_cap;
+        ha.mult16 = mult16.as<unsigned char>();
+        for (int l = 0; l <= depth; ++l) {
+          ha.level_off[l] = level_off[l];
+          ha.part_off[l] = part_off[l];
+          ha.m16_off[l] = m16_off[l];
+        }
+        LFMM_CUDA(cudaMemsetAsync(hm_level_max.p, 0, hm_level_max.bytes, stream));
+        launch(ST_DOWN, [&] {
+          k_level_absmax<<<dim3((unsigned)std::max<int64_t>(1, ((1LL << (3 * depth)) + 63) / 64), depth), 256, 0,
+                           stream>>>(ha.mult, ha, hm_level_max.as<unsigned int>());
+        });
+        launch(ST_DOWN, [&] {
+          k_pack_mult16<<<dim3((unsigned)((hm_plane_rows(depth) + 127) / 128), depth, 8), 128, 0, stream>>>(ha);
+        });
+        launch(ST_DOWN, [&] {
+          k_m2l_halo<<<hm_njobs, HM_THREADS, hm_smem_bytes(hm_rw_cap), stream>>>(ha);
+        });
+      } else if (use_tc && sizeof(T) == 4) {
         TcArgs ta{};
         ta.mult = reinterpret_cast<const float*>(mult.p);
         ta.partial = reinterpret_cast<float*>(partial.p);
@@ -1088,6 +1288,7 @@ int lfmm_plan_create(const double* positions, int64_t n, double box_length, int 
       const bool force_simt = env && std::string(env) == "simt";
       pl->use_tc = pl->fp32 && depth >= 1 && pl->nc > 64 && pl->nc <= 128 && !force_simt;
       if (pl->use_tc) pl->ncp = 128;
+      pl->use_halo = pl->use_tc && !(env && std::string(env) == "gather");
     }
     pl->nleaf = 1 << (3 * depth);
     pl->size = box_length / double(1 << depth);
@@ -1114,6 +1315,7 @@ int lfmm_plan_create(const double* positions, int64_t n, double box_length, int 
     pl->leaf_sorted.ensure(sizeof(int) * nn);
     pl->xq.ensure(4 * t * nn);
     pl->mult.ensure(t * pl->ncp * off);
+    pl->boxq.ensure(sizeof(double) * off);
     pl->loc.ensure(t * pl->ncp * off);
     LFMM_CUDA(cudaMemsetAsync(pl->mult.p, 0, pl->mult.bytes, pl->stream));
     LFMM_CUDA(cudaMemsetAsync(pl->loc.p, 0, pl->loc.bytes, pl->stream));
