@@ -16,3 +16,7 @@ clean:
 	rm -f $(LIB)
 
 .PHONY: all clean
+
+# profiling variant of the M2L kernel (per-CTA wait counters), never shipped
+prof: $(SRC)/lfmm_api.cu $(HDRS)
+	$(NVCC) $(NVFLAGS) -DLFMM_HM_PROF -shared -o paper_2410_01754_b200/_lib/liblfmm_prof.so $(SRC)/lfmm_api.cu -lcudart 2> /dev/null

@@ -13,7 +13,7 @@ import os
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "_lib", "liblfmm.so")
+LIB_PATH = os.environ.get("LFMM_LIB") or os.path.join(_HERE, "_lib", "liblfmm.so")
 
 LFMM_LATTICE = {"off": 0, "converged": 1, "shells": 2}
 F_DIPOLE, F_PERIODIC_NEAR, F_FP32, F_INTRA_MINIMUM = 1, 2, 4, 8

@@ -1245,6 +1245,16 @@ extern "C" {
 
 const char* lfmm_version(void) { return "lfmm-b200 0.1.0 sm_100a"; }
 
+#ifdef LFMM_HM_PROF
+// profiling build only: copy the per-CTA M2L timing records (tools/hm_prof.py)
+int lfmm_debug_hm_prof(unsigned long long* out, int64_t n) {
+  return guarded([&] {
+    LFMM_CUDA(cudaDeviceSynchronize());
+    LFMM_CUDA(cudaMemcpyFromSymbol(out, g_hm_prof, sizeof(unsigned long long) * 8 * std::min<int64_t>(n, 8192)));
+  });
+}
+#endif
+
 int lfmm_last_error(char* buf, int64_t len) {
   if (!buf || len <= 0) return LFMM_EINVAL;
   std::strncpy(buf, g_last_error.c_str(), (size_t)len - 1);

@@ -48,7 +48,7 @@ constexpr int HM_NMAX = 256;       // target rows per job (MMA N)
 constexpr int HM_KC = 16;          // coefficients per iteration (one f16 MMA K)
 constexpr int HM_NKC = 8;          // 128 / 16
 constexpr int HM_ATILE = 8192;     // one operator chunk: hi 4 KB | lo 4 KB
-constexpr int HM_ASTAGES = 8;
+constexpr int HM_ASTAGES = 14;
 constexpr int HM_THREADS = 352;
 constexpr int HM_WORKERS = 256;
 
@@ -219,12 +219,38 @@ __global__ void k_pack_mult16(HaloArgs g) {
   }
 }
 
+#ifdef LFMM_HM_PROF
+// profiling build only (tools/hm_prof.py): per CTA {start, end, wait halo,
+// wait acc_empty, wait a_full, terms, MMA issue end, smid}
+__device__ unsigned long long g_hm_prof[8192][8];
+#define HM_T0() const unsigned long long _t0 = clock64()
+#define HM_ACC(slot) atomicAdd(&g_hm_prof[blockIdx.x][slot], clock64() - _t0)
+#else
+#define HM_T0()
+#define HM_ACC(slot)
+#endif
+
 __global__ void __launch_bounds__(HM_THREADS, 1) k_m2l_halo(HaloArgs g) {
+#ifdef LFMM_HM_PROF
+  unsigned long long _tstart = 0;
+  if (threadIdx.x == 0) {
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(_tstart));
+    g_hm_prof[blockIdx.x][0] = _tstart;
+    unsigned sm;
+    asm volatile("mov.u32 %0, %%smid;" : "=r"(sm));
+    g_hm_prof[blockIdx.x][7] = sm;
+    for (int i = 2; i < 7; ++i) g_hm_prof[blockIdx.x][i] = 0;
+  }
+#endif
   extern __shared__ __align__(1024) unsigned char hm_smem_raw[];
   unsigned char* smem = reinterpret_cast<unsigned char*>(((uintptr_t)hm_smem_raw + 1023) & ~(uintptr_t)1023);
   __shared__ __align__(8) uint64_t halo_full[2], halo_empty[2], acc_full[2], acc_empty[2];
   __shared__ __align__(8) uint64_t a_full[HM_ASTAGES], a_empty[HM_ASTAGES];
   __shared__ uint32_t tmem_base_sh;
+  // the job's (tc, sc) term lists: B row offset (16-B units) and operator row
+  __shared__ uint32_t s_boff[2][27];
+  __shared__ int s_orow[2][27];
+  __shared__ int s_nt[2];
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int4 job = g.jobs[blockIdx.x];
@@ -249,6 +275,19 @@ __global__ void __launch_bounds__(HM_THREADS, 1) k_m2l_halo(HaloArgs g) {
       mbar_init(smem_u32(&a_empty[s]), 1);
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (tid >= 64 && tid < 64 + 2 * 27) {
+    const int k = (tid - 64) / 27, t = (tid - 64) % 27;
+    if (k < nsc) {
+      const int sc = tc ^ hm_group_rel(G, grp, k);
+      const int tab = tc * 8 + sc;
+      if (t == 0) s_nt[k] = c_hterm_n[tab];
+      if (t < c_hterm_n[tab]) {
+        const char4 d = c_hterm_d[tab * 27 + t];
+        s_boff[k][t] = (uint32_t)((d.x + 1) * rw + (Z + 1) + d.y * Z + d.z);
+        s_orow[k][t] = c_hterm_row[tab * 27 + t];
+      }
+    }
   }
   if (warp == 0) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(smem_u32(&tmem_base_sh)));
@@ -310,27 +349,44 @@ __global__ void __launch_bounds__(HM_THREADS, 1) k_m2l_halo(HaloArgs g) {
     if (lane == 0) {
       const uint32_t idesc = hm_idesc(N);
       const uint32_t lbo = 3u * rw * 16u;
+      // descriptors are advanced by adding (bytes >> 4) to the start-address
+      // field (shared addresses < 256 KB: no carry out of its 14 bits)
+      const uint64_t a_desc0 = hm_desc(smem_u32(abase), 128, 256);
       int stage = 0, aphase = 0;
       for (int it = 0; it < niter; ++it) {
-        const int sc = tc ^ hm_group_rel(G, grp, it / HM_NKC);
-        const int tab = tc * 8 + sc, nt = c_hterm_n[tab];
-        mbar_wait(smem_u32(&halo_full[it & 1]), (it >> 1) & 1);
-        if (it >= 2) mbar_wait(smem_u32(&acc_empty[it & 1]), ((it - 2) >> 1) & 1);
+        const int k = it / HM_NKC;
+        const int nt = s_nt[k];
+        {
+          HM_T0();
+          mbar_wait(smem_u32(&halo_full[it & 1]), (it >> 1) & 1);
+          HM_ACC(2);
+        }
+        {
+          HM_T0();
+          if (it >= 2) mbar_wait(smem_u32(&acc_empty[it & 1]), ((it - 2) >> 1) & 1);
+          HM_ACC(3);
+        }
         asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-        const uint32_t hb = smem_u32(smem + (it & 1) * bufb);
+        const uint64_t b_desc0 = hm_desc(smem_u32(smem + (it & 1) * bufb), lbo, 128);
+        const uint64_t b_lo = (2u * lbo) >> 4;
         const uint32_t dacc = tmem + (uint32_t)((it & 1) * 256);
+        uint32_t boff = s_boff[k][0];
         for (int t = 0; t < nt; ++t) {
-          const char4 d = c_hterm_d[tab * 27 + t];
-          const uint32_t row0 = (uint32_t)((d.x + 1) * rw + (Z + 1) + d.y * Z + d.z);
-          const uint32_t bh = hb + row0 * 16u, bl = bh + 2u * lbo;
-          mbar_wait(smem_u32(&a_full[stage]), aphase);
+          const uint64_t dbh = b_desc0 + boff;
+          if (t + 1 < nt) boff = s_boff[k][t + 1];
+          const uint64_t dah = a_desc0 + (uint64_t)(stage * (HM_ATILE >> 4));
+          {
+            HM_T0();
+            mbar_wait(smem_u32(&a_full[stage]), aphase);
+            HM_ACC(4);
+          }
+#ifdef LFMM_HM_PROF
+          atomicAdd(&g_hm_prof[blockIdx.x][5], 1ull);
+#endif
           asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-          const uint32_t ah = smem_u32(abase + stage * HM_ATILE), al = ah + 4096u;
-          const uint64_t dah = hm_desc(ah, 128, 256), dal = hm_desc(al, 128, 256);
-          const uint64_t dbh = hm_desc(bh, lbo, 128), dbl = hm_desc(bl, lbo, 128);
           hm_mma(dacc, dah, dbh, idesc, t > 0 ? 1u : 0u);
-          hm_mma(dacc, dah, dbl, idesc, 1u);
-          hm_mma(dacc, dal, dbh, idesc, 1u);
+          hm_mma(dacc, dah, dbh + b_lo, idesc, 1u);
+          hm_mma(dacc, dah + (4096 >> 4), dbh, idesc, 1u);
           tc_commit(smem_u32(&a_empty[stage]));
           if (++stage == HM_ASTAGES) {
             stage = 0;
@@ -340,6 +396,11 @@ __global__ void __launch_bounds__(HM_THREADS, 1) k_m2l_halo(HaloArgs g) {
         tc_commit(smem_u32(&acc_full[it & 1]));
         tc_commit(smem_u32(&halo_empty[it & 1]));
       }
+#ifdef LFMM_HM_PROF
+      unsigned long long te;
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(te));
+      g_hm_prof[blockIdx.x][6] = te;
+#endif
     }
     __syncwarp();
   } else if (warp == 9) {
@@ -347,12 +408,12 @@ __global__ void __launch_bounds__(HM_THREADS, 1) k_m2l_halo(HaloArgs g) {
     if (lane == 0) {
       int stage = 0, ephase = 0, uses = 0;
       for (int it = 0; it < niter; ++it) {
-        const int sc = tc ^ hm_group_rel(G, grp, it / HM_NKC);
+        const int k = it / HM_NKC;
         const int kc = it % HM_NKC;
-        const int tab = tc * 8 + sc, nt = c_hterm_n[tab];
+        const int nt = s_nt[k];
         for (int t = 0; t < nt; ++t) {
+          const int row = s_orow[k][t];
           if (uses >= HM_ASTAGES) mbar_wait(smem_u32(&a_empty[stage]), ephase);
-          const int row = c_hterm_row[tab * 27 + t];
           bulk_load(smem_u32(abase + stage * HM_ATILE), g.ops16 + ((size_t)row * HM_NKC + kc) * HM_ATILE, HM_ATILE,
                     smem_u32(&a_full[stage]));
           ++uses;
@@ -392,6 +453,13 @@ __global__ void __launch_bounds__(HM_THREADS, 1) k_m2l_halo(HaloArgs g) {
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
   __syncthreads();
   if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem));
+#ifdef LFMM_HM_PROF
+  if (threadIdx.x == 0) {
+    unsigned long long te;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(te));
+    g_hm_prof[blockIdx.x][1] = te;
+  }
+#endif
 }
 
 }  // namespace lfmm
