@@ -429,6 +429,7 @@ struct lfmm_plan {
   // expansions / operators
   bool use_tc = false;    // M2L on tcgen05 (fp32, (p+1)^2 <= 128)
   bool use_halo = false;  // ... as shifted-window fp16x3 GEMMs (lfmm_m2l_halo.cuh)
+  bool p2p_scalar = false;  // fp32 P2P on the scalar kernel (LFMM_P2P=scalar, A/B checks)
   DevBuf ops_tc, up_part, up_cnt, counters;
   DevBuf ops16, hm_inv_r, hm_inv_c, hm_jobs, hm_level_max, mult16;
   int64_t m16_off[DMAX + 2] = {0};
@@ -714,6 +715,10 @@ struct lfmm_plan {
       });
       LFMM_CUDA(cudaFuncSetAttribute(k_m2l_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, TC_SMEM_WS));
     }
+    if (fp32) {
+      LFMM_CUDA(cudaFuncSetAttribute(k_p2p2<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, P2P2_SMEM));
+      LFMM_CUDA(cudaFuncSetAttribute(k_p2p2<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, P2P2_SMEM));
+    }
     LFMM_CUDA(cudaStreamSynchronize(stream));
     vecs.release();
     vals.release();
@@ -918,6 +923,18 @@ struct lfmm_plan {
     const int periodic = (flags & LFMM_F_PERIODIC_NEAR) ? 1 : 0;
     const unsigned lb = nblk(nleaf, P2P_WARPS);
     launch(ST_P2P, [&] {
+      if (sizeof(T) == 4 && !p2p_scalar) {
+        const unsigned lb2 = nblk(nleaf, P2P2_WARPS);
+        if (grad)
+          k_p2p2<true><<<lb2, P2P2_WARPS * 32, P2P2_SMEM, stream>>>(reinterpret_cast<const float4*>(xq.p), leaf_start.as<int>(),
+                                                                      depth, (float)size, periodic, vnear.as<float>(),
+                                                                      gnear.as<float>());
+        else
+          k_p2p2<false><<<lb2, P2P2_WARPS * 32, P2P2_SMEM, stream>>>(reinterpret_cast<const float4*>(xq.p), leaf_start.as<int>(),
+                                                               depth, (float)size, periodic, vnear.as<float>(),
+                                                               gnear.as<float>());
+        return;
+      }
       if (grad)
         k_p2p<T, true><<<lb, P2P_WARPS * 32, 0, stream>>>(xq.as<vec4_t<T>>(), leaf_start.as<int>(), depth, tsize,
                                                            periodic, vnear.as<T>(), gnear.as<T>());
@@ -1299,6 +1316,8 @@ int lfmm_plan_create(const double* positions, int64_t n, double box_length, int 
       pl->use_tc = pl->fp32 && depth >= 1 && pl->nc > 64 && pl->nc <= 128 && !force_simt;
       if (pl->use_tc) pl->ncp = 128;
       pl->use_halo = pl->use_tc && !(env && std::string(env) == "gather");
+      const char* penv = std::getenv("LFMM_P2P");
+      pl->p2p_scalar = penv && std::string(penv) == "scalar";
     }
     pl->nleaf = 1 << (3 * depth);
     pl->size = box_length / double(1 << depth);

@@ -97,4 +97,275 @@ __global__ void __launch_bounds__(P2P_WARPS * 32) k_p2p(const vec4_t<T>* __restr
   }
 }
 
+
+// ------------------------------------------------------------------------
+// fp32 near field on packed f32x2 arithmetic (FADD2/FMUL2/FFMA2, sm_100).
+//
+// One warp per target leaf.  The leaf's whole 27-image neighbourhood is
+// staged once in shared memory, shifted into the target leaf's frame, as
+// pairs of sources in SoA form (x_k, x_k+1, y_k, y_k+1 | z_k, z_k+1, q_k,
+// q_k+1), so one lane processes two sources per step with packed
+// instructions (two MUFU.RSQ).  Staged order: the home image first (the only
+// one where the self pair can occur, masked there), then the 26 others.
+// Lane use: a leaf's targets run in passes of up to 32; a pass with r < 32
+// targets splits the sources over P = 2^k <= 32 / r lane groups, which are
+// reduced with xor shuffles at the end (keeps ~91% of lanes busy on water,
+// where leaves hold 9..55 atoms).  Neighbourhoods longer than one staging
+// buffer are processed in chunks.  Every output is the sum of a fixed
+// sequence of operations: reruns are bit identical.
+constexpr int P2P2_WARPS = 4;
+constexpr int P2P2_SMAX = 512;  // staged sources per warp and chunk (even): 32 KB per CTA, 6 CTAs/SM
+constexpr int P2P2_SMEM = P2P2_WARPS * P2P2_SMAX * 16;  // dynamic shared memory per CTA
+
+__device__ __forceinline__ uint64_t f2pack(float a, float b) {
+  uint64_t r;
+  asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(a), "f"(b));
+  return r;
+}
+__device__ __forceinline__ void f2unpack(uint64_t v, float& a, float& b) {
+  asm("mov.b64 {%0, %1}, %2;" : "=f"(a), "=f"(b) : "l"(v));
+}
+__device__ __forceinline__ uint64_t f2add(uint64_t a, uint64_t b) {
+  uint64_t r;
+  asm("add.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
+  return r;
+}
+__device__ __forceinline__ uint64_t f2sub(uint64_t a, uint64_t b) {
+  uint64_t r;
+  asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
+  return r;
+}
+__device__ __forceinline__ uint64_t f2mul(uint64_t a, uint64_t b) {
+  uint64_t r;
+  asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
+  return r;
+}
+__device__ __forceinline__ uint64_t f2fma(uint64_t a, uint64_t b, uint64_t c) {
+  uint64_t r;
+  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(r) : "l"(a), "l"(b), "l"(c));
+  return r;
+}
+__device__ __forceinline__ float rsqrt_fast(float x) {
+  float r;
+  asm("rsqrt.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
+  return r;
+}
+
+// two sources (pair index k) against one target; MASK: zero the pair halves
+// whose staged index equals `self`
+template <bool GRAD, bool MASK>
+__device__ __forceinline__ void p2p2_step(const float4* __restrict__ A, const float4* __restrict__ B, int k,
+                                          uint64_t x2, uint64_t y2, uint64_t z2, int self, uint64_t& v2,
+                                          uint64_t& gx2, uint64_t& gy2, uint64_t& gz2) {
+  const float4 a = A[k], b = B[k];
+  const uint64_t dx = f2sub(x2, f2pack(a.x, a.y));
+  const uint64_t dy = f2sub(y2, f2pack(a.z, a.w));
+  const uint64_t dz = f2sub(z2, f2pack(b.x, b.y));
+  uint64_t r2 = f2mul(dx, dx);
+  r2 = f2fma(dy, dy, r2);
+  r2 = f2fma(dz, dz, r2);
+  float ra, rb;
+  f2unpack(r2, ra, rb);
+  float ia = rsqrt_fast(ra), ib = rsqrt_fast(rb);
+  if (MASK) {
+    ia = (2 * k == self) ? 0.f : ia;
+    ib = (2 * k + 1 == self) ? 0.f : ib;
+  }
+  const uint64_t inv = f2pack(ia, ib);
+  const uint64_t qi = f2mul(f2pack(b.z, b.w), inv);
+  v2 = f2add(v2, qi);
+  if (GRAD) {
+    const uint64_t q3 = f2mul(qi, f2mul(inv, inv));
+    gx2 = f2fma(dx, q3, gx2);
+    gy2 = f2fma(dy, q3, gy2);
+    gz2 = f2fma(dz, q3, gz2);
+  }
+}
+
+// The potential is summed in two levels: blocks of <= 32 pair terms into a
+// fresh fp32 partial, partials into a Kahan-compensated total.  A leaf's
+// ~1800 terms summed into one fp32 running sum leave ~1e-5 absolute error,
+// which small near-neutral systems turn into ~3e-4 relative energy error (the
+// reference's "single" mode rounds only once per stage, solver.py:95-102).
+__device__ __forceinline__ void kahan_fold(uint64_t& v2, uint64_t& c2, uint64_t p2) {
+  const uint64_t y = f2sub(p2, c2);
+  const uint64_t t = f2add(v2, y);
+  c2 = f2sub(f2sub(t, v2), y);
+  v2 = t;
+}
+
+template <bool GRAD>
+__global__ void __launch_bounds__(P2P2_WARPS * 32) k_p2p2(const float4* __restrict__ xq,
+                                                          const int* __restrict__ leaf_start, int depth,
+                                                          float size, int periodic, float* __restrict__ vout,
+                                                          float* __restrict__ gout) {
+  extern __shared__ float4 p2p2_smem[];  // [warp][A | B][SMAX / 2]
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int b = blockIdx.x * P2P2_WARPS + w;
+  const int nleaf = 1 << (3 * depth);
+  if (b >= nleaf) return;
+  float4* A = p2p2_smem + (size_t)w * P2P2_SMAX;
+  float4* B = A + P2P2_SMAX / 2;
+  const int t0 = leaf_start[b], n = leaf_start[b + 1] - t0;
+  if (n == 0) return;
+  // images: lane t < nimg holds image t (home = lane 0) — start, count, shift
+  const int nimg = periodic ? 27 : 1;
+  int i_start = 0, i_cnt = 0;
+  float i_ox = 0.f, i_oy = 0.f, i_oz = 0.f;
+  if (lane < nimg) {
+    // lane 0 = home image (row 13); lanes 1..26 = rows 0..12, 14..26
+    const int t = (lane == 0 || !periodic) ? 13 : (lane <= 13 ? lane - 1 : lane);
+    int nb, sx, sy, sz;
+    neighbor(b, t, depth, nb, sx, sy, sz);
+    i_start = leaf_start[nb];
+    i_cnt = leaf_start[nb + 1] - i_start;
+    i_ox = (float)(t / 9 - 1) * size;
+    i_oy = (float)((t / 3) % 3 - 1) * size;
+    i_oz = (float)(t % 3 - 1) * size;
+  }
+  // staged offsets: home [0, nh2), others packed from nh2 (each image
+  // contiguous), total padded to even
+  const int nh2 = (n + 1) & ~1;
+  int excl = i_cnt;  // inclusive scan over lanes 1..nimg-1 of the other images
+  if (lane == 0) excl = 0;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int y = __shfl_up_sync(0xffffffffu, excl, o);
+    if (lane >= o) excl += y;
+  }
+  const int i_off = (lane == 0) ? 0 : nh2 + excl - i_cnt;  // staged offset of my image
+  const int s_rest = __shfl_sync(0xffffffffu, excl, 31);   // other images' sources
+  const int total = nh2 + ((s_rest + 1) & ~1);
+  const int nchunk = (total + P2P2_SMAX - 1) / P2P2_SMAX;
+
+  for (int pb = 0; pb < n; pb += 32) {
+    const int nt = min(32, n - pb);
+    int P = 1;
+    while (P < 32 && nt * (2 * P) <= 32) P *= 2;
+    const int W = 32 / P, slot = lane & (W - 1), part = lane / W;
+    const bool act = slot < nt;
+    const int ti = t0 + pb + (act ? slot : 0);
+    const float4 me = xq[ti];
+    const uint64_t x2 = f2pack(me.x, me.x), y2 = f2pack(me.y, me.y), z2 = f2pack(me.z, me.z);
+    const int self = pb + slot;  // staged index of my target in the home block
+    uint64_t v2 = 0, c2 = 0, gx2 = 0, gy2 = 0, gz2 = 0;
+    for (int c = 0; c < nchunk; ++c) {
+      const int cb = c * P2P2_SMAX, ce = min(total, cb + P2P2_SMAX);
+      if (nchunk > 1 || pb == 0) {
+        // ---- stage entries [cb, ce) ----
+        __syncwarp();
+        for (int im = 0; im < nimg; ++im) {
+          const int off = __shfl_sync(0xffffffffu, i_off, im), cnt = __shfl_sync(0xffffffffu, i_cnt, im);
+          const int st = __shfl_sync(0xffffffffu, i_start, im);
+          const float ox = __shfl_sync(0xffffffffu, i_ox, im), oy = __shfl_sync(0xffffffffu, i_oy, im),
+                      oz = __shfl_sync(0xffffffffu, i_oz, im);
+          const int lo = max(off, cb), hi = min(off + cnt, ce);
+          for (int e = lo + lane; e < hi; e += 32) {
+            const float4 s = xq[st + (e - off)];
+            float* a = reinterpret_cast<float*>(&A[(e - cb) >> 1]);
+            float* bb = reinterpret_cast<float*>(&B[(e - cb) >> 1]);
+            const int h = e & 1;
+            a[h] = s.x + ox;
+            a[2 + h] = s.y + oy;
+            bb[h] = s.z + oz;
+            bb[2 + h] = s.w;
+          }
+        }
+        // padding entries (home pad at n when n is odd, tail pad at total-1)
+        if (lane < 2) {
+          const int e = lane == 0 ? n : total - 1;
+          const bool pad = lane == 0 ? (n & 1) : ((s_rest & 1) != 0);
+          if (pad && e >= cb && e < ce) {
+            float* a = reinterpret_cast<float*>(&A[(e - cb) >> 1]);
+            float* bb = reinterpret_cast<float*>(&B[(e - cb) >> 1]);
+            const int h = e & 1;
+            a[h] = 1.0e4f;
+            a[2 + h] = 1.0e4f;
+            bb[h] = 1.0e4f;
+            bb[2 + h] = 0.f;
+          }
+        }
+        __syncwarp();
+      }
+      // ---- home block (self masked): pairs [cb, min(ce, nh2)) ----
+      {
+        const int lo = cb >> 1, hi = max(lo, min(ce, nh2) >> 1);
+        const int np = hi - lo;
+        const int k0 = lo + (np * part) / P, k1 = lo + (np * (part + 1)) / P;
+        uint64_t p2 = 0;
+        for (int k = k0; k < k1; ++k)
+          p2p2_step<GRAD, true>(A - (cb >> 1), B - (cb >> 1), k, x2, y2, z2, self, p2, gx2, gy2, gz2);
+        kahan_fold(v2, c2, p2);
+      }
+      // ---- other images: pairs [max(cb, nh2), ce) ----
+      {
+        const int lo = max(cb, nh2) >> 1, hi = max(lo, ce >> 1);
+        const int np = hi - lo;
+        const int k0 = lo + (np * part) / P, k1 = lo + (np * (part + 1)) / P;
+        const float4* Ab = A - (cb >> 1);
+        const float4* Bb = B - (cb >> 1);
+        // two independent accumulator sets per step pair (ILP); potential
+        // partials folded every 16 steps
+        uint64_t hx2 = 0, hy2 = 0, hz2 = 0;
+        int k = k0;
+#pragma unroll 1
+        for (; k + 16 <= k1; k += 16) {
+          uint64_t p2 = 0, q2 = 0;
+#pragma unroll
+          for (int u = 0; u < 16; u += 2) {
+            p2p2_step<GRAD, false>(Ab, Bb, k + u, x2, y2, z2, 0, p2, gx2, gy2, gz2);
+            p2p2_step<GRAD, false>(Ab, Bb, k + u + 1, x2, y2, z2, 0, q2, hx2, hy2, hz2);
+          }
+          kahan_fold(v2, c2, f2add(p2, q2));
+        }
+        {
+          uint64_t p2 = 0, q2 = 0;
+#pragma unroll 1
+          for (; k + 2 <= k1; k += 2) {
+            p2p2_step<GRAD, false>(Ab, Bb, k, x2, y2, z2, 0, p2, gx2, gy2, gz2);
+            p2p2_step<GRAD, false>(Ab, Bb, k + 1, x2, y2, z2, 0, q2, hx2, hy2, hz2);
+          }
+          if (k < k1) p2p2_step<GRAD, false>(Ab, Bb, k, x2, y2, z2, 0, q2, hx2, hy2, hz2);
+          kahan_fold(v2, c2, f2add(p2, q2));
+        }
+        if (GRAD) {
+          gx2 = f2add(gx2, hx2);
+          gy2 = f2add(gy2, hy2);
+          gz2 = f2add(gz2, hz2);
+        }
+      }
+    }
+    float v, gx, gy, gz, u;
+    {
+      float ca, cb2;
+      f2unpack(c2, ca, cb2);
+      f2unpack(v2, v, u);
+      v = (v - ca) + (u - cb2);
+    }
+    f2unpack(gx2, gx, u);
+    gx += u;
+    f2unpack(gy2, gy, u);
+    gy += u;
+    f2unpack(gz2, gz, u);
+    gz += u;
+    for (int m = 16; m >= W; m >>= 1) {
+      v += __shfl_xor_sync(0xffffffffu, v, m);
+      if (GRAD) {
+        gx += __shfl_xor_sync(0xffffffffu, gx, m);
+        gy += __shfl_xor_sync(0xffffffffu, gy, m);
+        gz += __shfl_xor_sync(0xffffffffu, gz, m);
+      }
+    }
+    if (act && part == 0) {
+      const int i = t0 + pb + slot;
+      vout[i] = v;
+      if (GRAD) {
+        gout[3 * (size_t)i] = -gx;
+        gout[3 * (size_t)i + 1] = -gy;
+        gout[3 * (size_t)i + 2] = -gz;
+      }
+    }
+  }
+}
+
 }  // namespace lfmm

@@ -1,0 +1,3 @@
+timeout 300 python -m pytest tests/test_gpu_hi.py -x -q -k "single and minimum" 2>&1 | grep -E "Error|assert|where|relerr" | head -20
+timeout 600 ncu --set full --import-source on --clock-control none -k regex:k_p2p2 -c 1 -o gpurun_out/p2p2 python bench.py --steps 1 --warmup 3 --no-cpu-baseline > gpurun_out/ncu_p2p.log 2>&1
+tail -2 gpurun_out/ncu_p2p.log

@@ -1,0 +1,3 @@
+python tools/diag_small.py
+timeout 900 python -m pytest tests -m gpu -q 2>&1 | tail -4
+bash tools/gpu_bench.sh

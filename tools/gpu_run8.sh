@@ -1,0 +1,3 @@
+python tools/diag_small.py
+timeout 600 python -m pytest tests/test_gpu_hi.py tests/test_gpu_solve.py -q -x 2>&1 | tail -2
+bash tools/gpu_bench.sh
