@@ -945,6 +945,11 @@ struct lfmm_plan {
     T* M = mult.as<T>();
     T* Lc = loc.as<T>();
     launch(ST_P2M, [&] {
+      if (p == 10) {
+        k_p2m_c<T, 10><<<nblk(nleaf, EXP_WARPS), EXP_WARPS * 32, 0, stream>>>(
+            xq.as<vec4_t<T>>(), leaf_start.as<int>(), depth, (T)(1.0 / size), ncp, M + level_off[depth] * ncp);
+        return;
+      }
       k_p2m<T><<<nblk(nleaf, EXP_WARPS), EXP_WARPS * 32, 0, stream>>>(
           xq.as<vec4_t<T>>(), leaf_start.as<int>(), depth, p, (T)(1.0 / size), ncp, M + level_off[depth] * ncp);
     });
@@ -1031,6 +1036,28 @@ struct lfmm_plan {
       while (warps > 1 && (size_t)warps * per_warp * sizeof(T) > 48 * 1024) warps >>= 1;
       const size_t smem = (size_t)warps * per_warp * sizeof(T);
       launch(ST_L2P, [&] {
+        if (p == 10 && sizeof(T) == 4) {
+          if (grad)
+            k_l2p_f2<true, 10><<<nblk(nleaf, EXP_WARPS), EXP_WARPS * 32, 0, stream>>>(
+                reinterpret_cast<const float4*>(xq.p), leaf_start.as<int>(), depth, (float)size, ncp,
+                reinterpret_cast<const float*>(Lc + level_off[depth] * ncp), vfar.as<float>(), gfar.as<float>());
+          else
+            k_l2p_f2<false, 10><<<nblk(nleaf, EXP_WARPS), EXP_WARPS * 32, 0, stream>>>(
+                reinterpret_cast<const float4*>(xq.p), leaf_start.as<int>(), depth, (float)size, ncp,
+                reinterpret_cast<const float*>(Lc + level_off[depth] * ncp), vfar.as<float>(), gfar.as<float>());
+          return;
+        }
+        if (p == 10) {
+          if (grad)
+            k_l2p_c<T, true, 10><<<nblk(nleaf, EXP_WARPS), EXP_WARPS * 32, 0, stream>>>(
+                xq.as<vec4_t<T>>(), leaf_start.as<int>(), depth, tsize, ncp, Lc + level_off[depth] * ncp,
+                vfar.as<T>(), gfar.as<T>());
+          else
+            k_l2p_c<T, false, 10><<<nblk(nleaf, EXP_WARPS), EXP_WARPS * 32, 0, stream>>>(
+                xq.as<vec4_t<T>>(), leaf_start.as<int>(), depth, tsize, ncp, Lc + level_off[depth] * ncp,
+                vfar.as<T>(), gfar.as<T>());
+          return;
+        }
         if (grad)
           k_l2p<T, true><<<nblk(nleaf, warps), warps * 32, smem, stream>>>(
               xq.as<vec4_t<T>>(), leaf_start.as<int>(), depth, p, tsize, ncp, Lc + level_off[depth] * ncp,

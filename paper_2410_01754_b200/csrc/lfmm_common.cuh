@@ -108,6 +108,38 @@ struct Vec4<double> {
 template <class T>
 using vec4_t = typename Vec4<T>::type;
 
+// packed fp32 pairs (FADD2 / FMUL2 / FFMA2 on sm_100): a uint64_t holds
+// (lo, hi) floats
+__device__ __forceinline__ uint64_t f2pack(float a, float b) {
+  uint64_t r;
+  asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(a), "f"(b));
+  return r;
+}
+__device__ __forceinline__ void f2unpack(uint64_t v, float& a, float& b) {
+  asm("mov.b64 {%0, %1}, %2;" : "=f"(a), "=f"(b) : "l"(v));
+}
+__device__ __forceinline__ uint64_t f2add(uint64_t a, uint64_t b) {
+  uint64_t r;
+  asm("add.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
+  return r;
+}
+__device__ __forceinline__ uint64_t f2sub(uint64_t a, uint64_t b) {
+  uint64_t r;
+  asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
+  return r;
+}
+__device__ __forceinline__ uint64_t f2mul(uint64_t a, uint64_t b) {
+  uint64_t r;
+  asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
+  return r;
+}
+__device__ __forceinline__ uint64_t f2fma(uint64_t a, uint64_t b, uint64_t c) {
+  uint64_t r;
+  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(r) : "l"(a), "l"(b), "l"(c));
+  return r;
+}
+
+
 __device__ __forceinline__ float rsqrt_t(float x) { return rsqrtf(x); }
 __device__ __forceinline__ double rsqrt_t(double x) { return rsqrt(x); }
 
@@ -133,6 +165,43 @@ __device__ __forceinline__ void regular_stream(T x, T y, T z, int p, F&& f) {
       f(m, m + 1, p1r, p1i);
       for (int l = m + 2; l <= p; ++l) {
         const T c = inv_lm<T>(l, m);
+        const T a = T(2 * l - 1) * z;
+        const T nr = (a * p1r - r2 * p2r) * c;
+        const T ni = (a * p1i - r2 * p2i) * c;
+        p2r = p1r;
+        p2i = p1i;
+        p1r = nr;
+        p1i = ni;
+        f(m, l, nr, ni);
+      }
+    }
+  }
+}
+
+// Compile-time-order variant of regular_stream: every loop unrolls, the
+// reciprocals become immediates, and f sees constant (m, l) — used by the
+// P2M/L2P kernels for the orders the benchmarks run.
+template <class T, int P, class F>
+__device__ __forceinline__ void regular_stream_c(T x, T y, T z, F&& f) {
+  const T r2 = x * x + y * y + z * z;
+  T mr = T(1), mi = T(0);
+#pragma unroll
+  for (int m = 0; m <= P; ++m) {
+    if (m > 0) {
+      const T c = T(1) / T(2 * m);
+      const T nr = (mr * x - mi * y) * c;
+      const T ni = (mr * y + mi * x) * c;
+      mr = nr;
+      mi = ni;
+    }
+    f(m, m, mr, mi);
+    if (m + 1 <= P) {
+      T p2r = mr, p2i = mi;
+      T p1r = z * mr, p1i = z * mi;
+      f(m, m + 1, p1r, p1i);
+#pragma unroll
+      for (int l = m + 2; l <= P; ++l) {
+        const T c = T(1) / T((l + m) * (l - m));
         const T a = T(2 * l - 1) * z;
         const T nr = (a * p1r - r2 * p2r) * c;
         const T ni = (a * p1i - r2 * p2i) * c;

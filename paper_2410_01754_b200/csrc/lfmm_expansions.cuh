@@ -76,6 +76,61 @@ __global__ void __launch_bounds__(EXP_WARPS * 32) k_p2m(const vec4_t<T>* __restr
   }
 }
 
+// Compile-time-order P2M: the transpose tile columns are static, so the
+// recurrence, the tile stores and the column sums fully unroll.
+template <class T, int P>
+__global__ void __launch_bounds__(EXP_WARPS * 32) k_p2m_c(const vec4_t<T>* __restrict__ xq,
+                                                          const int* __restrict__ leaf_start, int depth,
+                                                          T inv_size, int ncp, T* __restrict__ mult) {
+  constexpr int NC = (P + 1) * (P + 1);
+  constexpr int NF = (NC + 31) / 32;  // flushes of 32 coefficients
+  __shared__ T buf[EXP_WARPS][32][33];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int b = blockIdx.x * EXP_WARPS + w;
+  const int nleaf = 1 << (3 * depth);
+  if (b >= nleaf) return;
+  T* out = mult + (size_t)b * ncp;
+  const int t0 = leaf_start[b], t1 = leaf_start[b + 1];
+  T(*tb)[33] = buf[w];
+  T acc[NF];
+#pragma unroll
+  for (int f = 0; f < NF; ++f) acc[f] = T(0);
+  for (int tc = t0; tc < t1; tc += 32) {
+    const int i = tc + lane;
+    T x = 0, y = 0, z = 0, q = 0;
+    if (i < t1) {
+      const vec4_t<T> v = xq[i];
+      x = v.x * inv_size;
+      y = v.y * inv_size;
+      z = v.z * inv_size;
+      q = v.w;
+    }
+    int col = 0, fl = 0;
+    auto flush = [&]() {
+      __syncwarp();
+      T s = T(0);
+#pragma unroll 8
+      for (int k = 0; k < 32; ++k) s += tb[lane][k];
+      if (lane < col) acc[fl] += s;
+      __syncwarp();
+      ++fl;
+      col = 0;
+    };
+    regular_stream_c<T, P>(x, y, z, [&](int m, int l, T re, T im) {
+      tb[col][lane] = q * re;
+      if (++col == 32) flush();
+      if (m > 0) {
+        tb[col][lane] = q * im;
+        if (++col == 32) flush();
+      }
+    });
+    if (col > 0) flush();
+  }
+#pragma unroll
+  for (int f = 0; f < NF; ++f)
+    if (f * 32 + lane < NC) out[f * 32 + lane] = acc[f];
+}
+
 // ---------------------------------------------------------------- L2P ----
 // Warp per leaf.  The leaf local L^ and its three gradient coefficient
 // vectors (order p-1, G_x = (L_{j+1}^{k+1} - L_{j+1}^{k-1})/2,
@@ -182,6 +237,262 @@ __global__ void __launch_bounds__(EXP_WARPS * 32) k_l2p(const vec4_t<T>* __restr
         gout[3 * (size_t)i] = dx * s2;
         gout[3 * (size_t)i + 1] = dy * s2;
         gout[3 * (size_t)i + 2] = dz * s2;
+      }
+    }
+  }
+}
+
+// Compile-time-order L2P(+gradient): same contraction as k_l2p with static
+// shared-memory offsets (broadcast loads) and an unrolled recurrence.
+template <class T, bool GRAD, int P>
+__global__ void __launch_bounds__(EXP_WARPS * 32) k_l2p_c(const vec4_t<T>* __restrict__ xq,
+                                                          const int* __restrict__ leaf_start, int depth,
+                                                          T size, int ncp, const T* __restrict__ loc,
+                                                          T* __restrict__ vout, T* __restrict__ gout) {
+  constexpr int NC = (P + 1) * (P + 1), NG = P * P;
+  __shared__ T sh[EXP_WARPS][NC + 3 * NG];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  T* Lh = sh[w];
+  T* Gx = Lh + NC;
+  T* Gy = Gx + NG;
+  T* Gz = Gy + NG;
+  const int b = blockIdx.x * (blockDim.x >> 5) + w;
+  const int nleaf = 1 << (3 * depth);
+  if (b >= nleaf) return;
+  const int t0 = leaf_start[b], t1 = leaf_start[b + 1];
+  if (t1 == t0) return;
+  const T* src = loc + (size_t)b * ncp;
+  for (int c = lane; c < NC; c += 32) Lh[c] = src[c];
+  __syncwarp();
+  if (GRAD) {
+    constexpr int Q = P - 1;
+    for (int a = lane; a < NG; a += 32) {
+      int j, k, part;
+      pk_decode(Q, a, j, k, part);
+      T ar, ai, br, bi, cr, ci;
+      ld_full(Lh, P, j + 1, k + 1, ar, ai);
+      ld_full(Lh, P, j + 1, k - 1, br, bi);
+      ld_full(Lh, P, j + 1, k, cr, ci);
+      const T gxr = T(0.5) * (ar - br), gxi = T(0.5) * (ai - bi);
+      const T gyr = T(-0.5) * (ai + bi), gyi = T(0.5) * (ar + br);
+      Gx[a] = part ? gxi : gxr;
+      Gy[a] = part ? gyi : gyr;
+      Gz[a] = part ? ci : cr;
+    }
+    __syncwarp();
+  }
+  const T inv_s = T(1) / size;
+  for (int tc = t0; tc < t1; tc += 32) {
+    const int i = tc + lane;
+    const bool act = i < t1;
+    T x = 0, y = 0, z = 0;
+    if (act) {
+      const vec4_t<T> v = xq[i];
+      x = v.x * inv_s;
+      y = v.y * inv_s;
+      z = v.z * inv_s;
+    }
+    T V = 0, dx = 0, dy = 0, dz = 0;
+    int a = 0, g = 0;
+    regular_stream_c<T, P>(x, y, z, [&](int m, int l, T re, T im) {
+      if (m == 0) {
+        V = fma(Lh[a], re, V);
+        ++a;
+        if (GRAD && l < P) {
+          dx = fma(Gx[g], re, dx);
+          dy = fma(Gy[g], re, dy);
+          dz = fma(Gz[g], re, dz);
+          ++g;
+        }
+      } else {
+        V += T(2) * (Lh[a] * re - Lh[a + 1] * im);
+        a += 2;
+        if (GRAD && l < P) {
+          dx += T(2) * (Gx[g] * re - Gx[g + 1] * im);
+          dy += T(2) * (Gy[g] * re - Gy[g + 1] * im);
+          dz += T(2) * (Gz[g] * re - Gz[g + 1] * im);
+          g += 2;
+        }
+      }
+    });
+    if (act) {
+      vout[i] = V * inv_s;
+      if (GRAD) {
+        const T s2 = inv_s * inv_s;
+        gout[3 * (size_t)i] = dx * s2;
+        gout[3 * (size_t)i + 1] = dy * s2;
+        gout[3 * (size_t)i + 2] = dz * s2;
+      }
+    }
+  }
+}
+
+// fp32 L2P(+gradient) on packed pairs: the complex (m > 0) coefficients are
+// staged as (2 Re, -2 Im) float2 so each term is one FFMA2 against the
+// (Re R, Im R) pair the recurrence produces (also in packed form); real
+// m = 0 terms stay scalar.  V = vs + acc.x + acc.y.
+template <bool GRAD, int P>
+__global__ void __launch_bounds__(EXP_WARPS * 32) k_l2p_f2(const float4* __restrict__ xq,
+                                                           const int* __restrict__ leaf_start, int depth,
+                                                           float size, int ncp, const float* __restrict__ loc,
+                                                           float* __restrict__ vout, float* __restrict__ gout) {
+  constexpr int Q = P - 1;
+  constexpr int NCC = P * (P + 1) / 2, NQC = Q * (Q + 1) / 2;  // complex coefficients (m > 0)
+  __shared__ float s0[EXP_WARPS][4][P + 1];                      // m = 0: L, Gx, Gy, Gz
+  __shared__ float2 sc[EXP_WARPS][NCC + 3 * NQC];                // m > 0: L | Gx | Gy | Gz
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int b = blockIdx.x * (blockDim.x >> 5) + w;
+  const int nleaf = 1 << (3 * depth);
+  if (b >= nleaf) return;
+  const int t0 = leaf_start[b], t1 = leaf_start[b + 1];
+  if (t1 == t0) return;
+  const float* Lh = loc + (size_t)b * ncp;
+  // ---- stage L and the gradient ladder G (harmonics.py:106-130) ----
+  for (int e = lane; e < (P + 1) + NCC; e += 32) {
+    if (e <= P) {
+      s0[w][0][e] = Lh[e];
+    } else {
+      const int a = (P + 1) + 2 * (e - (P + 1));
+      sc[w][e - (P + 1)] = make_float2(2.f * Lh[a], -2.f * Lh[a + 1]);
+    }
+  }
+  if (GRAD) {
+    for (int e = lane; e < (Q + 1) + NQC; e += 32) {
+      int j, k;
+      if (e <= Q) {
+        j = e;
+        k = 0;
+      } else {  // m-major packed order of the order-Q complex block
+        int r = e - (Q + 1);
+        k = 1;
+        while (r >= Q + 1 - k) {
+          r -= Q + 1 - k;
+          ++k;
+        }
+        j = k + r;
+      }
+      float ar, ai, br, bi, cr, ci;
+      ld_full(Lh, P, j + 1, k + 1, ar, ai);
+      ld_full(Lh, P, j + 1, k - 1, br, bi);
+      ld_full(Lh, P, j + 1, k, cr, ci);
+      const float gxr = 0.5f * (ar - br), gxi = 0.5f * (ai - bi);
+      const float gyr = -0.5f * (ai + bi), gyi = 0.5f * (ar + br);
+      if (e <= Q) {
+        s0[w][1][e] = gxr;
+        s0[w][2][e] = gyr;
+        s0[w][3][e] = cr;
+      } else {
+        const int c = e - (Q + 1);
+        sc[w][NCC + c] = make_float2(2.f * gxr, -2.f * gxi);
+        sc[w][NCC + NQC + c] = make_float2(2.f * gyr, -2.f * gyi);
+        sc[w][NCC + 2 * NQC + c] = make_float2(2.f * cr, -2.f * ci);
+      }
+    }
+  }
+  __syncwarp();
+  const float* S0 = &s0[w][0][0];
+  const uint64_t* SC = reinterpret_cast<const uint64_t*>(&sc[w][0]);
+  const float inv_s = 1.f / size;
+  for (int tc = t0; tc < t1; tc += 32) {
+    const int i = tc + lane;
+    const bool act = i < t1;
+    float x = 0.f, y = 0.f, z = 0.f;
+    if (act) {
+      const float4 v = xq[i];
+      x = v.x * inv_s;
+      y = v.y * inv_s;
+      z = v.z * inv_s;
+    }
+    const float r2 = x * x + y * y + z * z;
+    float vs = 0.f, gxs = 0.f, gys = 0.f, gzs = 0.f;
+    uint64_t va = 0, gxa = 0, gya = 0, gza = 0;
+    // m = 0 column (real)
+    {
+      float p2 = 1.f, p1 = z;
+      vs = fmaf(S0[0], p2, vs);
+      if (GRAD) {
+        gxs = fmaf(S0[(P + 1) + 0], p2, gxs);
+        gys = fmaf(S0[2 * (P + 1) + 0], p2, gys);
+        gzs = fmaf(S0[3 * (P + 1) + 0], p2, gzs);
+      }
+      vs = fmaf(S0[1], p1, vs);
+      if (GRAD && 1 <= Q) {
+        gxs = fmaf(S0[(P + 1) + 1], p1, gxs);
+        gys = fmaf(S0[2 * (P + 1) + 1], p1, gys);
+        gzs = fmaf(S0[3 * (P + 1) + 1], p1, gzs);
+      }
+#pragma unroll
+      for (int l = 2; l <= P; ++l) {
+        const float c = 1.f / float(l * l);
+        const float nv = (float(2 * l - 1) * z * p1 - r2 * p2) * c;
+        p2 = p1;
+        p1 = nv;
+        vs = fmaf(S0[l], nv, vs);
+        if (GRAD && l <= Q) {
+          gxs = fmaf(S0[(P + 1) + l], nv, gxs);
+          gys = fmaf(S0[2 * (P + 1) + l], nv, gys);
+          gzs = fmaf(S0[3 * (P + 1) + l], nv, gzs);
+        }
+      }
+    }
+    // m > 0 columns (packed complex)
+    float mr = 1.f, mi = 0.f;
+    int ci = 0, gi = 0;
+#pragma unroll
+    for (int m = 1; m <= P; ++m) {
+      const float c = 1.f / float(2 * m);
+      const float nr = (mr * x - mi * y) * c, ni = (mr * y + mi * x) * c;
+      mr = nr;
+      mi = ni;
+      uint64_t q2 = f2pack(mr, mi);
+      uint64_t q1 = f2mul(q2, f2pack(z, z));
+      va = f2fma(SC[ci], q2, va);
+      if (GRAD && m <= Q) {
+        gxa = f2fma(SC[NCC + gi], q2, gxa);
+        gya = f2fma(SC[NCC + NQC + gi], q2, gya);
+        gza = f2fma(SC[NCC + 2 * NQC + gi], q2, gza);
+      }
+      ++ci;
+      if (m <= Q) ++gi;
+      if (m + 1 <= P) {
+        va = f2fma(SC[ci], q1, va);
+        if (GRAD && m + 1 <= Q) {
+          gxa = f2fma(SC[NCC + gi], q1, gxa);
+          gya = f2fma(SC[NCC + NQC + gi], q1, gya);
+          gza = f2fma(SC[NCC + 2 * NQC + gi], q1, gza);
+        }
+        ++ci;
+        if (m + 1 <= Q) ++gi;
+      }
+#pragma unroll
+      for (int l = m + 2; l <= P; ++l) {
+        const float cc = 1.f / float((l + m) * (l - m));
+        const float a = float(2 * l - 1) * z * cc, bcoef = -r2 * cc;
+        const uint64_t nq = f2fma(q1, f2pack(a, a), f2mul(q2, f2pack(bcoef, bcoef)));
+        q2 = q1;
+        q1 = nq;
+        va = f2fma(SC[ci], nq, va);
+        if (GRAD && l <= Q) {
+          gxa = f2fma(SC[NCC + gi], nq, gxa);
+          gya = f2fma(SC[NCC + NQC + gi], nq, gya);
+          gza = f2fma(SC[NCC + 2 * NQC + gi], nq, gza);
+        }
+        ++ci;
+        if (l <= Q) ++gi;
+      }
+    }
+    if (act) {
+      float u0, u1;
+      f2unpack(va, u0, u1);
+      vout[i] = (vs + (u0 + u1)) * inv_s;
+      if (GRAD) {
+        const float s2 = inv_s * inv_s;
+        f2unpack(gxa, u0, u1);
+        gout[3 * (size_t)i] = (gxs + (u0 + u1)) * s2;
+        f2unpack(gya, u0, u1);
+        gout[3 * (size_t)i + 1] = (gys + (u0 + u1)) * s2;
+        f2unpack(gza, u0, u1);
+        gout[3 * (size_t)i + 2] = (gzs + (u0 + u1)) * s2;
       }
     }
   }
