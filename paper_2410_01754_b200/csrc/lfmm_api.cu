@@ -115,6 +115,20 @@ __global__ void k_stage_q(const double* __restrict__ q, int K, int c, const int*
   if (last_block(cnt)) reduce_parts_dev<4>(part, gridDim.x, scal);
 }
 
+template <class T>
+__global__ void k_transpose_ops(const T* __restrict__ in, T* __restrict__ out, int ncp, int nmat) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= (int64_t)nmat * ncp * ncp) return;
+  const int64_t m = i / ((int64_t)ncp * ncp);
+  const int r = (int)((i / ncp) % ncp), k = (int)(i % ncp);
+  out[(m * ncp + k) * ncp + r] = in[i];
+}
+
+template <class T>
+inline size_t tr_smem_bytes(int ncp) {
+  return sizeof(T) * (2 * (size_t)TR_KC * ncp + 2 * (size_t)TR_PT * TR_KC);
+}
+
 // Exact box charges (the l = 0 multipole) at every level.  The fp32 P2M/M2M
 // sums of the ~30 repeated water charges per leaf round coherently: summed
 // over 32k leaves they leave a fake net charge of ~5e-3 e that the M2L turns
@@ -438,6 +452,8 @@ struct lfmm_plan {
   std::vector<double2> lat_unit;  // unit-box complex lattice operator (nc x nc)
   // solve work
   DevBuf boxq;
+  DevBuf ops_m2m_t, ops_l2l_t, tr_cnt;  // k_translate operators ([8][k][row]) and tile counters
+  bool use_tr = false;                  // M2M / L2L on k_translate (ncp == 128)
   DevBuf q_in, qs, vnear, vfar, gnear, gfar, part, scal, epart, roots;
   DevBuf out_pot, out_near, out_far, out_dip, out_forces, energies, dvec, qtot;
   int64_t last_k = 0;
@@ -499,7 +515,7 @@ struct lfmm_plan {
       cudaEventDestroy(e.b);
     }
     for (auto e : free_events) cudaEventDestroy(e);
-    DevBuf* hbufs[] = {&ops16, &hm_inv_r, &hm_inv_c, &hm_jobs, &hm_level_max, &mult16, &boxq};
+    DevBuf* hbufs[] = {&ops16, &hm_inv_r, &hm_inv_c, &hm_jobs, &hm_level_max, &mult16, &boxq, &ops_m2m_t, &ops_l2l_t, &tr_cnt};
     for (auto* b : hbufs) b->release();
     DevBuf* bufs[] = {&pos_in, &pos_wrap, &leaf_of, &counts, &cursor, &leaf_start, &bucket, &perm,
                       &inv_perm, &pos_sorted, &leaf_sorted, &xq, &mult, &loc, &partial, &ops_tc, &up_part, &up_cnt, &counters, &ops_m2l, &ops_m2m,
@@ -684,6 +700,23 @@ struct lfmm_plan {
       else
         realify<T>(OP_L2L, 8, vals.as<double2>(), ncr, 0.5, 1, 1.0, ops_l2l.as<T>());
       LFMM_CUDA(cudaStreamSynchronize(stream));
+    }
+    use_tr = (ncp == 128) && depth >= 1;
+    if (use_tr) {
+      ops_m2m_t.ensure(opb * 8);
+      ops_l2l_t.ensure(opb * 8);
+      const int64_t tot = (int64_t)8 * ncp * ncp;
+      launch(ST_SETUP, [&] {
+        k_transpose_ops<T><<<nblk(tot, 256), 256, 0, stream>>>(ops_m2m.as<T>(), ops_m2m_t.as<T>(), ncp, 8);
+      });
+      launch(ST_SETUP, [&] {
+        k_transpose_ops<T><<<nblk(tot, 256), 256, 0, stream>>>(ops_l2l.as<T>(), ops_l2l_t.as<T>(), ncp, 8);
+      });
+      const int64_t tiles = std::max<int64_t>(1, ((1LL << (3 * (depth - 1))) + TR_PT - 1) / TR_PT);
+      tr_cnt.ensure(sizeof(int) * tiles);
+      LFMM_CUDA(cudaMemsetAsync(tr_cnt.p, 0, tr_cnt.bytes, stream));
+      LFMM_CUDA(cudaFuncSetAttribute(k_translate<T>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     (int)tr_smem_bytes<T>(ncp)));
     }
     if (lattice_mode != LFMM_LATTICE_OFF) {
       lat_unit = build_lattice_unit();
@@ -956,6 +989,22 @@ struct lfmm_plan {
     const unsigned rowb = (unsigned)((ncp + GB_M - 1) / GB_M);
     GemmArgs ga = gemm_base();
     for (int l = depth - 1; l >= 0; --l) {
+      if (use_tr) {
+        TrArgs ta{};
+        ta.mode = 0;
+        ta.level = l;
+        ta.ncp = ncp;
+        ta.ops_t = ops_m2m_t.p;
+        ta.src = M + level_off[l + 1] * ncp;
+        ta.dst = M + level_off[l] * ncp;
+        ta.slots = up_part.p;
+        ta.cnt = tr_cnt.as<int>();
+        const unsigned tiles = (unsigned)(((1LL << (3 * l)) + TR_PT - 1) / TR_PT);
+        launch(ST_M2M, [&] {
+          k_translate<T><<<dim3(tiles, 8), TR_THREADS, tr_smem_bytes<T>(ncp), stream>>>(ta);
+        });
+        continue;
+      }
       ga.mode = GEMM_UP;
       ga.level = l;
       dim3 grid(tiles_all(l) * ga.up_split, rowb);
@@ -1024,6 +1073,22 @@ struct lfmm_plan {
         launch(ST_DOWN, [&] { k_gemm_gather<T><<<grid, G_THREADS, 0, stream>>>(ga); });
       }
       for (int l = 1; l <= depth; ++l) {
+        if (use_tr) {
+          TrArgs ta{};
+          ta.mode = 1;
+          ta.level = l;
+          ta.ncp = ncp;
+          ta.ops_t = ops_l2l_t.p;
+          ta.src = Lc + level_off[l - 1] * ncp;
+          ta.dst = Lc + level_off[l] * ncp;
+          ta.partial = static_cast<const char*>(partial.p) + tsz() * (size_t)part_off[l] * ncp;
+          ta.nsplit = nsplit[l];
+          const unsigned tiles = (unsigned)(((1LL << (3 * (l - 1))) + TR_PT - 1) / TR_PT);
+          launch(ST_L2L, [&] {
+            k_translate<T><<<dim3(tiles, 8), TR_THREADS, tr_smem_bytes<T>(ncp), stream>>>(ta);
+          });
+          continue;
+        }
         ga.mode = GEMM_L2L;
         ga.level = l;
         dim3 g2(8 * tiles_per_parity(l), rowb);

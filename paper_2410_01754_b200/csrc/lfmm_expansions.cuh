@@ -578,6 +578,20 @@ __device__ __forceinline__ void ldv(const T* __restrict__ p, T (&r)[N]) {
   }
 }
 
+// vector store of N consecutive T (16-B aligned)
+template <class T, int N>
+__device__ __forceinline__ void stv(T* __restrict__ p, const T (&r)[N]) {
+  constexpr int VW = 16 / sizeof(T);
+  static_assert(N % VW == 0, "vector width");
+#pragma unroll
+  for (int u = 0; u < N / VW; ++u) {
+    if constexpr (sizeof(T) == 4)
+      reinterpret_cast<float4*>(p)[u] = make_float4(r[4 * u], r[4 * u + 1], r[4 * u + 2], r[4 * u + 3]);
+    else
+      reinterpret_cast<double2*>(p)[u] = make_double2(r[2 * u], r[2 * u + 1]);
+  }
+}
+
 // box index of the q-th target of parity `par` at `level`
 __device__ __forceinline__ int parity_box(int level, int par, int q) {
   const int lsub = level - 1, sub = 1 << lsub;
@@ -815,6 +829,173 @@ __global__ void __launch_bounds__(G_THREADS) k_gemm_gather(GemmArgs g) {
         dst[(size_t)box * ncp + r] = v;
       }
       if (tid == 0) g.up_cnt[tile * gridDim.y + blockIdx.y] = 0;
+    }
+  }
+}
+
+}  // namespace lfmm
+
+namespace lfmm {
+
+// ---------------------------------------------------- M2M / L2L sweeps ----
+// One CTA = (tile of TR_PT target columns, octant o): D = Op_o (ncp x ncp)
+// x B (ncp x TR_PT) over the whole K = ncp, K streamed through shared memory
+// in TR_KC chunks with cp.async double buffering.  Operators are stored
+// transposed ([k][row]) so a K chunk is one contiguous block.
+//   UP  (M2M, upward_pass solver.py:248-258): parent tile p, octant o:
+//       B = child(p, o) multipoles; D goes to partial slot o; the last of the
+//       8 octant CTAs of a tile adds the slots in octant order (fixed-order,
+//       deterministic) and writes the parent multipoles.
+//   DOWN (L2L, downward_pass solver.py:276-281): parent tile p, octant o:
+//       B = parent locals; child(p, o) local = D + the level's M2L partial
+//       slots in slot order.
+// 256 threads: lane -> 4 consecutive rows (coefficients), warp -> 2 columns.
+constexpr int TR_PT = 16, TR_KC = 32, TR_THREADS = 256;
+
+struct TrArgs {
+  int mode;            // 0 UP (M2M), 1 DOWN (L2L)
+  int level;           // UP: parent level; DOWN: child level
+  int ncp;
+  const void* ops_t;   // [8][ncp (k)][ncp (row)]
+  const void* src;     // UP: child-level multipoles; DOWN: parent-level locals
+  void* dst;           // UP: parent-level multipoles; DOWN: child-level locals
+  void* slots;         // UP: [8][nparents][ncp] scratch
+  int* cnt;            // UP: one counter per tile
+  const void* partial; // DOWN: M2L partial slots of the child level ([nsplit][nchild][ncp])
+  int nsplit;
+};
+
+template <class T>
+__device__ __forceinline__ void tr_cp16(T* sdst, const T* gsrc) {
+  const uint32_t s = static_cast<uint32_t>(__cvta_generic_to_shared(sdst));
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(s), "l"(gsrc) : "memory");
+}
+
+template <class T>
+__global__ void __launch_bounds__(TR_THREADS) k_translate(TrArgs g) {
+  constexpr int VW = 16 / sizeof(T);  // elements per 16-B copy
+  extern __shared__ __align__(16) unsigned char tr_smem[];
+  T* As = reinterpret_cast<T*>(tr_smem);              // [2][TR_KC][ncp]
+  const int ncp = g.ncp;
+  T* Bs = As + 2 * TR_KC * ncp;                        // [2][TR_PT][TR_KC]
+  __shared__ int col_src[TR_PT], col_dst[TR_PT];
+  const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+  const int o = blockIdx.y;
+  const int tile = blockIdx.x;
+  const int pl = g.mode == 0 ? g.level : g.level - 1;  // parent level
+  const int np = 1 << (3 * pl), pn = 1 << pl, cn = 2 * pn;
+  if (tid < TR_PT) {
+    const int p = tile * TR_PT + tid;
+    int s = -1, d = -1;
+    if (p < np) {
+      const int px = p >> (2 * pl), py = (p >> pl) & (pn - 1), pz = p & (pn - 1);
+      const int c = ((((2 * px + ((o >> 2) & 1)) * cn) + 2 * py + ((o >> 1) & 1)) * cn) + 2 * pz + (o & 1);
+      if (g.mode == 0) {
+        s = c;
+        d = p;
+      } else {
+        s = p;
+        d = c;
+      }
+    }
+    col_src[tid] = s;
+    col_dst[tid] = d;
+  }
+  __syncthreads();
+  const T* ops = reinterpret_cast<const T*>(g.ops_t) + (size_t)o * ncp * ncp;
+  const T* src = reinterpret_cast<const T*>(g.src);
+  const int nk = ncp / TR_KC;
+  auto stage = [&](int kc, int buf) {
+    T* a = As + (size_t)buf * TR_KC * ncp;
+    const T* ga = ops + (size_t)kc * TR_KC * ncp;
+    for (int e = tid; e < TR_KC * ncp / VW; e += TR_THREADS) tr_cp16(a + e * VW, ga + e * VW);
+    T* b = Bs + (size_t)buf * TR_PT * TR_KC;
+    for (int e = tid; e < TR_PT * TR_KC / VW; e += TR_THREADS) {
+      const int c = e / (TR_KC / VW), u = e % (TR_KC / VW);
+      const int sb = col_src[c];
+      if (sb >= 0)
+        tr_cp16(b + c * TR_KC + u * VW, src + (size_t)sb * ncp + kc * TR_KC + u * VW);
+      else
+#pragma unroll
+        for (int v = 0; v < VW; ++v) b[c * TR_KC + u * VW + v] = T(0);
+    }
+    asm volatile("cp.async.commit_group;" ::: "memory");
+  };
+  T acc[4][2];
+#pragma unroll
+  for (int i = 0; i < 4; ++i) acc[i][0] = acc[i][1] = T(0);
+  const int r0 = 4 * lane;       // rows r0..r0+3 (ncp = 128 for the 4-row mapping; see below)
+  const int rows_per_lane = ncp / 32;  // 4 when ncp == 128; general ncp handled by the row loop
+  stage(0, 0);
+  for (int kc = 0; kc < nk; ++kc) {
+    if (kc + 1 < nk) {
+      stage(kc + 1, (kc + 1) & 1);
+      asm volatile("cp.async.wait_group 1;" ::: "memory");
+    } else {
+      asm volatile("cp.async.wait_group 0;" ::: "memory");
+    }
+    __syncthreads();
+    const T* a = As + (size_t)(kc & 1) * TR_KC * ncp;
+    const T* b = Bs + (size_t)(kc & 1) * TR_PT * TR_KC;
+    if (rows_per_lane == 4) {
+#pragma unroll 8
+      for (int k = 0; k < TR_KC; ++k) {
+        T av[4];
+        ldv<T, 4>(a + k * ncp + r0, av);
+        const T b0 = b[(2 * w) * TR_KC + k], b1 = b[(2 * w + 1) * TR_KC + k];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          acc[u][0] = fma(av[u], b0, acc[u][0]);
+          acc[u][1] = fma(av[u], b1, acc[u][1]);
+        }
+      }
+    }
+    __syncthreads();
+  }
+  if (rows_per_lane != 4) return;  // (the plan only routes ncp == 128 here)
+  // ---- epilogue ----
+  if (g.mode == 0) {
+    T* slots = reinterpret_cast<T*>(g.slots);
+#pragma unroll
+    for (int j = 0; j < 2; ++j) {
+      const int c = 2 * w + j, d = col_dst[c];
+      if (d < 0) continue;
+      T v4[4] = {acc[0][j], acc[1][j], acc[2][j], acc[3][j]};
+      stv<T, 4>(slots + ((size_t)o * np + d) * ncp + r0, v4);
+    }
+    __shared__ int last;
+    __threadfence();
+    __syncthreads();
+    if (tid == 0) last = (atomicAdd(&g.cnt[tile], 1) == 7);
+    __syncthreads();
+    if (!last) return;
+    __threadfence();
+    T* dst = reinterpret_cast<T*>(g.dst);
+    for (int e = tid; e < TR_PT * ncp; e += TR_THREADS) {
+      const int c = e / ncp, r = e % ncp, d = col_dst[c];
+      if (d < 0) continue;
+      T v = T(0);
+#pragma unroll
+      for (int s = 0; s < 8; ++s) v += __ldcg(&slots[((size_t)s * np + d) * ncp + r]);
+      dst[(size_t)d * ncp + r] = v;
+    }
+    if (tid == 0) g.cnt[tile] = 0;
+  } else {
+    const T* part = reinterpret_cast<const T*>(g.partial);
+    T* dst = reinterpret_cast<T*>(g.dst);
+    const size_t nchild = (size_t)np * 8;
+#pragma unroll
+    for (int j = 0; j < 2; ++j) {
+      const int c = 2 * w + j, d = col_dst[c];
+      if (d < 0) continue;
+      T v4[4] = {acc[0][j], acc[1][j], acc[2][j], acc[3][j]};
+      for (int s = 0; s < g.nsplit; ++s) {
+        T q4[4];
+        ldv<T, 4>(part + ((size_t)s * nchild + d) * ncp + r0, q4);
+#pragma unroll
+        for (int u = 0; u < 4; ++u) v4[u] += q4[u];
+      }
+      stv<T, 4>(dst + (size_t)d * ncp + r0, v4);
     }
   }
 }
