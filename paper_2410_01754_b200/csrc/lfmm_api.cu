@@ -142,17 +142,40 @@ template <class T>
 __global__ void k_box_charges(const double* __restrict__ qs, const int* __restrict__ leaf_start, int depth,
                               int64_t leaf_off, int ncp, T* __restrict__ mult, double* __restrict__ boxq,
                               int* __restrict__ cnt) {
-  const int nleaf = 1 << (3 * depth);
-  const int b = blockIdx.x * blockDim.x + threadIdx.x;
-  if (b < nleaf) {
+  // phase 1: thread per leaf, grouped 8 per level-(d-1) parent in octant
+  // order; lane 8g of each group then adds its 8 leaves in octant order
+  if (depth >= 1) {
+    const int pl = depth - 1, pn = 1 << pl, cn = 2 * pn;
+    const int t = blockIdx.x * blockDim.x + threadIdx.x;
+    const int pb = t >> 3, o = t & 7;
+    const bool valid = pb < (1 << (3 * pl));
     double c = 0.0;
-    for (int i = leaf_start[b]; i < leaf_start[b + 1]; ++i) c += qs[i];
-    boxq[leaf_off + b] = c;
-    mult[(size_t)(leaf_off + b) * ncp] = (T)c;
+    if (valid) {
+      const int x = pb >> (2 * pl), y = (pb >> pl) & (pn - 1), z = pb & (pn - 1);
+      const int leaf = (((2 * x + ((o >> 2) & 1)) * cn) + 2 * y + ((o >> 1) & 1)) * cn + 2 * z + (o & 1);
+      for (int i = leaf_start[leaf]; i < leaf_start[leaf + 1]; ++i) c += qs[i];
+      boxq[leaf_off + leaf] = c;
+      mult[(size_t)(leaf_off + leaf) * ncp] = (T)c;
+    }
+    double pc = 0.0;
+    const int base = (threadIdx.x & 31) & ~7;
+#pragma unroll
+    for (int k = 0; k < 8; ++k) pc += __shfl_sync(0xffffffffu, c, base + k);
+    if (valid && o == 0) {
+      const int64_t poff = leaf_off - (1LL << (3 * pl));
+      boxq[poff + pb] = pc;
+      mult[(size_t)(poff + pb) * ncp] = (T)pc;
+    }
+  } else if (blockIdx.x == 0 && threadIdx.x == 0) {
+    double c = 0.0;
+    for (int i = leaf_start[0]; i < leaf_start[1]; ++i) c += qs[i];
+    boxq[0] = c;
+    mult[0] = (T)c;
   }
-  if (!last_block(cnt)) return;
-  int64_t child_off = leaf_off;
-  for (int l = depth - 1; l >= 0; --l) {
+  if (depth < 2 || !last_block(cnt)) return;
+  // phase 2 (last block): levels d-2 .. 0, 8 children each in octant order
+  int64_t child_off = leaf_off - (1LL << (3 * (depth - 1)));
+  for (int l = depth - 2; l >= 0; --l) {
     const int n = 1 << l, nb = 1 << (3 * l);
     const int64_t off = child_off - nb;  // level_off[l] (levels are stored consecutively)
     for (int pb = threadIdx.x; pb < nb; pb += blockDim.x) {
@@ -248,6 +271,27 @@ __global__ void k_finalize(int64_t n, int K, int c, const int* __restrict__ perm
       qtot[c] = scal[3];
     }
   }
+}
+
+// Total potential at the site atoms straight from the canonical-order
+// pieces (the step path skips the input-order potential arrays):
+// V = V_near + V_far + 2 eta gamma (r - L/2).D   (solver.py:373-379)
+template <class T>
+__global__ void k_site_pot(const int* __restrict__ atom_idx, int n, const int* __restrict__ inv_perm,
+                           const T* __restrict__ vnear, const T* __restrict__ vfar,
+                           const double* __restrict__ pos_sorted, const double* __restrict__ scal, int dipole,
+                           double box, double* __restrict__ out) {
+  const int a = blockIdx.x * blockDim.x + threadIdx.x;
+  if (a >= n) return;
+  const int k = inv_perm[atom_idx[a]];
+  double v = (double)vnear[k] + (double)vfar[k];
+  if (dipole) {
+    const double gam = 2.0 * 3.14159265358979323846 / (3.0 * box * box * box), h = 0.5 * box;
+    v += 2.0 * DIPOLE_ETA * gam *
+         ((pos_sorted[3 * k] - h) * scal[0] + (pos_sorted[3 * k + 1] - h) * scal[1] +
+          (pos_sorted[3 * k + 2] - h) * scal[2]);
+  }
+  out[a] = v;
 }
 
 // energies (4,K) rows total/near/far/dip; dipole (3,K); qtot (K)
@@ -444,6 +488,7 @@ struct lfmm_plan {
   bool use_tc = false;    // M2L on tcgen05 (fp32, (p+1)^2 <= 128)
   bool use_halo = false;  // ... as shifted-window fp16x3 GEMMs (lfmm_m2l_halo.cuh)
   bool p2p_scalar = false;  // fp32 P2P on the scalar kernel (LFMM_P2P=scalar, A/B checks)
+  bool step_mode = false;   // lfmm_step: skip the input-order potential arrays
   DevBuf ops_tc, up_part, up_cnt, counters;
   DevBuf ops16, hm_inv_r, hm_inv_c, hm_jobs, hm_level_max, mult16;
   int64_t m16_off[DMAX + 2] = {0};
@@ -451,8 +496,8 @@ struct lfmm_plan {
   DevBuf mult, loc, partial, ops_m2l, ops_m2m, ops_l2l, ops_lat, lat64t;
   std::vector<double2> lat_unit;  // unit-box complex lattice operator (nc x nc)
   // solve work
-  DevBuf boxq;
-  DevBuf ops_m2m_t, ops_l2l_t, tr_cnt;  // k_translate operators ([8][k][row]) and tile counters
+  DevBuf boxq, site_pot;
+  DevBuf ops_m2m_t, ops_l2l_t, ops_lat_t, tr_cnt;  // k_translate operators ([k][row]) and tile counters
   bool use_tr = false;                  // M2M / L2L on k_translate (ncp == 128)
   DevBuf q_in, qs, vnear, vfar, gnear, gfar, part, scal, epart, roots;
   DevBuf out_pot, out_near, out_far, out_dip, out_forces, energies, dvec, qtot;
@@ -515,7 +560,7 @@ struct lfmm_plan {
       cudaEventDestroy(e.b);
     }
     for (auto e : free_events) cudaEventDestroy(e);
-    DevBuf* hbufs[] = {&ops16, &hm_inv_r, &hm_inv_c, &hm_jobs, &hm_level_max, &mult16, &boxq, &ops_m2m_t, &ops_l2l_t, &tr_cnt};
+    DevBuf* hbufs[] = {&ops16, &hm_inv_r, &hm_inv_c, &hm_jobs, &hm_level_max, &mult16, &boxq, &site_pot, &ops_m2m_t, &ops_l2l_t, &ops_lat_t, &tr_cnt};
     for (auto* b : hbufs) b->release();
     DevBuf* bufs[] = {&pos_in, &pos_wrap, &leaf_of, &counts, &cursor, &leaf_start, &bucket, &perm,
                       &inv_perm, &pos_sorted, &leaf_sorted, &xq, &mult, &loc, &partial, &ops_tc, &up_part, &up_cnt, &counters, &ops_m2l, &ops_m2m,
@@ -725,6 +770,12 @@ struct lfmm_plan {
       LFMM_CUDA(cudaMemcpyAsync(vals.p, lat_unit.data(), sizeof(double2) * nn, cudaMemcpyHostToDevice, stream));
       ops_lat.ensure(opb);
       realify<T>(OP_DENSE, 1, vals.as<double2>(), nn, 1.0, 0, 1.0, ops_lat.as<T>());
+      if (use_tr) {
+        ops_lat_t.ensure(opb);
+        launch(ST_SETUP, [&] {
+          k_transpose_ops<T><<<nblk((int64_t)ncp * ncp, 256), 256, 0, stream>>>(ops_lat.as<T>(), ops_lat_t.as<T>(), ncp, 1);
+        });
+      }
       // fp64 transposed copy for the HI lattice kernel
       DevBuf l64;
       l64.ensure(sizeof(double) * ncp * ncp);
@@ -1015,7 +1066,16 @@ struct lfmm_plan {
                                                              level_off[depth], ncp, M, boxq.as<double>(),
                                                              counters.as<int>() + 2);
     });
-    if (lattice_mode != LFMM_LATTICE_OFF) {
+    if (lattice_mode != LFMM_LATTICE_OFF && use_tr) {
+      TrArgs ta{};
+      ta.mode = 2;
+      ta.ncols = 1;
+      ta.ncp = ncp;
+      ta.ops_t = ops_lat_t.p;
+      ta.src = M;
+      ta.dst = Lc;
+      launch(ST_ROOT, [&] { k_translate<T><<<dim3(1, 1), TR_THREADS, tr_smem_bytes<T>(ncp), stream>>>(ta); });
+    } else if (lattice_mode != LFMM_LATTICE_OFF) {
       ga.mode = GEMM_ROOT;
       ga.level = 0;
       dim3 grid(1, rowb);
@@ -1138,8 +1198,9 @@ struct lfmm_plan {
       if (grad)
         k_finalize<T, true><<<(unsigned)nb, 256, 0, stream>>>(
             N, K, c, perm.as<int>(), pos_sorted.as<double>(), qs.as<double>(), vnear.as<T>(), vfar.as<T>(),
-            gnear.as<T>(), gfar.as<T>(), scal.as<double>(), dip, L, out_pot.as<double>(), out_near.as<double>(),
-            out_far.as<double>(), out_dip.as<double>(), out_forces.as<double>(), part.as<dd>(), counters.as<int>() + 1,
+            gnear.as<T>(), gfar.as<T>(), scal.as<double>(), dip, L, step_mode ? nullptr : out_pot.as<double>(),
+            step_mode ? nullptr : out_near.as<double>(), step_mode ? nullptr : out_far.as<double>(),
+            step_mode ? nullptr : out_dip.as<double>(), out_forces.as<double>(), part.as<dd>(), counters.as<int>() + 1,
             epart.as<double>(), energies.as<double>(), dvec.as<double>(), qtot.as<double>());
       else
         k_finalize<T, false><<<(unsigned)nb, 256, 0, stream>>>(
@@ -1299,7 +1360,7 @@ void upload_lambdas(lfmm_plan* pl, const double* lambdas, const int32_t* n_lambd
   LFMM_CUDA(cudaMemcpyAsync(pl->nlam.p, n_lambda, sizeof(int32_t) * S, kind, pl->stream));
 }
 
-void run_hi(lfmm_plan* pl, int mode, const double* pot_dev) {
+void run_hi(lfmm_plan* pl, int mode, const double* pot_dev, const double* pot_site = nullptr) {
   if (pl->n_sites == 0) {
     LFMM_CUDA(cudaMemsetAsync(pl->offset_total.p, 0, sizeof(double), pl->stream));
     return;
@@ -1307,6 +1368,7 @@ void run_hi(lfmm_plan* pl, int mode, const double* pot_dev) {
   HiArgs g{};
   hi_args(pl, g);
   g.pot = pot_dev;
+  g.pot_site = pot_site;
   g.mode = mode;
   g.c_p2p = pl->c_p2p.as<double>();
   g.c_lat = pl->c_lat.as<double>();
@@ -1314,6 +1376,37 @@ void run_hi(lfmm_plan* pl, int mode, const double* pot_dev) {
   g.blend = pl->blend.as<double>();
   g.forces = pl->lam_forces.as<double>();
   g.offset = pl->offsets.as<double>();
+  if (mode == LFMM_MODE_HI && g.images_full && g.lat_t) {
+    // lattice pair kernel inputs for all site atoms at once: R_t, U_t = T1 R_t
+    const int na = (int)pl->n_site_atoms;
+    pl->launch(ST_HI, [&] {
+      k_hi_rvec<<<nblk(na, 128), 128, 0, pl->stream>>>(g.site_pos, na, g.box, g.p, g.ncp, g.rscratch);
+    });
+    if (g.ncp == 128) {
+      TrArgs ta{};
+      ta.mode = 2;
+      ta.ncols = na;
+      ta.ncp = g.ncp;
+      ta.ops_t = g.lat_t;
+      ta.src = g.rscratch;
+      ta.dst = g.uscratch;
+      static bool attr_set = false;
+      if (!attr_set) {
+        LFMM_CUDA(cudaFuncSetAttribute(k_translate<double>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       (int)tr_smem_bytes<double>(g.ncp)));
+        attr_set = true;
+      }
+      pl->launch(ST_HI, [&] {
+        k_translate<double><<<dim3((unsigned)((na + TR_PT - 1) / TR_PT), 1), TR_THREADS, tr_smem_bytes<double>(g.ncp),
+                              pl->stream>>>(ta);
+      });
+    } else {
+      pl->launch(ST_HI, [&] {
+        k_hi_umat<<<nblk((int64_t)na * g.ncp, 128), 128, 0, pl->stream>>>(g.lat_t, g.rscratch, na, ncoef(g.p), g.ncp,
+                                                                          g.uscratch);
+      });
+    }
+  }
   const int ns = pl->ns_max;
   const size_t smem = sizeof(double) * ((size_t)ns + 2 * (size_t)ns * ns + 3 * (size_t)ns);
   if (smem > 48 * 1024) {
@@ -1800,10 +1893,31 @@ int lfmm_step(lfmm_plan* plan, const double* positions, const double* charges, c
       LFMM_CUDA(cudaMemcpyAsync(plan->q_tmp.p, charges, sizeof(double) * N, kind, plan->stream));
       run_scale(plan, plan->q_tmp.as<double>(), plan->q_in.as<double>());
     }
+    plan->step_mode = potentials == nullptr;
     plan->run_solve(1, true);
+    const bool step_mode = plan->step_mode;
+    plan->step_mode = false;
     if (!plain && plan->n_sites > 0) {
       gather_site_positions(plan, nullptr, 0);
-      run_hi(plan, mode, plan->out_pot.as<double>());
+      if (step_mode) {
+        plan->site_pot.ensure(sizeof(double) * std::max<int64_t>(plan->n_site_atoms, 1));
+        const int na = (int)plan->n_site_atoms;
+        const int dip = (plan->flags & LFMM_F_DIPOLE) ? 1 : 0;
+        plan->launch(ST_HI, [&] {
+          if (plan->fp32)
+            k_site_pot<float><<<nblk(na, 128), 128, 0, plan->stream>>>(
+                plan->atom_idx.as<int>(), na, plan->inv_perm.as<int>(), plan->vnear.as<float>(), plan->vfar.as<float>(),
+                plan->pos_sorted.as<double>(), plan->scal.as<double>(), dip, plan->L, plan->site_pot.as<double>());
+          else
+            k_site_pot<double><<<nblk(na, 128), 128, 0, plan->stream>>>(
+                plan->atom_idx.as<int>(), na, plan->inv_perm.as<int>(), plan->vnear.as<double>(),
+                plan->vfar.as<double>(), plan->pos_sorted.as<double>(), plan->scal.as<double>(), dip, plan->L,
+                plan->site_pot.as<double>());
+        });
+        run_hi(plan, mode, nullptr, plan->site_pot.as<double>());
+      } else {
+        run_hi(plan, mode, plan->out_pot.as<double>());
+      }
     }
     // energy = E_solve + sum of site offsets (hi_energy_and_forces :273)
     const bool add_off = !plain && plan->n_sites > 0 && mode == LFMM_MODE_HI;

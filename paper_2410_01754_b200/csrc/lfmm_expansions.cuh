@@ -853,7 +853,8 @@ namespace lfmm {
 constexpr int TR_PT = 16, TR_KC = 32, TR_THREADS = 256;
 
 struct TrArgs {
-  int mode;            // 0 UP (M2M), 1 DOWN (L2L)
+  int mode;            // 0 UP (M2M), 1 DOWN (L2L), 2 plain columns (dst[:, c] = Op src[:, c])
+  int ncols;           // mode 2: number of columns
   int level;           // UP: parent level; DOWN: child level
   int ncp;
   const void* ops_t;   // [8][ncp (k)][ncp (row)]
@@ -887,7 +888,9 @@ __global__ void __launch_bounds__(TR_THREADS) k_translate(TrArgs g) {
   if (tid < TR_PT) {
     const int p = tile * TR_PT + tid;
     int s = -1, d = -1;
-    if (p < np) {
+    if (g.mode == 2) {
+      if (p < g.ncols) s = d = p;
+    } else if (p < np) {
       const int px = p >> (2 * pl), py = (p >> pl) & (pn - 1), pz = p & (pn - 1);
       const int c = ((((2 * px + ((o >> 2) & 1)) * cn) + 2 * py + ((o >> 1) & 1)) * cn) + 2 * pz + (o & 1);
       if (g.mode == 0) {
@@ -954,7 +957,16 @@ __global__ void __launch_bounds__(TR_THREADS) k_translate(TrArgs g) {
   }
   if (rows_per_lane != 4) return;  // (the plan only routes ncp == 128 here)
   // ---- epilogue ----
-  if (g.mode == 0) {
+  if (g.mode == 2) {
+    T* dst = reinterpret_cast<T*>(g.dst);
+#pragma unroll
+    for (int j = 0; j < 2; ++j) {
+      const int d = col_dst[2 * w + j];
+      if (d < 0) continue;
+      T v4[4] = {acc[0][j], acc[1][j], acc[2][j], acc[3][j]};
+      stv<T, 4>(dst + (size_t)d * ncp + r0, v4);
+    }
+  } else if (g.mode == 0) {
     T* slots = reinterpret_cast<T*>(g.slots);
 #pragma unroll
     for (int j = 0; j < 2; ++j) {

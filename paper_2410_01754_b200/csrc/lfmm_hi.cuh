@@ -36,6 +36,7 @@ struct HiArgs {
   const int* nlam;         // S
   const double* site_pos;  // A x 3 (caller-supplied site positions)
   const double* pot;       // input-order potentials (N), may be null (corrections only)
+  const double* pot_site;  // or: potentials at the site atoms (A), from k_site_pot
   double box;
   int p, ncp;
   const double* lat_t;     // packed lattice operator, transposed [in][out], fp64, or null
@@ -134,37 +135,12 @@ __global__ void __launch_bounds__(HI_THREADS) k_hi_site(HiArgs g) {
       }
       KG[e] = k;
     }
-    // ---- lattice kernel G ----
+    // ---- lattice kernel G: R_t and U_t = T1 R_t come precomputed for all
+    // site atoms (k_hi_rvec + one batched GEMM, k_translate mode 2) ----
     if (lattice) {
-      double* R = g.rscratch + (size_t)a0 * ncp;
-      double* U = g.uscratch + (size_t)a0 * ncp;
+      const double* R = g.rscratch + (size_t)a0 * ncp;
+      const double* U = g.uscratch + (size_t)a0 * ncp;
       const double invL = 1.0 / L;
-      for (int t = tid; t < ns; t += blockDim.x) {
-        double* Rt = R + (size_t)t * ncp;
-        const double x = (pos[3 * t] - 0.5 * L) * invL, y = (pos[3 * t + 1] - 0.5 * L) * invL,
-                     z = (pos[3 * t + 2] - 0.5 * L) * invL;
-        int a = 0;
-        regular_stream<double>(x, y, z, p, [&](int m, int l, double re, double im) {
-          Rt[a++] = re;
-          if (m > 0) Rt[a++] = im;
-        });
-      }
-      __syncthreads();
-      // U_t = T1 R_t  (lat_t stored transposed: [in b][out a])
-      for (int t0 = 0; t0 < ns; t0 += 8) {
-        const int tn = min(8, ns - t0);
-        for (int a = tid; a < nc; a += blockDim.x) {
-          double acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-          for (int b = 0; b < nc; ++b) {
-            const double tv = g.lat_t[(size_t)b * ncp + a];
-#pragma unroll
-            for (int u = 0; u < 8; ++u)
-              if (u < tn) acc[u] = fma(tv, R[(size_t)(t0 + u) * ncp + b], acc[u]);
-          }
-          for (int u = 0; u < tn; ++u) U[(size_t)(t0 + u) * ncp + a] = acc[u];
-        }
-      }
-      __syncthreads();
       // G_st = (1/L) <R_s, U_t>, one warp per pair
       for (int e = wid; e < ns * ns; e += blockDim.x / 32) {
         const int i = e / ns, j = e % ns;
@@ -196,7 +172,10 @@ __global__ void __launch_bounds__(HI_THREADS) k_hi_site(HiArgs g) {
         ddy += dev * (pos[3 * i + 1] - 0.5 * L);
         ddz += dev * (pos[3 * i + 2] - 0.5 * L);
       }
-      if (g.pot) sv += Qr[i] * g.pot[g.atom_idx[a0 + i]];
+      if (g.pot_site)
+        sv += Qr[i] * g.pot_site[a0 + i];
+      else if (g.pot)
+        sv += Qr[i] * g.pot[g.atom_idx[a0 + i]];
     }
     for (int off = 16; off > 0; off >>= 1) {
       cp += __shfl_down_sync(0xffffffffu, cp, off);
@@ -236,13 +215,44 @@ __global__ void __launch_bounds__(HI_THREADS) k_hi_site(HiArgs g) {
       if (g.forces) {
         for (int k = 0; k < 4; ++k) {
           double f = 0.0;
-          if (k < nl && g.pot)
+          if (k < nl && (g.pot || g.pot_site))
             for (int r = 0; r < nf; ++r) f += hi_wgrad(lam, nl, k, r) * (Sv[r] - (qi ? 0.0 : Cv[r]));
           g.forces[4 * s + k] = k < nl ? -f : 0.0;
         }
       }
     }
   }
+}
+
+// R(r_t - L/2) / L-normalised regular harmonics of every site atom (packed,
+// fp64), the right-hand sides of the batched U = T1 R GEMM
+__global__ void k_hi_rvec(const double* __restrict__ site_pos, int n_atoms, double box, int p, int ncp,
+                          double* __restrict__ rscratch) {
+  const int a = blockIdx.x * blockDim.x + threadIdx.x;
+  if (a >= n_atoms) return;
+  const double invL = 1.0 / box;
+  const double x = (site_pos[3 * a] - 0.5 * box) * invL, y = (site_pos[3 * a + 1] - 0.5 * box) * invL,
+               z = (site_pos[3 * a + 2] - 0.5 * box) * invL;
+  double* Rt = rscratch + (size_t)a * ncp;
+  int c = 0;
+  regular_stream<double>(x, y, z, p, [&](int m, int l, double re, double im) {
+    Rt[c++] = re;
+    if (m > 0) Rt[c++] = im;
+  });
+  for (; c < ncp; ++c) Rt[c] = 0.0;
+}
+
+// generic U_t = T1 R_t (any ncp): thread per (site atom, output row)
+__global__ void k_hi_umat(const double* __restrict__ lat_t, const double* __restrict__ rscratch, int n_atoms,
+                          int nc, int ncp, double* __restrict__ uscratch) {
+  const int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (e >= (int64_t)n_atoms * ncp) return;
+  const int a = (int)(e / ncp), r = (int)(e % ncp);
+  const double* R = rscratch + (size_t)a * ncp;
+  double acc = 0.0;
+  if (r < nc)
+    for (int b = 0; b < nc; ++b) acc = fma(lat_t[(size_t)b * ncp + r], R[b], acc);
+  uscratch[(size_t)a * ncp + r] = acc;
 }
 
 // fixed-order sum of per-site offsets (CorrectionSet.energy_offset, :153-154)
