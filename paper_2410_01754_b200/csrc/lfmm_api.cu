@@ -98,18 +98,18 @@ __global__ void k_stage_q(const double* __restrict__ q, int K, int c, const int*
                           const double* __restrict__ pos_sorted, int64_t n, double box,
                           vec4_t<T>* __restrict__ xq, double* __restrict__ qs, dd* __restrict__ part,
                           int* __restrict__ cnt, double* __restrict__ scal) {
-  const int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   dd v[4] = {dd{0, 0}, dd{0, 0}, dd{0, 0}, dd{0, 0}};
-  if (k < n) {
+  // grid-stride (a few blocks per SM: the last-block counter sees few atomics)
+  for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < n; k += (int64_t)gridDim.x * blockDim.x) {
     const int i = perm[k];
     const double qv = q[(size_t)i * K + c];
     xq[k].w = (T)qv;
     qs[k] = qv;
     const double h = 0.5 * box;
-    v[0] = dd_from((pos_sorted[3 * k] - h) * qv);
-    v[1] = dd_from((pos_sorted[3 * k + 1] - h) * qv);
-    v[2] = dd_from((pos_sorted[3 * k + 2] - h) * qv);
-    v[3] = dd_from(qv);
+    v[0] = dd_add(v[0], dd_from((pos_sorted[3 * k] - h) * qv));
+    v[1] = dd_add(v[1], dd_from((pos_sorted[3 * k + 1] - h) * qv));
+    v[2] = dd_add(v[2], dd_from((pos_sorted[3 * k + 2] - h) * qv));
+    v[3] = dd_add(v[3], dd_from(qv));
   }
   block_reduce_dd<4>(v, part + (size_t)blockIdx.x * 4);
   if (last_block(cnt)) reduce_parts_dev<4>(part, gridDim.x, scal);
@@ -223,9 +223,8 @@ __global__ void k_finalize(int64_t n, int K, int c, const int* __restrict__ perm
                            double* __restrict__ out_forces, dd* __restrict__ part, int* __restrict__ cnt,
                            double* __restrict__ epart, double* __restrict__ energies, double* __restrict__ dvec,
                            double* __restrict__ qtot) {
-  const int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   dd v[2] = {dd{0, 0}, dd{0, 0}};
-  if (k < n) {
+  for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < n; k += (int64_t)gridDim.x * blockDim.x) {
     const int i = perm[k];
     const double q = qs[k];
     const double vn = (double)vnear[k], vf = (double)vfar[k];
@@ -249,8 +248,8 @@ __global__ void k_finalize(int64_t n, int K, int c, const int* __restrict__ perm
         out_forces[3 * (size_t)i + a] = f;
       }
     }
-    v[0] = dd_from(q * vn);
-    v[1] = dd_from(q * vf);
+    v[0] = dd_add(v[0], dd_from(q * vn));
+    v[1] = dd_add(v[1], dd_from(q * vf));
   }
   block_reduce_dd<2>(v, part + (size_t)blockIdx.x * 2);
   if (last_block(cnt)) {
@@ -981,7 +980,7 @@ struct lfmm_plan {
                                                           cursor.as<int>(), bucket.as<int>());
       });
       launch(ST_TREE, [&] {
-        k_leaf_rank<<<nblk((int64_t)nleaf * 32, 128), 128, 0, stream>>>(
+        k_leaf_rank<<<nblk((int64_t)nleaf * 32, RANK_WARPS * 32), RANK_WARPS * 32, 0, stream>>>(
             pos_wrap.as<double>(), leaf_start.as<int>(), bucket.as<int>(), nleaf, perm.as<int>(), inv_perm.as<int>());
       });
       launch(ST_TREE, [&] {
@@ -997,7 +996,7 @@ struct lfmm_plan {
   // ---------------------------------------------------------- solve ----
   template <class T>
   void solve_column(int K, int c, bool grad) {
-    const int64_t nb = nblk(N, 256);
+    const int64_t nb = std::min<int64_t>(nblk(N, 256), 148 * 4);
     const T tsize = (T)size;
     launch(ST_STAGE, [&] {
       k_stage_q<T><<<(unsigned)nb, 256, 0, stream>>>(q_in.as<double>(), K, c, perm.as<int>(), pos_sorted.as<double>(),
@@ -1408,7 +1407,9 @@ void run_hi(lfmm_plan* pl, int mode, const double* pot_dev, const double* pot_si
     }
   }
   const int ns = pl->ns_max;
-  const size_t smem = sizeof(double) * ((size_t)ns + 2 * (size_t)ns * ns + 3 * (size_t)ns);
+  const bool lat_smem = mode == LFMM_MODE_HI && g.images_full && g.lat_t;
+  const size_t smem = sizeof(double) * ((size_t)ns + 2 * (size_t)ns * ns + 3 * (size_t)ns +
+                                        (lat_smem ? 2 * (size_t)ns * g.ncp : 0));
   if (smem > 48 * 1024) {
     LFMM_CUDA(cudaFuncSetAttribute(k_hi_site, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   }

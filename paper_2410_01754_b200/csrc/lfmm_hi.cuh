@@ -136,17 +136,28 @@ __global__ void __launch_bounds__(HI_THREADS) k_hi_site(HiArgs g) {
       KG[e] = k;
     }
     // ---- lattice kernel G: R_t and U_t = T1 R_t come precomputed for all
-    // site atoms (k_hi_rvec + one batched GEMM, k_translate mode 2) ----
+    // site atoms (k_hi_rvec + one batched GEMM, k_translate mode 2); staged
+    // in shared memory, G_st = (1/L) <R_s, U_t>_packed, thread per pair ----
     if (lattice) {
+      double* Rs = pos + 3 * ns;         // ns x ncp
+      double* Us = Rs + (size_t)ns * ncp;  // ns x ncp
       const double* R = g.rscratch + (size_t)a0 * ncp;
       const double* U = g.uscratch + (size_t)a0 * ncp;
+      for (int e = tid; e < ns * ncp; e += blockDim.x) {
+        Rs[e] = R[e];
+        Us[e] = U[e];
+      }
+      __syncthreads();
       const double invL = 1.0 / L;
-      // G_st = (1/L) <R_s, U_t>, one warp per pair
-      for (int e = wid; e < ns * ns; e += blockDim.x / 32) {
+      for (int e = tid; e < ns * ns; e += blockDim.x) {
         const int i = e / ns, j = e % ns;
-        double v = packed_pair(R + (size_t)i * ncp, U + (size_t)j * ncp, p, lane, 32);
-        for (int off = 16; off > 0; off >>= 1) v += __shfl_down_sync(0xffffffffu, v, off);
-        if (lane == 0) GG[e] = v * invL;
+        const double* a = Rs + (size_t)i * ncp;
+        const double* b = Us + (size_t)j * ncp;
+        double v = 0.0;
+        for (int c = 0; c <= p; ++c) v = fma(a[c], b[c], v);  // m = 0 block
+        double w2 = 0.0;
+        for (int c = p + 1; c < nc; c += 2) w2 = fma(a[c], b[c], fma(-a[c + 1], b[c + 1], w2));
+        GG[e] = (v + 2.0 * w2) * invL;
       }
     }
   }

@@ -125,11 +125,18 @@ __device__ __forceinline__ bool key_less(double ax, double ay, double az, int ai
 }
 
 // One warp per leaf: rank of every bucket entry under (x, y, z, index).
-// Keys of 32 entries at a time are held by the lanes and broadcast with
-// shuffles, so the O(n^2) comparison loop touches no memory.
-__global__ void k_leaf_rank(const double* __restrict__ pos_wrap, const int* __restrict__ start,
-                            const int* __restrict__ bucket, int nleaf, int* __restrict__ perm,
-                            int* __restrict__ inv_perm) {
+// Fast path: x rounded to fp32 is monotone, so x32_j < x32_i (or >) decides
+// the fp64 order; the rank is the count of strictly smaller x32 in the leaf,
+// read as shared-memory broadcasts.  If any lane sees an x32 tie with another
+// entry (rare: fp32 resolves ~1e-6 nm), the warp recomputes that pass with
+// the exact (x, y, z, index) comparison, keys broadcast by shuffles.
+constexpr int RANK_WARPS = 4;
+__global__ void __launch_bounds__(RANK_WARPS * 32) k_leaf_rank(const double* __restrict__ pos_wrap,
+                                                              const int* __restrict__ start,
+                                                              const int* __restrict__ bucket, int nleaf,
+                                                              int* __restrict__ perm, int* __restrict__ inv_perm) {
+  __shared__ float kx[RANK_WARPS][32];
+  const int wl = threadIdx.x >> 5;
   const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
   if (warp >= nleaf) return;
@@ -144,23 +151,39 @@ __global__ void k_leaf_rank(const double* __restrict__ pos_wrap, const int* __re
       y = pos_wrap[3 * i + 1];
       z = pos_wrap[3 * i + 2];
     }
-    int rank = 0;
+    const float x32 = (float)x;
+    int rank = 0, eq = 0;
     for (int f0 = s0; f0 < s1; f0 += 32) {
       const int f = f0 + lane;
-      int jf = -1;
-      double xf = 0, yf = 0, zf = 0;
-      if (f < s1) {
-        jf = bucket[f];
-        xf = pos_wrap[3 * jf];
-        yf = pos_wrap[3 * jf + 1];
-        zf = pos_wrap[3 * jf + 2];
-      }
+      __syncwarp();
+      kx[wl][lane] = f < s1 ? (float)pos_wrap[3 * bucket[f]] : 0.f;
+      __syncwarp();
       const int cnt = min(32, s1 - f0);
       for (int k = 0; k < cnt; ++k) {
-        const int j = __shfl_sync(0xffffffffu, jf, k);
-        const double xj = __shfl_sync(0xffffffffu, xf, k), yj = __shfl_sync(0xffffffffu, yf, k),
-                     zj = __shfl_sync(0xffffffffu, zf, k);
-        rank += key_less(xj, yj, zj, j, x, y, z, i);
+        const float xj = kx[wl][k];
+        rank += xj < x32;
+        eq += xj == x32;
+      }
+    }
+    if (__any_sync(0xffffffffu, e < s1 && eq > 1)) {
+      rank = 0;
+      for (int f0 = s0; f0 < s1; f0 += 32) {
+        const int f = f0 + lane;
+        int jf = -1;
+        double xf = 0, yf = 0, zf = 0;
+        if (f < s1) {
+          jf = bucket[f];
+          xf = pos_wrap[3 * jf];
+          yf = pos_wrap[3 * jf + 1];
+          zf = pos_wrap[3 * jf + 2];
+        }
+        const int cnt = min(32, s1 - f0);
+        for (int k = 0; k < cnt; ++k) {
+          const int j = __shfl_sync(0xffffffffu, jf, k);
+          const double xj = __shfl_sync(0xffffffffu, xf, k), yj = __shfl_sync(0xffffffffu, yf, k),
+                       zj = __shfl_sync(0xffffffffu, zf, k);
+          rank += key_less(xj, yj, zj, j, x, y, z, i);
+        }
       }
     }
     if (e < s1) {
