@@ -26,12 +26,18 @@
 // chunk, hi/lo, 8-wide k group); a halo window is then one contiguous
 // cp.async.bulk per plane.
 //
-// Roles (352 threads, one CTA per SM):
+// Roles (384 threads, one CTA per SM):
 //   warps 0-7  workers: drain the accumulator of each iteration (tcgen05.ld)
 //              into fp32 register sums; final epilogue (partial slot)
-//   warp 8     MMA issuer (one lane)
-//   warp 9     A loader (one lane): one 8 KB cp.async.bulk per term
-//   warp 10    halo loader (one lane): 12 cp.async.bulk per iteration
+//   warps 8, 9 MMA issuers (one lane each): even / odd iterations into TMEM
+//              accumulators 0 / 1.  One issuing thread sustains only one
+//              MMA per ~130-190 clk (tools/tc_rate.cu), less than the 128
+//              clk an N = 256 MMA occupies the tensor core; two issuers reach
+//              it, and one issuer's MMAs overlap the other accumulator's drain.
+//              Each accumulator still sees its MMAs in one fixed order.
+//   warp 10    A loader (one lane): one 8 KB cp.async.bulk per term, the two
+//              iterations of a pair interleaved term by term in the ring
+//   warp 11    halo loader (one lane): 12 cp.async.bulk per iteration
 // Pipelines: halo buffers x2 (full/empty), TMEM accumulators x2 (full/empty),
 // A stages x HM_ASTAGES (full/empty).
 #pragma once
@@ -49,7 +55,7 @@ constexpr int HM_KC = 16;          // coefficients per iteration (one f16 MMA K)
 constexpr int HM_NKC = 8;          // 128 / 16
 constexpr int HM_ATILE = 8192;     // one operator chunk: hi 4 KB | lo 4 KB
 constexpr int HM_ASTAGES = 14;
-constexpr int HM_THREADS = 352;
+constexpr int HM_THREADS = 384;
 constexpr int HM_WORKERS = 256;
 
 // (tc, sc) term tables: count and {operator row, dx, dy, dz}
@@ -344,18 +350,20 @@ __global__ void __launch_bounds__(HM_THREADS, 1) k_m2l_halo(HaloArgs g) {
         }
       }
     }
-  } else if (warp == 8) {
-    // ================================================= MMA issuer ======
+  } else if (warp == 8 || warp == 9) {
+    // ================================================= MMA issuers =====
     if (lane == 0) {
+      const int par = warp - 8;
       const uint32_t idesc = hm_idesc(N);
       const uint32_t lbo = 3u * rw * 16u;
       // descriptors are advanced by adding (bytes >> 4) to the start-address
       // field (shared addresses < 256 KB: no carry out of its 14 bits)
       const uint64_t a_desc0 = hm_desc(smem_u32(abase), 128, 256);
-      int stage = 0, aphase = 0;
-      for (int it = 0; it < niter; ++it) {
-        const int k = it / HM_NKC;
+      int seq = 0;  // ring sequence number of this pair's first tile
+      for (int it0 = 0; it0 < niter; it0 += 2) {
+        const int k = it0 / HM_NKC;
         const int nt = s_nt[k];
+        const int it = it0 + par;
         {
           HM_T0();
           mbar_wait(smem_u32(&halo_full[it & 1]), (it >> 1) & 1);
@@ -372,12 +380,14 @@ __global__ void __launch_bounds__(HM_THREADS, 1) k_m2l_halo(HaloArgs g) {
         const uint32_t dacc = tmem + (uint32_t)((it & 1) * 256);
         uint32_t boff = s_boff[k][0];
         for (int t = 0; t < nt; ++t) {
+          const int sq = seq + 2 * t + par;
+          const int stage = sq % HM_ASTAGES;
           const uint64_t dbh = b_desc0 + boff;
           if (t + 1 < nt) boff = s_boff[k][t + 1];
           const uint64_t dah = a_desc0 + (uint64_t)(stage * (HM_ATILE >> 4));
           {
             HM_T0();
-            mbar_wait(smem_u32(&a_full[stage]), aphase);
+            mbar_wait(smem_u32(&a_full[stage]), (sq / HM_ASTAGES) & 1);
             HM_ACC(4);
           }
 #ifdef LFMM_HM_PROF
@@ -388,13 +398,10 @@ __global__ void __launch_bounds__(HM_THREADS, 1) k_m2l_halo(HaloArgs g) {
           hm_mma(dacc, dah, dbh + b_lo, idesc, 1u);
           hm_mma(dacc, dah + (4096 >> 4), dbh, idesc, 1u);
           tc_commit(smem_u32(&a_empty[stage]));
-          if (++stage == HM_ASTAGES) {
-            stage = 0;
-            aphase ^= 1;
-          }
         }
         tc_commit(smem_u32(&acc_full[it & 1]));
         tc_commit(smem_u32(&halo_empty[it & 1]));
+        seq += 2 * nt;
       }
 #ifdef LFMM_HM_PROF
       unsigned long long te;
@@ -403,23 +410,22 @@ __global__ void __launch_bounds__(HM_THREADS, 1) k_m2l_halo(HaloArgs g) {
 #endif
     }
     __syncwarp();
-  } else if (warp == 9) {
+  } else if (warp == 10) {
     // ================================================= A loader ========
     if (lane == 0) {
-      int stage = 0, ephase = 0, uses = 0;
-      for (int it = 0; it < niter; ++it) {
-        const int k = it / HM_NKC;
-        const int kc = it % HM_NKC;
+      int seq = 0;
+      for (int it0 = 0; it0 < niter; it0 += 2) {
+        const int k = it0 / HM_NKC;
         const int nt = s_nt[k];
         for (int t = 0; t < nt; ++t) {
           const int row = s_orow[k][t];
-          if (uses >= HM_ASTAGES) mbar_wait(smem_u32(&a_empty[stage]), ephase);
-          bulk_load(smem_u32(abase + stage * HM_ATILE), g.ops16 + ((size_t)row * HM_NKC + kc) * HM_ATILE, HM_ATILE,
-                    smem_u32(&a_full[stage]));
-          ++uses;
-          if (++stage == HM_ASTAGES) {
-            stage = 0;
-            if (uses > HM_ASTAGES) ephase ^= 1;
+#pragma unroll
+          for (int par = 0; par < 2; ++par, ++seq) {
+            const int kc = (it0 + par) % HM_NKC;
+            const int stage = seq % HM_ASTAGES, use = seq / HM_ASTAGES;
+            if (use >= 1) mbar_wait(smem_u32(&a_empty[stage]), (use - 1) & 1);
+            bulk_load(smem_u32(abase + stage * HM_ATILE), g.ops16 + ((size_t)row * HM_NKC + kc) * HM_ATILE, HM_ATILE,
+                      smem_u32(&a_full[stage]));
           }
         }
       }
