@@ -124,9 +124,29 @@ __global__ void k_transpose_ops(const T* __restrict__ in, T* __restrict__ out, i
   out[(m * ncp + k) * ncp + r] = in[i];
 }
 
-template <class T>
+template <class T, int CPW>
 inline size_t tr_smem_bytes(int ncp) {
-  return sizeof(T) * (2 * (size_t)TR_KC * ncp + 2 * (size_t)TR_PT * TR_KC);
+  return sizeof(T) * (2 * (size_t)TR_KC * ncp + 2 * (size_t)(8 * CPW) * TR_KC);
+}
+
+// one k_translate launch: CPW = 8 columns per warp (64 per CTA) once there
+// are enough target columns to fill the GPU, else 2 (16 per CTA)
+template <class T>
+inline void tr_launch(const TrArgs& ta, int ncols_total, int noct, cudaStream_t st) {
+  if (ncols_total >= 4096) {
+    const unsigned tiles = (unsigned)((ncols_total + 63) / 64);
+    k_translate<T, 8><<<dim3(tiles, noct), TR_THREADS, tr_smem_bytes<T, 8>(ta.ncp), st>>>(ta);
+  } else {
+    const unsigned tiles = (unsigned)((ncols_total + 15) / 16);
+    k_translate<T, 2><<<dim3(tiles, noct), TR_THREADS, tr_smem_bytes<T, 2>(ta.ncp), st>>>(ta);
+  }
+}
+template <class T>
+inline void tr_set_attrs(int ncp) {
+  LFMM_CUDA(cudaFuncSetAttribute(k_translate<T, 8>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)tr_smem_bytes<T, 8>(ncp)));
+  LFMM_CUDA(cudaFuncSetAttribute(k_translate<T, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)tr_smem_bytes<T, 2>(ncp)));
 }
 
 // Exact box charges (the l = 0 multipole) at every level.  The fp32 P2M/M2M
@@ -756,11 +776,10 @@ struct lfmm_plan {
       launch(ST_SETUP, [&] {
         k_transpose_ops<T><<<nblk(tot, 256), 256, 0, stream>>>(ops_l2l.as<T>(), ops_l2l_t.as<T>(), ncp, 8);
       });
-      const int64_t tiles = std::max<int64_t>(1, ((1LL << (3 * (depth - 1))) + TR_PT - 1) / TR_PT);
+      const int64_t tiles = std::max<int64_t>(1, ((1LL << (3 * (depth - 1))) + 15) / 16);
       tr_cnt.ensure(sizeof(int) * tiles);
       LFMM_CUDA(cudaMemsetAsync(tr_cnt.p, 0, tr_cnt.bytes, stream));
-      LFMM_CUDA(cudaFuncSetAttribute(k_translate<T>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                     (int)tr_smem_bytes<T>(ncp)));
+      tr_set_attrs<T>(ncp);
     }
     if (lattice_mode != LFMM_LATTICE_OFF) {
       lat_unit = build_lattice_unit();
@@ -980,14 +999,9 @@ struct lfmm_plan {
                                                           cursor.as<int>(), bucket.as<int>());
       });
       launch(ST_TREE, [&] {
-        k_leaf_rank<<<nblk((int64_t)nleaf * 32, RANK_WARPS * 32), RANK_WARPS * 32, 0, stream>>>(
-            pos_wrap.as<double>(), leaf_start.as<int>(), bucket.as<int>(), nleaf, perm.as<int>(), inv_perm.as<int>());
-      });
-      launch(ST_TREE, [&] {
-        k_sorted_arrays<T><<<nblk(N, 256), 256, 0, stream>>>(pos_wrap.as<double>(), perm.as<int>(),
-                                                              leaf_of.as<int>(), N, depth, size,
-                                                              pos_sorted.as<double>(), xq.as<vec4_t<T>>(),
-                                                              leaf_sorted.as<int>());
+        k_leaf_rank<T><<<nblk((int64_t)nleaf * 32, RANK_WARPS * 32), RANK_WARPS * 32, 0, stream>>>(
+            pos_wrap.as<double>(), leaf_start.as<int>(), bucket.as<int>(), nleaf, perm.as<int>(), inv_perm.as<int>(),
+            depth, size, pos_sorted.as<double>(), xq.as<vec4_t<T>>(), leaf_sorted.as<int>());
       });
     }
     last_valid = false;
@@ -1049,10 +1063,7 @@ struct lfmm_plan {
         ta.dst = M + level_off[l] * ncp;
         ta.slots = up_part.p;
         ta.cnt = tr_cnt.as<int>();
-        const unsigned tiles = (unsigned)(((1LL << (3 * l)) + TR_PT - 1) / TR_PT);
-        launch(ST_M2M, [&] {
-          k_translate<T><<<dim3(tiles, 8), TR_THREADS, tr_smem_bytes<T>(ncp), stream>>>(ta);
-        });
+        launch(ST_M2M, [&] { tr_launch<T>(ta, 1 << (3 * l), 8, stream); });
         continue;
       }
       ga.mode = GEMM_UP;
@@ -1073,7 +1084,7 @@ struct lfmm_plan {
       ta.ops_t = ops_lat_t.p;
       ta.src = M;
       ta.dst = Lc;
-      launch(ST_ROOT, [&] { k_translate<T><<<dim3(1, 1), TR_THREADS, tr_smem_bytes<T>(ncp), stream>>>(ta); });
+      launch(ST_ROOT, [&] { tr_launch<T>(ta, 1, 1, stream); });
     } else if (lattice_mode != LFMM_LATTICE_OFF) {
       ga.mode = GEMM_ROOT;
       ga.level = 0;
@@ -1142,10 +1153,7 @@ struct lfmm_plan {
           ta.dst = Lc + level_off[l] * ncp;
           ta.partial = static_cast<const char*>(partial.p) + tsz() * (size_t)part_off[l] * ncp;
           ta.nsplit = nsplit[l];
-          const unsigned tiles = (unsigned)(((1LL << (3 * (l - 1))) + TR_PT - 1) / TR_PT);
-          launch(ST_L2L, [&] {
-            k_translate<T><<<dim3(tiles, 8), TR_THREADS, tr_smem_bytes<T>(ncp), stream>>>(ta);
-          });
+          launch(ST_L2L, [&] { tr_launch<T>(ta, 1 << (3 * (l - 1)), 8, stream); });
           continue;
         }
         ga.mode = GEMM_L2L;
@@ -1391,14 +1399,10 @@ void run_hi(lfmm_plan* pl, int mode, const double* pot_dev, const double* pot_si
       ta.dst = g.uscratch;
       static bool attr_set = false;
       if (!attr_set) {
-        LFMM_CUDA(cudaFuncSetAttribute(k_translate<double>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       (int)tr_smem_bytes<double>(g.ncp)));
+        tr_set_attrs<double>(g.ncp);
         attr_set = true;
       }
-      pl->launch(ST_HI, [&] {
-        k_translate<double><<<dim3((unsigned)((na + TR_PT - 1) / TR_PT), 1), TR_THREADS, tr_smem_bytes<double>(g.ncp),
-                              pl->stream>>>(ta);
-      });
+      pl->launch(ST_HI, [&] { tr_launch<double>(ta, na, 1, pl->stream); });
     } else {
       pl->launch(ST_HI, [&] {
         k_hi_umat<<<nblk((int64_t)na * g.ncp, 128), 128, 0, pl->stream>>>(g.lat_t, g.rscratch, na, ncoef(g.p), g.ncp,

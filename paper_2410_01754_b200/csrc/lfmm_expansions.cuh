@@ -850,7 +850,7 @@ namespace lfmm {
 //       B = parent locals; child(p, o) local = D + the level's M2L partial
 //       slots in slot order.
 // 256 threads: lane -> 4 consecutive rows (coefficients), warp -> 2 columns.
-constexpr int TR_PT = 16, TR_KC = 32, TR_THREADS = 256;
+constexpr int TR_KC = 32, TR_THREADS = 256;  // columns per CTA: 8 warps x CPW (template)
 
 struct TrArgs {
   int mode;            // 0 UP (M2M), 1 DOWN (L2L), 2 plain columns (dst[:, c] = Op src[:, c])
@@ -872,21 +872,22 @@ __device__ __forceinline__ void tr_cp16(T* sdst, const T* gsrc) {
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(s), "l"(gsrc) : "memory");
 }
 
-template <class T>
+template <class T, int CPW>
 __global__ void __launch_bounds__(TR_THREADS) k_translate(TrArgs g) {
   constexpr int VW = 16 / sizeof(T);  // elements per 16-B copy
+  constexpr int PT = 8 * CPW;         // target columns per CTA (8 warps x CPW)
   extern __shared__ __align__(16) unsigned char tr_smem[];
   T* As = reinterpret_cast<T*>(tr_smem);              // [2][TR_KC][ncp]
   const int ncp = g.ncp;
-  T* Bs = As + 2 * TR_KC * ncp;                        // [2][TR_PT][TR_KC]
-  __shared__ int col_src[TR_PT], col_dst[TR_PT];
+  T* Bs = As + 2 * TR_KC * ncp;                        // [2][PT][TR_KC]
+  __shared__ int col_src[PT], col_dst[PT];
   const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
   const int o = blockIdx.y;
   const int tile = blockIdx.x;
   const int pl = g.mode == 0 ? g.level : g.level - 1;  // parent level
   const int np = 1 << (3 * pl), pn = 1 << pl, cn = 2 * pn;
-  if (tid < TR_PT) {
-    const int p = tile * TR_PT + tid;
+  if (tid < PT) {
+    const int p = tile * PT + tid;
     int s = -1, d = -1;
     if (g.mode == 2) {
       if (p < g.ncols) s = d = p;
@@ -912,8 +913,8 @@ __global__ void __launch_bounds__(TR_THREADS) k_translate(TrArgs g) {
     T* a = As + (size_t)buf * TR_KC * ncp;
     const T* ga = ops + (size_t)kc * TR_KC * ncp;
     for (int e = tid; e < TR_KC * ncp / VW; e += TR_THREADS) tr_cp16(a + e * VW, ga + e * VW);
-    T* b = Bs + (size_t)buf * TR_PT * TR_KC;
-    for (int e = tid; e < TR_PT * TR_KC / VW; e += TR_THREADS) {
+    T* b = Bs + (size_t)buf * PT * TR_KC;
+    for (int e = tid; e < PT * TR_KC / VW; e += TR_THREADS) {
       const int c = e / (TR_KC / VW), u = e % (TR_KC / VW);
       const int sb = col_src[c];
       if (sb >= 0)
@@ -924,11 +925,12 @@ __global__ void __launch_bounds__(TR_THREADS) k_translate(TrArgs g) {
     }
     asm volatile("cp.async.commit_group;" ::: "memory");
   };
-  T acc[4][2];
+  T acc[4][CPW];
 #pragma unroll
-  for (int i = 0; i < 4; ++i) acc[i][0] = acc[i][1] = T(0);
-  const int r0 = 4 * lane;       // rows r0..r0+3 (ncp = 128 for the 4-row mapping; see below)
-  const int rows_per_lane = ncp / 32;  // 4 when ncp == 128; general ncp handled by the row loop
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int j = 0; j < CPW; ++j) acc[i][j] = T(0);
+  const int r0 = 4 * lane;  // rows r0..r0+3 (the plan routes only ncp == 128 here)
   stage(0, 0);
   for (int kc = 0; kc < nk; ++kc) {
     if (kc + 1 < nk) {
@@ -939,29 +941,30 @@ __global__ void __launch_bounds__(TR_THREADS) k_translate(TrArgs g) {
     }
     __syncthreads();
     const T* a = As + (size_t)(kc & 1) * TR_KC * ncp;
-    const T* b = Bs + (size_t)(kc & 1) * TR_PT * TR_KC;
-    if (rows_per_lane == 4) {
-#pragma unroll 8
-      for (int k = 0; k < TR_KC; ++k) {
-        T av[4];
-        ldv<T, 4>(a + k * ncp + r0, av);
-        const T b0 = b[(2 * w) * TR_KC + k], b1 = b[(2 * w + 1) * TR_KC + k];
+    const T* b = Bs + (size_t)(kc & 1) * PT * TR_KC + (size_t)(CPW * w) * TR_KC;
+#pragma unroll 2
+    for (int k = 0; k < TR_KC; k += 4) {
+      T av[4][4];
 #pragma unroll
-        for (int u = 0; u < 4; ++u) {
-          acc[u][0] = fma(av[u], b0, acc[u][0]);
-          acc[u][1] = fma(av[u], b1, acc[u][1]);
-        }
+      for (int kk = 0; kk < 4; ++kk) ldv<T, 4>(a + (k + kk) * ncp + r0, av[kk]);
+#pragma unroll
+      for (int j = 0; j < CPW; ++j) {
+        T bv[4];
+        ldv<T, 4>(b + j * TR_KC + k, bv);
+#pragma unroll
+        for (int kk = 0; kk < 4; ++kk)
+#pragma unroll
+          for (int u = 0; u < 4; ++u) acc[u][j] = fma(av[kk][u], bv[kk], acc[u][j]);
       }
     }
     __syncthreads();
   }
-  if (rows_per_lane != 4) return;  // (the plan only routes ncp == 128 here)
   // ---- epilogue ----
   if (g.mode == 2) {
     T* dst = reinterpret_cast<T*>(g.dst);
 #pragma unroll
-    for (int j = 0; j < 2; ++j) {
-      const int d = col_dst[2 * w + j];
+    for (int j = 0; j < CPW; ++j) {
+      const int d = col_dst[CPW * w + j];
       if (d < 0) continue;
       T v4[4] = {acc[0][j], acc[1][j], acc[2][j], acc[3][j]};
       stv<T, 4>(dst + (size_t)d * ncp + r0, v4);
@@ -969,8 +972,8 @@ __global__ void __launch_bounds__(TR_THREADS) k_translate(TrArgs g) {
   } else if (g.mode == 0) {
     T* slots = reinterpret_cast<T*>(g.slots);
 #pragma unroll
-    for (int j = 0; j < 2; ++j) {
-      const int c = 2 * w + j, d = col_dst[c];
+    for (int j = 0; j < CPW; ++j) {
+      const int d = col_dst[CPW * w + j];
       if (d < 0) continue;
       T v4[4] = {acc[0][j], acc[1][j], acc[2][j], acc[3][j]};
       stv<T, 4>(slots + ((size_t)o * np + d) * ncp + r0, v4);
@@ -983,7 +986,7 @@ __global__ void __launch_bounds__(TR_THREADS) k_translate(TrArgs g) {
     if (!last) return;
     __threadfence();
     T* dst = reinterpret_cast<T*>(g.dst);
-    for (int e = tid; e < TR_PT * ncp; e += TR_THREADS) {
+    for (int e = tid; e < PT * ncp; e += TR_THREADS) {
       const int c = e / ncp, r = e % ncp, d = col_dst[c];
       if (d < 0) continue;
       T v = T(0);
@@ -997,8 +1000,8 @@ __global__ void __launch_bounds__(TR_THREADS) k_translate(TrArgs g) {
     T* dst = reinterpret_cast<T*>(g.dst);
     const size_t nchild = (size_t)np * 8;
 #pragma unroll
-    for (int j = 0; j < 2; ++j) {
-      const int c = 2 * w + j, d = col_dst[c];
+    for (int j = 0; j < CPW; ++j) {
+      const int d = col_dst[CPW * w + j];
       if (d < 0) continue;
       T v4[4] = {acc[0][j], acc[1][j], acc[2][j], acc[3][j]};
       for (int s = 0; s < g.nsplit; ++s) {

@@ -130,11 +130,18 @@ __device__ __forceinline__ bool key_less(double ax, double ay, double az, int ai
 // read as shared-memory broadcasts.  If any lane sees an x32 tie with another
 // entry (rare: fp32 resolves ~1e-6 nm), the warp recomputes that pass with
 // the exact (x, y, z, index) comparison, keys broadcast by shuffles.
+// The ranked entry also writes its canonical-order arrays (fp64 sorted
+// positions, leaf-relative coordinates x - c_leaf with c_leaf = (grid + 0.5)
+// size (octree.py:65-66) in T, leaf index), which it holds in registers.
 constexpr int RANK_WARPS = 4;
+template <class T>
 __global__ void __launch_bounds__(RANK_WARPS * 32) k_leaf_rank(const double* __restrict__ pos_wrap,
                                                               const int* __restrict__ start,
                                                               const int* __restrict__ bucket, int nleaf,
-                                                              int* __restrict__ perm, int* __restrict__ inv_perm) {
+                                                              int* __restrict__ perm, int* __restrict__ inv_perm,
+                                                              int depth, double size, double* __restrict__ pos_sorted,
+                                                              vec4_t<T>* __restrict__ xq,
+                                                              int* __restrict__ leaf_sorted) {
   __shared__ float kx[RANK_WARPS][32];
   const int wl = threadIdx.x >> 5;
   const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
@@ -187,8 +194,21 @@ __global__ void __launch_bounds__(RANK_WARPS * 32) k_leaf_rank(const double* __r
       }
     }
     if (e < s1) {
-      perm[s0 + rank] = i;
-      inv_perm[i] = s0 + rank;
+      const int k = s0 + rank;
+      perm[k] = i;
+      inv_perm[i] = k;
+      const int nside = 1 << depth, msk = nside - 1;
+      const int leaf = warp;
+      pos_sorted[3 * (size_t)k] = x;
+      pos_sorted[3 * (size_t)k + 1] = y;
+      pos_sorted[3 * (size_t)k + 2] = z;
+      vec4_t<T> v;
+      v.x = (T)(x - ((leaf >> (2 * depth)) + 0.5) * size);
+      v.y = (T)(y - (((leaf >> depth) & msk) + 0.5) * size);
+      v.z = (T)(z - ((leaf & msk) + 0.5) * size);
+      v.w = T(0);
+      xq[k] = v;
+      leaf_sorted[k] = leaf;
     }
   }
 }

@@ -44,9 +44,12 @@ __global__ void k_rate(int N, int terms, int nacc, int mode, unsigned long long*
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
   // mode bit1: the whole warp 0 runs the loop (converged); bit2: warps 0 and 1
   // each issue half of the terms into their own accumulators
-  const bool issuer = (mode & 6) ? ((mode & 4) ? threadIdx.x < 64 : threadIdx.x < 32) : threadIdx.x == 0;
+  // bit3: issuers are lane 0 of warps 0..(1 << (mode >> 4)) - 1 (one thread each)
+  const int nw_iss = (mode & 8) ? (1 << (mode >> 4)) : 1;
+  const bool issuer = (mode & 8) ? ((threadIdx.x & 31) == 0 && (threadIdx.x >> 5) < nw_iss)
+                                 : ((mode & 6) ? ((mode & 4) ? threadIdx.x < 64 : threadIdx.x < 32) : threadIdx.x == 0);
   if (issuer) {
-    const int wsplit = (mode & 4) ? 2 : 1, wid = threadIdx.x >> 5;
+    const int wsplit = (mode & 8) ? nw_iss : ((mode & 4) ? 2 : 1), wid = threadIdx.x >> 5;
     const uint32_t idesc = (1u << 4) | ((uint32_t)(N >> 3) << 17) | (8u << 24);
     const uint64_t da = desc(su32(sm), 128, 256);
     const uint64_t db = desc(su32(sm + 8192), 300 * 16, 128);
@@ -85,9 +88,9 @@ int main() {
   cudaFuncSetAttribute(k_rate, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024);
   const int terms = 2000;
   printf("clk per MMA (3 MMAs per term, %d terms): issue-loop / until-complete\n", terms);
-  for (int mode : {0, 2, 4 + 2})
+  for (int mode : {0, 8 + 16, 8 + 32})
     for (int N : {16, 128, 256})
-      for (int nacc : {2, 4}) {
+      for (int nacc : {4}) {
         if (N * nacc > 512) continue;
         k_rate<<<1, 128, 64 * 1024>>>(N, terms, nacc, mode, d);
         unsigned long long h[2];
