@@ -1004,11 +1004,16 @@ __global__ void __launch_bounds__(TR_THREADS) k_translate(TrArgs g) {
       const int d = col_dst[CPW * w + j];
       if (d < 0) continue;
       T v4[4] = {acc[0][j], acc[1][j], acc[2][j], acc[3][j]};
-      for (int s = 0; s < g.nsplit; ++s) {
-        T q4[4];
-        ldv<T, 4>(part + ((size_t)s * nchild + d) * ncp + r0, q4);
+      for (int s0 = 0; s0 < g.nsplit; s0 += 8) {  // slots in fixed order, 8 loads in flight
+        T q4[8][4];
 #pragma unroll
-        for (int u = 0; u < 4; ++u) v4[u] += q4[u];
+        for (int s = 0; s < 8; ++s)
+          if (s0 + s < g.nsplit) ldv<T, 4>(part + ((size_t)(s0 + s) * nchild + d) * ncp + r0, q4[s]);
+#pragma unroll
+        for (int s = 0; s < 8; ++s)
+          if (s0 + s < g.nsplit)
+#pragma unroll
+            for (int u = 0; u < 4; ++u) v4[u] += q4[s][u];
       }
       stv<T, 4>(dst + (size_t)d * ncp + r0, v4);
     }
