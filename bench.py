@@ -326,20 +326,42 @@ def run_ours(args):
             row["algorithmic_gflop"] = round(fl / 1e9, 3)
             row["achieved_tflops"] = round(fl / (ms * 1e-3) / 1e12, 3) if ms > 0 else None
         stage_rows[name] = row
-    dom = max(stage_rows, key=lambda k: stage_rows[k]["ms"])
-    # dominant kernel roofline: per launch = per-step work / launches
-    fl = work.get(dom, {}).get("flop", 0.0) if isinstance(work.get(dom), dict) else 0.0
-    dom_ms = stage_rows[dom]["ms"]
-    achieved = fl / (dom_ms * 1e-3) / 1e12 if dom_ms > 0 else 0.0
-    fp32_pipe = 62.2  # TFLOP/s, profiles/r01_pipe_peaks.txt (FFMA microbenchmark on this pool)
+    # Roofline of the dominant tensor-core kernel, k_m2l_halo ("m2l" stage =
+    # that launch alone; its absmax/pack passes are "m2l_pack").  Algorithmic
+    # work = 2 (p+1)^4 flop per M2L translation (dense real-packed operator,
+    # SURVEY.md 8d) x 189 sum_l 8^l translations per launch; the kernel issues
+    # 3 fp16 products per term on 128x128 padded operators, counted separately
+    # as "issued_tflops".  Peak = measured dense bf16 (= fp16) tensor rate.
+    peaks, peak_kind = measured_peaks()
+    m2l_ms = stage_rows.get("m2l", {}).get("ms", 0.0)
+    fl = work["m2l"]["flop"]
+    achieved = fl / (m2l_ms * 1e-3) / 1e12 if m2l_ms > 0 else 0.0
+    t_m2l = work["t_m2l"]
+    issued = 3 * 2.0 * 128 * 128 * t_m2l
+    traffic = None
+    try:
+        with open(os.path.join(ROOT, "profiles", "r01_m2l_traffic.json")) as fh:
+            traffic = json.load(fh).get("dram_bytes_per_launch")
+    except OSError:
+        pass
     roofline = {
-        "kernel": dom, "bound": "tensor", "achieved": round(achieved, 3), "peak": peaks.get("bf16_tflops"),
-        "unit": "TFLOP/s", "frac": round(achieved / peaks.get("bf16_tflops", 1.0), 5), "traffic": None,
-        "peak_source": f"{peak_kind} bf16 dense (MEASURED_PEAKS.json); kernel runs on FP32 SIMT pipes",
-        "fp32_simt_peak": fp32_pipe, "frac_of_fp32_simt": round(achieved / fp32_pipe, 4),
-        "algorithmic": "2*(p+1)^4 flop per M2L translation (dense real-packed operator), 189*sum_l 8^l "
-                       "translations per step" if dom == "m2l" else "see stages",
+        "kernel": "k_m2l_halo (M2L, tcgen05 kind::f16 3-product split)", "bound": "tensor",
+        "achieved": round(achieved, 3), "peak": peaks.get("bf16_tflops"), "unit": "TFLOP/s",
+        "frac": round(achieved / peaks.get("bf16_tflops", 1.0), 5), "traffic": traffic,
+        "peak_source": f"{peak_kind} dense bf16 tensor rate (MEASURED_PEAKS.json; fp16 runs at the same rate)",
+        "algorithmic": "2*(p+1)^4 flop per M2L translation x 189*sum_l 8^l translations per launch "
+                       f"({t_m2l} translations)",
+        "issued_tflops": round(issued / (m2l_ms * 1e-3) / 1e12, 3) if m2l_ms > 0 else None,
+        "traffic_source": "ncu --set full dram__bytes_read.sum + dram__bytes_write.sum of one launch "
+                          "(profiles/r01_m2l_traffic.json)",
     }
+    p2p_ms = stage_rows.get("p2p", {}).get("ms", 0.0)
+    fp32_pipe = 62.2  # TFLOP/s, FFMA microbenchmark on this pool (profiles/r01_pipe_peaks.txt)
+    p2p_tf = work["p2p"]["flop"] / (p2p_ms * 1e-3) / 1e12 if p2p_ms > 0 else 0.0
+    roofline_p2p = {"kernel": "k_p2p2 (near field, packed f32x2)", "bound": "fp32 pipe",
+                    "achieved": round(p2p_tf, 3), "peak": fp32_pipe, "unit": "TFLOP/s",
+                    "frac": round(p2p_tf / fp32_pipe, 4),
+                    "algorithmic": "20 flop per ordered pair (potential + gradient), exact pair count"}
 
     cpu = None
     if rank == 0 and not args.no_cpu_baseline and world == 1:
@@ -363,6 +385,7 @@ def run_ours(args):
         "gpu_launches": launches,
         "clocks": clk.summary(),
         "roofline": roofline,
+        "roofline_p2p": roofline_p2p,
         "stages": stage_rows,
         "p2p_pairs": pairs,
         "cpu_baseline": cpu,

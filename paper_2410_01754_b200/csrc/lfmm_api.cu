@@ -48,10 +48,11 @@ enum Stage {
   ST_HI,
   ST_SCALE,
   ST_SETUP,
+  ST_PACK,
   ST_COUNT
 };
 const char* kStageNames[ST_COUNT] = {"tree",  "stage_q", "p2p",      "p2m", "m2m",   "lattice",
-                                     "m2l", "l2l", "l2p",   "finalize", "hi",  "scale", "setup"};
+                                     "m2l", "l2l", "l2p",   "finalize", "hi",  "scale", "setup", "m2l_pack"};
 
 // ------------------------------------------------------------ kernels ----
 // Fixed-order reduction of NQ double-double block partials by one block.
@@ -1113,11 +1114,11 @@ struct lfmm_plan {
           ha.m16_off[l] = m16_off[l];
         }
         LFMM_CUDA(cudaMemsetAsync(hm_level_max.p, 0, hm_level_max.bytes, stream));
-        launch(ST_DOWN, [&] {
+        launch(ST_PACK, [&] {
           k_level_absmax<<<dim3((unsigned)std::max<int64_t>(1, ((1LL << (3 * depth)) + 63) / 64), depth), 256, 0,
                            stream>>>(ha.mult, ha, hm_level_max.as<unsigned int>());
         });
-        launch(ST_DOWN, [&] {
+        launch(ST_PACK, [&] {
           k_pack_mult16<<<dim3((unsigned)((hm_plane_rows(depth) + 127) / 128), depth, 8), 128, 0, stream>>>(ha);
         });
         launch(ST_DOWN, [&] {
