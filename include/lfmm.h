@@ -170,6 +170,41 @@ int lfmm_stage_times(lfmm_plan* plan, double* ms, int64_t* launches, int n);
 /* Number of kernel launches the library issued since plan creation. */
 int64_t lfmm_launch_count(const lfmm_plan* plan);
 
+/* ---- Octree slab decomposition (driven by
+ * paper_2410_01754_b200/distributed.py, one rank per GPU).  Each rank owns
+ * the leaves with x index in [x0, x1) of the global grid and holds its owned
+ * atoms plus a one-leaf halo; levels < lg (boxes spanning ranks) are
+ * computed redundantly from the gathered level lg.  No reference counterpart:
+ * the reference is single-process. */
+
+/* Re-size the plan's particle arrays for n particles (the local count
+ * changes from step to step). */
+int lfmm_plan_set_count(lfmm_plan* plan, int64_t n);
+
+/* Owned leaf x-range and shared-level count; restricts P2P/L2P/energies/
+ * dipole sums to owned leaves and the tensor-core M2L jobs to owned targets. */
+int lfmm_dist_configure(lfmm_plan* plan, int x0, int x1, int lg);
+
+/* phase 1: [tree from positions] + charges [+ lambda scaling] + P2P + P2M +
+ * M2M of levels >= lg + exact box charges.  phase 2: levels < lg, lattice,
+ * M2L, L2L, L2P, finalize, owned site-atom potentials.  Device pointers.
+ * Between the phases the caller all-gathers the owned multipoles of levels
+ * >= lg and replaces scal[0..3] by the global dipole and charge sums. */
+int lfmm_dist_phase(lfmm_plan* plan, int phase, const double* positions, const double* charges,
+                    const double* lambdas, const int32_t* n_lambda, int grad);
+
+/* Device pointers of the exchanged buffers: ptrs[0] multipoles (all levels,
+ * ncp per box), [1] scal (D_x, D_y, D_z, Q fp64), [2] energies (total, near,
+ * far, dipole), [3] forces (N x 3 local input order), [4] site-atom
+ * potentials, [5] lambda forces (S x 4), [6] HI energy offset, [7] the plan's
+
+ * cudaStream_t.  level_off (8 entries): first box of each level. */
+int lfmm_dist_buffers(lfmm_plan* plan, void** ptrs, int64_t* level_off);
+
+/* HI corrections + lambda forces for every site from the gathered site-atom
+ * potentials (ptrs[4]); site_positions (A x 3, device) caller-supplied. */
+int lfmm_dist_hi(lfmm_plan* plan, const double* site_positions, int mode);
+
 #ifdef __cplusplus
 }
 #endif

@@ -60,6 +60,11 @@ def _declare(lib):
         "lfmm_stage_name": (_c.c_char_p, [_i32]),
         "lfmm_stage_times": (_i32, [_vp, _vp, _vp, _i32]),
         "lfmm_launch_count": (_i64, [_vp]),
+        "lfmm_plan_set_count": (_i32, [_vp, _i64]),
+        "lfmm_dist_configure": (_i32, [_vp, _i32, _i32, _i32]),
+        "lfmm_dist_phase": (_i32, [_vp, _i32, _vp, _vp, _vp, _vp, _i32]),
+        "lfmm_dist_buffers": (_i32, [_vp, _vp, _vp]),
+        "lfmm_dist_hi": (_i32, [_vp, _vp, _i32]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(lib, name)
@@ -75,6 +80,7 @@ def exported_symbols():
         "lfmm_export_lists", "lfmm_lattice_matrix", "lfmm_solve", "lfmm_sites_set", "lfmm_hi",
         "lfmm_assemble", "lfmm_scale_charges", "lfmm_step", "lfmm_profile_enable",
         "lfmm_stage_count", "lfmm_stage_name", "lfmm_stage_times", "lfmm_launch_count",
+        "lfmm_plan_set_count", "lfmm_dist_configure", "lfmm_dist_phase", "lfmm_dist_buffers", "lfmm_dist_hi",
     ]
 
 
@@ -273,6 +279,27 @@ class Plan:
 
     def launch_count(self):
         return int(lib().lfmm_launch_count(self.h))
+
+    # ---- slab decomposition (distributed.py) ----
+    def set_count(self, n):
+        check(lib().lfmm_plan_set_count(self.h, int(n)))
+        self.n = int(n)
+
+    def dist_configure(self, x0, x1, lg):
+        check(lib().lfmm_dist_configure(self.h, int(x0), int(x1), int(lg)))
+
+    def dist_phase(self, phase, positions=None, charges=None, lambdas=None, n_lambda=None, grad=True):
+        check(lib().lfmm_dist_phase(self.h, int(phase), ptr(positions), ptr(charges), ptr(lambdas), ptr(n_lambda),
+                                    1 if grad else 0))
+
+    def dist_buffers(self):
+        ptrs = (ctypes.c_void_p * 8)()
+        offs = np.zeros(8, np.int64)
+        check(lib().lfmm_dist_buffers(self.h, ptrs, ptr(offs)))
+        return [p if p is not None else 0 for p in ptrs], offs
+
+    def dist_hi(self, site_positions, mode=MODE_HI):
+        check(lib().lfmm_dist_hi(self.h, ptr(site_positions), int(mode)))
 
 
 def assemble(atom_offsets, atom_index, n_forms, form_offsets, form_charges, lambdas, n_lambda, c_total,

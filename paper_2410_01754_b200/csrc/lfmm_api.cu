@@ -98,7 +98,8 @@ template <class T>
 __global__ void k_stage_q(const double* __restrict__ q, int K, int c, const int* __restrict__ perm,
                           const double* __restrict__ pos_sorted, int64_t n, double box,
                           vec4_t<T>* __restrict__ xq, double* __restrict__ qs, dd* __restrict__ part,
-                          int* __restrict__ cnt, double* __restrict__ scal) {
+                          int* __restrict__ cnt, double* __restrict__ scal, const int* __restrict__ leaf_sorted,
+                          int depth, int x0, int x1) {
   dd v[4] = {dd{0, 0}, dd{0, 0}, dd{0, 0}, dd{0, 0}};
   // grid-stride (a few blocks per SM: the last-block counter sees few atomics)
   for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < n; k += (int64_t)gridDim.x * blockDim.x) {
@@ -106,6 +107,8 @@ __global__ void k_stage_q(const double* __restrict__ q, int K, int c, const int*
     const double qv = q[(size_t)i * K + c];
     xq[k].w = (T)qv;
     qs[k] = qv;
+    const int lx = leaf_sorted[k] >> (2 * depth);
+    if (lx < x0 || lx >= x1) continue;  // halo atom: not this rank's dipole / charge
     const double h = 0.5 * box;
     v[0] = dd_add(v[0], dd_from((pos_sorted[3 * k] - h) * qv));
     v[1] = dd_add(v[1], dd_from((pos_sorted[3 * k + 1] - h) * qv));
@@ -243,7 +246,8 @@ __global__ void k_finalize(int64_t n, int K, int c, const int* __restrict__ perm
                            double* __restrict__ out_far, double* __restrict__ out_dip,
                            double* __restrict__ out_forces, dd* __restrict__ part, int* __restrict__ cnt,
                            double* __restrict__ epart, double* __restrict__ energies, double* __restrict__ dvec,
-                           double* __restrict__ qtot) {
+                           double* __restrict__ qtot, const int* __restrict__ leaf_sorted, int depth, int x0,
+                           int x1) {
   dd v[2] = {dd{0, 0}, dd{0, 0}};
   for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < n; k += (int64_t)gridDim.x * blockDim.x) {
     const int i = perm[k];
@@ -269,6 +273,8 @@ __global__ void k_finalize(int64_t n, int K, int c, const int* __restrict__ perm
         out_forces[3 * (size_t)i + a] = f;
       }
     }
+    const int lx = leaf_sorted[k] >> (2 * depth);
+    if (lx < x0 || lx >= x1) continue;  // halo atom: energy counted by its owner
     v[0] = dd_add(v[0], dd_from(q * vn));
     v[1] = dd_add(v[1], dd_from(q * vf));
   }
@@ -300,10 +306,20 @@ template <class T>
 __global__ void k_site_pot(const int* __restrict__ atom_idx, int n, const int* __restrict__ inv_perm,
                            const T* __restrict__ vnear, const T* __restrict__ vfar,
                            const double* __restrict__ pos_sorted, const double* __restrict__ scal, int dipole,
-                           double box, double* __restrict__ out) {
+                           double box, double* __restrict__ out, const int* __restrict__ leaf_sorted, int depth,
+                           int x0, int x1) {
   const int a = blockIdx.x * blockDim.x + threadIdx.x;
   if (a >= n) return;
+  if (atom_idx[a] < 0) {  // site atom held by another rank (distributed.py)
+    out[a] = 0.0;
+    return;
+  }
   const int k = inv_perm[atom_idx[a]];
+  const int lx = leaf_sorted[k] >> (2 * depth);
+  if (lx < x0 || lx >= x1) {  // halo atom: its owner supplies the potential
+    out[a] = 0.0;
+    return;
+  }
   double v = (double)vnear[k] + (double)vfar[k];
   if (dipole) {
     const double gam = 2.0 * 3.14159265358979323846 / (3.0 * box * box * box), h = 0.5 * box;
@@ -509,6 +525,11 @@ struct lfmm_plan {
   bool use_halo = false;  // ... as shifted-window fp16x3 GEMMs (lfmm_m2l_halo.cuh)
   bool p2p_scalar = false;  // fp32 P2P on the scalar kernel (LFMM_P2P=scalar, A/B checks)
   bool step_mode = false;   // lfmm_step: skip the input-order potential arrays
+  // Slab decomposition (distributed.py): this rank owns leaves with x index in
+  // [own_x0, own_x1); levels < dist_lg have boxes spanning ranks and are
+  // computed redundantly from the gathered level dist_lg.  dist_phase: 0 whole
+  // solve, 1 up to the owned multipoles, 2 the rest.
+  int own_x0 = 0, own_x1 = 1 << 30, dist_lg = 0, dist_phase = 0;
   DevBuf ops_tc, up_part, up_cnt, counters;
   DevBuf ops16, hm_inv_r, hm_inv_c, hm_jobs, hm_level_max, mult16;
   int64_t m16_off[DMAX + 2] = {0};
@@ -896,13 +917,27 @@ struct lfmm_plan {
     for (int l = depth; l >= 1; --l) {
       const int h = 1 << (l - 1), Z = h + 2, S = Z * Z + Z + 1, last = h * S;
       const int G = nsplit[l];
-      for (int t0 = S; t0 <= last; t0 += HM_NMAX) {
-        const int N = std::min(HM_NMAX, ((last + 1 - t0) + 15) / 16 * 16);
-        hm_rw_cap = std::max(hm_rw_cap, hm_rw(N, Z));
-        for (int tc = 0; tc < 8; ++tc)
+      // target classes' x rows owned by this rank (all of them unless a slab
+      // decomposition restricts levels >= dist_lg): class position i with
+      // 2i + tcx inside the rank's box range at level l
+      for (int tc = 0; tc < 8; ++tc) {
+        int ia = 0, ib = h;
+        if (dist_lg > 0 && l >= dist_lg) {
+          const int xl0 = own_x0 >> (depth - l), xl1 = own_x1 >> (depth - l), tcx = (tc >> 2) & 1;
+          ia = (xl0 - tcx + 1) >> 1;
+          ib = (xl1 - tcx + 1) >> 1;
+          if (ia >= ib) continue;
+        }
+        const int r0 = S + ia * Z * Z, r1 = std::min(last, S + (ib - 1) * Z * Z + h * Z + h);
+        for (int t0 = r0; t0 <= r1; t0 += HM_NMAX) {
+          const int N = std::min(HM_NMAX, ((r1 + 1 - t0) + 15) / 16 * 16);
+          hm_rw_cap = std::max(hm_rw_cap, hm_rw(N, Z));
           for (int grp = 0; grp < G; ++grp) jobs.push_back(make_int4(l | (tc << 4) | (grp << 8) | (G << 12), t0, N, 0));
+        }
       }
     }
+    // big jobs first: the small levels fill the tail of the launch
+    std::stable_sort(jobs.begin(), jobs.end(), [](const int4& a, const int4& b) { return a.z > b.z; });
     int64_t moff = 0;
     for (int l = 1; l <= depth; ++l) {
       m16_off[l] = moff;
@@ -1013,47 +1048,11 @@ struct lfmm_plan {
   void solve_column(int K, int c, bool grad) {
     const int64_t nb = std::min<int64_t>(nblk(N, 256), 148 * 4);
     const T tsize = (T)size;
-    launch(ST_STAGE, [&] {
-      k_stage_q<T><<<(unsigned)nb, 256, 0, stream>>>(q_in.as<double>(), K, c, perm.as<int>(), pos_sorted.as<double>(),
-                                                     N, L, xq.as<vec4_t<T>>(), qs.as<double>(), part.as<dd>(),
-                                                     counters.as<int>(), scal.as<double>());
-    });
-    const int periodic = (flags & LFMM_F_PERIODIC_NEAR) ? 1 : 0;
-    const unsigned lb = nblk(nleaf, P2P_WARPS);
-    launch(ST_P2P, [&] {
-      if (sizeof(T) == 4 && !p2p_scalar) {
-        const unsigned lb2 = nblk(nleaf, P2P2_WARPS);
-        if (grad)
-          k_p2p2<true><<<lb2, P2P2_WARPS * 32, P2P2_SMEM, stream>>>(reinterpret_cast<const float4*>(xq.p), leaf_start.as<int>(),
-                                                                      depth, (float)size, periodic, vnear.as<float>(),
-                                                                      gnear.as<float>());
-        else
-          k_p2p2<false><<<lb2, P2P2_WARPS * 32, P2P2_SMEM, stream>>>(reinterpret_cast<const float4*>(xq.p), leaf_start.as<int>(),
-                                                               depth, (float)size, periodic, vnear.as<float>(),
-                                                               gnear.as<float>());
-        return;
-      }
-      if (grad)
-        k_p2p<T, true><<<lb, P2P_WARPS * 32, 0, stream>>>(xq.as<vec4_t<T>>(), leaf_start.as<int>(), depth, tsize,
-                                                           periodic, vnear.as<T>(), gnear.as<T>());
-      else
-        k_p2p<T, false><<<lb, P2P_WARPS * 32, 0, stream>>>(xq.as<vec4_t<T>>(), leaf_start.as<int>(), depth, tsize,
-                                                            periodic, vnear.as<T>(), gnear.as<T>());
-    });
     T* M = mult.as<T>();
     T* Lc = loc.as<T>();
-    launch(ST_P2M, [&] {
-      if (p == 10) {
-        k_p2m_c<T, 10><<<nblk(nleaf, EXP_WARPS), EXP_WARPS * 32, 0, stream>>>(
-            xq.as<vec4_t<T>>(), leaf_start.as<int>(), depth, (T)(1.0 / size), ncp, M + level_off[depth] * ncp);
-        return;
-      }
-      k_p2m<T><<<nblk(nleaf, EXP_WARPS), EXP_WARPS * 32, 0, stream>>>(
-          xq.as<vec4_t<T>>(), leaf_start.as<int>(), depth, p, (T)(1.0 / size), ncp, M + level_off[depth] * ncp);
-    });
     const unsigned rowb = (unsigned)((ncp + GB_M - 1) / GB_M);
     GemmArgs ga = gemm_base();
-    for (int l = depth - 1; l >= 0; --l) {
+    auto m2m_level = [&](int l) {
       if (use_tr) {
         TrArgs ta{};
         ta.mode = 0;
@@ -1065,18 +1064,62 @@ struct lfmm_plan {
         ta.slots = up_part.p;
         ta.cnt = tr_cnt.as<int>();
         launch(ST_M2M, [&] { tr_launch<T>(ta, 1 << (3 * l), 8, stream); });
-        continue;
+        return;
       }
       ga.mode = GEMM_UP;
       ga.level = l;
       dim3 grid(tiles_all(l) * ga.up_split, rowb);
       launch(ST_M2M, [&] { k_gemm_gather<T><<<grid, G_THREADS, 0, stream>>>(ga); });
-    }
+    };
+    if (dist_phase == 2) {
+      // levels spanning several ranks, from the gathered level dist_lg
+      for (int l = std::min(dist_lg, depth) - 1; l >= 0; --l) m2m_level(l);
+    } else {
+    launch(ST_STAGE, [&] {
+      k_stage_q<T><<<(unsigned)nb, 256, 0, stream>>>(q_in.as<double>(), K, c, perm.as<int>(), pos_sorted.as<double>(),
+                                                     N, L, xq.as<vec4_t<T>>(), qs.as<double>(), part.as<dd>(),
+                                                     counters.as<int>(), scal.as<double>(), leaf_sorted.as<int>(),
+                                                     depth, own_x0, own_x1);
+    });
+    const int periodic = (flags & LFMM_F_PERIODIC_NEAR) ? 1 : 0;
+    const unsigned lb = nblk(nleaf, P2P_WARPS);
+    launch(ST_P2P, [&] {
+      if (sizeof(T) == 4 && !p2p_scalar) {
+        const unsigned lb2 = nblk(nleaf, P2P2_WARPS);
+        if (grad)
+          k_p2p2<true><<<lb2, P2P2_WARPS * 32, P2P2_SMEM, stream>>>(reinterpret_cast<const float4*>(xq.p), leaf_start.as<int>(),
+                                                                      depth, (float)size, periodic, vnear.as<float>(),
+                                                                      gnear.as<float>(), own_x0, own_x1);
+        else
+          k_p2p2<false><<<lb2, P2P2_WARPS * 32, P2P2_SMEM, stream>>>(reinterpret_cast<const float4*>(xq.p), leaf_start.as<int>(),
+                                                               depth, (float)size, periodic, vnear.as<float>(),
+                                                               gnear.as<float>(), own_x0, own_x1);
+        return;
+      }
+      if (grad)
+        k_p2p<T, true><<<lb, P2P_WARPS * 32, 0, stream>>>(xq.as<vec4_t<T>>(), leaf_start.as<int>(), depth, tsize,
+                                                           periodic, vnear.as<T>(), gnear.as<T>(), own_x0, own_x1);
+      else
+        k_p2p<T, false><<<lb, P2P_WARPS * 32, 0, stream>>>(xq.as<vec4_t<T>>(), leaf_start.as<int>(), depth, tsize,
+                                                            periodic, vnear.as<T>(), gnear.as<T>(), own_x0, own_x1);
+    });
+    launch(ST_P2M, [&] {
+      if (p == 10) {
+        k_p2m_c<T, 10><<<nblk(nleaf, EXP_WARPS), EXP_WARPS * 32, 0, stream>>>(
+            xq.as<vec4_t<T>>(), leaf_start.as<int>(), depth, (T)(1.0 / size), ncp, M + level_off[depth] * ncp);
+        return;
+      }
+      k_p2m<T><<<nblk(nleaf, EXP_WARPS), EXP_WARPS * 32, 0, stream>>>(
+          xq.as<vec4_t<T>>(), leaf_start.as<int>(), depth, p, (T)(1.0 / size), ncp, M + level_off[depth] * ncp);
+    });
+    for (int l = depth - 1; l >= (dist_phase == 1 ? dist_lg : 0); --l) m2m_level(l);
     launch(ST_M2M, [&] {
       k_box_charges<T><<<nblk(nleaf, 256), 256, 0, stream>>>(qs.as<double>(), leaf_start.as<int>(), depth,
                                                              level_off[depth], ncp, M, boxq.as<double>(),
                                                              counters.as<int>() + 2);
     });
+    if (dist_phase == 1) return;  // owned multipoles ready for the all-gather
+    }  // up
     if (lattice_mode != LFMM_LATTICE_OFF && use_tr) {
       TrArgs ta{};
       ta.mode = 2;
@@ -1173,32 +1216,32 @@ struct lfmm_plan {
           if (grad)
             k_l2p_f2<true, 10><<<nblk(nleaf, EXP_WARPS), EXP_WARPS * 32, 0, stream>>>(
                 reinterpret_cast<const float4*>(xq.p), leaf_start.as<int>(), depth, (float)size, ncp,
-                reinterpret_cast<const float*>(Lc + level_off[depth] * ncp), vfar.as<float>(), gfar.as<float>());
+                reinterpret_cast<const float*>(Lc + level_off[depth] * ncp), vfar.as<float>(), gfar.as<float>(), own_x0, own_x1);
           else
             k_l2p_f2<false, 10><<<nblk(nleaf, EXP_WARPS), EXP_WARPS * 32, 0, stream>>>(
                 reinterpret_cast<const float4*>(xq.p), leaf_start.as<int>(), depth, (float)size, ncp,
-                reinterpret_cast<const float*>(Lc + level_off[depth] * ncp), vfar.as<float>(), gfar.as<float>());
+                reinterpret_cast<const float*>(Lc + level_off[depth] * ncp), vfar.as<float>(), gfar.as<float>(), own_x0, own_x1);
           return;
         }
         if (p == 10) {
           if (grad)
             k_l2p_c<T, true, 10><<<nblk(nleaf, EXP_WARPS), EXP_WARPS * 32, 0, stream>>>(
                 xq.as<vec4_t<T>>(), leaf_start.as<int>(), depth, tsize, ncp, Lc + level_off[depth] * ncp,
-                vfar.as<T>(), gfar.as<T>());
+                vfar.as<T>(), gfar.as<T>(), own_x0, own_x1);
           else
             k_l2p_c<T, false, 10><<<nblk(nleaf, EXP_WARPS), EXP_WARPS * 32, 0, stream>>>(
                 xq.as<vec4_t<T>>(), leaf_start.as<int>(), depth, tsize, ncp, Lc + level_off[depth] * ncp,
-                vfar.as<T>(), gfar.as<T>());
+                vfar.as<T>(), gfar.as<T>(), own_x0, own_x1);
           return;
         }
         if (grad)
           k_l2p<T, true><<<nblk(nleaf, warps), warps * 32, smem, stream>>>(
               xq.as<vec4_t<T>>(), leaf_start.as<int>(), depth, p, tsize, ncp, Lc + level_off[depth] * ncp,
-              vfar.as<T>(), gfar.as<T>());
+              vfar.as<T>(), gfar.as<T>(), own_x0, own_x1);
         else
           k_l2p<T, false><<<nblk(nleaf, warps), warps * 32, smem, stream>>>(
               xq.as<vec4_t<T>>(), leaf_start.as<int>(), depth, p, tsize, ncp, Lc + level_off[depth] * ncp,
-              vfar.as<T>(), gfar.as<T>());
+              vfar.as<T>(), gfar.as<T>(), own_x0, own_x1);
       });
     }
     const int dip = (flags & LFMM_F_DIPOLE) ? 1 : 0;
@@ -1209,13 +1252,15 @@ struct lfmm_plan {
             gnear.as<T>(), gfar.as<T>(), scal.as<double>(), dip, L, step_mode ? nullptr : out_pot.as<double>(),
             step_mode ? nullptr : out_near.as<double>(), step_mode ? nullptr : out_far.as<double>(),
             step_mode ? nullptr : out_dip.as<double>(), out_forces.as<double>(), part.as<dd>(), counters.as<int>() + 1,
-            epart.as<double>(), energies.as<double>(), dvec.as<double>(), qtot.as<double>());
+            epart.as<double>(), energies.as<double>(), dvec.as<double>(), qtot.as<double>(),
+            leaf_sorted.as<int>(), depth, own_x0, own_x1);
       else
         k_finalize<T, false><<<(unsigned)nb, 256, 0, stream>>>(
             N, K, c, perm.as<int>(), pos_sorted.as<double>(), qs.as<double>(), vnear.as<T>(), vfar.as<T>(),
             gnear.as<T>(), gfar.as<T>(), scal.as<double>(), dip, L, out_pot.as<double>(), out_near.as<double>(),
             out_far.as<double>(), out_dip.as<double>(), nullptr, part.as<dd>(), counters.as<int>() + 1,
-            epart.as<double>(), energies.as<double>(), dvec.as<double>(), qtot.as<double>());
+            epart.as<double>(), energies.as<double>(), dvec.as<double>(), qtot.as<double>(),
+            leaf_sorted.as<int>(), depth, own_x0, own_x1);
     });
   }
 
@@ -1725,7 +1770,9 @@ int lfmm_sites_set(lfmm_plan* plan, int64_t n_sites, const int64_t* atom_offsets
     const int64_t A = atom_offsets[S];
     aidx.resize(A);
     for (int64_t a = 0; a < A; ++a) {
-      LFMM_REQUIRE(atom_index[a] >= 0 && atom_index[a] < plan->N, "site particle index out of range");
+      // -1 marks a site atom held by another rank of a slab decomposition
+      LFMM_REQUIRE(atom_index[a] >= (plan->dist_lg > 0 ? -1 : 0) && atom_index[a] < plan->N,
+                   "site particle index out of range");
       aidx[a] = (int)atom_index[a];
     }
     fsl[0] = 0;
@@ -1913,12 +1960,13 @@ int lfmm_step(lfmm_plan* plan, const double* positions, const double* charges, c
           if (plan->fp32)
             k_site_pot<float><<<nblk(na, 128), 128, 0, plan->stream>>>(
                 plan->atom_idx.as<int>(), na, plan->inv_perm.as<int>(), plan->vnear.as<float>(), plan->vfar.as<float>(),
-                plan->pos_sorted.as<double>(), plan->scal.as<double>(), dip, plan->L, plan->site_pot.as<double>());
+                plan->pos_sorted.as<double>(), plan->scal.as<double>(), dip, plan->L, plan->site_pot.as<double>(),
+                plan->leaf_sorted.as<int>(), plan->depth, plan->own_x0, plan->own_x1);
           else
             k_site_pot<double><<<nblk(na, 128), 128, 0, plan->stream>>>(
                 plan->atom_idx.as<int>(), na, plan->inv_perm.as<int>(), plan->vnear.as<double>(),
                 plan->vfar.as<double>(), plan->pos_sorted.as<double>(), plan->scal.as<double>(), dip, plan->L,
-                plan->site_pot.as<double>());
+                plan->site_pot.as<double>(), plan->leaf_sorted.as<int>(), plan->depth, plan->own_x0, plan->own_x1);
         });
         run_hi(plan, mode, nullptr, plan->site_pot.as<double>());
       } else {
@@ -1938,6 +1986,138 @@ int lfmm_step(lfmm_plan* plan, const double* positions, const double* charges, c
     if (!plain) copy_out(plan, lambda_forces, plan->lam_forces, sizeof(double) * 4 * plan->n_sites, io_on_device);
     copy_out(plan, potentials, plan->out_pot, sizeof(double) * N, io_on_device);
     if (!io_on_device) LFMM_CUDA(cudaStreamSynchronize(plan->stream));
+  });
+}
+
+// ---- slab decomposition (paper_2410_01754_b200/distributed.py) ----
+int lfmm_plan_set_count(lfmm_plan* plan, int64_t n) {
+  if (!plan) return fail(Error{LFMM_EINVAL, "plan is NULL"});
+  return guarded([&] {
+    LFMM_REQUIRE(n >= 0 && n < (1LL << 31), "particle count out of range");
+    const int64_t nn = std::max<int64_t>(n, 1);
+    const size_t t = plan->tsz();
+    plan->pos_in.ensure(sizeof(double) * 3 * nn);
+    plan->pos_wrap.ensure(sizeof(double) * 3 * nn);
+    plan->leaf_of.ensure(sizeof(int) * nn);
+    plan->bucket.ensure(sizeof(int) * nn);
+    plan->perm.ensure(sizeof(int) * nn);
+    plan->inv_perm.ensure(sizeof(int) * nn);
+    plan->pos_sorted.ensure(sizeof(double) * 3 * nn);
+    plan->leaf_sorted.ensure(sizeof(int) * nn);
+    plan->xq.ensure(4 * t * nn);
+    plan->N = n;
+    plan->last_valid = false;
+  });
+}
+
+int lfmm_dist_configure(lfmm_plan* plan, int x0, int x1, int lg) {
+  if (!plan) return fail(Error{LFMM_EINVAL, "plan is NULL"});
+  return guarded([&] {
+    const int n = 1 << plan->depth;
+    LFMM_REQUIRE(0 <= x0 && x0 < x1 && x1 <= n, "owned leaf x-range outside the grid");
+    LFMM_REQUIRE(lg >= 0 && lg <= plan->depth, "bad shared-level count");
+    plan->own_x0 = x0;
+    plan->own_x1 = x1;
+    plan->dist_lg = lg;
+    if (plan->use_halo) {
+      plan->plan_halo_jobs();
+      LFMM_CUDA(cudaFuncSetAttribute(k_m2l_halo, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     (int)hm_smem_bytes(plan->hm_rw_cap)));
+    }
+  });
+}
+
+// phase 1: tree + charges (+ lambda scaling) + P2P (owned leaves) + P2M +
+// M2M of the levels >= lg + box charges.  phase 2 (after the caller gathered
+// the owned multipoles and the dipole/charge sums into the buffers exported
+// by lfmm_dist_buffers): shared levels, lattice, M2L, L2L, L2P, finalize,
+// owned site-atom potentials.  All pointers are device pointers.
+int lfmm_dist_phase(lfmm_plan* plan, int phase, const double* positions, const double* charges,
+                    const double* lambdas, const int32_t* n_lambda, int grad) {
+  if (!plan) return fail(Error{LFMM_EINVAL, "plan is NULL"});
+  return guarded([&] {
+    LFMM_REQUIRE(phase == 1 || phase == 2, "phase must be 1 or 2");
+    const int64_t N = plan->N;
+    if (phase == 1) {
+      if (positions) {
+        if (plan->fp32)
+          plan->build_tree<float>(positions, true);
+        else
+          plan->build_tree<double>(positions, true);
+      }
+      plan->ensure_solve_buffers(1, grad != 0);
+      plan->q_tmp.ensure(sizeof(double) * std::max<int64_t>(N, 1));
+      if (lambdas && plan->n_sites > 0) {
+        upload_lambdas(plan, lambdas, n_lambda, 1);
+        LFMM_CUDA(cudaMemcpyAsync(plan->q_tmp.p, charges, sizeof(double) * N, cudaMemcpyDeviceToDevice, plan->stream));
+        run_scale(plan, plan->q_tmp.as<double>(), plan->q_in.as<double>());
+      } else if (N > 0) {
+        LFMM_CUDA(cudaMemcpyAsync(plan->q_in.p, charges, sizeof(double) * N, cudaMemcpyDeviceToDevice, plan->stream));
+      }
+    }
+    plan->dist_phase = phase;
+    plan->step_mode = true;
+    try {
+      if (plan->fp32)
+        plan->solve_column<float>(1, 0, grad != 0);
+      else
+        plan->solve_column<double>(1, 0, grad != 0);
+    } catch (...) {
+      plan->dist_phase = 0;
+      plan->step_mode = false;
+      throw;
+    }
+    plan->dist_phase = 0;
+    plan->step_mode = false;
+    if (phase == 2 && plan->n_sites > 0) {
+      plan->site_pot.ensure(sizeof(double) * std::max<int64_t>(plan->n_site_atoms, 1));
+      const int na = (int)plan->n_site_atoms;
+      const int dip = (plan->flags & LFMM_F_DIPOLE) ? 1 : 0;
+      plan->launch(ST_HI, [&] {
+        if (plan->fp32)
+          k_site_pot<float><<<nblk(na, 128), 128, 0, plan->stream>>>(
+              plan->atom_idx.as<int>(), na, plan->inv_perm.as<int>(), plan->vnear.as<float>(), plan->vfar.as<float>(),
+              plan->pos_sorted.as<double>(), plan->scal.as<double>(), dip, plan->L, plan->site_pot.as<double>(),
+              plan->leaf_sorted.as<int>(), plan->depth, plan->own_x0, plan->own_x1);
+        else
+          k_site_pot<double><<<nblk(na, 128), 128, 0, plan->stream>>>(
+              plan->atom_idx.as<int>(), na, plan->inv_perm.as<int>(), plan->vnear.as<double>(),
+              plan->vfar.as<double>(), plan->pos_sorted.as<double>(), plan->scal.as<double>(), dip, plan->L,
+              plan->site_pot.as<double>(), plan->leaf_sorted.as<int>(), plan->depth, plan->own_x0, plan->own_x1);
+      });
+    }
+  });
+}
+
+// device pointers of the buffers the slab decomposition exchanges:
+// [0] multipoles (all levels, ncp per box, T), [1] scal (D_x, D_y, D_z, Q as
+// fp64), [2] energies (total, near, far, dipole), [3] forces (N x 3, local
+// input order), [4] site-atom potentials, [5] lambda forces (S x 4),
+// [6] HI energy offset (1), [7] stream; level_off[l] = first box of level l
+int lfmm_dist_buffers(lfmm_plan* plan, void** ptrs, int64_t* level_off) {
+  if (!plan) return fail(Error{LFMM_EINVAL, "plan is NULL"});
+  return guarded([&] {
+    ptrs[0] = plan->mult.p;
+    ptrs[1] = plan->scal.p;
+    ptrs[2] = plan->energies.p;
+    ptrs[3] = plan->out_forces.p;
+    ptrs[4] = plan->site_pot.p;
+    ptrs[5] = plan->lam_forces.p;
+    ptrs[6] = plan->offset_total.p;
+    ptrs[7] = reinterpret_cast<void*>(plan->stream);
+    for (int l = 0; l <= DMAX + 1; ++l) level_off[l] = l <= plan->depth + 1 ? plan->level_off[l] : 0;
+  });
+}
+
+// HI for every site of the (global) site table from the gathered site-atom
+// potentials; site positions are caller-supplied (device)
+int lfmm_dist_hi(lfmm_plan* plan, const double* site_positions, int mode) {
+  if (!plan) return fail(Error{LFMM_EINVAL, "plan is NULL"});
+  return guarded([&] {
+    LFMM_REQUIRE(mode == LFMM_MODE_HI || mode == LFMM_MODE_QI, "unknown mode");
+    if (plan->n_sites == 0) return;
+    gather_site_positions(plan, site_positions, 1);
+    run_hi(plan, mode, nullptr, plan->site_pot.as<double>());
   });
 }
 

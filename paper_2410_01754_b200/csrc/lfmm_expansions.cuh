@@ -162,7 +162,7 @@ __global__ void __launch_bounds__(EXP_WARPS * 32) k_l2p(const vec4_t<T>* __restr
                                                         const int* __restrict__ leaf_start, int depth,
                                                         int p, T size, int ncp,
                                                         const T* __restrict__ loc,
-                                                        T* __restrict__ vout, T* __restrict__ gout) {
+                                                        T* __restrict__ vout, T* __restrict__ gout, int x0, int x1) {
   extern __shared__ unsigned char smem_raw[];
   const int nc = ncoef(p), ng = p * p;
   const int per_warp = nc + 3 * ng;
@@ -174,6 +174,7 @@ __global__ void __launch_bounds__(EXP_WARPS * 32) k_l2p(const vec4_t<T>* __restr
   const int b = blockIdx.x * (blockDim.x >> 5) + w;
   const int nleaf = 1 << (3 * depth);
   if (b >= nleaf) return;
+  if ((b >> (2 * depth)) < x0 || (b >> (2 * depth)) >= x1) return;  // leaf outside this rank's slab
   const int t0 = leaf_start[b], t1 = leaf_start[b + 1];
   if (t1 == t0) return;
   const T* src = loc + (size_t)b * ncp;
@@ -248,7 +249,7 @@ template <class T, bool GRAD, int P>
 __global__ void __launch_bounds__(EXP_WARPS * 32) k_l2p_c(const vec4_t<T>* __restrict__ xq,
                                                           const int* __restrict__ leaf_start, int depth,
                                                           T size, int ncp, const T* __restrict__ loc,
-                                                          T* __restrict__ vout, T* __restrict__ gout) {
+                                                          T* __restrict__ vout, T* __restrict__ gout, int x0, int x1) {
   constexpr int NC = (P + 1) * (P + 1), NG = P * P;
   __shared__ T sh[EXP_WARPS][NC + 3 * NG];
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
@@ -259,6 +260,7 @@ __global__ void __launch_bounds__(EXP_WARPS * 32) k_l2p_c(const vec4_t<T>* __res
   const int b = blockIdx.x * (blockDim.x >> 5) + w;
   const int nleaf = 1 << (3 * depth);
   if (b >= nleaf) return;
+  if ((b >> (2 * depth)) < x0 || (b >> (2 * depth)) >= x1) return;  // leaf outside this rank's slab
   const int t0 = leaf_start[b], t1 = leaf_start[b + 1];
   if (t1 == t0) return;
   const T* src = loc + (size_t)b * ncp;
@@ -335,7 +337,7 @@ template <bool GRAD, int P>
 __global__ void __launch_bounds__(EXP_WARPS * 32) k_l2p_f2(const float4* __restrict__ xq,
                                                            const int* __restrict__ leaf_start, int depth,
                                                            float size, int ncp, const float* __restrict__ loc,
-                                                           float* __restrict__ vout, float* __restrict__ gout) {
+                                                           float* __restrict__ vout, float* __restrict__ gout, int x0, int x1) {
   constexpr int Q = P - 1;
   constexpr int NCC = P * (P + 1) / 2, NQC = Q * (Q + 1) / 2;  // complex coefficients (m > 0)
   __shared__ float s0[EXP_WARPS][4][P + 1];                      // m = 0: L, Gx, Gy, Gz
@@ -344,6 +346,7 @@ __global__ void __launch_bounds__(EXP_WARPS * 32) k_l2p_f2(const float4* __restr
   const int b = blockIdx.x * (blockDim.x >> 5) + w;
   const int nleaf = 1 << (3 * depth);
   if (b >= nleaf) return;
+  if ((b >> (2 * depth)) < x0 || (b >> (2 * depth)) >= x1) return;  // leaf outside this rank's slab
   const int t0 = leaf_start[b], t1 = leaf_start[b + 1];
   if (t1 == t0) return;
   const float* Lh = loc + (size_t)b * ncp;

@@ -301,7 +301,8 @@ __global__ void k_blend_sites(HiArgs g, double* __restrict__ q_out) {
   for (int t = threadIdx.x; t < ns; t += blockDim.x) {
     double acc = 0.0;
     for (int r = 0; r < nf; ++r) acc += hi_weight(lam, nl, r) * Q[r * ns + t];
-    q_out[g.atom_idx[a0 + t]] = acc;
+    const int i = g.atom_idx[a0 + t];
+    if (i >= 0) q_out[i] = acc;  // < 0: atom held by another rank (distributed.py)
   }
 }
 

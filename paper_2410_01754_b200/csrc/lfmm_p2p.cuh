@@ -43,12 +43,13 @@ template <class T, bool GRAD>
 __global__ void __launch_bounds__(P2P_WARPS * 32) k_p2p(const vec4_t<T>* __restrict__ xq,
                                                         const int* __restrict__ leaf_start, int depth,
                                                         T size, int periodic, T* __restrict__ vout,
-                                                        T* __restrict__ gout) {
+                                                        T* __restrict__ gout, int x0, int x1) {
   __shared__ vec4_t<T> tiles[P2P_WARPS][32];
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   const int b = blockIdx.x * P2P_WARPS + w;
   const int nleaf = 1 << (3 * depth);
   if (b >= nleaf) return;
+  if ((b >> (2 * depth)) < x0 || (b >> (2 * depth)) >= x1) return;  // leaf outside this rank's slab
   vec4_t<T>* tile = tiles[w];
   const int t0 = leaf_start[b], t1 = leaf_start[b + 1];
   const int tlo = periodic ? 0 : 13, thi = periodic ? 27 : 14;
@@ -170,12 +171,13 @@ template <bool GRAD>
 __global__ void __launch_bounds__(P2P2_WARPS * 32) k_p2p2(const float4* __restrict__ xq,
                                                           const int* __restrict__ leaf_start, int depth,
                                                           float size, int periodic, float* __restrict__ vout,
-                                                          float* __restrict__ gout) {
+                                                          float* __restrict__ gout, int x0, int x1) {
   extern __shared__ float4 p2p2_smem[];  // [warp][A | B][SMAX / 2]
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   const int b = blockIdx.x * P2P2_WARPS + w;
   const int nleaf = 1 << (3 * depth);
   if (b >= nleaf) return;
+  if ((b >> (2 * depth)) < x0 || (b >> (2 * depth)) >= x1) return;  // leaf outside this rank's slab
   float4* A = p2p2_smem + (size_t)w * P2P2_SMAX;
   float4* B = A + P2P2_SMAX / 2;
   const int t0 = leaf_start[b], n = leaf_start[b + 1] - t0;

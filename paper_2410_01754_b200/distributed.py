@@ -1,0 +1,303 @@
+"""Octree slab decomposition of the FMM + HI step over ranks.
+
+One rank per GPU.  Rank r of G (G a power of two, G <= 2^depth) owns the
+leaves with x index in [r w, (r+1) w), w = 2^depth / G, i.e. the level-lg
+boxes with x index r for lg = log2 G (G = 8: the 8 level-1 octants become x
+slabs of the leaf grid; the reference is single-process, so the layout is
+ours).  Per step and rank:
+
+1. select the owned atoms and a one-leaf halo (the leaf planes x0-1 and x1,
+   periodic) from the step's positions — the P2P sources of the owned
+   leaves (solver.py:126-195);
+2. native phase 1 (lfmm_dist_phase): tree, charges (+ scale_charges), P2P of
+   owned leaves, P2M, M2M of levels >= lg (owned subtrees are complete),
+   exact box charges;
+3. exchange: all-gather of the owned multipoles of every level >= lg (each
+   rank's boxes are one contiguous x-slab of every level array) and of the
+   per-rank dipole / charge sums, added in rank order;
+4. native phase 2: M2M of the shared levels < lg (redundant on every rank),
+   lattice, M2L restricted to owned targets (levels >= lg), L2L, L2P of owned
+   leaves, finalize (energies of owned atoms), owned site-atom potentials;
+5. exchange: energies (near/far partials, rank order), site-atom potentials
+   (each atom owned by exactly one rank: exact), owned forces;
+6. HI corrections + lambda forces for all sites (redundant, cheap) from the
+   gathered site potentials (corrections.py:157-238).
+
+Every reduction adds per-rank partials in rank order, so results do not
+depend on the collective's internal order; multipoles, M2L and P2P of a box
+are computed exactly as on one GPU (same jobs restricted to owned targets).
+
+Collectives go through a small `Comm` interface: `TorchComm` wraps a
+torch.distributed process group (NCCL for device tensors; gloo stages through
+host memory), `LocalComm` simulates G ranks as threads of one process on one
+GPU (used by the GPU tests, since the test boxes have one GPU).
+"""
+
+import math
+import os
+import threading
+
+import numpy as np
+
+from . import _native
+from .fmm.solver import SolverConfig
+
+_DEBUG = os.environ.get('LFMM_DIST_DEBUG') == '1'
+
+# --------------------------------------------------------------- layout ----
+
+
+def slab_partition(depth, world):
+    """(lg, [(x0, x1) per rank]) for the x-slab decomposition of the leaf grid."""
+    n = 1 << depth
+    if world < 1 or world & (world - 1):
+        raise ValueError(f"world size {world} is not a power of two")
+    if world > n:
+        raise ValueError(f"world size {world} exceeds the {n} leaf planes of depth {depth}")
+    lg = int(round(math.log2(world)))
+    w = n // world
+    return lg, [(r * w, (r + 1) * w) for r in range(world)]
+
+
+def leaf_x(positions_wrapped, box_length, depth, xp=np):
+    """Leaf x index of wrapped positions, as octree.build_octree assigns it
+    (floor(x / size) clipped, octree.py:121-123)."""
+    n = 1 << depth
+    size = box_length / n
+    c = xp.floor(positions_wrapped[:, 0] / size)
+    return xp.clip(c, 0, n - 1).astype(xp.int64) if xp is np else c.clamp(0, n - 1).long()
+
+
+def wrap(positions, box_length, xp=np):
+    """np.mod wrap with exact box multiples -> 0 (system.py:103-108)."""
+    w = xp.remainder(positions, box_length)
+    return xp.where(w >= box_length, xp.zeros_like(w), w)
+
+
+def select_local(lx, x0, x1, depth, xp=np):
+    """Owned atom indices (leaf x in [x0, x1)) and halo indices (leaf planes
+    x0-1 and x1, periodic, not owned), each in global input order."""
+    n = 1 << depth
+    owned = (lx >= x0) & (lx < x1)
+    hx = {(x0 - 1) % n, x1 % n}
+    halo = xp.zeros_like(owned)
+    for h in hx:
+        halo = halo | (lx == h)
+    halo = halo & ~owned
+    if xp is np:
+        return np.flatnonzero(owned), np.flatnonzero(halo)
+    return owned.nonzero().flatten(), halo.nonzero().flatten()
+
+
+# ------------------------------------------------------------ collectives ----
+
+
+class TorchComm:
+    """torch.distributed group; deterministic sums (all-gather + rank order)."""
+
+    def __init__(self, group=None):
+        import torch.distributed as dist
+
+        self.dist = dist
+        self.group = group
+        self.rank = dist.get_rank(group)
+        self.world = dist.get_world_size(group)
+        self.backend = dist.get_backend(group)
+
+    def _staged(self, t):
+        return self.backend == "gloo" and t.is_cuda
+
+    def allgather_(self, out, chunk_numel):
+        """In place: out (world * chunk) holds this rank's chunk at rank*chunk."""
+        mine = out[self.rank * chunk_numel:(self.rank + 1) * chunk_numel].clone()
+        if self._staged(out):
+            host = out.cpu()
+            self.dist.all_gather_into_tensor(host, mine.cpu(), group=self.group)
+            out.copy_(host)
+        else:
+            self.dist.all_gather_into_tensor(out, mine, group=self.group)
+
+    def sum_ordered(self, t):
+        """Sum of every rank's t, added in rank order (bit-reproducible)."""
+        import torch
+
+        buf = torch.empty((self.world,) + tuple(t.shape), dtype=t.dtype, device=t.device)
+        flat = buf.reshape(-1)
+        n = t.numel()
+        flat[self.rank * n:(self.rank + 1) * n].copy_(t.reshape(-1))
+        self.allgather_(flat, n)
+        acc = buf[0].clone()
+        for r in range(1, self.world):
+            acc += buf[r]
+        return acc
+
+
+class LocalComm:
+    """G ranks as threads of one process sharing one GPU (tests)."""
+
+    def __init__(self, world):
+        self.world = world
+        self.barrier = threading.Barrier(world)
+        self.slots = [None] * world
+
+    def for_rank(self, rank):
+        return _LocalRankComm(self, rank)
+
+
+class _LocalRankComm:
+    def __init__(self, shared, rank):
+        self.shared = shared
+        self.rank = rank
+        self.world = shared.world
+
+    def allgather_(self, out, chunk_numel):
+        import torch
+
+        torch.cuda.current_stream().synchronize()
+        self.shared.slots[self.rank] = out[self.rank * chunk_numel:(self.rank + 1) * chunk_numel]
+        self.shared.barrier.wait()
+        for r in range(self.world):
+            if r != self.rank:
+                out[r * chunk_numel:(r + 1) * chunk_numel].copy_(self.shared.slots[r])
+        torch.cuda.current_stream().synchronize()
+        self.shared.barrier.wait()
+
+    def sum_ordered(self, t):
+        import torch
+
+        buf = torch.empty((self.world,) + tuple(t.shape), dtype=t.dtype, device=t.device)
+        flat = buf.reshape(-1)
+        n = t.numel()
+        flat[self.rank * n:(self.rank + 1) * n].copy_(t.reshape(-1))
+        self.allgather_(flat, n)
+        acc = buf[0].clone()
+        for r in range(1, self.world):
+            acc += buf[r]
+        return acc
+
+
+# --------------------------------------------------------------- solver ----
+
+
+def _device_view(address, shape, dtype_str, torch):
+    """A torch tensor over native device memory (__cuda_array_interface__)."""
+
+    class _Arr:
+        __cuda_array_interface__ = {"shape": tuple(shape), "typestr": dtype_str, "data": (int(address), False),
+                                    "version": 3, "strides": None}
+
+    return torch.as_tensor(_Arr(), device="cuda")
+
+
+class DistributedSolver:
+    """One rank of the slab-decomposed FMM + HI step.
+
+    `step` takes the global step inputs (positions, charges, lambda table,
+    global site tables and site positions) as device tensors on every rank
+    and returns the global energy, this rank's owned forces (global indices)
+    and the lambda forces of every site.
+    """
+
+    def __init__(self, box_length, config=None, comm=None, depth=None):
+        import torch
+
+        self.torch = torch
+        self.cfg = (config or SolverConfig()).validated()
+        if self.cfg.depth < 1:
+            raise ValueError("the slab decomposition needs depth >= 1")
+        self.box = float(box_length)
+        self.comm = comm
+        self.rank, self.world = comm.rank, comm.world
+        self.lg, ranges = slab_partition(self.cfg.depth, self.world)
+        self.x0, self.x1 = ranges[self.rank]
+        self.plan = None
+        self.flags = (_native.F_DIPOLE if self.cfg.dipole else 0) | _native.F_PERIODIC_NEAR | (
+            _native.F_FP32 if self.cfg.precision == "single" else 0) | (
+            _native.F_INTRA_MINIMUM if self.cfg.intra_site_images == "minimum" else 0)
+        self.tsize = 4 if self.cfg.precision == "single" else 8
+        self.stream = None
+
+    def _ensure_plan(self, pos_local_host):
+        if self.plan is None:
+            self.plan = _native.Plan(pos_local_host, self.box, self.cfg.p, self.cfg.depth,
+                                     _native.LFMM_LATTICE[self.cfg.lattice_mode], self.cfg.shell_cap, self.flags)
+            # the plan's kernels and torch's copies / collectives share one
+            # (non-default) stream, so they are ordered
+            self.plan.set_stream(self.stream.cuda_stream)
+            self.plan.dist_configure(self.x0, self.x1, self.lg)
+
+    def step(self, positions, charges, lambdas=None, n_lambda=None, sites=None, site_positions=None,
+             mode=_native.MODE_HI):
+        """positions (N,3) f64, charges (N,) f64 on the device (global, input
+        order); lambdas (S,4) f64 / n_lambda (S,) i32 device; sites = (atom
+        offsets (S+1), global atom indices (A), n_forms (S), form offsets
+        (S+1), form charges) host arrays; site_positions (A,3) device."""
+        if self.stream is None:
+            self.stream = self.torch.cuda.Stream()
+        self.stream.wait_stream(self.torch.cuda.current_stream())
+        with self.torch.cuda.stream(self.stream):
+            out = self._step(positions, charges, lambdas, n_lambda, sites, site_positions, mode)
+        self.torch.cuda.current_stream().wait_stream(self.stream)
+        return out
+
+    def _step(self, positions, charges, lambdas, n_lambda, sites, site_positions, mode):
+        torch = self.torch
+        d = self.cfg.depth
+        w = wrap(positions, self.box, xp=torch)
+        lx = leaf_x(w, self.box, d, xp=torch)
+        own, halo = select_local(lx, self.x0, self.x1, d, xp=torch)
+        idx = torch.cat([own, halo])
+        n_own, n_loc = own.numel(), idx.numel()
+        pos_l = positions[idx].contiguous()
+        q_l = charges[idx].contiguous()
+        self._ensure_plan(pos_l.cpu().numpy())
+        plan = self.plan
+        plan.set_count(n_loc)
+        n_sites = 0
+        if sites is not None:
+            ao, ai, nf, fo, fq = sites
+            loc = torch.full((positions.shape[0],), -1, dtype=torch.int64, device=positions.device)
+            loc[idx] = torch.arange(n_loc, device=positions.device)
+            ai_l = loc[torch.as_tensor(np.asarray(ai, np.int64), device=positions.device)].cpu().numpy()
+            plan.set_sites(ao, ai_l, nf, fo, fq)
+            n_sites = len(nf)
+        plan.dist_phase(1, pos_l, q_l, lambdas if n_sites else None, n_lambda if n_sites else None, grad=True)
+        ptrs, loff = plan.dist_buffers()
+        # ---- exchange 1: owned multipoles of levels >= lg, dipole / charge ----
+        ncp = self._ncp()
+        tdt = "<f4" if self.tsize == 4 else "<f8"
+        for lvl in range(self.lg, d + 1):
+            nbox = 1 << (3 * lvl)
+            view = _device_view(ptrs[0] + int(loff[lvl]) * ncp * self.tsize, (nbox * ncp,), tdt, torch)
+            self.comm.allgather_(view, nbox * ncp // self.world)
+        scal = _device_view(ptrs[1], (4,), "<f8", torch)
+        scal.copy_(self.comm.sum_ordered(scal.clone()))
+        plan.dist_phase(2, grad=True)
+        ptrs, _ = plan.dist_buffers()  # phase 2 may (re)allocate the site-potential buffer
+        # ---- exchange 2: energies, site potentials, forces ----
+        en = _device_view(ptrs[2], (4,), "<f8", torch).clone()
+        if _DEBUG:
+            torch.cuda.synchronize()
+            print("rank", self.rank, "energies", en.cpu().numpy(), "scal", _device_view(ptrs[1], (4,), "<f8", torch).cpu().numpy(), flush=True)
+        parts = self.comm.sum_ordered(en[1:3].clone())
+        e_solve = float(parts[0] + parts[1] + en[3])
+        forces_l = _device_view(ptrs[3], (n_loc, 3), "<f8", torch)[:n_own].clone()
+        out = {"energy_solve": e_solve, "near_energy": float(parts[0]), "far_energy": float(parts[1]),
+               "dipole_energy": float(en[3]), "owned": own, "forces": forces_l}
+        if n_sites:
+            a_tot = int(np.asarray(sites[0])[-1])
+            sp = _device_view(ptrs[4], (a_tot,), "<f8", torch)
+            sp.copy_(self.comm.sum_ordered(sp.clone()))
+            plan.dist_hi(site_positions.contiguous(), mode)
+            ptrs, _ = plan.dist_buffers()
+            out["lambda_forces"] = _device_view(ptrs[5], (n_sites, 4), "<f8", torch).clone()
+            off = float(_device_view(ptrs[6], (1,), "<f8", torch)[0])
+            out["energy"] = e_solve + (off if mode == _native.MODE_HI else 0.0)
+        else:
+            out["energy"] = e_solve
+        return out
+
+    def _ncp(self):
+        nc = (self.cfg.p + 1) ** 2
+        use_tc = self.cfg.precision == "single" and 64 < nc <= 128
+        return 128 if use_tc else (nc + 15) // 16 * 16

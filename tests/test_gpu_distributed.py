@@ -1,0 +1,99 @@
+"""Slab-decomposed step on one GPU: G ranks simulated as
+threads (LocalComm) must reproduce the single-GPU step — energy, every
+atom's force, every site's lambda forces — since each box's multipoles, M2L
+and P2P are computed as on one GPU and every reduction adds rank partials in
+rank order."""
+
+import threading
+
+import numpy as np
+import pytest
+
+from conftest import relerr
+
+pytestmark = pytest.mark.gpu
+
+from paper_2410_01754_b200 import _native  # noqa: E402
+from paper_2410_01754_b200.distributed import DistributedSolver, LocalComm  # noqa: E402
+from paper_2410_01754_b200.fmm.solver import PeriodicSolver, SolverConfig  # noqa: E402
+from paper_2410_01754_b200.system import lambda_table, site_tables  # noqa: E402
+from paper_2410_01754_b200.waterbox import generate_water_box  # noqa: E402
+
+
+@pytest.fixture(scope="module")
+def wb():
+    system, lam, _ = generate_water_box(40_000, 24, seed=11)
+    return system, lam
+
+
+def _single(system, lam_values, cfg):
+    s = PeriodicSolver(system.positions, system.box_length, cfg)
+    plan = s.plan
+    plan.set_sites(*site_tables(system))
+    lam, nl = lambda_table(system, lam_values)
+    n = system.num_particles
+    e = np.empty(1)
+    f = np.empty((n, 3))
+    lf = np.empty((len(system.sites), 4))
+    plan.step(system.positions, system.charges, lam, nl, mode=_native.MODE_HI, energy=e, forces=f,
+              lambda_forces=lf)
+    return float(e[0]), f, lf
+
+
+def _distributed(system, lam_values, cfg, world):
+    import torch
+
+    dev = torch.device("cuda", 0)
+    pos = torch.from_numpy(np.ascontiguousarray(system.positions)).to(dev)
+    q = torch.from_numpy(np.ascontiguousarray(system.charges)).to(dev)
+    lam, nl = lambda_table(system, lam_values)
+    d_lam = torch.from_numpy(lam).to(dev)
+    d_nl = torch.from_numpy(nl).to(dev)
+    tables = site_tables(system)
+    site_pos = pos[torch.from_numpy(tables[1]).to(dev)].contiguous()
+    shared = LocalComm(world)
+    outs = [None] * world
+    errs = []
+
+    def run(rank):
+        try:
+            torch.cuda.set_device(0)
+            solver = DistributedSolver(system.box_length, cfg, comm=shared.for_rank(rank))
+            outs[rank] = solver.step(pos, q, d_lam, d_nl, sites=tables, site_positions=site_pos)
+            torch.cuda.synchronize()
+        except Exception as e:  # surfaced below
+            errs.append(e)
+            shared.barrier.abort()
+
+    threads = [threading.Thread(target=run, args=(r,)) for r in range(world)]
+    for t in threads:
+        t.start()
+    for t in threads:
+        t.join(timeout=600)
+    if errs:
+        raise errs[0]
+    n = system.num_particles
+    forces = np.zeros((n, 3))
+    count = np.zeros(n, int)
+    for o in outs:
+        idx = o["owned"].cpu().numpy()
+        forces[idx] = o["forces"].cpu().numpy()
+        count[idx] += 1
+    assert np.all(count == 1), "every atom is owned by exactly one rank"
+    return outs, forces
+
+
+@pytest.mark.parametrize("precision", ["single", "double"])
+@pytest.mark.parametrize("world", [2, 4, 8])
+def test_slab_decomposition_matches_single_gpu(wb, precision, world):
+    system, lam = wb
+    cfg = SolverConfig(p=10, depth=4, precision=precision)
+    e1, f1, lf1 = _single(system, lam.values, cfg)
+    outs, fd = _distributed(system, lam.values, cfg, world)
+    tol = 1e-10 if precision == "double" else 1e-6
+    energies = [o["energy"] for o in outs]
+    assert len(set(energies)) == 1, "every rank reports the same energy"
+    assert abs(energies[0] - e1) <= tol * abs(e1)
+    assert relerr(fd, f1) <= tol
+    for o in outs:
+        assert relerr(o["lambda_forces"].cpu().numpy(), lf1) <= tol
