@@ -12,8 +12,11 @@ overhead.
 
     python bench.py [--gpus N --steps K --warmup W] [--impl reference]
 
-Under torchrun each rank runs an independent replica (its own water box,
-seed = rank); value = all ranks' steps / max-over-ranks time.
+Under torchrun (N > 1) the step is the slab-decomposed one
+(paper_2410_01754_b200/distributed.py): one global water box
+of N x 1M atoms (weak scaling, depth 5 for N <= 2 and 6 for N >= 4 so that
+leaves keep ~15-30 atoms), 512 sites, each rank owning an x slab of leaves;
+value = N 1M-atom units / max-over-ranks step time.
 """
 
 import argparse
@@ -48,6 +51,8 @@ def parse():
     ap.add_argument("--cpu-fraction", type=float, default=1.0 / 32)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--seed", type=int, default=0)
+    ap.add_argument("--dist-backend", default="nccl", choices=["nccl", "gloo"],
+                    help="N>1 collectives (gloo only for single-GPU functional checks)")
     return ap.parse_args()
 
 
@@ -182,8 +187,155 @@ def algorithmic_work(p, depth, n_atoms, pairs, n_sites, ns=10, nf=2):
     return w
 
 
+# ------------------------------------------------- our arm, N > 1 ----
+def run_distributed(args):
+    import torch
+    import torch.distributed as dist
+
+    rank, world, local = dist_env()
+    dev_index = local if args.dist_backend == "nccl" else 0
+    torch.cuda.set_device(dev_index)
+    dist.init_process_group(args.dist_backend)
+    dev = torch.device("cuda", dev_index)
+    from paper_2410_01754_b200 import _native
+    from paper_2410_01754_b200.distributed import DistributedSolver, TorchComm
+    from paper_2410_01754_b200.fmm.solver import SolverConfig
+    from paper_2410_01754_b200.system import lambda_table, site_tables
+
+    depth = args.depth + (1 if world >= 4 else 0)
+    gargs = argparse.Namespace(**vars(args))
+    gargs.atoms = args.atoms * world
+    # one global system (same seed on every rank); rank 0 generates and caches it first
+    if rank == 0:
+        system, lam_state = load_system(gargs, 0)
+    dist.barrier()
+    if rank != 0:
+        system, lam_state = load_system(gargs, 0)
+    n = system.num_particles
+    cfg = SolverConfig(p=args.p, depth=depth, precision=args.precision)
+    comm = TorchComm()
+    solver = DistributedSolver(system.box_length, cfg, comm=comm)
+    tables = site_tables(system)
+    lam, nl = lambda_table(system, lam_state.values)
+    s = len(system.sites)
+    d_pos = torch.from_numpy(np.ascontiguousarray(system.positions)).to(dev)
+    d_q = torch.from_numpy(np.ascontiguousarray(system.charges)).to(dev)
+    d_lam = torch.from_numpy(lam).to(dev)
+    d_nl = torch.from_numpy(nl).to(dev)
+    d_site_idx = torch.from_numpy(tables[1]).to(dev)
+    flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)
+
+    def step_dev(plain=False):
+        if plain:
+            return solver.step(d_pos, d_qt)
+        return solver.step(d_pos, d_q, d_lam, d_nl, sites=tables, site_positions=d_pos[d_site_idx])
+
+    # plain FMM: the same blended charges, no lambda machinery
+    from paper_2410_01754_b200.system import scale_charges
+    from paper_2410_01754_b200.weights import expand_weights
+
+    qt = scale_charges(system, [expand_weights(np.asarray(v).reshape(-1)) for v in lam_state.values])
+    d_qt = torch.from_numpy(np.ascontiguousarray(qt)).to(dev)
+    out = step_dev()  # builds the plan
+
+    def timed(fn, k):
+        times = []
+        for _ in range(k):
+            flush.fill_(1.0)
+            e0 = torch.cuda.Event(enable_timing=True)
+            e1 = torch.cuda.Event(enable_timing=True)
+            e0.record()
+            fn()
+            e1.record()
+            e1.synchronize()
+            times.append(e0.elapsed_time(e1))
+        return times
+
+    def max_over_ranks(x):
+        t = torch.tensor([x], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    for _ in range(max(3, args.warmup)):
+        step_dev()
+        step_dev(plain=True)
+    torch.cuda.synchronize()
+    dist.barrier()
+    torch.cuda.synchronize()
+    l0 = solver.plan.launch_count()
+    clk = ClockSampler(dev_index).__enter__()
+    t_full = timed(step_dev, args.steps)
+    launches = (solver.plan.launch_count() - l0) // args.steps
+    t_plain = timed(lambda: step_dev(plain=True), args.steps)
+    torch.cuda.synchronize()
+    dist.barrier()
+    ms_full = max_over_ranks(sum(t_full) / len(t_full))
+    ms_plain = max_over_ranks(sum(t_plain) / len(t_plain))
+
+    # e2e: host inputs copied to the device every step, owned forces and lambda forces back
+    h_pos = torch.from_numpy(np.ascontiguousarray(system.positions)).pin_memory()
+    h_q = torch.from_numpy(np.ascontiguousarray(system.charges)).pin_memory()
+
+    def step_host():
+        d_pos.copy_(h_pos, non_blocking=True)
+        d_q.copy_(h_q, non_blocking=True)
+        o = step_dev()
+        f = o["forces"].to("cpu", non_blocking=True)
+        lf = o["lambda_forces"].to("cpu", non_blocking=True) if s else None
+        torch.cuda.current_stream().synchronize()
+        return f, lf
+
+    step_host()
+    dist.barrier()
+    t_e2e = timed(step_host, args.steps)
+    clk.__exit__(None, None, None)
+    ms_e2e = max_over_ranks(sum(t_e2e) / len(t_e2e))
+    n_own = int(out["owned"].numel())
+    h2d = n * 3 * 8 + n * 8
+    d2h = n_own * 3 * 8 + s * 4 * 8
+
+    solver.plan.profile(True)
+    kprof = max(3, min(args.steps, 10))
+    for _ in range(kprof):
+        step_dev()
+    torch.cuda.synchronize()
+    stages = solver.plan.stage_times()
+    solver.plan.profile(False)
+    stage_rows = {}
+    for name, (ms_tot, cnt) in stages.items():
+        if cnt == 0 or name == "setup":
+            continue
+        stage_rows[name] = {"ms": round(ms_tot / kprof, 4), "launches_per_step": cnt // kprof}
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": round(world * 1000.0 / ms_full, 3), "unit": "steps/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms_full, 4), "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f32" if args.precision == "single" else "f64",
+            "data": "synthetic",
+            "config": {"workload": f"C5-style weak scaling: one ~{n} atom water box ({args.atoms} per GPU), {s} "
+                                   f"sites x 2 forms, p={args.p}, depth={depth}, x-slab octree decomposition over "
+                                   f"{world} GPUs (distributed.py); value in 1M-atom step units",
+                       "atoms": n, "sites": s, "p": args.p, "depth": depth,
+                       "parallelism": f"slab decomposition x{world}, {args.dist_backend}",
+                       "l2": "flushed between timed steps (256 MiB write)"},
+            "hi_overhead_pct": round(100.0 * (ms_full / ms_plain - 1.0), 2),
+            "plain_fmm_ms_per_step": round(ms_plain, 4),
+            "e2e": {"value": round(world * 1000.0 / ms_e2e, 3), "unit": "steps/s", "h2d_bytes_per_step": h2d,
+                    "d2h_bytes_per_step": d2h, "ms_per_step": round(ms_e2e, 4)},
+            "gpu_launches": launches,
+            "clocks": clk.summary(),
+            "roofline": None,
+            "stages_rank0": stage_rows,
+            "cpu_baseline": None,
+        }
+        print(json.dumps(line), flush=True)
+    dist.destroy_process_group()
+
+
 # ----------------------------------------------------------- our arm ----
 def run_ours(args):
+    if dist_env()[1] > 1:
+        return run_distributed(args)
     import torch
 
     rank, world, local = dist_env()

@@ -216,6 +216,7 @@ class DistributedSolver:
             _native.F_INTRA_MINIMUM if self.cfg.intra_site_images == "minimum" else 0)
         self.tsize = 4 if self.cfg.precision == "single" else 8
         self.stream = None
+        self._site_dev = self._site_key = self._site_local = None
 
     def _ensure_plan(self, pos_local_host):
         if self.plan is None:
@@ -256,10 +257,17 @@ class DistributedSolver:
         n_sites = 0
         if sites is not None:
             ao, ai, nf, fo, fq = sites
+            if self._site_dev is None or self._site_key is not sites:
+                self._site_dev = torch.as_tensor(np.asarray(ai, np.int64), device=positions.device)
+                self._site_key = sites
+                self._site_local = None
             loc = torch.full((positions.shape[0],), -1, dtype=torch.int64, device=positions.device)
             loc[idx] = torch.arange(n_loc, device=positions.device)
-            ai_l = loc[torch.as_tensor(np.asarray(ai, np.int64), device=positions.device)].cpu().numpy()
-            plan.set_sites(ao, ai_l, nf, fo, fq)
+            ai_l = loc[self._site_dev]
+            # re-upload the local site tables only when the local indices moved
+            if self._site_local is None or not torch.equal(ai_l, self._site_local):
+                plan.set_sites(ao, ai_l.cpu().numpy(), nf, fo, fq)
+                self._site_local = ai_l
             n_sites = len(nf)
         plan.dist_phase(1, pos_l, q_l, lambdas if n_sites else None, n_lambda if n_sites else None, grad=True)
         ptrs, loff = plan.dist_buffers()
