@@ -507,6 +507,10 @@ struct lfmm_plan {
   int64_t level_off[DMAX + 2] = {0};
   int64_t nbox_total = 0;
   cudaStream_t stream = nullptr, own_stream = nullptr;
+  // host-I/O overlap for lfmm_step: charges upload and forces download run on
+  // io_stream beside the tree build / HI work of `stream`
+  cudaStream_t io_stream = nullptr;
+  cudaEvent_t ev_q = nullptr, ev_f = nullptr;
   int64_t launches = 0;
   bool profiling = false;
   struct Ev {
@@ -612,6 +616,9 @@ struct lfmm_plan {
                       &lam_forces, &offsets, &offset_total, &pot_tmp, &q_tmp, &finite_flag};
     for (auto* b : bufs) b->release();
     if (own_stream) cudaStreamDestroy(own_stream);
+    if (io_stream) cudaStreamDestroy(io_stream);
+    if (ev_q) cudaEventDestroy(ev_q);
+    if (ev_f) cudaEventDestroy(ev_f);
   }
 
   // ------------------------------------------------ operator setup ----
@@ -1939,17 +1946,36 @@ int lfmm_step(lfmm_plan* plan, const double* positions, const double* charges, c
     plan->ensure_solve_buffers(1, true);
     plan->q_tmp.ensure(sizeof(double) * std::max<int64_t>(N, 1));
     const auto kind = io_on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice;
-    if (plain || plan->n_sites == 0) {
-      LFMM_CUDA(cudaMemcpyAsync(plan->q_in.p, charges, sizeof(double) * N, kind, plan->stream));
+    const bool overlap = !io_on_device;
+    if (overlap && !plan->io_stream) {
+      LFMM_CUDA(cudaStreamCreateWithFlags(&plan->io_stream, cudaStreamNonBlocking));
+      LFMM_CUDA(cudaEventCreateWithFlags(&plan->ev_q, cudaEventDisableTiming));
+      LFMM_CUDA(cudaEventCreateWithFlags(&plan->ev_f, cudaEventDisableTiming));
+    }
+    double* qdst = (plain || plan->n_sites == 0) ? plan->q_in.as<double>() : plan->q_tmp.as<double>();
+    if (overlap) {
+      // the charges upload overlaps the tree build
+      LFMM_CUDA(cudaMemcpyAsync(qdst, charges, sizeof(double) * N, kind, plan->io_stream));
+      LFMM_CUDA(cudaEventRecord(plan->ev_q, plan->io_stream));
+      LFMM_CUDA(cudaStreamWaitEvent(plan->stream, plan->ev_q, 0));
     } else {
+      LFMM_CUDA(cudaMemcpyAsync(qdst, charges, sizeof(double) * N, kind, plan->stream));
+    }
+    if (!(plain || plan->n_sites == 0)) {
       upload_lambdas(plan, lambdas, n_lambda, io_on_device);
-      LFMM_CUDA(cudaMemcpyAsync(plan->q_tmp.p, charges, sizeof(double) * N, kind, plan->stream));
       run_scale(plan, plan->q_tmp.as<double>(), plan->q_in.as<double>());
     }
     plan->step_mode = potentials == nullptr;
     plan->run_solve(1, true);
     const bool step_mode = plan->step_mode;
     plan->step_mode = false;
+    if (overlap && forces) {
+      // the forces download overlaps the HI corrections
+      LFMM_CUDA(cudaEventRecord(plan->ev_f, plan->stream));
+      LFMM_CUDA(cudaStreamWaitEvent(plan->io_stream, plan->ev_f, 0));
+      LFMM_CUDA(cudaMemcpyAsync(forces, plan->out_forces.p, sizeof(double) * 3 * N, cudaMemcpyDeviceToHost,
+                                plan->io_stream));
+    }
     if (!plain && plan->n_sites > 0) {
       gather_site_positions(plan, nullptr, 0);
       if (step_mode) {
@@ -1982,10 +2008,13 @@ int lfmm_step(lfmm_plan* plan, const double* positions, const double* charges, c
     if (energy)
       LFMM_CUDA(cudaMemcpyAsync(energy, plan->scal.as<double>() + 6, sizeof(double),
                                 io_on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost, plan->stream));
-    copy_out(plan, forces, plan->out_forces, sizeof(double) * 3 * N, io_on_device);
+    if (!overlap) copy_out(plan, forces, plan->out_forces, sizeof(double) * 3 * N, io_on_device);
     if (!plain) copy_out(plan, lambda_forces, plan->lam_forces, sizeof(double) * 4 * plan->n_sites, io_on_device);
     copy_out(plan, potentials, plan->out_pot, sizeof(double) * N, io_on_device);
-    if (!io_on_device) LFMM_CUDA(cudaStreamSynchronize(plan->stream));
+    if (!io_on_device) {
+      LFMM_CUDA(cudaStreamSynchronize(plan->stream));
+      LFMM_CUDA(cudaStreamSynchronize(plan->io_stream));
+    }
   });
 }
 
