@@ -123,11 +123,12 @@ __global__ void __launch_bounds__(HI_THREADS) k_hi_site(HiArgs g) {
                    dz = pos[3 * i + 2] - pos[3 * j + 2];
       double k = 0.0;
       if (g.images_full) {
+#pragma unroll
         for (int n = 0; n < 27; ++n) {
           const int nx = n / 9 - 1, ny = (n / 3) % 3 - 1, nz = n % 3 - 1;
-          if (i == j && n == 13) continue;
           const double ex = dx + nx * L, ey = dy + ny * L, ez = dz + nz * L;
-          k += 1.0 / sqrt(ex * ex + ey * ey + ez * ez);
+          const double t = rsqrt(ex * ex + ey * ey + ez * ez);
+          k += (i == j && n == 13) ? 0.0 : t;
         }
       } else if (i != j) {
         const double ex = dx - L * rint(dx / L), ey = dy - L * rint(dy / L), ez = dz - L * rint(dz / L);
@@ -143,9 +144,27 @@ __global__ void __launch_bounds__(HI_THREADS) k_hi_site(HiArgs g) {
       double* Us = Rs + (size_t)ns * ncp;  // ns x ncp
       const double* R = g.rscratch + (size_t)a0 * ncp;
       const double* U = g.uscratch + (size_t)a0 * ncp;
-      for (int e = tid; e < ns * ncp; e += blockDim.x) {
-        Rs[e] = R[e];
-        Us[e] = U[e];
+      {  // every load in flight at once (16-B vectors, unrolled)
+        const int nv = ns * ncp / 2;
+        const double2* R2 = reinterpret_cast<const double2*>(R);
+        const double2* U2 = reinterpret_cast<const double2*>(U);
+        double2* Rs2 = reinterpret_cast<double2*>(Rs);
+        double2* Us2 = reinterpret_cast<double2*>(Us);
+        for (int e0 = tid; e0 < nv; e0 += 8 * HI_THREADS) {
+          double2 a[8], b[8];
+#pragma unroll
+          for (int u = 0; u < 8; ++u)
+            if (e0 + u * HI_THREADS < nv) {
+              a[u] = R2[e0 + u * HI_THREADS];
+              b[u] = U2[e0 + u * HI_THREADS];
+            }
+#pragma unroll
+          for (int u = 0; u < 8; ++u)
+            if (e0 + u * HI_THREADS < nv) {
+              Rs2[e0 + u * HI_THREADS] = a[u];
+              Us2[e0 + u * HI_THREADS] = b[u];
+            }
+        }
       }
       __syncthreads();
       const double invL = 1.0 / L;
@@ -239,18 +258,48 @@ __global__ void __launch_bounds__(HI_THREADS) k_hi_site(HiArgs g) {
 // fp64), the right-hand sides of the batched U = T1 R GEMM
 __global__ void k_hi_rvec(const double* __restrict__ site_pos, int n_atoms, double box, int p, int ncp,
                           double* __restrict__ rscratch) {
-  const int a = blockIdx.x * blockDim.x + threadIdx.x;
+  // thread per (site atom, order m): the diagonal R_m^m by m complex steps,
+  // then the m column (harmonics.py:62-76), written to its packed slots
+  const int e = blockIdx.x * blockDim.x + threadIdx.x;
+  const int a = e / (p + 1), m = e % (p + 1);
   if (a >= n_atoms) return;
   const double invL = 1.0 / box;
   const double x = (site_pos[3 * a] - 0.5 * box) * invL, y = (site_pos[3 * a + 1] - 0.5 * box) * invL,
                z = (site_pos[3 * a + 2] - 0.5 * box) * invL;
+  const double r2 = x * x + y * y + z * z;
   double* Rt = rscratch + (size_t)a * ncp;
-  int c = 0;
-  regular_stream<double>(x, y, z, p, [&](int m, int l, double re, double im) {
-    Rt[c++] = re;
-    if (m > 0) Rt[c++] = im;
-  });
-  for (; c < ncp; ++c) Rt[c] = 0.0;
+  double mr = 1.0, mi = 0.0;
+  for (int k = 1; k <= m; ++k) {
+    const double c = 1.0 / (2.0 * k);
+    const double nr = (mr * x - mi * y) * c, ni = (mr * y + mi * x) * c;
+    mr = nr;
+    mi = ni;
+  }
+  auto put = [&](int l, double re, double im) {
+    if (m == 0) {
+      Rt[l] = re;
+    } else {
+      const int c = pk_index(p, l, m, 0);
+      Rt[c] = re;
+      Rt[c + 1] = im;
+    }
+  };
+  put(m, mr, mi);
+  if (m + 1 <= p) {
+    double p2r = mr, p2i = mi, p1r = z * mr, p1i = z * mi;
+    put(m + 1, p1r, p1i);
+    for (int l = m + 2; l <= p; ++l) {
+      const double c = 1.0 / double((l + m) * (l - m));
+      const double nr = ((2 * l - 1) * z * p1r - r2 * p2r) * c, ni = ((2 * l - 1) * z * p1i - r2 * p2i) * c;
+      p2r = p1r;
+      p2i = p1i;
+      p1r = nr;
+      p1i = ni;
+      put(l, nr, ni);
+    }
+  }
+  if (m == 0)
+    for (int c = (p + 1) * (p + 1); c < ncp; ++c) Rt[c] = 0.0;
 }
 
 // generic U_t = T1 R_t (any ncp): thread per (site atom, output row)

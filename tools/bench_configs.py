@@ -83,11 +83,15 @@ def measure(atoms, sites, depth, precision, steps=10, warmup=3, seed=0, reuse=Fa
 
 def main():
     out = {"gpu": "B200 x1", "how": __doc__.split("\n\n")[0].replace("\n", " "), "runs": []}
-    for kw in (dict(atoms=100_000, sites=64, depth=4, precision="single"),
+    only = sys.argv[1:]  # optional run indices
+    runs = (dict(atoms=100_000, sites=64, depth=4, precision="single"),
                dict(atoms=100_000, sites=64, depth=4, precision="double"),
                dict(atoms=1_000_000, sites=512, depth=5, precision="single", reuse=True),
                dict(atoms=1_000_000, sites=512, depth=5, precision="double"),
-               dict(atoms=1_000_000, sites=4096, depth=5, precision="single")):
+               dict(atoms=1_000_000, sites=4096, depth=5, precision="single"))
+    for i, kw in enumerate(runs):
+        if only and str(i) not in only:
+            continue
         r = measure(**kw)
         print(json.dumps(r), flush=True)
         out["runs"].append(r)
