@@ -511,6 +511,12 @@ struct lfmm_plan {
   // io_stream beside the tree build / HI work of `stream`
   cudaStream_t io_stream = nullptr;
   cudaEvent_t ev_q = nullptr, ev_f = nullptr;
+  // P2P runs on near_stream (lower priority) beside the far-field chain on
+  // `stream`: the latency-bound translation / tree / HI kernels of the chain
+  // leave SMs the near field fills.  Serialised when profiling.
+  cudaStream_t near_stream = nullptr;
+  cudaEvent_t ev_near_in = nullptr, ev_near_out = nullptr;
+  bool near_pending = false;
   int64_t launches = 0;
   bool profiling = false;
   struct Ev {
@@ -617,6 +623,9 @@ struct lfmm_plan {
     for (auto* b : bufs) b->release();
     if (own_stream) cudaStreamDestroy(own_stream);
     if (io_stream) cudaStreamDestroy(io_stream);
+    if (near_stream) cudaStreamDestroy(near_stream);
+    if (ev_near_in) cudaEventDestroy(ev_near_in);
+    if (ev_near_out) cudaEventDestroy(ev_near_out);
     if (ev_q) cudaEventDestroy(ev_q);
     if (ev_f) cudaEventDestroy(ev_f);
   }
@@ -1090,7 +1099,22 @@ struct lfmm_plan {
     });
     const int periodic = (flags & LFMM_F_PERIODIC_NEAR) ? 1 : 0;
     const unsigned lb = nblk(nleaf, P2P_WARPS);
+    const bool side = !profiling;
+    if (side && !near_stream) {
+      int lo = 0, hi = 0;
+      LFMM_CUDA(cudaDeviceGetStreamPriorityRange(&lo, &hi));
+      LFMM_CUDA(cudaStreamCreateWithPriority(&near_stream, cudaStreamNonBlocking, lo));
+      LFMM_CUDA(cudaEventCreateWithFlags(&ev_near_in, cudaEventDisableTiming));
+      LFMM_CUDA(cudaEventCreateWithFlags(&ev_near_out, cudaEventDisableTiming));
+    }
+    cudaStream_t pst = stream;
+    if (side) {
+      LFMM_CUDA(cudaEventRecord(ev_near_in, stream));
+      LFMM_CUDA(cudaStreamWaitEvent(near_stream, ev_near_in, 0));
+      pst = near_stream;
+    }
     launch(ST_P2P, [&] {
+      cudaStream_t stream = pst;
       if (sizeof(T) == 4 && !p2p_scalar) {
         const unsigned lb2 = nblk(nleaf, P2P2_WARPS);
         if (grad)
@@ -1110,6 +1134,10 @@ struct lfmm_plan {
         k_p2p<T, false><<<lb, P2P_WARPS * 32, 0, stream>>>(xq.as<vec4_t<T>>(), leaf_start.as<int>(), depth, tsize,
                                                             periodic, vnear.as<T>(), gnear.as<T>(), own_x0, own_x1);
     });
+    if (side) {
+      LFMM_CUDA(cudaEventRecord(ev_near_out, near_stream));
+      near_pending = true;
+    }
     launch(ST_P2M, [&] {
       if (p == 10) {
         k_p2m_c<T, 10><<<nblk(nleaf, EXP_WARPS), EXP_WARPS * 32, 0, stream>>>(
@@ -1252,6 +1280,10 @@ struct lfmm_plan {
       });
     }
     const int dip = (flags & LFMM_F_DIPOLE) ? 1 : 0;
+    if (near_pending) {  // near field done
+      LFMM_CUDA(cudaStreamWaitEvent(stream, ev_near_out, 0));
+      near_pending = false;
+    }
     launch(ST_FINAL, [&] {
       if (grad)
         k_finalize<T, true><<<(unsigned)nb, 256, 0, stream>>>(
