@@ -517,6 +517,9 @@ struct lfmm_plan {
   cudaStream_t near_stream = nullptr;
   cudaEvent_t ev_near_in = nullptr, ev_near_out = nullptr;
   bool near_pending = false;
+  // HI corrections (site geometry only) run on hi_stream beside the solve
+  cudaStream_t hi_stream = nullptr;
+  cudaEvent_t ev_hi_in = nullptr, ev_hi_out = nullptr;
   int64_t launches = 0;
   bool profiling = false;
   struct Ev {
@@ -624,6 +627,9 @@ struct lfmm_plan {
     if (own_stream) cudaStreamDestroy(own_stream);
     if (io_stream) cudaStreamDestroy(io_stream);
     if (near_stream) cudaStreamDestroy(near_stream);
+    if (hi_stream) cudaStreamDestroy(hi_stream);
+    if (ev_hi_in) cudaEventDestroy(ev_hi_in);
+    if (ev_hi_out) cudaEventDestroy(ev_hi_out);
     if (ev_near_in) cudaEventDestroy(ev_near_in);
     if (ev_near_out) cudaEventDestroy(ev_near_out);
     if (ev_q) cudaEventDestroy(ev_q);
@@ -1998,6 +2004,31 @@ int lfmm_step(lfmm_plan* plan, const double* positions, const double* charges, c
       upload_lambdas(plan, lambdas, n_lambda, io_on_device);
       run_scale(plan, plan->q_tmp.as<double>(), plan->q_in.as<double>());
     }
+    // HI corrections depend on the site geometry and lambdas only: they run
+    // beside the solve (unless profiling, which wants serial stage times)
+    const bool hi_side = !plain && plan->n_sites > 0 && !plan->profiling && potentials == nullptr;
+    if (hi_side) {
+      if (!plan->hi_stream) {
+        int lo = 0, hi = 0;
+        LFMM_CUDA(cudaDeviceGetStreamPriorityRange(&lo, &hi));
+        LFMM_CUDA(cudaStreamCreateWithPriority(&plan->hi_stream, cudaStreamNonBlocking, lo));
+        LFMM_CUDA(cudaEventCreateWithFlags(&plan->ev_hi_in, cudaEventDisableTiming));
+        LFMM_CUDA(cudaEventCreateWithFlags(&plan->ev_hi_out, cudaEventDisableTiming));
+      }
+      LFMM_CUDA(cudaEventRecord(plan->ev_hi_in, plan->stream));
+      LFMM_CUDA(cudaStreamWaitEvent(plan->hi_stream, plan->ev_hi_in, 0));
+      cudaStream_t main = plan->stream;
+      plan->stream = plan->hi_stream;
+      try {
+        gather_site_positions(plan, nullptr, 0);
+        run_hi(plan, mode, nullptr, nullptr);  // C_rho, blend energies, offsets
+      } catch (...) {
+        plan->stream = main;
+        throw;
+      }
+      plan->stream = main;
+      LFMM_CUDA(cudaEventRecord(plan->ev_hi_out, plan->hi_stream));
+    }
     plan->step_mode = potentials == nullptr;
     plan->run_solve(1, true);
     const bool step_mode = plan->step_mode;
@@ -2010,7 +2041,7 @@ int lfmm_step(lfmm_plan* plan, const double* positions, const double* charges, c
                                 plan->io_stream));
     }
     if (!plain && plan->n_sites > 0) {
-      gather_site_positions(plan, nullptr, 0);
+      if (!hi_side) gather_site_positions(plan, nullptr, 0);
       if (step_mode) {
         plan->site_pot.ensure(sizeof(double) * std::max<int64_t>(plan->n_site_atoms, 1));
         const int na = (int)plan->n_site_atoms;
@@ -2027,7 +2058,22 @@ int lfmm_step(lfmm_plan* plan, const double* positions, const double* charges, c
                 plan->vfar.as<double>(), plan->pos_sorted.as<double>(), plan->scal.as<double>(), dip, plan->L,
                 plan->site_pot.as<double>(), plan->leaf_sorted.as<int>(), plan->depth, plan->own_x0, plan->own_x1);
         });
-        run_hi(plan, mode, nullptr, plan->site_pot.as<double>());
+        if (hi_side) {
+          LFMM_CUDA(cudaStreamWaitEvent(plan->stream, plan->ev_hi_out, 0));
+          HiArgs g{};
+          hi_args(plan, g);
+          g.pot_site = plan->site_pot.as<double>();
+          g.mode = mode;
+          g.c_p2p = plan->c_p2p.as<double>();
+          g.c_lat = plan->c_lat.as<double>();
+          g.c_dip = plan->c_dip.as<double>();
+          g.forces = plan->lam_forces.as<double>();
+          plan->launch(ST_HI, [&] {
+            k_hi_lambda_forces<<<nblk(plan->n_sites, 4), 128, 0, plan->stream>>>(g);
+          });
+        } else {
+          run_hi(plan, mode, nullptr, plan->site_pot.as<double>());
+        }
       } else {
         run_hi(plan, mode, plan->out_pot.as<double>());
       }

@@ -315,6 +315,32 @@ __global__ void k_hi_umat(const double* __restrict__ lat_t, const double* __rest
   uscratch[(size_t)a * ncp + r] = acc;
 }
 
+// Lambda forces from the site-atom potentials and the per-form C_rho of a
+// corrections-only k_hi_site pass (assemble_lambda_forces, corrections.py:
+// 221-238), warp per site; S_rho and the force sums in exactly k_hi_site's
+// order, so splitting the HI step this way changes no bit.
+__global__ void k_hi_lambda_forces(HiArgs g) {
+  const int s = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  const int lane = threadIdx.x & 31;
+  if (s >= g.n_sites) return;
+  const int a0 = g.atom_off[s], ns = g.atom_off[s + 1] - a0;
+  const int nf = g.nforms[s], nl = g.nlam[s];
+  const double* Q = g.form_q + g.form_off[s];
+  const double* lam = g.lambdas + 4 * s;
+  const bool qi = g.mode == 1;
+  double f[4] = {0, 0, 0, 0};
+  for (int r = 0; r < nf; ++r) {
+    double sv = 0.0;
+    for (int i = lane; i < ns; i += 32) sv += Q[r * ns + i] * g.pot_site[a0 + i];
+    for (int off = 16; off > 0; off >>= 1) sv += __shfl_down_sync(0xffffffffu, sv, off);
+    const int slot = g.fslot_off[s] + r;
+    const double cv = qi ? 0.0 : (g.c_p2p[slot] + g.c_lat[slot] + g.c_dip[slot]);
+    for (int k = 0; k < nl; ++k) f[k] += hi_wgrad(lam, nl, k, r) * (sv - cv);
+  }
+  if (lane == 0)
+    for (int k = 0; k < 4; ++k) g.forces[4 * s + k] = k < nl ? -f[k] : 0.0;
+}
+
 // fixed-order sum of per-site offsets (CorrectionSet.energy_offset, :153-154)
 __global__ void k_sum_offsets(const double* __restrict__ v, int n, double* __restrict__ out) {
   dd acc[1] = {dd{0.0, 0.0}};
