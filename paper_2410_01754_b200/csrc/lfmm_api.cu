@@ -494,6 +494,25 @@ std::map<std::tuple<int, int, int>, std::vector<double2>> g_lat_cache;
 
 inline unsigned nblk(int64_t n, int t) { return (unsigned)((n + t - 1) / t); }
 
+// The dynamic shared-memory limit is a per-function, process-wide attribute;
+// plans with different halo tiles (e.g. ranks of a slab decomposition driven
+// from threads of one process) must not lower it under each other: set it
+// once to the device's opt-in maximum.
+void halo_smem_attr(size_t need) {
+  static std::once_flag once;
+  static int max_optin = 0;
+  std::call_once(once, [] {
+    int dev = 0;
+    LFMM_CUDA(cudaGetDevice(&dev));
+    LFMM_CUDA(cudaDeviceGetAttribute(&max_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev));
+    cudaFuncAttributes fa{};
+    LFMM_CUDA(cudaFuncGetAttributes(&fa, k_m2l_halo));
+    max_optin -= (int)fa.sharedSizeBytes;  // static shared memory counts against the same limit
+    LFMM_CUDA(cudaFuncSetAttribute(k_m2l_halo, cudaFuncAttributeMaxDynamicSharedMemorySize, max_optin));
+  });
+  LFMM_REQUIRE(need <= (size_t)max_optin, "halo M2L tile needs more shared memory than the device offers");
+}
+
 }  // namespace
 
 // ----------------------------------------------------------------- plan ----
@@ -918,8 +937,7 @@ struct lfmm_plan {
     });
     LFMM_CUDA(cudaStreamSynchronize(stream));
     hm_level_max.ensure(sizeof(unsigned int) * (DMAX + 2));
-    LFMM_CUDA(cudaFuncSetAttribute(k_m2l_halo, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                   (int)hm_smem_bytes(hm_rw_cap)));
+    halo_smem_attr(hm_smem_bytes(hm_rw_cap));
   }
 
   // Halo M2L jobs: (level, target class, 256-row tile of the padded linear
@@ -1506,8 +1524,14 @@ void run_hi(lfmm_plan* pl, int mode, const double* pot_dev, const double* pot_si
   const bool lat_smem = mode == LFMM_MODE_HI && g.images_full && g.lat_t;
   const size_t smem = sizeof(double) * ((size_t)ns + 2 * (size_t)ns * ns + 3 * (size_t)ns +
                                         (lat_smem ? 2 * (size_t)ns * g.ncp : 0));
-  if (smem > 48 * 1024) {
-    LFMM_CUDA(cudaFuncSetAttribute(k_hi_site, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  if (smem > 48 * 1024) {  // raise only (process-wide attribute, see halo_smem_attr)
+    static std::mutex mu;
+    static size_t cur = 48 * 1024;
+    std::lock_guard<std::mutex> lk(mu);
+    if (smem > cur) {
+      LFMM_CUDA(cudaFuncSetAttribute(k_hi_site, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+      cur = smem;
+    }
   }
   pl->launch(ST_HI, [&] { k_hi_site<<<(unsigned)pl->n_sites, HI_THREADS, smem, pl->stream>>>(g); });
   pl->launch(ST_HI, [&] {
@@ -2129,8 +2153,7 @@ int lfmm_dist_configure(lfmm_plan* plan, int x0, int x1, int lg) {
     plan->dist_lg = lg;
     if (plan->use_halo) {
       plan->plan_halo_jobs();
-      LFMM_CUDA(cudaFuncSetAttribute(k_m2l_halo, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                     (int)hm_smem_bytes(plan->hm_rw_cap)));
+      halo_smem_attr(hm_smem_bytes(plan->hm_rw_cap));
     }
   });
 }
