@@ -349,8 +349,12 @@ __global__ void __launch_bounds__(EXP_WARPS * 32) k_l2p_f2(const float4* __restr
   if ((b >> (2 * depth)) < x0 || (b >> (2 * depth)) >= x1) return;  // leaf outside this rank's slab
   const int t0 = leaf_start[b], t1 = leaf_start[b + 1];
   if (t1 == t0) return;
-  const float* Lh = loc + (size_t)b * ncp;
-  // ---- stage L and the gradient ladder G (harmonics.py:106-130) ----
+  // ---- stage L (one 16-B vector per lane) and build the gradient ladder G
+  // (harmonics.py:106-130) from the shared copy ----
+  __shared__ __align__(16) float sL[EXP_WARPS][128];
+  if (lane * 4 < ncp) reinterpret_cast<float4*>(sL[w])[lane] = reinterpret_cast<const float4*>(loc + (size_t)b * ncp)[lane];
+  __syncwarp();
+  const float* Lh = sL[w];
   for (int e = lane; e < (P + 1) + NCC; e += 32) {
     if (e <= P) {
       s0[w][0][e] = Lh[e];
