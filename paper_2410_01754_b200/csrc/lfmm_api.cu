@@ -99,7 +99,7 @@ __global__ void k_stage_q(const double* __restrict__ q, int K, int c, const int*
                           const double* __restrict__ pos_sorted, int64_t n, double box,
                           vec4_t<T>* __restrict__ xq, double* __restrict__ qs, dd* __restrict__ part,
                           int* __restrict__ cnt, double* __restrict__ scal, const int* __restrict__ leaf_sorted,
-                          int depth, int x0, int x1) {
+                          int depth, int x0, int x1, const int* __restrict__ leaf_start, float4* __restrict__ pb) {
   dd v[4] = {dd{0, 0}, dd{0, 0}, dd{0, 0}, dd{0, 0}};
   // grid-stride (a few blocks per SM: the last-block counter sees few atomics)
   for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < n; k += (int64_t)gridDim.x * blockDim.x) {
@@ -107,7 +107,12 @@ __global__ void k_stage_q(const double* __restrict__ q, int K, int c, const int*
     const double qv = q[(size_t)i * K + c];
     xq[k].w = (T)qv;
     qs[k] = qv;
-    const int lx = leaf_sorted[k] >> (2 * depth);
+    const int leaf = leaf_sorted[k];
+    if (pb) {  // charge half of the source pair (lfmm_tree.cuh k_leaf_rank)
+      const int s0 = leaf_start[leaf], r = (int)k - s0;
+      reinterpret_cast<float*>(pb + ((s0 + leaf + 1) >> 1) + (r >> 1))[2 + (r & 1)] = (float)qv;
+    }
+    const int lx = leaf >> (2 * depth);
     if (lx < x0 || lx >= x1) continue;  // halo atom: not this rank's dipole / charge
     const double h = 0.5 * box;
     v[0] = dd_add(v[0], dd_from((pos_sorted[3 * k] - h) * qv));
@@ -552,6 +557,11 @@ struct lfmm_plan {
 
   // tree
   DevBuf pos_in, pos_wrap, leaf_of, counts, cursor, leaf_start, bucket, perm, inv_perm, pos_sorted, leaf_sorted, xq;
+  // fp32 near-field source pairs (k_p2p2): [pair_cap] float4 x/y halves, then [pair_cap] z/q halves
+  DevBuf pairs;
+  int64_t pair_cap = 0;
+  float4* pair_a() { return fp32 ? reinterpret_cast<float4*>(pairs.p) : nullptr; }
+  float4* pair_b() { return fp32 ? reinterpret_cast<float4*>(pairs.p) + pair_cap : nullptr; }
   // expansions / operators
   bool use_tc = false;    // M2L on tcgen05 (fp32, (p+1)^2 <= 128)
   bool use_halo = false;  // ... as shifted-window fp16x3 GEMMs (lfmm_m2l_halo.cuh)
@@ -585,6 +595,12 @@ struct lfmm_plan {
   DevBuf finite_flag;
 
   size_t tsz() const { return fp32 ? sizeof(float) : sizeof(double); }
+  // leaf b's pairs start at (leaf_start[b] + b + 1) / 2 (lfmm_p2p.cuh)
+  void ensure_pairs(int64_t nn) {
+    if (!fp32) return;
+    pair_cap = (nn + nleaf + 2) / 2 + 1;
+    pairs.ensure(2 * sizeof(float4) * pair_cap);
+  }
 
   // --- launch bookkeeping ---
   cudaEvent_t get_event() {
@@ -1077,7 +1093,7 @@ struct lfmm_plan {
       launch(ST_TREE, [&] {
         k_leaf_rank<T><<<nblk((int64_t)nleaf * 32, RANK_WARPS * 32), RANK_WARPS * 32, 0, stream>>>(
             pos_wrap.as<double>(), leaf_start.as<int>(), bucket.as<int>(), nleaf, perm.as<int>(), inv_perm.as<int>(),
-            depth, size, pos_sorted.as<double>(), xq.as<vec4_t<T>>(), leaf_sorted.as<int>());
+            depth, size, pos_sorted.as<double>(), xq.as<vec4_t<T>>(), leaf_sorted.as<int>(), pair_a(), pair_b());
       });
     }
     last_valid = false;
@@ -1119,7 +1135,8 @@ struct lfmm_plan {
       k_stage_q<T><<<(unsigned)nb, 256, 0, stream>>>(q_in.as<double>(), K, c, perm.as<int>(), pos_sorted.as<double>(),
                                                      N, L, xq.as<vec4_t<T>>(), qs.as<double>(), part.as<dd>(),
                                                      counters.as<int>(), scal.as<double>(), leaf_sorted.as<int>(),
-                                                     depth, own_x0, own_x1);
+                                                     depth, own_x0, own_x1, leaf_start.as<int>(),
+                                                     p2p_scalar ? nullptr : pair_b());
     });
     const int periodic = (flags & LFMM_F_PERIODIC_NEAR) ? 1 : 0;
     const unsigned lb = nblk(nleaf, P2P_WARPS);
@@ -1142,11 +1159,11 @@ struct lfmm_plan {
       if (sizeof(T) == 4 && !p2p_scalar) {
         const unsigned lb2 = nblk(nleaf, P2P2_WARPS);
         if (grad)
-          k_p2p2<true><<<lb2, P2P2_WARPS * 32, P2P2_SMEM, stream>>>(reinterpret_cast<const float4*>(xq.p), leaf_start.as<int>(),
+          k_p2p2<true><<<lb2, P2P2_WARPS * 32, P2P2_SMEM, stream>>>(reinterpret_cast<const float4*>(xq.p), pair_a(), pair_b(), leaf_start.as<int>(),
                                                                       depth, (float)size, periodic, vnear.as<float>(),
                                                                       gnear.as<float>(), own_x0, own_x1);
         else
-          k_p2p2<false><<<lb2, P2P2_WARPS * 32, P2P2_SMEM, stream>>>(reinterpret_cast<const float4*>(xq.p), leaf_start.as<int>(),
+          k_p2p2<false><<<lb2, P2P2_WARPS * 32, P2P2_SMEM, stream>>>(reinterpret_cast<const float4*>(xq.p), pair_a(), pair_b(), leaf_start.as<int>(),
                                                                depth, (float)size, periodic, vnear.as<float>(),
                                                                gnear.as<float>(), own_x0, own_x1);
         return;
@@ -1649,6 +1666,7 @@ int lfmm_plan_create(const double* positions, int64_t n, double box_length, int 
     pl->pos_sorted.ensure(sizeof(double) * 3 * nn);
     pl->leaf_sorted.ensure(sizeof(int) * nn);
     pl->xq.ensure(4 * t * nn);
+    pl->ensure_pairs(nn);
     pl->mult.ensure(t * pl->ncp * off);
     pl->boxq.ensure(sizeof(double) * off);
     pl->loc.ensure(t * pl->ncp * off);
@@ -2137,6 +2155,7 @@ int lfmm_plan_set_count(lfmm_plan* plan, int64_t n) {
     plan->pos_sorted.ensure(sizeof(double) * 3 * nn);
     plan->leaf_sorted.ensure(sizeof(int) * nn);
     plan->xq.ensure(4 * t * nn);
+    plan->ensure_pairs(nn);
     plan->N = n;
     plan->last_valid = false;
   });

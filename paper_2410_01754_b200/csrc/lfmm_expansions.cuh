@@ -585,6 +585,27 @@ __device__ __forceinline__ void ldv(const T* __restrict__ p, T (&r)[N]) {
   }
 }
 
+// ldv through L2 only (data written by other CTAs of the same launch)
+template <class T, int N>
+__device__ __forceinline__ void ldv_cg(const T* __restrict__ p, T (&r)[N]) {
+  constexpr int VW = 16 / sizeof(T);
+  static_assert(N % VW == 0, "vector width");
+#pragma unroll
+  for (int u = 0; u < N / VW; ++u) {
+    if constexpr (sizeof(T) == 4) {
+      const float4 v = __ldcg(reinterpret_cast<const float4*>(p) + u);
+      r[4 * u] = v.x;
+      r[4 * u + 1] = v.y;
+      r[4 * u + 2] = v.z;
+      r[4 * u + 3] = v.w;
+    } else {
+      const double2 v = __ldcg(reinterpret_cast<const double2*>(p) + u);
+      r[2 * u] = v.x;
+      r[2 * u + 1] = v.y;
+    }
+  }
+}
+
 // vector store of N consecutive T (16-B aligned)
 template <class T, int N>
 __device__ __forceinline__ void stv(T* __restrict__ p, const T (&r)[N]) {
@@ -993,36 +1014,57 @@ __global__ void __launch_bounds__(TR_THREADS) k_translate(TrArgs g) {
     if (!last) return;
     __threadfence();
     T* dst = reinterpret_cast<T*>(g.dst);
-    for (int e = tid; e < PT * ncp; e += TR_THREADS) {
-      const int c = e / ncp, r = e % ncp, d = col_dst[c];
-      if (d < 0) continue;
-      T v = T(0);
+    // 4-row vectors, two per thread per round: 16 independent loads in flight
+    const int nv = PT * ncp / 4;
+    for (int e0 = tid; e0 < nv; e0 += 2 * TR_THREADS) {
+      T q[2][8][4];
+      int dd[2], rr[2];
 #pragma unroll
-      for (int s = 0; s < 8; ++s) v += __ldcg(&slots[((size_t)s * np + d) * ncp + r]);
-      dst[(size_t)d * ncp + r] = v;
+      for (int u = 0; u < 2; ++u) {
+        const int e = e0 + u * TR_THREADS;
+        dd[u] = e < nv ? col_dst[e / (ncp / 4)] : -1;
+        rr[u] = 4 * (e % (ncp / 4));
+        if (dd[u] >= 0)
+#pragma unroll
+          for (int s = 0; s < 8; ++s) ldv_cg<T, 4>(slots + ((size_t)s * np + dd[u]) * ncp + rr[u], q[u][s]);
+      }
+#pragma unroll
+      for (int u = 0; u < 2; ++u) {
+        if (dd[u] < 0) continue;
+        T v[4] = {T(0), T(0), T(0), T(0)};
+#pragma unroll
+        for (int s = 0; s < 8; ++s)
+#pragma unroll
+          for (int x = 0; x < 4; ++x) v[x] += q[u][s][x];
+        stv<T, 4>(dst + (size_t)dd[u] * ncp + rr[u], v);
+      }
     }
     if (tid == 0) g.cnt[tile] = 0;
   } else {
     const T* part = reinterpret_cast<const T*>(g.partial);
     T* dst = reinterpret_cast<T*>(g.dst);
     const size_t nchild = (size_t)np * 8;
+    // M2L partial slots added in fixed slot order; all CPW columns of one
+    // slot loaded together (loads issued before any store)
+    int dcol[CPW];
+#pragma unroll
+    for (int j = 0; j < CPW; ++j) dcol[j] = col_dst[CPW * w + j];
+    for (int s = 0; s < g.nsplit; ++s) {
+      T q4[CPW][4];
+#pragma unroll
+      for (int j = 0; j < CPW; ++j)
+        if (dcol[j] >= 0) ldv<T, 4>(part + ((size_t)s * nchild + dcol[j]) * ncp + r0, q4[j]);
+#pragma unroll
+      for (int j = 0; j < CPW; ++j)
+        if (dcol[j] >= 0)
+#pragma unroll
+          for (int u = 0; u < 4; ++u) acc[u][j] += q4[j][u];
+    }
 #pragma unroll
     for (int j = 0; j < CPW; ++j) {
-      const int d = col_dst[CPW * w + j];
-      if (d < 0) continue;
+      if (dcol[j] < 0) continue;
       T v4[4] = {acc[0][j], acc[1][j], acc[2][j], acc[3][j]};
-      for (int s0 = 0; s0 < g.nsplit; s0 += 8) {  // slots in fixed order, 8 loads in flight
-        T q4[8][4];
-#pragma unroll
-        for (int s = 0; s < 8; ++s)
-          if (s0 + s < g.nsplit) ldv<T, 4>(part + ((size_t)(s0 + s) * nchild + d) * ncp + r0, q4[s]);
-#pragma unroll
-        for (int s = 0; s < 8; ++s)
-          if (s0 + s < g.nsplit)
-#pragma unroll
-            for (int u = 0; u < 4; ++u) v4[u] += q4[s][u];
-      }
-      stv<T, 4>(dst + (size_t)d * ncp + r0, v4);
+      stv<T, 4>(dst + (size_t)dcol[j] * ncp + r0, v4);
     }
   }
 }

@@ -114,8 +114,14 @@ __global__ void __launch_bounds__(P2P_WARPS * 32) k_p2p(const vec4_t<T>* __restr
 // where leaves hold 9..55 atoms).  Neighbourhoods longer than one staging
 // buffer are processed in chunks.  Every output is the sum of a fixed
 // sequence of operations: reruns are bit identical.
-constexpr int P2P2_WARPS = 4;
-constexpr int P2P2_SMAX = 512;  // staged sources per warp and chunk (even): 32 KB per CTA, 6 CTAs/SM
+#ifndef LFMM_P2P2_WARPS
+#define LFMM_P2P2_WARPS 4
+#endif
+#ifndef LFMM_P2P2_SMAX
+#define LFMM_P2P2_SMAX 512
+#endif
+constexpr int P2P2_WARPS = LFMM_P2P2_WARPS;
+constexpr int P2P2_SMAX = LFMM_P2P2_SMAX;  // staged sources per warp and chunk (even): 32 KB per CTA, 6 CTAs/SM
 constexpr int P2P2_SMEM = P2P2_WARPS * P2P2_SMAX * 16;  // dynamic shared memory per CTA
 
 __device__ __forceinline__ float rsqrt_fast(float x) {
@@ -169,10 +175,15 @@ __device__ __forceinline__ void kahan_fold(uint64_t& v2, uint64_t& c2, uint64_t 
 
 template <bool GRAD>
 __global__ void __launch_bounds__(P2P2_WARPS * 32) k_p2p2(const float4* __restrict__ xq,
+                                                          const float4* __restrict__ pair_a,
+                                                          const float4* __restrict__ pair_b,
                                                           const int* __restrict__ leaf_start, int depth,
                                                           float size, int periodic, float* __restrict__ vout,
                                                           float* __restrict__ gout, int x0, int x1) {
   extern __shared__ float4 p2p2_smem[];  // [warp][A | B][SMAX / 2]
+  __shared__ __align__(8) uint64_t s_bar[P2P2_WARPS];
+  __shared__ int2 s_img[P2P2_WARPS][28];  // {first staged pair, pair count}; sentinel at nimg
+  __shared__ float4 s_shift[P2P2_WARPS][27];
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   const int b = blockIdx.x * P2P2_WARPS + w;
   const int nleaf = 1 << (3 * depth);
@@ -182,35 +193,47 @@ __global__ void __launch_bounds__(P2P2_WARPS * 32) k_p2p2(const float4* __restri
   float4* B = A + P2P2_SMAX / 2;
   const int t0 = leaf_start[b], n = leaf_start[b + 1] - t0;
   if (n == 0) return;
-  // images: lane t < nimg holds image t (home = lane 0) — start, count, shift
+  const uint32_t bar = smem_u32(&s_bar[w]);
+  if (lane == 0) {
+    mbar_init(bar, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  // images: lane t < nimg holds image t (home = lane 0): its leaf's first
+  // source pair, pair count, shift into the target leaf's frame
   const int nimg = periodic ? 27 : 1;
-  int i_start = 0, i_cnt = 0;
+  int i_pair = 0, i_np = 0;
   float i_ox = 0.f, i_oy = 0.f, i_oz = 0.f;
   if (lane < nimg) {
     // lane 0 = home image (row 13); lanes 1..26 = rows 0..12, 14..26
     const int t = (lane == 0 || !periodic) ? 13 : (lane <= 13 ? lane - 1 : lane);
     int nb, sx, sy, sz;
     neighbor(b, t, depth, nb, sx, sy, sz);
-    i_start = leaf_start[nb];
-    i_cnt = leaf_start[nb + 1] - i_start;
+    const int st = leaf_start[nb];
+    i_pair = (st + nb + 1) >> 1;  // leaf nb's pairs (lfmm_tree.cuh k_leaf_rank)
+    i_np = (leaf_start[nb + 1] - st + 1) >> 1;
     i_ox = (float)(t / 9 - 1) * size;
     i_oy = (float)((t / 3) % 3 - 1) * size;
     i_oz = (float)(t % 3 - 1) * size;
   }
-  // staged offsets: home [0, nh2), others packed from nh2 (each image
-  // contiguous), total padded to even
-  const int nh2 = (n + 1) & ~1;
-  int excl = i_cnt;  // inclusive scan over lanes 1..nimg-1 of the other images
-  if (lane == 0) excl = 0;
+  // staged pair offsets: home [0, hp), the others packed after it
+  const int hp = (n + 1) >> 1;
+  int excl = i_np;  // inclusive scan of pair counts over the images
 #pragma unroll
   for (int o = 1; o < 32; o <<= 1) {
     const int y = __shfl_up_sync(0xffffffffu, excl, o);
     if (lane >= o) excl += y;
   }
-  const int i_off = (lane == 0) ? 0 : nh2 + excl - i_cnt;  // staged offset of my image
-  const int s_rest = __shfl_sync(0xffffffffu, excl, 31);   // other images' sources
-  const int total = nh2 + ((s_rest + 1) & ~1);
-  const int nchunk = (total + P2P2_SMAX - 1) / P2P2_SMAX;
+  const int i_off = excl - i_np;                        // staged pair offset of my image
+  const int tp = __shfl_sync(0xffffffffu, excl, 31);  // total staged pairs
+  if (lane < nimg) {
+    s_img[w][lane] = make_int2(i_off, i_np);
+    s_shift[w][lane] = make_float4(i_ox, i_oy, i_oz, 0.f);
+  }
+  if (lane == nimg) s_img[w][lane] = make_int2(0x7fffffff, 0);
+  constexpr int CH = P2P2_SMAX / 2;  // pairs per staging chunk
+  const int nchunk = (tp + CH - 1) / CH;
+  uint32_t phase = 0;
+  __syncwarp();
 
   for (int pb = 0; pb < n; pb += 32) {
     const int nt = min(32, n - pb);
@@ -224,60 +247,72 @@ __global__ void __launch_bounds__(P2P2_WARPS * 32) k_p2p2(const float4* __restri
     const int self = pb + slot;  // staged index of my target in the home block
     uint64_t v2 = 0, c2 = 0, gx2 = 0, gy2 = 0, gz2 = 0;
     for (int c = 0; c < nchunk; ++c) {
-      const int cb = c * P2P2_SMAX, ce = min(total, cb + P2P2_SMAX);
+      const int cb = c * CH, ce = min(tp, cb + CH);  // pairs [cb, ce)
       if (nchunk > 1 || pb == 0) {
-        // ---- stage entries [cb, ce) ----
+        // ---- stage pairs [cb, ce): one bulk copy per image and half (TMA
+        // engine, no registers), then the images' frame shifts in place ----
+        __syncwarp();  // every lane is done reading the previous contents
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        if (lane == 0)
+          asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar),
+                       "r"((uint32_t)(ce - cb) * 32u)
+                       : "memory");
         __syncwarp();
-        for (int im = 0; im < nimg; ++im) {
-          const int off = __shfl_sync(0xffffffffu, i_off, im), cnt = __shfl_sync(0xffffffffu, i_cnt, im);
-          const int st = __shfl_sync(0xffffffffu, i_start, im);
-          const float ox = __shfl_sync(0xffffffffu, i_ox, im), oy = __shfl_sync(0xffffffffu, i_oy, im),
-                      oz = __shfl_sync(0xffffffffu, i_oz, im);
-          const int lo = max(off, cb), hi = min(off + cnt, ce);
-          for (int e = lo + lane; e < hi; e += 32) {
-            const float4 s = xq[st + (e - off)];
-            float* a = reinterpret_cast<float*>(&A[(e - cb) >> 1]);
-            float* bb = reinterpret_cast<float*>(&B[(e - cb) >> 1]);
-            const int h = e & 1;
-            a[h] = s.x + ox;
-            a[2 + h] = s.y + oy;
-            bb[h] = s.z + oz;
-            bb[2 + h] = s.w;
+        {
+          const int lo = max(i_off, cb), hi = min(i_off + i_np, ce);
+          if (lane < nimg && hi > lo) {
+            const uint32_t bytes = (uint32_t)(hi - lo) * 16u;
+            const int src = i_pair + (lo - i_off);
+            asm volatile(
+                "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                    smem_u32(A + (lo - cb))),
+                "l"(pair_a + src), "r"(bytes), "r"(bar)
+                : "memory");
+            asm volatile(
+                "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                    smem_u32(B + (lo - cb))),
+                "l"(pair_b + src), "r"(bytes), "r"(bar)
+                : "memory");
           }
         }
-        // padding entries (home pad at n when n is odd, tail pad at total-1)
-        if (lane < 2) {
-          const int e = lane == 0 ? n : total - 1;
-          const bool pad = lane == 0 ? (n & 1) : ((s_rest & 1) != 0);
-          if (pad && e >= cb && e < ce) {
-            float* a = reinterpret_cast<float*>(&A[(e - cb) >> 1]);
-            float* bb = reinterpret_cast<float*>(&B[(e - cb) >> 1]);
-            const int h = e & 1;
-            a[h] = 1.0e4f;
-            a[2 + h] = 1.0e4f;
-            bb[h] = 1.0e4f;
-            bb[2 + h] = 0.f;
+        mbar_wait(bar, phase);
+        phase ^= 1;
+        if (nimg > 1) {
+          int im = 0;
+          for (int q = max(cb, hp) + lane; q < ce; q += 32) {
+            while (q >= s_img[w][im + 1].x) ++im;
+            const float4 sh = s_shift[w][im];
+            float4 av = A[q - cb];
+            float4 bv = B[q - cb];
+            av.x += sh.x;
+            av.y += sh.x;
+            av.z += sh.y;
+            av.w += sh.y;
+            bv.x += sh.z;
+            bv.y += sh.z;
+            A[q - cb] = av;
+            B[q - cb] = bv;
           }
         }
         __syncwarp();
       }
-      // ---- home block (self masked): pairs [cb, min(ce, nh2)) ----
+      // ---- home block (self masked): pairs [cb, min(ce, hp)) ----
       {
-        const int lo = cb >> 1, hi = max(lo, min(ce, nh2) >> 1);
+        const int lo = cb, hi = max(lo, min(ce, hp));
         const int np = hi - lo;
         const int k0 = lo + (np * part) / P, k1 = lo + (np * (part + 1)) / P;
         uint64_t p2 = 0;
         for (int k = k0; k < k1; ++k)
-          p2p2_step<GRAD, true>(A - (cb >> 1), B - (cb >> 1), k, x2, y2, z2, self, p2, gx2, gy2, gz2);
+          p2p2_step<GRAD, true>(A - cb, B - cb, k, x2, y2, z2, self, p2, gx2, gy2, gz2);
         kahan_fold(v2, c2, p2);
       }
-      // ---- other images: pairs [max(cb, nh2), ce) ----
+      // ---- other images: pairs [max(cb, hp), ce) ----
       {
-        const int lo = max(cb, nh2) >> 1, hi = max(lo, ce >> 1);
+        const int lo = max(cb, hp), hi = max(lo, ce);
         const int np = hi - lo;
         const int k0 = lo + (np * part) / P, k1 = lo + (np * (part + 1)) / P;
-        const float4* Ab = A - (cb >> 1);
-        const float4* Bb = B - (cb >> 1);
+        const float4* Ab = A - cb;
+        const float4* Bb = B - cb;
         // two independent accumulator sets per step pair (ILP); potential
         // partials folded every 16 steps
         uint64_t hx2 = 0, hy2 = 0, hz2 = 0;

@@ -141,7 +141,8 @@ __global__ void __launch_bounds__(RANK_WARPS * 32) k_leaf_rank(const double* __r
                                                               int* __restrict__ perm, int* __restrict__ inv_perm,
                                                               int depth, double size, double* __restrict__ pos_sorted,
                                                               vec4_t<T>* __restrict__ xq,
-                                                              int* __restrict__ leaf_sorted) {
+                                                              int* __restrict__ leaf_sorted, float4* __restrict__ pa,
+                                                              float4* __restrict__ pb) {
   __shared__ float kx[RANK_WARPS][32];
   const int wl = threadIdx.x >> 5;
   const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
@@ -209,7 +210,21 @@ __global__ void __launch_bounds__(RANK_WARPS * 32) k_leaf_rank(const double* __r
       v.w = T(0);
       xq[k] = v;
       leaf_sorted[k] = leaf;
+      if (pa) {  // fp32 source pairs for k_p2p2 (charges written by k_stage_q)
+        const int pp = ((s0 + leaf + 1) >> 1) + (rank >> 1), h = rank & 1;
+        reinterpret_cast<float*>(pa + pp)[h] = (float)v.x;
+        reinterpret_cast<float*>(pa + pp)[2 + h] = (float)v.y;
+        reinterpret_cast<float*>(pb + pp)[h] = (float)v.z;
+      }
     }
+  }
+  // odd leaf: the last pair's second half is a far, chargeless pad
+  if (pa && lane == 0 && ((s1 - s0) & 1)) {
+    const int pp = ((s0 + warp + 1) >> 1) + ((s1 - s0) >> 1);
+    reinterpret_cast<float*>(pa + pp)[1] = 1.0e4f;
+    reinterpret_cast<float*>(pa + pp)[3] = 1.0e4f;
+    reinterpret_cast<float*>(pb + pp)[1] = 1.0e4f;
+    reinterpret_cast<float*>(pb + pp)[3] = 0.f;
   }
 }
 
