@@ -133,29 +133,30 @@ __global__ void k_transpose_ops(const T* __restrict__ in, T* __restrict__ out, i
   out[(m * ncp + k) * ncp + r] = in[i];
 }
 
-template <class T, int CPW>
+template <class T, int CPW, int NS>
 inline size_t tr_smem_bytes(int ncp) {
-  return sizeof(T) * (2 * (size_t)TR_KC * ncp + 2 * (size_t)(8 * CPW) * TR_KC);
+  return sizeof(T) * (NS * (size_t)TR_KC * ncp + NS * (size_t)(8 * CPW) * TR_KC);
 }
 
 // one k_translate launch: CPW = 8 columns per warp (64 per CTA) once there
-// are enough target columns to fill the GPU, else 2 (16 per CTA)
+// are enough target columns to fill the GPU (2-stage ring), else 2 (16 per
+// CTA) with the whole K extent in flight (latency-bound small levels)
 template <class T>
 inline void tr_launch(const TrArgs& ta, int ncols_total, int noct, cudaStream_t st) {
   if (ncols_total >= 4096) {
     const unsigned tiles = (unsigned)((ncols_total + 63) / 64);
-    k_translate<T, 8><<<dim3(tiles, noct), TR_THREADS, tr_smem_bytes<T, 8>(ta.ncp), st>>>(ta);
+    k_translate<T, 8, 2><<<dim3(tiles, noct), TR_THREADS, tr_smem_bytes<T, 8, 2>(ta.ncp), st>>>(ta);
   } else {
     const unsigned tiles = (unsigned)((ncols_total + 15) / 16);
-    k_translate<T, 2><<<dim3(tiles, noct), TR_THREADS, tr_smem_bytes<T, 2>(ta.ncp), st>>>(ta);
+    k_translate<T, 2, 4><<<dim3(tiles, noct), TR_THREADS, tr_smem_bytes<T, 2, 4>(ta.ncp), st>>>(ta);
   }
 }
 template <class T>
 inline void tr_set_attrs(int ncp) {
-  LFMM_CUDA(cudaFuncSetAttribute(k_translate<T, 8>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 (int)tr_smem_bytes<T, 8>(ncp)));
-  LFMM_CUDA(cudaFuncSetAttribute(k_translate<T, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 (int)tr_smem_bytes<T, 2>(ncp)));
+  LFMM_CUDA(cudaFuncSetAttribute(k_translate<T, 8, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)tr_smem_bytes<T, 8, 2>(ncp)));
+  LFMM_CUDA(cudaFuncSetAttribute(k_translate<T, 2, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)tr_smem_bytes<T, 2, 4>(ncp)));
 }
 
 // Exact box charges (the l = 0 multipole) at every level.  The fp32 P2M/M2M
@@ -170,7 +171,7 @@ inline void tr_set_attrs(int ncp) {
 template <class T>
 __global__ void k_box_charges(const double* __restrict__ qs, const int* __restrict__ leaf_start, int depth,
                               int64_t leaf_off, int ncp, T* __restrict__ mult, double* __restrict__ boxq,
-                              int* __restrict__ cnt) {
+                              int* __restrict__ cnt, int wmin) {
   // phase 1: thread per leaf, grouped 8 per level-(d-1) parent in octant
   // order; lane 8g of each group then adds its 8 leaves in octant order
   if (depth >= 1) {
@@ -193,7 +194,7 @@ __global__ void k_box_charges(const double* __restrict__ qs, const int* __restri
     if (valid && o == 0) {
       const int64_t poff = leaf_off - (1LL << (3 * pl));
       boxq[poff + pb] = pc;
-      mult[(size_t)(poff + pb) * ncp] = (T)pc;
+      if (depth - 1 >= wmin) mult[(size_t)(poff + pb) * ncp] = (T)pc;
     }
   } else if (blockIdx.x == 0 && threadIdx.x == 0) {
     double c = 0.0;
@@ -215,12 +216,22 @@ __global__ void k_box_charges(const double* __restrict__ qs, const int* __restri
         c += __ldcg(&boxq[child_off + ((((int64_t)cx << (l + 1)) | (cy)) << (l + 1) | cz)]);
       }
       boxq[off + pb] = c;
-      mult[(size_t)(off + pb) * ncp] = (T)c;
+      if (l >= wmin) mult[(size_t)(off + pb) * ncp] = (T)c;
     }
     __syncthreads();
     __threadfence_block();
     child_off = off;
   }
+}
+
+// coefficient 0 of levels [0, lmax) from the exact box charges of
+// k_box_charges (its wmin = lmax run left them out while the small levels'
+// M2M ran beside it)
+template <class T>
+__global__ void k_apply_boxq(const double* __restrict__ boxq, int lmax, int ncp, T* __restrict__ mult) {
+  const int64_t nb = ((1LL << (3 * lmax)) - 1) / 7;  // boxes of levels 0 .. lmax-1
+  for (int64_t b = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; b < nb; b += (int64_t)gridDim.x * blockDim.x)
+    mult[(size_t)b * ncp] = (T)boxq[b];
 }
 
 template <int NQ>
@@ -396,6 +407,14 @@ __global__ void k_check_finite(const double* __restrict__ v, int64_t n, int* __r
 struct DevBuf {
   void* p = nullptr;
   size_t bytes = 0;
+  DevBuf() = default;
+  DevBuf(const DevBuf&) = delete;
+  DevBuf& operator=(const DevBuf&) = delete;
+  ~DevBuf() { release(); }
+  friend void swap(DevBuf& a, DevBuf& b) noexcept {
+    std::swap(a.p, b.p);
+    std::swap(a.bytes, b.bytes);
+  }
   void ensure(size_t b) {
     if (b <= bytes) return;
     if (p) cudaFree(p);
@@ -541,6 +560,10 @@ struct lfmm_plan {
   cudaStream_t near_stream = nullptr;
   cudaEvent_t ev_near_in = nullptr, ev_near_out = nullptr;
   bool near_pending = false;
+  // far_overlapped(): the latency-bound small levels of the far field run on
+  // far_stream (highest priority) beside the big levels' M2L
+  cudaStream_t far_stream = nullptr;
+  cudaEvent_t ev_far_fork = nullptr, ev_far_join = nullptr;
   // HI corrections (site geometry only) run on hi_stream beside the solve
   cudaStream_t hi_stream = nullptr;
   cudaEvent_t ev_hi_in = nullptr, ev_hi_out = nullptr;
@@ -575,7 +598,7 @@ struct lfmm_plan {
   DevBuf ops_tc, up_part, up_cnt, counters;
   DevBuf ops16, hm_inv_r, hm_inv_c, hm_jobs, hm_level_max, mult16;
   int64_t m16_off[DMAX + 2] = {0};
-  int hm_njobs = 0, hm_rw_cap = 0;
+  int hm_njobs = 0, hm_rw_cap = 0, hm_lsplit = 1, hm_nbig = 0;
   DevBuf mult, loc, partial, ops_m2l, ops_m2m, ops_l2l, ops_lat, lat64t;
   std::vector<double2> lat_unit;  // unit-box complex lattice operator (nc x nc)
   // solve work
@@ -663,6 +686,9 @@ struct lfmm_plan {
     if (io_stream) cudaStreamDestroy(io_stream);
     if (near_stream) cudaStreamDestroy(near_stream);
     if (hi_stream) cudaStreamDestroy(hi_stream);
+    if (far_stream) cudaStreamDestroy(far_stream);
+    if (ev_far_fork) cudaEventDestroy(ev_far_fork);
+    if (ev_far_join) cudaEventDestroy(ev_far_join);
     if (ev_hi_in) cudaEventDestroy(ev_hi_in);
     if (ev_hi_out) cudaEventDestroy(ev_hi_out);
     if (ev_near_in) cudaEventDestroy(ev_near_in);
@@ -776,7 +802,7 @@ struct lfmm_plan {
           launch(ST_SETUP, [&] {
             k_zgemm<<<zg, zb, 0, stream>>>(s_hat.as<double2>(), bmat.as<double2>(), tmp.as<double2>(), nco);
           });
-          std::swap(bmat, tmp);
+          swap(bmat, tmp);
         }
       }
       launch(ST_SETUP, [&] {
@@ -992,8 +1018,17 @@ struct lfmm_plan {
         }
       }
     }
-    // big jobs first: the small levels fill the tail of the launch
-    std::stable_sort(jobs.begin(), jobs.end(), [](const int4& a, const int4& b) { return a.z > b.z; });
+    // two launches when the far field is overlapped (far_overlap): levels >=
+    // hm_lsplit first, then the small levels; big jobs first within each
+    hm_lsplit = (depth >= 3 && dist_lg == 0) ? depth - 1 : 1;
+    const int ls = hm_lsplit;
+    std::stable_sort(jobs.begin(), jobs.end(), [ls](const int4& a, const int4& b) {
+      const int ga = (a.x & 15) >= ls ? 0 : 1, gb = (b.x & 15) >= ls ? 0 : 1;
+      if (ga != gb) return ga < gb;
+      return a.z > b.z;
+    });
+    hm_nbig = 0;
+    for (const int4& j : jobs) hm_nbig += (j.x & 15) >= ls ? 1 : 0;
     int64_t moff = 0;
     for (int l = 1; l <= depth; ++l) {
       m16_off[l] = moff;
@@ -1100,6 +1135,116 @@ struct lfmm_plan {
   }
 
   // ---------------------------------------------------------- solve ----
+  // Far field with the small levels beside the big ones (fp32 halo path,
+  // single rank, depth >= 3).  The levels < ls = hm_lsplit hold <= 8^(d-2)
+  // boxes: their M2M / M2L / L2L launches are latency-bound chains of a few
+  // us each that would otherwise sit on the critical path.
+  //   stream:     M2M (>= ls) -> box charges -> [fork] -> pack + M2L (>= ls)
+  //               -> [join] -> L2L (>= ls)
+  //   far_stream: [fork] -> M2M (< ls) -> exact charges (< ls) -> lattice
+  //               -> pack + M2L (< ls) -> L2L (< ls) -> [join]
+  // Every buffer region is written by exactly one side (levels are disjoint;
+  // the fork orders the small M2M after the level-ls box charges), so the
+  // result is the same sequence of operations on every run.
+  bool far_overlap() const {
+    return use_halo && fp32 && use_tr && !profiling && dist_lg == 0 && dist_phase == 0 && depth >= 3 &&
+           hm_lsplit > 1 && hm_nbig > 0 && hm_nbig < hm_njobs;
+  }
+  void tr_m2m(int l, cudaStream_t st) {
+    TrArgs ta{};
+    ta.mode = 0;
+    ta.level = l;
+    ta.ncp = ncp;
+    ta.ops_t = ops_m2m_t.p;
+    ta.src = mult.as<float>() + level_off[l + 1] * ncp;
+    ta.dst = mult.as<float>() + level_off[l] * ncp;
+    ta.slots = up_part.p;
+    ta.cnt = tr_cnt.as<int>();
+    launch(ST_M2M, [&] { tr_launch<float>(ta, 1 << (3 * l), 8, st); });
+  }
+  void tr_l2l(int l, cudaStream_t st) {
+    TrArgs ta{};
+    ta.mode = 1;
+    ta.level = l;
+    ta.ncp = ncp;
+    ta.ops_t = ops_l2l_t.p;
+    ta.src = loc.as<float>() + level_off[l - 1] * ncp;
+    ta.dst = loc.as<float>() + level_off[l] * ncp;
+    ta.partial = static_cast<const char*>(partial.p) + sizeof(float) * (size_t)part_off[l] * ncp;
+    ta.nsplit = nsplit[l];
+    launch(ST_L2L, [&] { tr_launch<float>(ta, 1 << (3 * (l - 1)), 8, st); });
+  }
+  void halo_levels(HaloArgs ha, int l0, int l1, int job0, int njobs, cudaStream_t st) {
+    ha.lvl0 = l0;
+    ha.jobs = hm_jobs.as<int4>() + job0;
+    const int nl = l1 - l0 + 1;
+    launch(ST_PACK, [&] {
+      k_level_absmax<<<dim3((unsigned)std::max<int64_t>(1, ((1LL << (3 * l1)) + 63) / 64), nl), 256, 0, st>>>(
+          ha.mult, ha, hm_level_max.as<unsigned int>());
+    });
+    launch(ST_PACK, [&] {
+      k_pack_mult16<<<dim3((unsigned)((hm_plane_rows(l1) + 127) / 128), nl, 8), 128, 0, st>>>(ha);
+    });
+    launch(ST_DOWN, [&] { k_m2l_halo<<<njobs, HM_THREADS, hm_smem_bytes(hm_rw_cap), st>>>(ha); });
+  }
+  void far_overlapped() {
+    const int ls = hm_lsplit;
+    if (!far_stream) {
+      int lo = 0, hi = 0;
+      LFMM_CUDA(cudaDeviceGetStreamPriorityRange(&lo, &hi));
+      LFMM_CUDA(cudaStreamCreateWithPriority(&far_stream, cudaStreamNonBlocking, hi));
+      LFMM_CUDA(cudaEventCreateWithFlags(&ev_far_fork, cudaEventDisableTiming));
+      LFMM_CUDA(cudaEventCreateWithFlags(&ev_far_join, cudaEventDisableTiming));
+    }
+    float* M = mult.as<float>();
+    float* Lc = loc.as<float>();
+    for (int l = depth - 1; l >= ls; --l) tr_m2m(l, stream);
+    launch(ST_M2M, [&] {
+      k_box_charges<float><<<nblk(nleaf, 256), 256, 0, stream>>>(qs.as<double>(), leaf_start.as<int>(), depth,
+                                                                 level_off[depth], ncp, M, boxq.as<double>(),
+                                                                 counters.as<int>() + 2, ls);
+    });
+    HaloArgs ha{};
+    ha.mult = M;
+    ha.partial = reinterpret_cast<float*>(partial.p);
+    ha.ops16 = ops16.as<unsigned char>();
+    ha.level_max = hm_level_max.as<unsigned int>();
+    ha.inv_r = hm_inv_r.as<float>();
+    ha.inv_c = hm_inv_c.as<float>();
+    ha.rw_cap = hm_rw_cap;
+    ha.mult16 = mult16.as<unsigned char>();
+    for (int l = 0; l <= depth; ++l) {
+      ha.level_off[l] = level_off[l];
+      ha.part_off[l] = part_off[l];
+      ha.m16_off[l] = m16_off[l];
+    }
+    LFMM_CUDA(cudaMemsetAsync(hm_level_max.p, 0, hm_level_max.bytes, stream));
+    LFMM_CUDA(cudaEventRecord(ev_far_fork, stream));
+    // ---- small levels ----
+    LFMM_CUDA(cudaStreamWaitEvent(far_stream, ev_far_fork, 0));
+    for (int l = ls - 1; l >= 0; --l) tr_m2m(l, far_stream);
+    launch(ST_M2M, [&] { k_apply_boxq<float><<<4, 256, 0, far_stream>>>(boxq.as<double>(), ls, ncp, M); });
+    if (lattice_mode != LFMM_LATTICE_OFF) {
+      TrArgs ta{};
+      ta.mode = 2;
+      ta.ncols = 1;
+      ta.ncp = ncp;
+      ta.ops_t = ops_lat_t.p;
+      ta.src = M;
+      ta.dst = Lc;
+      launch(ST_ROOT, [&] { tr_launch<float>(ta, 1, 1, far_stream); });
+    } else {
+      LFMM_CUDA(cudaMemsetAsync(Lc, 0, sizeof(float) * ncp, far_stream));
+    }
+    halo_levels(ha, 1, ls - 1, hm_nbig, hm_njobs - hm_nbig, far_stream);
+    for (int l = 1; l < ls; ++l) tr_l2l(l, far_stream);
+    LFMM_CUDA(cudaEventRecord(ev_far_join, far_stream));
+    // ---- big levels ----
+    halo_levels(ha, ls, depth, 0, hm_nbig, stream);
+    LFMM_CUDA(cudaStreamWaitEvent(stream, ev_far_join, 0));
+    for (int l = ls; l <= depth; ++l) tr_l2l(l, stream);
+  }
+
   template <class T>
   void solve_column(int K, int c, bool grad) {
     const int64_t nb = std::min<int64_t>(nblk(N, 256), 148 * 4);
@@ -1127,6 +1272,7 @@ struct lfmm_plan {
       dim3 grid(tiles_all(l) * ga.up_split, rowb);
       launch(ST_M2M, [&] { k_gemm_gather<T><<<grid, G_THREADS, 0, stream>>>(ga); });
     };
+    bool far_done = false;
     if (dist_phase == 2) {
       // levels spanning several ranks, from the gathered level dist_lg
       for (int l = std::min(dist_lg, depth) - 1; l >= 0; --l) m2m_level(l);
@@ -1188,15 +1334,22 @@ struct lfmm_plan {
       k_p2m<T><<<nblk(nleaf, EXP_WARPS), EXP_WARPS * 32, 0, stream>>>(
           xq.as<vec4_t<T>>(), leaf_start.as<int>(), depth, p, (T)(1.0 / size), ncp, M + level_off[depth] * ncp);
     });
+    if (sizeof(T) == 4 && far_overlap()) {
+      far_done = true;
+      far_overlapped();
+    } else {
     for (int l = depth - 1; l >= (dist_phase == 1 ? dist_lg : 0); --l) m2m_level(l);
     launch(ST_M2M, [&] {
       k_box_charges<T><<<nblk(nleaf, 256), 256, 0, stream>>>(qs.as<double>(), leaf_start.as<int>(), depth,
                                                              level_off[depth], ncp, M, boxq.as<double>(),
-                                                             counters.as<int>() + 2);
+                                                             counters.as<int>() + 2, 0);
     });
+    }
     if (dist_phase == 1) return;  // owned multipoles ready for the all-gather
     }  // up
-    if (lattice_mode != LFMM_LATTICE_OFF && use_tr) {
+    if (far_done) {
+      // lattice, M2L and L2L already issued by far_overlapped()
+    } else if (lattice_mode != LFMM_LATTICE_OFF && use_tr) {
       TrArgs ta{};
       ta.mode = 2;
       ta.ncols = 1;
@@ -1213,7 +1366,7 @@ struct lfmm_plan {
     } else {
       LFMM_CUDA(cudaMemsetAsync(Lc, 0, sizeof(T) * ncp, stream));
     }
-    if (depth >= 1) {
+    if (depth >= 1 && !far_done) {
       // M2L of every level in one launch (terms split over CTAs), then the
       // L2L sweep adds the partial slots level by level
       if (use_halo && sizeof(T) == 4) {
@@ -1226,6 +1379,7 @@ struct lfmm_plan {
         ha.inv_r = hm_inv_r.as<float>();
         ha.inv_c = hm_inv_c.as<float>();
         ha.rw_cap = hm_rw_cap;
+        ha.lvl0 = 1;
         ha.mult16 = mult16.as<unsigned char>();
         for (int l = 0; l <= depth; ++l) {
           ha.level_off[l] = level_off[l];

@@ -900,14 +900,14 @@ __device__ __forceinline__ void tr_cp16(T* sdst, const T* gsrc) {
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(s), "l"(gsrc) : "memory");
 }
 
-template <class T, int CPW>
+template <class T, int CPW, int NS>
 __global__ void __launch_bounds__(TR_THREADS) k_translate(TrArgs g) {
   constexpr int VW = 16 / sizeof(T);  // elements per 16-B copy
   constexpr int PT = 8 * CPW;         // target columns per CTA (8 warps x CPW)
   extern __shared__ __align__(16) unsigned char tr_smem[];
-  T* As = reinterpret_cast<T*>(tr_smem);              // [2][TR_KC][ncp]
+  T* As = reinterpret_cast<T*>(tr_smem);              // [NS][TR_KC][ncp]
   const int ncp = g.ncp;
-  T* Bs = As + 2 * TR_KC * ncp;                        // [2][PT][TR_KC]
+  T* Bs = As + NS * TR_KC * ncp;                       // [NS][PT][TR_KC]
   __shared__ int col_src[PT], col_dst[PT];
   const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
   const int o = blockIdx.y;
@@ -951,7 +951,6 @@ __global__ void __launch_bounds__(TR_THREADS) k_translate(TrArgs g) {
 #pragma unroll
         for (int v = 0; v < VW; ++v) b[c * TR_KC + u * VW + v] = T(0);
     }
-    asm volatile("cp.async.commit_group;" ::: "memory");
   };
   T acc[4][CPW];
 #pragma unroll
@@ -959,17 +958,20 @@ __global__ void __launch_bounds__(TR_THREADS) k_translate(TrArgs g) {
 #pragma unroll
     for (int j = 0; j < CPW; ++j) acc[i][j] = T(0);
   const int r0 = 4 * lane;  // rows r0..r0+3 (the plan routes only ncp == 128 here)
-  stage(0, 0);
+  // NS-stage cp.async ring: NS - 1 chunks in flight ahead of the one in use
+  // (small levels use NS = nk: the whole K extent is requested at once)
+#pragma unroll
+  for (int s = 0; s < NS - 1; ++s) {
+    if (s < nk) stage(s, s);
+    asm volatile("cp.async.commit_group;" ::: "memory");
+  }
   for (int kc = 0; kc < nk; ++kc) {
-    if (kc + 1 < nk) {
-      stage(kc + 1, (kc + 1) & 1);
-      asm volatile("cp.async.wait_group 1;" ::: "memory");
-    } else {
-      asm volatile("cp.async.wait_group 0;" ::: "memory");
-    }
+    if (kc + NS - 1 < nk) stage(kc + NS - 1, (kc + NS - 1) % NS);
+    asm volatile("cp.async.commit_group;" ::: "memory");
+    asm volatile("cp.async.wait_group %0;" ::"n"(NS - 1) : "memory");
     __syncthreads();
-    const T* a = As + (size_t)(kc & 1) * TR_KC * ncp;
-    const T* b = Bs + (size_t)(kc & 1) * PT * TR_KC + (size_t)(CPW * w) * TR_KC;
+    const T* a = As + (size_t)(kc % NS) * TR_KC * ncp;
+    const T* b = Bs + (size_t)(kc % NS) * PT * TR_KC + (size_t)(CPW * w) * TR_KC;
 #pragma unroll 2
     for (int k = 0; k < TR_KC; k += 4) {
       T av[4][4];

@@ -76,6 +76,7 @@ struct HaloArgs {
   int64_t level_off[DMAX + 2];
   int64_t part_off[DMAX + 2];
   int rw_cap;                        // rows per window the buffers were sized for
+  int lvl0;                          // first level of a k_level_absmax / k_pack_mult16 launch (grid.y = levels)
 };
 
 __host__ __device__ inline int hm_rw(int N, int Z) { return N + 2 * Z + 2; }
@@ -141,9 +142,9 @@ __global__ void k_h16_arrange(const float* __restrict__ ops, const float* __rest
   *reinterpret_cast<__half*>(base + 4096 + off) = lo;
 }
 
-// per level (blockIdx.y + 1): max over boxes and coefficients of |M^ / c|
+// per level (blockIdx.y + lvl0): max over boxes and coefficients of |M^ / c|
 __global__ void k_level_absmax(const float* __restrict__ mult, HaloArgs g, unsigned int* __restrict__ out) {
-  const int level = blockIdx.y + 1;
+  const int level = blockIdx.y + g.lvl0;
   const int nbox = 1 << (3 * level);
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const float4 ic = reinterpret_cast<const float4*>(g.inv_c)[lane];
@@ -181,7 +182,7 @@ __host__ __device__ inline int hm_plane_rows(int level) {
 
 // multipoles -> fp16 planes: thread per (level, source class, padded row)
 __global__ void k_pack_mult16(HaloArgs g) {
-  const int level = blockIdx.y + 1, sc = blockIdx.z;
+  const int level = blockIdx.y + g.lvl0, sc = blockIdx.z;
   const int prow = hm_plane_rows(level);
   const int r = blockIdx.x * blockDim.x + threadIdx.x;
   if (r >= prow) return;

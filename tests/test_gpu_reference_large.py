@@ -1,0 +1,83 @@
+"""Parity against the REFERENCE at the benchmark sizes.
+
+tests/golden/make_golden_large.py ran the reference (lambdafmm, fp64) on the
+C2 (100k atoms, 64 sites, depth 4) and C3 (1M atoms, 512 sites, depth 5)
+water boxes and stored energies, HI lambda-forces and correction scalars in
+full, plus potentials and spatial forces on a 10k-atom sample.  The boxes are
+regenerated here from their seeds (checksum-verified).  Metric: the
+reference's max-normalised error (bench.py:46-52), normalised by the
+reference's max over ALL atoms; tolerances are the north_star's (1e-6 fp64,
+1e-4 fp32)."""
+
+import os
+
+import numpy as np
+import pytest
+
+pytestmark = [pytest.mark.gpu, pytest.mark.slow]
+
+from paper_2410_01754_b200 import (  # noqa: E402
+    PeriodicSolver,
+    SolverConfig,
+    expand_weights,
+    hi_energy_and_forces,
+    scale_charges,
+)
+from paper_2410_01754_b200.waterbox import generate_water_box  # noqa: E402
+
+GOLDEN = os.path.join(os.path.dirname(__file__), "golden")
+CASES = {"c2": "ref_c2_d4.npz", "c3": "ref_c3_d5.npz"}
+_systems = {}
+
+
+def _load(case):
+    path = os.path.join(GOLDEN, CASES[case])
+    if not os.path.exists(path):
+        pytest.fail(f"missing fixture {path}: run tests/golden/make_golden_large.py")
+    g = np.load(path)
+    if case not in _systems:
+        _systems[case] = generate_water_box(int(g["n_atoms"]), int(g["n_sites"]), seed=int(g["seed"]))
+    system, lam, _ = _systems[case]
+    ck = np.array([system.positions.sum(), (system.positions ** 2).sum(), system.charges.sum(),
+                   np.abs(system.charges).sum(), float(system.num_particles)])
+    np.testing.assert_allclose(ck, g["checksum"], rtol=1e-13, err_msg="regenerated water box differs")
+    return g, system, lam
+
+
+def _err(got, ref, absmax):
+    return float(np.max(np.abs(np.asarray(got) - np.asarray(ref))) / absmax)
+
+
+@pytest.mark.parametrize("precision", ["double", "single"])
+@pytest.mark.parametrize("case", ["c2", "c3"])
+def test_matches_reference(case, precision):
+    g, system, lam = _load(case)
+    tol = 1e-6 if precision == "double" else 1e-4
+    cfg = SolverConfig(p=int(g["p"]), depth=int(g["depth"]), precision=precision)
+    solver = PeriodicSolver(system.positions, system.box_length, cfg)
+    r = hi_energy_and_forces(system, lam.values, solver=solver)
+    qt = scale_charges(system, [expand_weights(v) for v in lam.values])
+    f = solver.spatial_forces(qt)
+    idx = g["idx"]
+    s = r.solve
+    err = {
+        "potentials": _err(s.potentials[idx], g["potentials"], g["absmax_potentials"]),
+        "near": _err(s.near_potentials[idx], g["near"], g["absmax_near"]),
+        "far": _err(s.far_potentials[idx], g["far"], g["absmax_far"]),
+        "dip": _err(s.dipole_potentials[idx], g["dip"], g["absmax_dip"]),
+        "forces": _err(f[idx], g["forces"], g["absmax_forces"]),
+        "lambda_forces": _err(np.concatenate(r.forces), g["hi_forces"], np.abs(g["hi_forces"]).max()),
+        "c_p2p": _err(np.concatenate([c.c_p2p for c in r.corrections.sites]), g["c_p2p"],
+                      np.abs(g["c_p2p"]).max()),
+        "c_lattice": _err(np.concatenate([c.c_lattice for c in r.corrections.sites]), g["c_lattice"],
+                          np.abs(g["c_lattice"]).max()),
+        "c_dipole": _err(np.concatenate([c.c_dipole for c in r.corrections.sites]), g["c_dipole"],
+                         np.abs(g["c_dipole"]).max()),
+    }
+    for k in ("energy", "near_energy", "far_energy", "dipole_energy"):
+        ref = float(g[k])
+        err[k] = abs(float(getattr(s, k)) - ref) / abs(ref)
+    err["hi_energy"] = abs(r.energy - float(g["hi_energy"])) / abs(float(g["hi_energy"]))
+    print(case, precision, {k: "%.2e" % v for k, v in err.items()})
+    bad = {k: v for k, v in err.items() if not v <= tol}
+    assert not bad, bad
