@@ -589,6 +589,7 @@ struct lfmm_plan {
   bool use_tc = false;    // M2L on tcgen05 (fp32, (p+1)^2 <= 128)
   bool use_halo = false;  // ... as shifted-window fp16x3 GEMMs (lfmm_m2l_halo.cuh)
   bool p2p_scalar = false;  // fp32 P2P on the scalar kernel (LFMM_P2P=scalar, A/B checks)
+  bool far_serial = false;  // no far_overlapped() (LFMM_FAR=serial, A/B checks and tools/hm_prof.py)
   bool step_mode = false;   // lfmm_step: skip the input-order potential arrays
   // Slab decomposition (distributed.py): this rank owns leaves with x index in
   // [own_x0, own_x1); levels < dist_lg have boxes spanning ranks and are
@@ -1147,7 +1148,7 @@ struct lfmm_plan {
   // the fork orders the small M2M after the level-ls box charges), so the
   // result is the same sequence of operations on every run.
   bool far_overlap() const {
-    return use_halo && fp32 && use_tr && !profiling && dist_lg == 0 && dist_phase == 0 && depth >= 3 &&
+    return use_halo && fp32 && use_tr && !profiling && !far_serial && dist_lg == 0 && dist_phase == 0 && depth >= 3 &&
            hm_lsplit > 1 && hm_nbig > 0 && hm_nbig < hm_njobs;
   }
   void tr_m2m(int l, cudaStream_t st) {
@@ -1795,6 +1796,8 @@ int lfmm_plan_create(const double* positions, int64_t n, double box_length, int 
       pl->use_halo = pl->use_tc && !(env && std::string(env) == "gather");
       const char* penv = std::getenv("LFMM_P2P");
       pl->p2p_scalar = penv && std::string(penv) == "scalar";
+      const char* fenv = std::getenv("LFMM_FAR");
+      pl->far_serial = fenv && std::string(fenv) == "serial";
     }
     pl->nleaf = 1 << (3 * depth);
     pl->size = box_length / double(1 << depth);

@@ -4,6 +4,7 @@ import ctypes, os, sys
 import numpy as np
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 os.environ.setdefault("LFMM_LIB", os.path.join(ROOT, "paper_2410_01754_b200/_lib/liblfmm_prof.so"))
+os.environ["LFMM_FAR"] = "serial"  # one k_m2l_halo launch (CTA index = job index)
 sys.path.insert(0, ROOT)
 from paper_2410_01754_b200 import PeriodicSolver, SolverConfig, _native
 from paper_2410_01754_b200.waterbox import generate_water_box
@@ -29,6 +30,9 @@ for l in range(depth, 0, -1):
             for g in range(G):
                 jobs.append((l, N, tc, g))
         t0 += 256
+# plan_halo_jobs order: levels >= depth-1 first, big N first within a group
+ls = depth - 1 if depth >= 3 else 1
+jobs = sorted(jobs, key=lambda j: (0 if j[0] >= ls else 1, -j[1]))
 nj = len(jobs)
 b = buf[:nj].astype(np.float64)
 t0 = b[:, 0].min()
