@@ -265,6 +265,7 @@ __global__ void k_finalize(int64_t n, int K, int c, const int* __restrict__ perm
                            double* __restrict__ qtot, const int* __restrict__ leaf_sorted, int depth, int x0,
                            int x1) {
   dd v[2] = {dd{0, 0}, dd{0, 0}};
+#pragma unroll 2
   for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < n; k += (int64_t)gridDim.x * blockDim.x) {
     const int i = perm[k];
     const double q = qs[k];

@@ -349,6 +349,9 @@ __global__ void __launch_bounds__(EXP_WARPS * 32) k_l2p_f2(const float4* __restr
   if ((b >> (2 * depth)) < x0 || (b >> (2 * depth)) >= x1) return;  // leaf outside this rank's slab
   const int t0 = leaf_start[b], t1 = leaf_start[b + 1];
   if (t1 == t0) return;
+  // first pass's atom, loaded before the staging so both latencies overlap
+  float4 vnext = make_float4(0.f, 0.f, 0.f, 0.f);
+  if (t0 + lane < t1) vnext = xq[t0 + lane];
   // ---- stage L (one 16-B vector per lane) and build the gradient ladder G
   // (harmonics.py:106-130) from the shared copy ----
   __shared__ __align__(16) float sL[EXP_WARPS][128];
@@ -403,13 +406,9 @@ __global__ void __launch_bounds__(EXP_WARPS * 32) k_l2p_f2(const float4* __restr
   for (int tc = t0; tc < t1; tc += 32) {
     const int i = tc + lane;
     const bool act = i < t1;
-    float x = 0.f, y = 0.f, z = 0.f;
-    if (act) {
-      const float4 v = xq[i];
-      x = v.x * inv_s;
-      y = v.y * inv_s;
-      z = v.z * inv_s;
-    }
+    const float4 v = vnext;
+    vnext = (tc + 32 + lane < t1) ? xq[tc + 32 + lane] : make_float4(0.f, 0.f, 0.f, 0.f);  // next pass
+    const float x = v.x * inv_s, y = v.y * inv_s, z = v.z * inv_s;
     const float r2 = x * x + y * y + z * z;
     float vs = 0.f, gxs = 0.f, gys = 0.f, gzs = 0.f;
     uint64_t va = 0, gxa = 0, gya = 0, gza = 0;
