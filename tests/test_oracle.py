@@ -146,3 +146,26 @@ def test_oracle_madelung():
     q = np.where(grid.sum(axis=1) % 2 == 0, 1.0, -1.0)
     r = orc.solve(pos, q, box, orc.default_config(p=22, depth=0))
     assert abs(r["energy"] - (-8.0 * 1.7475645946331822 / box)) <= 1e-10 * 8 * 1.7475645946331822 / box
+
+
+def test_oracle_matches_reference_c2(golden):
+    # tests/golden/make_golden_large.py: the reference on the C2 water box
+    # (100k atoms, 64 sites, p=10, depth 4); the box is regenerated from its
+    # seed here (checksum-verified) and the oracle reproduces the reference's
+    # energies and sampled potentials / spatial forces
+    from paper_2410_01754_b200 import expand_weights, scale_charges
+    from paper_2410_01754_b200.waterbox import generate_water_box
+
+    g = golden("ref_c2_d4.npz")
+    system, lam, _ = generate_water_box(int(g["n_atoms"]), int(g["n_sites"]), seed=int(g["seed"]))
+    ck = np.array([system.positions.sum(), (system.positions ** 2).sum(), system.charges.sum(),
+                   np.abs(system.charges).sum(), float(system.num_particles)])
+    np.testing.assert_allclose(ck, g["checksum"], rtol=1e-13)
+    qt = scale_charges(system, [expand_weights(v) for v in lam.values])
+    r = orc.solve(system.positions, qt, system.box_length, orc.default_config(p=10, depth=4), forces=True)
+    idx = g["idx"]
+    for key, ref, amax in (("potentials", "potentials", "absmax_potentials"), ("near", "near", "absmax_near"),
+                           ("far", "far", "absmax_far"), ("forces", "forces", "absmax_forces")):
+        assert np.abs(r[key][idx] - g[ref]).max() / float(g[amax]) <= 1e-11, key
+    for k in ("energy", "near_energy", "far_energy", "dipole_energy"):
+        assert abs(r[k] - float(g[k])) <= 1e-11 * abs(float(g[k])), k
