@@ -136,6 +136,32 @@ int lfmm_hi(lfmm_plan* plan, const double* lambdas, const int32_t* n_lambda,
  * Site tables as in lfmm_sites_set; c_total (sum n_forms) f64 per form, or
  * NULL for the plain charge-route (QI) forces; potentials (n_particles,)
  * input order.  All pointers are host pointers.  out: (S,4) f64. */
+/* Per-site form Gram B_s = Q_s (K_s + G_s) Q_s^T (HI_MAXF x HI_MAXF = 16 x 16
+ * per site, row-major, host output): the correction table of
+ * FrozenLambdaForceField (dynamics.py:137-145; K = near_kernel, G =
+ * lattice_kernel, corrections.py:46-77), from the same k_hi_site pass as
+ * lfmm_hi. */
+int lfmm_site_gram(lfmm_plan* plan, const double* lambdas, const int32_t* n_lambda,
+                   const double* site_positions, double* gram);
+
+/* Device-resident BAOAB step pieces for the titration coordinates
+ * (dynamics.py:214-285 run_trajectory).  All arrays are DEVICE pointers in the
+ * (S,4) padded layout of lfmm_step; launched on the plan's stream.
+ * stage 0: B A O A with f_total; stage 1: f_total = coulomb f_engine + bias +
+ * wall at the current lambdas, then B; stage 2: f_total only.  Normals from a
+ * Philox stream indexed by (seed, step, slot). */
+int lfmm_lambda_baoab(lfmm_plan* plan, int64_t n_sites, double* lambdas, double* velocities,
+                      const int32_t* n_lambda, const double* masses, const double* f_engine,
+                      double* f_total, int stage, double dt, double coulomb, double bias_height,
+                      double c1, double noise, uint64_t seed, uint64_t step);
+/* Trajectory sample `sample` of the live slots (compacted by slot_offsets)
+ * into device arrays (n_samples x n_slots) plus the energy in kJ/mol. */
+int lfmm_lambda_record(lfmm_plan* plan, int64_t n_sites, const int32_t* slot_offsets,
+                       const int32_t* n_lambda, const double* lambdas, const double* velocities,
+                       const double* f_total, const double* energy, double coulomb, int64_t n_slots,
+                       double* out_lambdas, double* out_velocities, double* out_forces,
+                       double* out_energies, int64_t sample);
+
 int lfmm_assemble(int64_t n_sites, const int64_t* atom_offsets, const int64_t* atom_index,
                   const int32_t* n_forms, const int64_t* form_offsets, const double* form_charges,
                   const double* lambdas, const int32_t* n_lambda, const double* c_total,

@@ -65,6 +65,11 @@ def _declare(lib):
         "lfmm_dist_phase": (_i32, [_vp, _i32, _vp, _vp, _vp, _vp, _i32]),
         "lfmm_dist_buffers": (_i32, [_vp, _vp, _vp]),
         "lfmm_dist_hi": (_i32, [_vp, _vp, _i32]),
+        "lfmm_site_gram": (_i32, [_vp, _vp, _vp, _vp, _vp]),
+        "lfmm_lambda_baoab": (_i32, [_vp, _i64, _vp, _vp, _vp, _vp, _vp, _vp, _i32, _dbl, _dbl, _dbl, _dbl, _dbl,
+                                     _c.c_uint64, _c.c_uint64]),
+        "lfmm_lambda_record": (_i32, [_vp, _i64, _vp, _vp, _vp, _vp, _vp, _vp, _dbl, _i64, _vp, _vp, _vp, _vp,
+                                      _i64]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(lib, name)
@@ -81,6 +86,7 @@ def exported_symbols():
         "lfmm_assemble", "lfmm_scale_charges", "lfmm_step", "lfmm_profile_enable",
         "lfmm_stage_count", "lfmm_stage_name", "lfmm_stage_times", "lfmm_launch_count",
         "lfmm_plan_set_count", "lfmm_dist_configure", "lfmm_dist_phase", "lfmm_dist_buffers", "lfmm_dist_hi",
+        "lfmm_site_gram", "lfmm_lambda_baoab", "lfmm_lambda_record",
     ]
 
 
@@ -279,6 +285,25 @@ class Plan:
 
     def launch_count(self):
         return int(lib().lfmm_launch_count(self.h))
+
+    # ---- lambda dynamics (dynamics.py) ----
+    def site_gram(self, lambdas, n_lambda, site_positions):
+        """(S, 16, 16) per-site Q (K + G) Q^T."""
+        out = np.zeros((self.n_sites, 16, 16))
+        check(lib().lfmm_site_gram(self.h, ptr(lambdas), ptr(n_lambda), ptr(site_positions), ptr(out)))
+        return out
+
+    def lambda_baoab(self, n_sites, lam, vel, n_lambda, masses, f_engine, f_total, stage, dt, coulomb, bias_height,
+                     c1, noise, seed, step):
+        check(lib().lfmm_lambda_baoab(self.h, int(n_sites), ptr(lam), ptr(vel), ptr(n_lambda), ptr(masses),
+                                      ptr(f_engine), ptr(f_total), int(stage), float(dt), float(coulomb),
+                                      float(bias_height), float(c1), float(noise), int(seed), int(step)))
+
+    def lambda_record(self, n_sites, slot_off, n_lambda, lam, vel, f_total, energy, coulomb, n_slots, out_x, out_v,
+                      out_f, out_e, sample):
+        check(lib().lfmm_lambda_record(self.h, int(n_sites), ptr(slot_off), ptr(n_lambda), ptr(lam), ptr(vel),
+                                       ptr(f_total), ptr(energy), float(coulomb), int(n_slots), ptr(out_x),
+                                       ptr(out_v), ptr(out_f), ptr(out_e), int(sample)))
 
     # ---- slab decomposition (distributed.py) ----
     def set_count(self, n):

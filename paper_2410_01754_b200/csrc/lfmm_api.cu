@@ -20,6 +20,7 @@
 #include <vector>
 
 #include "lfmm_common.cuh"
+#include "lfmm_dynamics.cuh"
 #include "lfmm_expansions.cuh"
 #include "lfmm_hi.cuh"
 #include "lfmm_m2l_halo.cuh"
@@ -584,6 +585,7 @@ struct lfmm_plan {
   // fp32 near-field source pairs (k_p2p2): [pair_cap] float4 x/y halves, then [pair_cap] z/q halves
   DevBuf pairs;
   int64_t pair_cap = 0;
+  DevBuf gram;  // lfmm_site_gram output
   float4* pair_a() { return fp32 ? reinterpret_cast<float4*>(pairs.p) : nullptr; }
   float4* pair_b() { return fp32 ? reinterpret_cast<float4*>(pairs.p) + pair_cap : nullptr; }
   // expansions / operators
@@ -1631,7 +1633,6 @@ void hi_args(lfmm_plan* pl, HiArgs& g) {
 }
 
 void upload_lambdas(lfmm_plan* pl, const double* lambdas, const int32_t* n_lambda, int on_device) {
-  LFMM_REQUIRE(pl->n_sites > 0 || true, "");
   const size_t S = (size_t)pl->n_sites;
   if (S == 0) return;
   LFMM_REQUIRE(lambdas && n_lambda, "lambdas and n_lambda are required");
@@ -1649,7 +1650,7 @@ void upload_lambdas(lfmm_plan* pl, const double* lambdas, const int32_t* n_lambd
   LFMM_CUDA(cudaMemcpyAsync(pl->nlam.p, n_lambda, sizeof(int32_t) * S, kind, pl->stream));
 }
 
-void run_hi(lfmm_plan* pl, int mode, const double* pot_dev, const double* pot_site = nullptr) {
+void run_hi(lfmm_plan* pl, int mode, const double* pot_dev, const double* pot_site = nullptr, double* gram = nullptr) {
   if (pl->n_sites == 0) {
     LFMM_CUDA(cudaMemsetAsync(pl->offset_total.p, 0, sizeof(double), pl->stream));
     return;
@@ -1665,6 +1666,7 @@ void run_hi(lfmm_plan* pl, int mode, const double* pot_dev, const double* pot_si
   g.blend = pl->blend.as<double>();
   g.forces = pl->lam_forces.as<double>();
   g.offset = pl->offsets.as<double>();
+  g.gram = gram;
   if (mode == LFMM_MODE_HI && g.images_full && g.lat_t) {
     // lattice pair kernel inputs for all site atoms at once: R_t, U_t = T1 R_t
     const int na = (int)pl->n_site_atoms;
@@ -1680,11 +1682,8 @@ void run_hi(lfmm_plan* pl, int mode, const double* pot_dev, const double* pot_si
       ta.ops_t = g.lat_t;
       ta.src = g.rscratch;
       ta.dst = g.uscratch;
-      static bool attr_set = false;
-      if (!attr_set) {
-        tr_set_attrs<double>(g.ncp);
-        attr_set = true;
-      }
+      static std::once_flag attr_once;  // process-wide function attribute
+      std::call_once(attr_once, [&] { tr_set_attrs<double>(g.ncp); });
       pl->launch(ST_HI, [&] { tr_launch<double>(ta, na, 1, pl->stream); });
     } else {
       pl->launch(ST_HI, [&] {
@@ -2092,6 +2091,53 @@ int lfmm_hi(lfmm_plan* plan, const double* lambdas, const int32_t* n_lambda, int
     copy_out(plan, lambda_forces, plan->lam_forces, sizeof(double) * 4 * S, io_on_device);
     copy_out(plan, energy_offset, plan->offset_total, sizeof(double), io_on_device);
     if (!io_on_device) LFMM_CUDA(cudaStreamSynchronize(plan->stream));
+  });
+}
+
+int lfmm_lambda_baoab(lfmm_plan* plan, int64_t n_sites, double* lambdas, double* velocities, const int32_t* n_lambda,
+                      const double* masses, const double* f_engine, double* f_total, int stage, double dt,
+                      double coulomb, double bias_height, double c1, double noise, uint64_t seed, uint64_t step) {
+  if (!plan) return fail(Error{LFMM_EINVAL, "plan is NULL"});
+  return guarded([&] {
+    LFMM_REQUIRE(stage >= 0 && stage <= 2, "stage must be 0, 1 or 2");
+    LFMM_REQUIRE(n_sites >= 0 && n_sites < (1 << 28), "n_sites out of range");
+    if (n_sites == 0) return;
+    plan->launch(ST_HI, [&] {
+      k_lambda_baoab<<<nblk(4 * n_sites, 128), 128, 0, plan->stream>>>(
+          (int)n_sites, lambdas, velocities, n_lambda, masses, f_engine, f_total, stage, dt, coulomb, bias_height, c1,
+          noise, (unsigned long long)seed, (unsigned long long)step);
+    });
+  });
+}
+
+int lfmm_lambda_record(lfmm_plan* plan, int64_t n_sites, const int32_t* slot_offsets, const int32_t* n_lambda,
+                       const double* lambdas, const double* velocities, const double* f_total, const double* energy,
+                       double coulomb, int64_t n_slots, double* out_lambdas, double* out_velocities,
+                       double* out_forces, double* out_energies, int64_t sample) {
+  if (!plan) return fail(Error{LFMM_EINVAL, "plan is NULL"});
+  return guarded([&] {
+    LFMM_REQUIRE(n_sites >= 0 && sample >= 0, "bad sample");
+    plan->launch(ST_HI, [&] {
+      k_lambda_record<<<nblk(std::max<int64_t>(4 * n_sites, 1), 128), 128, 0, plan->stream>>>(
+          (int)n_sites, slot_offsets, n_lambda, lambdas, velocities, f_total, energy, coulomb, (int)n_slots,
+          out_lambdas, out_velocities, out_forces, out_energies, (int)sample);
+    });
+  });
+}
+
+int lfmm_site_gram(lfmm_plan* plan, const double* lambdas, const int32_t* n_lambda, const double* site_positions,
+                   double* gram) {
+  if (!plan) return fail(Error{LFMM_EINVAL, "plan is NULL"});
+  return guarded([&] {
+    LFMM_REQUIRE(gram != nullptr, "gram is NULL");
+    upload_lambdas(plan, lambdas, n_lambda, 0);
+    gather_site_positions(plan, site_positions, 0);
+    const size_t n = (size_t)plan->n_sites * HI_MAXF * HI_MAXF;
+    plan->gram.ensure(sizeof(double) * std::max<size_t>(n, 1));
+    LFMM_CUDA(cudaMemsetAsync(plan->gram.p, 0, sizeof(double) * std::max<size_t>(n, 1), plan->stream));
+    run_hi(plan, LFMM_MODE_HI, nullptr, nullptr, plan->gram.as<double>());
+    if (n) LFMM_CUDA(cudaMemcpyAsync(gram, plan->gram.p, sizeof(double) * n, cudaMemcpyDeviceToHost, plan->stream));
+    LFMM_CUDA(cudaStreamSynchronize(plan->stream));
   });
 }
 

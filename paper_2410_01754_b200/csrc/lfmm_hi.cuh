@@ -52,6 +52,7 @@ struct HiArgs {
   double* blend;       // S
   double* forces;      // S x 4
   double* offset;      // S
+  double* gram;        // optional: S x HI_MAXF x HI_MAXF, Q (K + G) Q^T (dynamics.py FrozenLambdaForceField)
 };
 
 __device__ inline double hi_weight(const double* lam, int nl, int rho) {
@@ -181,6 +182,22 @@ __global__ void __launch_bounds__(HI_THREADS) k_hi_site(HiArgs g) {
     }
   }
   __syncthreads();
+
+  // ---- optional form Gram B = Q (K + G) Q^T (dynamics.py:137-145) ----
+  if (g.gram && !qi) {
+    for (int e = tid; e < nf * nf; e += blockDim.x) {
+      const int r = e / nf, r2 = e % nf;
+      const double* Qa = Q + r * ns;
+      const double* Qb = Q + r2 * ns;
+      double acc = 0.0;
+      for (int j = 0; j < ns; ++j) {
+        double t = 0.0;  // (Q_r (K + G))_j
+        for (int i = 0; i < ns; ++i) t += Qa[i] * (KG[i * ns + j] + (lattice ? GG[i * ns + j] : 0.0));
+        acc += t * Qb[j];
+      }
+      g.gram[((size_t)s * HI_MAXF + r) * HI_MAXF + r2] = acc;
+    }
+  }
 
   // ---- per-form scalars (warp per form) ----
   const double gamma = 2.0 * 3.14159265358979323846 / (3.0 * L * L * L);

@@ -64,6 +64,10 @@ class LambdaState:
         self.velocities = [np.asarray(v, dtype=np.float64).copy() for v in self.velocities]
         self.masses = [float(m) for m in self.masses]
 
+    def copy(self):
+        return LambdaState(values=[v.copy() for v in self.values], velocities=[v.copy() for v in self.velocities],
+                           masses=list(self.masses))
+
     def fingerprint(self):
         return tuple(tuple(float(x) for x in v) for v in self.values)
 
