@@ -429,6 +429,11 @@ def run_ours(args):
     t_plain = timed(lambda: step_dev(plain=True), args.steps)
     ms_full = max_over_ranks(sum(t_full) / len(t_full))
     ms_plain = max_over_ranks(sum(t_plain) / len(t_plain))
+    # plan reuse: tree frozen (positions not passed), as PeriodicSolver
+    # holds one set of positions (solver.py:328-343)
+    t_reuse = timed(lambda: plan.step(None, d_q, d_lam, d_nl, mode=_native.MODE_HI, plain=False, on_device=True,
+                                      energy=d_e, forces=d_f, lambda_forces=d_lf), args.steps)
+    ms_reuse = max_over_ranks(sum(t_reuse) / len(t_reuse))
 
     # e2e through the C-ABI with pinned host buffers
     h_pos = torch.from_numpy(np.ascontiguousarray(system.positions)).pin_memory()
@@ -532,6 +537,7 @@ def run_ours(args):
                    "l2": "flushed between timed steps (256 MiB write)"},
         "hi_overhead_pct": round(100.0 * (ms_full / ms_plain - 1.0), 2),
         "plain_fmm_ms_per_step": round(ms_plain, 4),
+        "plan_reuse_ms_per_step": round(ms_reuse, 4),
         "e2e": {"value": round(world * 1000.0 / ms_e2e, 3), "unit": "steps/s", "h2d_bytes_per_step": h2d,
                 "d2h_bytes_per_step": d2h, "ms_per_step": round(ms_e2e, 4)},
         "gpu_launches": launches,
