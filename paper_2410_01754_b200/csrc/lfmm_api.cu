@@ -1187,7 +1187,7 @@ struct lfmm_plan {
           ha.mult, ha, hm_level_max.as<unsigned int>());
     });
     launch(ST_PACK, [&] {
-      k_pack_mult16<<<dim3((unsigned)((hm_plane_rows(l1) + 127) / 128), nl, 8), 128, 0, st>>>(ha);
+      k_pack_mult16<<<dim3((unsigned)((8 * hm_plane_rows(l1) + 255) / 256), nl, 8), 256, 0, st>>>(ha);
     });
     launch(ST_DOWN, [&] { k_m2l_halo<<<njobs, HM_THREADS, hm_smem_bytes(hm_rw_cap), st>>>(ha); });
   }
@@ -1396,7 +1396,7 @@ struct lfmm_plan {
                            stream>>>(ha.mult, ha, hm_level_max.as<unsigned int>());
         });
         launch(ST_PACK, [&] {
-          k_pack_mult16<<<dim3((unsigned)((hm_plane_rows(depth) + 127) / 128), depth, 8), 128, 0, stream>>>(ha);
+          k_pack_mult16<<<dim3((unsigned)((8 * hm_plane_rows(depth) + 255) / 256), depth, 8), 256, 0, stream>>>(ha);
         });
         launch(ST_DOWN, [&] {
           k_m2l_halo<<<hm_njobs, HM_THREADS, hm_smem_bytes(hm_rw_cap), stream>>>(ha);

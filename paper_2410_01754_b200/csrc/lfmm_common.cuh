@@ -182,12 +182,29 @@ __device__ __forceinline__ void regular_stream(T x, T y, T z, int p, F&& f) {
 // reciprocals become immediates, and f sees constant (m, l) — used by the
 // P2M/L2P kernels for the orders the benchmarks run.
 template <class T, int P, class F>
-__device__ __forceinline__ void regular_stream_c(T x, T y, T z, F&& f) {
+__device__ __forceinline__ void regular_stream_c(T x, T y, T z, F&& f, T seed = T(1)) {
+  // seed scales every term (the recurrences are homogeneous): P2M passes q
   const T r2 = x * x + y * y + z * z;
-  T mr = T(1), mi = T(0);
+  T mr = seed, mi = T(0);
 #pragma unroll
   for (int m = 0; m <= P; ++m) {
-    if (m > 0) {
+    if (m == 0) {  // real column: no imaginary recurrence
+      f(0, 0, mr, T(0));
+      if (P >= 1) {
+        T p2 = mr, p1 = z * mr;
+        f(0, 1, p1, T(0));
+#pragma unroll
+        for (int l = 2; l <= P; ++l) {
+          const T c = T(1) / T(l * l);
+          const T nr = (T(2 * l - 1) * z * p1 - r2 * p2) * c;
+          p2 = p1;
+          p1 = nr;
+          f(0, l, nr, T(0));
+        }
+      }
+      continue;
+    }
+    {
       const T c = T(1) / T(2 * m);
       const T nr = (mr * x - mi * y) * c;
       const T ni = (mr * y + mi * x) * c;

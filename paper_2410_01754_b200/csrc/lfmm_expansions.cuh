@@ -84,14 +84,15 @@ __global__ void __launch_bounds__(EXP_WARPS * 32) k_p2m_c(const vec4_t<T>* __res
                                                           T inv_size, int ncp, T* __restrict__ mult) {
   constexpr int NC = (P + 1) * (P + 1);
   constexpr int NF = (NC + 31) / 32;  // flushes of 32 coefficients
-  __shared__ T buf[EXP_WARPS][32][33];
+  constexpr int TBS = sizeof(T) == 4 ? 36 : 33;  // row stride: 16-B rows (LDS.128) for fp32
+  __shared__ __align__(16) T buf[EXP_WARPS][32][TBS];
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   const int b = blockIdx.x * EXP_WARPS + w;
   const int nleaf = 1 << (3 * depth);
   if (b >= nleaf) return;
   T* out = mult + (size_t)b * ncp;
   const int t0 = leaf_start[b], t1 = leaf_start[b + 1];
-  T(*tb)[33] = buf[w];
+  T(*tb)[TBS] = buf[w];
   T acc[NF];
 #pragma unroll
   for (int f = 0; f < NF; ++f) acc[f] = T(0);
@@ -109,21 +110,35 @@ __global__ void __launch_bounds__(EXP_WARPS * 32) k_p2m_c(const vec4_t<T>* __res
     auto flush = [&]() {
       __syncwarp();
       T s = T(0);
+      if constexpr (sizeof(T) == 4) {
+#pragma unroll
+        for (int k = 0; k < 32; k += 4) {
+          const float4 v = *reinterpret_cast<const float4*>(&tb[lane][k]);
+          s += v.x;
+          s += v.y;
+          s += v.z;
+          s += v.w;
+        }
+      } else {
 #pragma unroll 8
-      for (int k = 0; k < 32; ++k) s += tb[lane][k];
+        for (int k = 0; k < 32; ++k) s += tb[lane][k];
+      }
       if (lane < col) acc[fl] += s;
       __syncwarp();
       ++fl;
       col = 0;
     };
-    regular_stream_c<T, P>(x, y, z, [&](int m, int l, T re, T im) {
-      tb[col][lane] = q * re;
-      if (++col == 32) flush();
-      if (m > 0) {
-        tb[col][lane] = q * im;
-        if (++col == 32) flush();
-      }
-    });
+    regular_stream_c<T, P>(
+        x, y, z,
+        [&](int m, int l, T re, T im) {
+          tb[col][lane] = re;
+          if (++col == 32) flush();
+          if (m > 0) {
+            tb[col][lane] = im;
+            if (++col == 32) flush();
+          }
+        },
+        q);
     if (col > 0) flush();
   }
 #pragma unroll

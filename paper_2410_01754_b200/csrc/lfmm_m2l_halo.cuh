@@ -182,48 +182,51 @@ __host__ __device__ inline int hm_plane_rows(int level) {
 
 // multipoles -> fp16 planes: thread per (level, source class, padded row)
 __global__ void k_pack_mult16(HaloArgs g) {
+  // thread per (padded row, 16-coefficient chunk kc): 8 threads read one
+  // box's 512 B contiguously, every plane store is a coalesced row run
   const int level = blockIdx.y + g.lvl0, sc = blockIdx.z;
   const int prow = hm_plane_rows(level);
-  const int r = blockIdx.x * blockDim.x + threadIdx.x;
+  const int t = blockIdx.x * blockDim.x + threadIdx.x;
+  const int r = t >> 3, kc = t & 7;
   if (r >= prow) return;
   const int h = 1 << (level - 1), Z = h + 2, YZ = Z * Z;
   const int x = ((r / YZ - 1) + h) & (h - 1), y = (((r / Z) % Z - 1) + h) & (h - 1), z = ((r % Z - 1) + h) & (h - 1);
   const int box = ((((2 * x + ((sc >> 2) & 1)) << level) | (2 * y + ((sc >> 1) & 1))) << level) |
                   (2 * z + (sc & 1));
   const float gl = hm_level_scale(g.level_max, level);
-  const float4* src = reinterpret_cast<const float4*>(g.mult + (g.level_off[level] + box) * 128);
-  const float4* icv = reinterpret_cast<const float4*>(g.inv_c);
+  const float4* src = reinterpret_cast<const float4*>(g.mult + (g.level_off[level] + box) * 128) + kc * 4;
+  const float4* icv = reinterpret_cast<const float4*>(g.inv_c) + kc * 4;
   unsigned char* base = g.mult16 + g.m16_off[level];
-#pragma unroll 2
-  for (int kc = 0; kc < HM_NKC; ++kc) {
-    uint4 hv[2], lv[2];
+  float4 v[4];
+#pragma unroll
+  for (int u = 0; u < 4; ++u) v[u] = __ldg(src + u);
+  uint4 hv[2], lv[2];
+#pragma unroll
+  for (int kg = 0; kg < 2; ++kg) {
+    float a[8];
+#pragma unroll
+    for (int u = 0; u < 2; ++u) {
+      const float4 w = v[kg * 2 + u];
+      const float4 c = icv[kg * 2 + u];
+      a[4 * u] = w.x * c.x * gl;
+      a[4 * u + 1] = w.y * c.y * gl;
+      a[4 * u + 2] = w.z * c.z * gl;
+      a[4 * u + 3] = w.w * c.w * gl;
+    }
+    float hf[8];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) hf[j] = __half2float(__float2half_rn(a[j]));
+    hv[kg] = make_uint4(pack_h2(hf[0], hf[1]), pack_h2(hf[2], hf[3]), pack_h2(hf[4], hf[5]), pack_h2(hf[6], hf[7]));
+    lv[kg] = make_uint4(pack_h2(a[0] - hf[0], a[1] - hf[1]), pack_h2(a[2] - hf[2], a[3] - hf[3]),
+                        pack_h2(a[4] - hf[4], a[5] - hf[5]), pack_h2(a[6] - hf[6], a[7] - hf[7]));
+  }
+#pragma unroll
+  for (int part = 0; part < 2; ++part)
 #pragma unroll
     for (int kg = 0; kg < 2; ++kg) {
-      float a[8];
-#pragma unroll
-      for (int u = 0; u < 2; ++u) {
-        const float4 v = __ldg(src + kc * 4 + kg * 2 + u);
-        const float4 c = icv[kc * 4 + kg * 2 + u];
-        a[4 * u] = v.x * c.x * gl;
-        a[4 * u + 1] = v.y * c.y * gl;
-        a[4 * u + 2] = v.z * c.z * gl;
-        a[4 * u + 3] = v.w * c.w * gl;
-      }
-      float hf[8];
-#pragma unroll
-      for (int j = 0; j < 8; ++j) hf[j] = __half2float(__float2half_rn(a[j]));
-      hv[kg] = make_uint4(pack_h2(hf[0], hf[1]), pack_h2(hf[2], hf[3]), pack_h2(hf[4], hf[5]), pack_h2(hf[6], hf[7]));
-      lv[kg] = make_uint4(pack_h2(a[0] - hf[0], a[1] - hf[1]), pack_h2(a[2] - hf[2], a[3] - hf[3]),
-                          pack_h2(a[4] - hf[4], a[5] - hf[5]), pack_h2(a[6] - hf[6], a[7] - hf[7]));
+      const size_t plane = (((size_t)sc * HM_NKC + kc) * 2 + part) * 2 + kg;
+      *reinterpret_cast<uint4*>(base + (plane * prow + r) * 16) = part == 0 ? hv[kg] : lv[kg];
     }
-#pragma unroll
-    for (int part = 0; part < 2; ++part)
-#pragma unroll
-      for (int kg = 0; kg < 2; ++kg) {
-        const size_t plane = (((size_t)sc * HM_NKC + kc) * 2 + part) * 2 + kg;
-        *reinterpret_cast<uint4*>(base + (plane * prow + r) * 16) = part == 0 ? hv[kg] : lv[kg];
-      }
-  }
 }
 
 #ifdef LFMM_HM_PROF
