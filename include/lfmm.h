@@ -223,8 +223,10 @@ int lfmm_dist_phase(lfmm_plan* plan, int phase, const double* positions, const d
  * ncp per box), [1] scal (D_x, D_y, D_z, Q fp64), [2] energies (total, near,
  * far, dipole), [3] forces (N x 3 local input order), [4] site-atom
  * potentials, [5] lambda forces (S x 4), [6] HI energy offset, [7] the plan's
-
- * cudaStream_t.  level_off (8 entries): first box of each level. */
+ * cudaStream_t, [8] per-level max |M/c| of the fp16 tensor-core M2L (uint32
+ * float bits, DMAX + 2 entries; after phase 1 it holds this rank's slab of the
+ * levels >= lg, which the caller max-reduces across ranks before phase 2).
+ * ptrs holds 9 entries; level_off (8 entries): first box of each level. */
 int lfmm_dist_buffers(lfmm_plan* plan, void** ptrs, int64_t* level_off);
 
 /* HI corrections + lambda forces for every site from the gathered site-atom

@@ -318,7 +318,7 @@ class Plan:
                                     1 if grad else 0))
 
     def dist_buffers(self):
-        ptrs = (ctypes.c_void_p * 8)()
+        ptrs = (ctypes.c_void_p * 9)()
         offs = np.zeros(8, np.int64)
         check(lib().lfmm_dist_buffers(self.h, ptrs, ptr(offs)))
         return [p if p is not None else 0 for p in ptrs], offs

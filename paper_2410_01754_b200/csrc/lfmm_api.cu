@@ -1349,7 +1349,29 @@ struct lfmm_plan {
                                                              counters.as<int>() + 2, 0);
     });
     }
-    if (dist_phase == 1) return;  // owned multipoles ready for the all-gather
+    if (dist_phase == 1) {
+      // owned multipoles ready for the exchange; the fp16 M2L's per-level
+      // scale needs max |M| over the whole level, so each rank reduces its
+      // own slab of the levels >= dist_lg here and the caller max-reduces
+      // them across ranks (lfmm_dist_buffers [8])
+      if (use_halo && sizeof(T) == 4 && dist_lg >= 1) {
+        HaloArgs ha{};
+        ha.inv_c = hm_inv_c.as<float>();
+        for (int l = 0; l <= depth; ++l) ha.level_off[l] = level_off[l];
+        const int l0 = std::max(dist_lg, 1);
+        ha.lvl0 = l0;
+        ha.own_x0 = own_x0;
+        ha.own_x1 = own_x1;
+        ha.own_depth = depth;
+        LFMM_CUDA(cudaMemsetAsync(hm_level_max.p, 0, hm_level_max.bytes, stream));
+        const int64_t nown = (int64_t)(own_x1 - own_x0) << (2 * depth);
+        launch(ST_PACK, [&] {
+          k_level_absmax<<<dim3((unsigned)std::max<int64_t>(1, (nown + 63) / 64), depth - l0 + 1), 256, 0, stream>>>(
+              reinterpret_cast<const float*>(mult.p), ha, hm_level_max.as<unsigned int>());
+        });
+      }
+      return;
+    }
     }  // up
     if (far_done) {
       // lattice, M2L and L2L already issued by far_overlapped()
@@ -1390,11 +1412,22 @@ struct lfmm_plan {
           ha.part_off[l] = part_off[l];
           ha.m16_off[l] = m16_off[l];
         }
-        LFMM_CUDA(cudaMemsetAsync(hm_level_max.p, 0, hm_level_max.bytes, stream));
-        launch(ST_PACK, [&] {
-          k_level_absmax<<<dim3((unsigned)std::max<int64_t>(1, ((1LL << (3 * depth)) + 63) / 64), depth), 256, 0,
-                           stream>>>(ha.mult, ha, hm_level_max.as<unsigned int>());
-        });
+        if (dist_phase == 2 && dist_lg >= 1) {
+          // levels >= dist_lg: max-reduced across ranks by the caller after
+          // phase 1; the shared levels below are complete on every rank
+          LFMM_CUDA(cudaMemsetAsync(hm_level_max.p, 0, sizeof(unsigned int) * dist_lg, stream));
+          if (dist_lg >= 2)
+            launch(ST_PACK, [&] {
+              k_level_absmax<<<dim3((unsigned)std::max<int64_t>(1, ((1LL << (3 * (dist_lg - 1))) + 63) / 64),
+                                    dist_lg - 1), 256, 0, stream>>>(ha.mult, ha, hm_level_max.as<unsigned int>());
+            });
+        } else {
+          LFMM_CUDA(cudaMemsetAsync(hm_level_max.p, 0, hm_level_max.bytes, stream));
+          launch(ST_PACK, [&] {
+            k_level_absmax<<<dim3((unsigned)std::max<int64_t>(1, ((1LL << (3 * depth)) + 63) / 64), depth), 256, 0,
+                             stream>>>(ha.mult, ha, hm_level_max.as<unsigned int>());
+          });
+        }
         launch(ST_PACK, [&] {
           k_pack_mult16<<<dim3((unsigned)((8 * hm_plane_rows(depth) + 255) / 256), depth, 8), 256, 0, stream>>>(ha);
         });
@@ -2447,7 +2480,9 @@ int lfmm_dist_phase(lfmm_plan* plan, int phase, const double* positions, const d
 // [0] multipoles (all levels, ncp per box, T), [1] scal (D_x, D_y, D_z, Q as
 // fp64), [2] energies (total, near, far, dipole), [3] forces (N x 3, local
 // input order), [4] site-atom potentials, [5] lambda forces (S x 4),
-// [6] HI energy offset (1), [7] stream; level_off[l] = first box of level l
+// [6] HI energy offset (1), [7] stream, [8] per-level max |M^/c| of the fp16
+// M2L (uint32 float bits, DMAX + 2 entries; NULL unless the fp32 tensor-core
+// M2L runs); level_off[l] = first box of level l
 int lfmm_dist_buffers(lfmm_plan* plan, void** ptrs, int64_t* level_off) {
   if (!plan) return fail(Error{LFMM_EINVAL, "plan is NULL"});
   return guarded([&] {
@@ -2459,6 +2494,7 @@ int lfmm_dist_buffers(lfmm_plan* plan, void** ptrs, int64_t* level_off) {
     ptrs[5] = plan->lam_forces.p;
     ptrs[6] = plan->offset_total.p;
     ptrs[7] = reinterpret_cast<void*>(plan->stream);
+    ptrs[8] = plan->hm_level_max.p;
     for (int l = 0; l <= DMAX + 1; ++l) level_off[l] = l <= plan->depth + 1 ? plan->level_off[l] : 0;
   });
 }

@@ -77,6 +77,7 @@ struct HaloArgs {
   int64_t part_off[DMAX + 2];
   int rw_cap;                        // rows per window the buffers were sized for
   int lvl0;                          // first level of a k_level_absmax / k_pack_mult16 launch (grid.y = levels)
+  int own_x0, own_x1, own_depth;     // k_level_absmax over one rank's leaf x-slab (own_x1 == 0: whole level)
 };
 
 __host__ __device__ inline int hm_rw(int N, int Z) { return N + 2 * Z + 2; }
@@ -149,7 +150,13 @@ __global__ void k_level_absmax(const float* __restrict__ mult, HaloArgs g, unsig
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const float4 ic = reinterpret_cast<const float4*>(g.inv_c)[lane];
   float m = 0.f;
-  for (int b = blockIdx.x * 64 + warp; b < min(nbox, (int)blockIdx.x * 64 + 64); b += 8) {
+  int b0 = 0, b1 = nbox;
+  if (g.own_x1 > 0) {  // slab decomposition: the boxes of x-planes [x0, x1) at this level are contiguous
+    const int sh = g.own_depth - level;
+    b0 = (g.own_x0 >> sh) << (2 * level);
+    b1 = (g.own_x1 >> sh) << (2 * level);
+  }
+  for (int b = b0 + blockIdx.x * 64 + warp; b < min(b1, b0 + (int)blockIdx.x * 64 + 64); b += 8) {
     const float4 v = reinterpret_cast<const float4*>(mult + (g.level_off[level] + b) * 128)[lane];
     m = fmaxf(m, fmaxf(fmaxf(fabsf(v.x * ic.x), fabsf(v.y * ic.y)), fmaxf(fabsf(v.z * ic.z), fabsf(v.w * ic.w))));
   }

@@ -43,6 +43,8 @@ from . import _native
 from .fmm.solver import SolverConfig
 
 _DEBUG = os.environ.get('LFMM_DIST_DEBUG') == '1'
+_POISON = os.environ.get('LFMM_DIST_POISON') == '1'
+HALO_PLANES = 2  # multipole halo width (x-planes) of the M2L sources at levels > lg
 
 # --------------------------------------------------------------- layout ----
 
@@ -92,6 +94,33 @@ def select_local(lx, x0, x1, depth, xp=np):
 # ------------------------------------------------------------ collectives ----
 
 
+def _halo_ops(rank, world, x0, x1, n, width=2):
+    """The point-to-point operations of one rank's halo-plane exchange, as
+    (kind, peer, first plane).  The owned slab [x0, x1) of n periodic planes
+    needs planes x0-width .. x0-1 (the left neighbour's last planes) and
+    x1 .. x1+width-1 (the right neighbour's first planes).  Per peer the
+    sends and receives are listed in matching order: a rank sends its last
+    planes before its first, and receives its left halo before its right
+    (with 2 ranks both neighbours are the same peer)."""
+    if x1 - x0 < width:
+        raise ValueError(f"slab of {x1 - x0} planes is thinner than the halo width {width}")
+    left, right = (rank - 1) % world, (rank + 1) % world
+    return [("send", right, x1 - width), ("send", left, x0),
+            ("recv", left, (x0 - width) % n), ("recv", right, x1 % n)]
+
+
+def halo_planes(x0, x1, n, width=2):
+    """Plane indices a slab's halo exchange fills (periodic)."""
+    return sorted({(x0 - k) % n for k in range(1, width + 1)} | {(x1 + k) % n for k in range(width)})
+
+
+def torch_empty_like_cpu(t):
+    import torch
+
+    return torch.empty(t.shape, dtype=t.dtype)
+
+
+
 class TorchComm:
     """torch.distributed group; deterministic sums (all-gather + rank order)."""
 
@@ -116,6 +145,42 @@ class TorchComm:
             out.copy_(host)
         else:
             self.dist.all_gather_into_tensor(out, mine, group=self.group)
+
+    def halo_(self, out, plane_numel, x0, x1, n, width=2):
+        """In place: out holds the n x-planes of one level (plane_numel
+        elements each), this rank's planes [x0, x1) filled.  Receives the
+        `width` planes either side of the slab (periodic) from the neighbour
+        ranks, which own them, and sends this rank's first / last `width`
+        planes to the left / right neighbour.  Requires x1 - x0 >= width."""
+        dist = self.dist
+        ops = []
+        for kind, peer, a in _halo_ops(self.rank, self.world, x0, x1, n, width):
+            seg = out[a * plane_numel:(a + width) * plane_numel]
+            ops.append((kind, peer, seg))
+        if self._staged(out):
+            host = [(k, pr, seg.cpu() if k == "send" else torch_empty_like_cpu(seg)) for k, pr, seg in ops]
+            reqs = dist.batch_isend_irecv([dist.P2POp(dist.isend if k == "send" else dist.irecv, h, pr, self.group)
+                                           for k, pr, h in host])
+            for r in reqs:
+                r.wait()
+            for (k, _, seg), (_, _, h) in zip(ops, host):
+                if k == "recv":
+                    seg.copy_(h)
+        else:
+            reqs = dist.batch_isend_irecv([dist.P2POp(dist.isend if k == "send" else dist.irecv, seg, pr, self.group)
+                                           for k, pr, seg in ops])
+            for r in reqs:
+                r.wait()
+
+    def max_(self, t):
+        """In place: elementwise max of t over ranks (exact in any order)."""
+        import torch
+
+        buf = torch.empty((self.world,) + tuple(t.shape), dtype=t.dtype, device=t.device)
+        n = t.numel()
+        buf.reshape(-1)[self.rank * n:(self.rank + 1) * n].copy_(t.reshape(-1))
+        self.allgather_(buf.reshape(-1), n)
+        t.copy_(buf.amax(0))
 
     def sum_ordered(self, t):
         """Sum of every rank's t, added in rank order (bit-reproducible)."""
@@ -161,6 +226,32 @@ class _LocalRankComm:
                 out[r * chunk_numel:(r + 1) * chunk_numel].copy_(self.shared.slots[r])
         torch.cuda.current_stream().synchronize()
         self.shared.barrier.wait()
+
+    def halo_(self, out, plane_numel, x0, x1, n, width=2):
+        import torch
+
+        torch.cuda.current_stream().synchronize()
+        self.shared.slots[self.rank] = out
+        self.shared.barrier.wait()
+        for kind, peer, a in _halo_ops(self.rank, self.world, x0, x1, n, width):
+            if kind == "recv":
+                out[a * plane_numel:(a + width) * plane_numel].copy_(
+                    self.shared.slots[peer][a * plane_numel:(a + width) * plane_numel])
+        torch.cuda.current_stream().synchronize()
+        self.shared.barrier.wait()
+
+    def max_(self, t):
+        import torch
+
+        torch.cuda.current_stream().synchronize()
+        self.shared.slots[self.rank] = t.clone()
+        self.shared.barrier.wait()
+        acc = self.shared.slots[0].clone()
+        for r in range(1, self.world):
+            acc = torch.maximum(acc, self.shared.slots[r])
+        torch.cuda.current_stream().synchronize()
+        self.shared.barrier.wait()
+        t.copy_(acc)
 
     def sum_ordered(self, t):
         import torch
@@ -274,10 +365,25 @@ class DistributedSolver:
         # ---- exchange 1: owned multipoles of levels >= lg, dipole / charge ----
         ncp = self._ncp()
         tdt = "<f4" if self.tsize == 4 else "<f8"
-        for lvl in range(self.lg, d + 1):
+        for lvl in range(self.lg, d + 1) if self.world > 1 else ():
             nbox = 1 << (3 * lvl)
             view = _device_view(ptrs[0] + int(loff[lvl]) * ncp * self.tsize, (nbox * ncp,), tdt, torch)
-            self.comm.allgather_(view, nbox * ncp // self.world)
+            n_l, sh = 1 << lvl, d - lvl
+            x0, x1 = self.x0 >> sh, self.x1 >> sh
+            if lvl > self.lg and n_l - (x1 - x0) > 2 * HALO_PLANES:
+                # M2L sources of the owned targets (children of the parents'
+                # neighbours) lie within 2 planes of the slab: halo only
+                self.comm.halo_(view, ncp << (2 * lvl), x0, x1, n_l, HALO_PLANES)
+            else:
+                # level lg (feeds the shared levels' M2M) or a halo that
+                # covers every other rank's slab
+                self.comm.allgather_(view, nbox * ncp // self.world)
+        if ptrs[8] and self.world > 1:
+            # fp16 M2L level scales: max over every rank's slab (exact)
+            lmax = _device_view(ptrs[8], (d + 1,), "<i4", torch)
+            self.comm.max_(lmax)
+        if _POISON:
+            self._poison(ptrs, loff, ncp, tdt)
         scal = _device_view(ptrs[1], (4,), "<f8", torch)
         scal.copy_(self.comm.sum_ordered(scal.clone()))
         plan.dist_phase(2, grad=True)
@@ -304,6 +410,23 @@ class DistributedSolver:
         else:
             out["energy"] = e_solve
         return out
+
+    def _poison(self, ptrs, loff, ncp, tdt):
+        """Test hook (LFMM_DIST_POISON=1): NaN into every multipole plane the
+        exchange did not fill, so a read outside the halo shows up in the
+        results."""
+        torch = self.torch
+        d = self.cfg.depth
+        for lvl in range(self.lg + 1, d + 1):
+            n_l, sh = 1 << lvl, d - lvl
+            x0, x1 = self.x0 >> sh, self.x1 >> sh
+            if n_l - (x1 - x0) <= 2 * HALO_PLANES:
+                continue
+            keep = set(range(x0, x1)) | set(halo_planes(x0, x1, n_l, HALO_PLANES))
+            view = _device_view(ptrs[0] + int(loff[lvl]) * ncp * self.tsize, (n_l, (ncp << (2 * lvl))), tdt, torch)
+            for x in range(n_l):
+                if x not in keep:
+                    view[x].fill_(float("nan"))
 
     def _ncp(self):
         nc = (self.cfg.p + 1) ** 2

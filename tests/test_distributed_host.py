@@ -10,7 +10,8 @@ import torch
 import torch.distributed as dist
 import torch.multiprocessing as mp
 
-from paper_2410_01754_b200.distributed import TorchComm, leaf_x, select_local, slab_partition, wrap
+from paper_2410_01754_b200.distributed import (TorchComm, _halo_ops, halo_planes, leaf_x, select_local,
+                                               slab_partition, wrap)
 
 
 @pytest.mark.parametrize("depth,world", [(3, 1), (3, 2), (4, 4), (4, 8), (5, 8), (1, 2)])
@@ -99,3 +100,76 @@ def test_torch_comm_gloo_world2():
     assert res[0][1].tobytes() == res[1][1].tobytes()
     ref = np.array([0.1, 1e16, -1e16]) + np.array([0.2, 1e16, -1e16 + 1])
     assert np.allclose(res[0][1], ref)
+
+
+@pytest.mark.parametrize("depth,world,level", [(4, 2, 4), (4, 4, 3), (4, 8, 4), (5, 8, 5), (6, 4, 6)])
+def test_halo_ops_deliver_every_m2l_source_plane(depth, world, level):
+    """The planes each rank receives are exactly the M2L source planes of its
+    owned targets outside its slab (children of the parents' neighbours:
+    x in [2(px-1), 2(px+1)+1], octree.py:96-111), and every receive is
+    matched by the owning neighbour's send, in order, per peer."""
+    lg, ranges = slab_partition(depth, world)
+    n = 1 << level
+    sh = depth - level
+    sends, recvs = {}, {}
+    for r, (a, b) in enumerate(ranges):
+        x0, x1 = a >> sh, b >> sh
+        need = set()
+        for x in range(x0, x1):
+            px = x // 2
+            need |= {(2 * (px + dp) + c) % n for dp in (-1, 0, 1) for c in (0, 1)}
+        need -= set(range(x0, x1))
+        assert set(halo_planes(x0, x1, n)) == need
+        for kind, peer, first in _halo_ops(r, world, x0, x1, n):
+            if kind == "send":
+                sends.setdefault((r, peer), []).append(first)
+            else:
+                pa, pb = ranges[peer]
+                assert pa >> sh <= first and first + 2 <= pb >> sh, "received planes are owned by the peer"
+                recvs.setdefault((peer, r), []).append(first)
+    assert sends == recvs
+
+
+def _halo_worker(rank, world, port, out_q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        comm = TorchComm()
+        n, plane = 16, 5
+        w = n // world
+        x0, x1 = rank * w, (rank + 1) * w
+        buf = torch.full((n * plane,), -1.0, dtype=torch.float64)
+        for x in range(x0, x1):
+            buf[x * plane:(x + 1) * plane] = 100.0 * x + torch.arange(plane, dtype=torch.float64)
+        comm.halo_(buf, plane, x0, x1, n)
+        m = torch.tensor([rank, 10 - rank, 7], dtype=torch.int32)
+        comm.max_(m)
+        out_q.put((rank, buf.numpy().copy(), m.numpy().copy()))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 4])
+def test_torch_comm_halo_gloo(world):
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = 30500 + world + (os.getpid() % 1000)
+    procs = [ctx.Process(target=_halo_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = dict((r, (b, m)) for r, b, m in [q.get(timeout=120) for _ in procs])
+    for p in procs:
+        p.join(timeout=60)
+    n, plane = 16, 5
+    w = n // world
+    for r in range(world):
+        x0, x1 = r * w, (r + 1) * w
+        filled = set(range(x0, x1)) | set(halo_planes(x0, x1, n))
+        buf = res[r][0].reshape(n, plane)
+        for x in range(n):
+            if x in filled:
+                assert np.array_equal(buf[x], 100.0 * x + np.arange(plane))
+            else:
+                assert np.all(buf[x] == -1.0)
+        assert list(res[r][1]) == [world - 1, 10, 7]

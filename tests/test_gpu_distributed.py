@@ -97,3 +97,24 @@ def test_slab_decomposition_matches_single_gpu(wb, precision, world):
     assert relerr(fd, f1) <= tol
     for o in outs:
         assert relerr(o["lambda_forces"].cpu().numpy(), lf1) <= tol
+
+
+@pytest.mark.parametrize("precision", ["single", "double"])
+@pytest.mark.parametrize("world", [2, 4, 8])
+def test_multipole_halo_exchange_reads_only_the_halo(wb, precision, world, monkeypatch):
+    """Levels above lg exchange only the 2-plane multipole halo: every plane
+    the exchange did not fill is set to NaN before phase 2, and the step
+    still reproduces the single-GPU forces and lambda forces."""
+    from paper_2410_01754_b200 import distributed
+
+    monkeypatch.setattr(distributed, "_POISON", True)
+    system, lam = wb
+    cfg = SolverConfig(p=10, depth=4, precision=precision)
+    e1, f1, lf1 = _single(system, lam.values, cfg)
+    outs, fd = _distributed(system, lam.values, cfg, world)
+    tol = 1e-10 if precision == "double" else 1e-6
+    assert np.all(np.isfinite(fd))
+    assert abs(outs[0]["energy"] - e1) <= tol * abs(e1)
+    assert relerr(fd, f1) <= tol
+    for o in outs:
+        assert relerr(o["lambda_forces"].cpu().numpy(), lf1) <= tol
