@@ -218,24 +218,30 @@ def run_distributed(args):
     tables = site_tables(system)
     lam, nl = lambda_table(system, lam_state.values)
     s = len(system.sites)
-    d_pos = torch.from_numpy(np.ascontiguousarray(system.positions)).to(dev)
-    d_q = torch.from_numpy(np.ascontiguousarray(system.charges)).to(dev)
+    # each rank holds only the atoms of its own slab (global ids); the
+    # boundary planes come from the neighbour ranks every step
+    from paper_2410_01754_b200.distributed import leaf_x, wrap
+
+    lx = leaf_x(wrap(system.positions, system.box_length), system.box_length, depth)
+    own = np.flatnonzero((lx >= solver.x0) & (lx < solver.x1))
+    d_pos = torch.from_numpy(np.ascontiguousarray(system.positions[own])).to(dev)
+    d_q = torch.from_numpy(np.ascontiguousarray(system.charges[own])).to(dev)
+    d_gid = torch.from_numpy(own.astype(np.int64)).to(dev)
     d_lam = torch.from_numpy(lam).to(dev)
     d_nl = torch.from_numpy(nl).to(dev)
-    d_site_idx = torch.from_numpy(tables[1]).to(dev)
     flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)
 
     def step_dev(plain=False):
         if plain:
-            return solver.step(d_pos, d_qt)
-        return solver.step(d_pos, d_q, d_lam, d_nl, sites=tables, site_positions=d_pos[d_site_idx])
+            return solver.step_owned(d_pos, d_qt, d_gid)
+        return solver.step_owned(d_pos, d_q, d_gid, d_lam, d_nl, sites=tables, n_global=n)
 
     # plain FMM: the same blended charges, no lambda machinery
     from paper_2410_01754_b200.system import scale_charges
     from paper_2410_01754_b200.weights import expand_weights
 
     qt = scale_charges(system, [expand_weights(np.asarray(v).reshape(-1)) for v in lam_state.values])
-    d_qt = torch.from_numpy(np.ascontiguousarray(qt)).to(dev)
+    d_qt = torch.from_numpy(np.ascontiguousarray(qt[own])).to(dev)
     out = step_dev()  # builds the plan
 
     def timed(fn, k):
@@ -273,8 +279,8 @@ def run_distributed(args):
     ms_plain = max_over_ranks(sum(t_plain) / len(t_plain))
 
     # e2e: host inputs copied to the device every step, owned forces and lambda forces back
-    h_pos = torch.from_numpy(np.ascontiguousarray(system.positions)).pin_memory()
-    h_q = torch.from_numpy(np.ascontiguousarray(system.charges)).pin_memory()
+    h_pos = torch.from_numpy(np.ascontiguousarray(system.positions[own])).pin_memory()
+    h_q = torch.from_numpy(np.ascontiguousarray(system.charges[own])).pin_memory()
 
     def step_host():
         d_pos.copy_(h_pos, non_blocking=True)
@@ -291,7 +297,7 @@ def run_distributed(args):
     clk.__exit__(None, None, None)
     ms_e2e = max_over_ranks(sum(t_e2e) / len(t_e2e))
     n_own = int(out["owned"].numel())
-    h2d = n * 3 * 8 + n * 8
+    h2d = len(own) * 3 * 8 + len(own) * 8
     d2h = n_own * 3 * 8 + s * 4 * 8
 
     solver.plan.profile(True)
@@ -436,8 +442,8 @@ def run_ours(args):
     ms_reuse = max_over_ranks(sum(t_reuse) / len(t_reuse))
 
     # e2e through the C-ABI with pinned host buffers
-    h_pos = torch.from_numpy(np.ascontiguousarray(system.positions)).pin_memory()
-    h_q = torch.from_numpy(np.ascontiguousarray(system.charges)).pin_memory()
+    h_pos = torch.from_numpy(np.ascontiguousarray(system.positions[own])).pin_memory()
+    h_q = torch.from_numpy(np.ascontiguousarray(system.charges[own])).pin_memory()
     h_lam = torch.from_numpy(np.ascontiguousarray(lam)).pin_memory()
     h_nl = torch.from_numpy(np.ascontiguousarray(nl)).pin_memory()
     h_e = torch.empty(1, dtype=torch.float64).pin_memory()

@@ -6,20 +6,23 @@ boxes with x index r for lg = log2 G (G = 8: the 8 level-1 octants become x
 slabs of the leaf grid; the reference is single-process, so the layout is
 ours).  Per step and rank:
 
-1. select the owned atoms and a one-leaf halo (the leaf planes x0-1 and x1,
-   periodic) from the step's positions — the P2P sources of the owned
-   leaves (solver.py:126-195);
+1. particle halo exchange with the two neighbour ranks (point-to-point):
+   each rank holds its own atoms (global ids) and sends the atoms of its
+   boundary leaf planes (the neighbours' P2P halo, solver.py:126-195) and
+   those that moved into a neighbour's slab (handed over); `step` starts
+   from global arrays and keeps the owned atoms;
 2. native phase 1 (lfmm_dist_phase): tree, charges (+ scale_charges), P2P of
    owned leaves, P2M, M2M of levels >= lg (owned subtrees are complete),
-   exact box charges;
-3. exchange: all-gather of the owned multipoles of every level >= lg (each
-   rank's boxes are one contiguous x-slab of every level array) and of the
-   per-rank dipole / charge sums, added in rank order;
+   exact box charges, the slab's per-level max |M| (fp16 M2L scales);
+3. exchange: level lg all-gathered (it feeds the shared levels); levels > lg
+   send/recv only the 2-plane multipole halo each side (the M2L sources of
+   the owned targets, octree.py:96-111); per-level max |M| max-reduced; the
+   per-rank dipole / charge sums added in rank order;
 4. native phase 2: M2M of the shared levels < lg (redundant on every rank),
    lattice, M2L restricted to owned targets (levels >= lg), L2L, L2P of owned
    leaves, finalize (energies of owned atoms), owned site-atom potentials;
 5. exchange: energies (near/far partials, rank order), site-atom potentials
-   (each atom owned by exactly one rank: exact), owned forces;
+   and positions (each atom owned by exactly one rank: exact);
 6. HI corrections + lambda forces for all sites (redundant, cheap) from the
    gathered site potentials (corrections.py:157-238).
 
@@ -172,6 +175,35 @@ class TorchComm:
             for r in reqs:
                 r.wait()
 
+    def exchange_(self, sends):
+        """Variable-size point-to-point exchange: sends = {peer: (m, k)
+        tensor}; returns {peer: the (m', k) tensor that peer sent here}.  The
+        row counts travel first (one host sync), then the payloads."""
+        import torch
+
+        dist = self.dist
+        peers = list(sends)
+        dev = next(iter(sends.values())).device
+        staged = self.backend == "gloo" and dev.type == "cuda"
+        cdev = "cpu" if staged else dev
+        cnt_out = {p: torch.tensor([sends[p].shape[0]], dtype=torch.int64, device=cdev) for p in peers}
+        cnt_in = {p: torch.empty(1, dtype=torch.int64, device=cdev) for p in peers}
+        ops = [dist.P2POp(dist.isend, cnt_out[p], p, self.group) for p in peers]
+        ops += [dist.P2POp(dist.irecv, cnt_in[p], p, self.group) for p in peers]
+        for r in dist.batch_isend_irecv(ops):
+            r.wait()
+        out = {}
+        ops = []
+        for p in peers:
+            t = sends[p]
+            src = t.cpu().contiguous() if staged else t.contiguous()
+            out[p] = torch.empty((int(cnt_in[p].item()),) + tuple(t.shape[1:]), dtype=t.dtype, device=cdev)
+            ops.append(dist.P2POp(dist.isend, src, p, self.group))
+            ops.append(dist.P2POp(dist.irecv, out[p], p, self.group))
+        for r in dist.batch_isend_irecv(ops):
+            r.wait()
+        return {p: v.to(dev) for p, v in out.items()} if staged else out
+
     def max_(self, t):
         """In place: elementwise max of t over ranks (exact in any order)."""
         import torch
@@ -240,6 +272,17 @@ class _LocalRankComm:
         torch.cuda.current_stream().synchronize()
         self.shared.barrier.wait()
 
+    def exchange_(self, sends):
+        import torch
+
+        torch.cuda.current_stream().synchronize()
+        self.shared.slots[self.rank] = sends
+        self.shared.barrier.wait()
+        out = {p: self.shared.slots[p][self.rank].clone() for p in sends}
+        torch.cuda.current_stream().synchronize()
+        self.shared.barrier.wait()
+        return out
+
     def max_(self, t):
         import torch
 
@@ -283,10 +326,11 @@ def _device_view(address, shape, dtype_str, torch):
 class DistributedSolver:
     """One rank of the slab-decomposed FMM + HI step.
 
-    `step` takes the global step inputs (positions, charges, lambda table,
-    global site tables and site positions) as device tensors on every rank
-    and returns the global energy, this rank's owned forces (global indices)
-    and the lambda forces of every site.
+    `step_owned` takes this rank's atoms (positions, charges, global ids)
+    plus the lambda table and global site tables, exchanges the boundary
+    atoms with the neighbour ranks and returns the global energy, the owned
+    forces (global ids) and the lambda forces of every site.  `step` takes
+    the global arrays on every rank and keeps the owned atoms.
     """
 
     def __init__(self, box_length, config=None, comm=None, depth=None):
@@ -320,28 +364,87 @@ class DistributedSolver:
 
     def step(self, positions, charges, lambdas=None, n_lambda=None, sites=None, site_positions=None,
              mode=_native.MODE_HI):
-        """positions (N,3) f64, charges (N,) f64 on the device (global, input
-        order); lambdas (S,4) f64 / n_lambda (S,) i32 device; sites = (atom
-        offsets (S+1), global atom indices (A), n_forms (S), form offsets
-        (S+1), form charges) host arrays; site_positions (A,3) device."""
+        """Global inputs on every rank: positions (N,3) f64, charges (N,) f64
+        on the device (input order); lambdas (S,4) f64 / n_lambda (S,) i32
+        device; sites = (atom offsets (S+1), global atom indices (A), n_forms
+        (S), form offsets (S+1), form charges) host arrays.  The rank keeps
+        its owned atoms and runs `step_owned` (the halo comes from the
+        neighbour ranks, not from the global arrays).  site_positions is
+        accepted for compatibility and ignored: the site-atom positions are
+        gathered from their owners."""
+        torch = self.torch
+        w = wrap(positions, self.box, xp=torch)
+        lx = leaf_x(w, self.box, self.cfg.depth, xp=torch)
+        own = ((lx >= self.x0) & (lx < self.x1)).nonzero().flatten()
+        return self.step_owned(positions[own], charges[own], own, lambdas, n_lambda, sites,
+                               n_global=positions.shape[0], mode=mode)
+
+    def step_owned(self, positions, charges, global_ids, lambdas=None, n_lambda=None, sites=None, n_global=None,
+                   mode=_native.MODE_HI):
+        """One step from this rank's own atoms: positions (n,3) f64 (raw,
+        unwrapped), charges (n,) f64 and global ids (n,) int64 on the device,
+        normally the atoms whose leaf x lies in the rank's slab.  Atoms that
+        moved into a neighbour's boundary plane (one leaf plane at most) are
+        handed over in the halo exchange.  Returns the global energies, the
+        lambda forces of every site, and "owned" / "owned_positions" /
+        "owned_charges" / "forces" for the atoms this rank owns after the
+        exchange (carry them into the next step)."""
         if self.stream is None:
             self.stream = self.torch.cuda.Stream()
         self.stream.wait_stream(self.torch.cuda.current_stream())
         with self.torch.cuda.stream(self.stream):
-            out = self._step(positions, charges, lambdas, n_lambda, sites, site_positions, mode)
+            out = self._step(positions, charges, global_ids, lambdas, n_lambda, sites, n_global, mode)
         self.torch.cuda.current_stream().wait_stream(self.stream)
         return out
 
-    def _step(self, positions, charges, lambdas, n_lambda, sites, site_positions, mode):
+    def _exchange_particles(self, positions, charges, global_ids):
+        """Halo particle exchange with the neighbour ranks (SURVEY.md §8e
+        exchange 1).  Sends to the left rank the atoms in leaf planes x0 (its
+        right halo) and x0-1 (migrated into its slab), to the right rank those
+        in x1-1 and x1; keeps the atoms in [x0, x1) and, as halo, the ones
+        that migrated out (they lie in planes x0-1 / x1).  Returns (positions,
+        charges, global ids) of the owned atoms followed by the halo atoms,
+        and the owned count."""
         torch = self.torch
         d = self.cfg.depth
-        w = wrap(positions, self.box, xp=torch)
-        lx = leaf_x(w, self.box, d, xp=torch)
-        own, halo = select_local(lx, self.x0, self.x1, d, xp=torch)
-        idx = torch.cat([own, halo])
-        n_own, n_loc = own.numel(), idx.numel()
-        pos_l = positions[idx].contiguous()
-        q_l = charges[idx].contiguous()
+        n = 1 << d
+        x0, x1 = self.x0, self.x1
+        lx = leaf_x(wrap(positions, self.box, xp=torch), self.box, d, xp=torch)
+        stay = (lx >= x0) & (lx < x1)
+        if self.world == 1:
+            if not bool(stay.all()):
+                raise ValueError("atom outside the grid")
+            return positions, charges, global_ids, positions.shape[0]
+        xl, xr = (x0 - 1) % n, x1 % n
+        to_left = (lx == x0) | (lx == xl)
+        to_right = (lx == x1 - 1) | (lx == xr)
+        if bool((~(stay | (lx == xl) | (lx == xr))).any()):
+            raise ValueError("an atom moved more than one leaf plane out of its rank's slab; "
+                             "re-partition from global positions (DistributedSolver.step)")
+        rows = torch.cat([positions, charges[:, None], global_ids.to(torch.float64)[:, None]], 1)
+        left, right = (self.rank - 1) % self.world, (self.rank + 1) % self.world
+        if left == right:
+            recv = self.comm.exchange_({left: rows[to_left | to_right]})
+            rec = recv[left]
+        else:
+            recv = self.comm.exchange_({left: rows[to_left], right: rows[to_right]})
+            rec = torch.cat([recv[left], recv[right]])
+        rlx = leaf_x(wrap(rec[:, :3].contiguous(), self.box, xp=torch), self.box, d, xp=torch)
+        r_own = (rlx >= x0) & (rlx < x1)
+        r_halo = ~r_own
+        gone = ~stay  # migrated to a neighbour's boundary plane: still in this rank's halo
+        pos = torch.cat([positions[stay], rec[r_own, :3], positions[gone], rec[r_halo, :3]]).contiguous()
+        q = torch.cat([charges[stay], rec[r_own, 3], charges[gone], rec[r_halo, 3]]).contiguous()
+        gid = torch.cat([global_ids[stay], rec[r_own, 4].to(torch.int64), global_ids[gone],
+                         rec[r_halo, 4].to(torch.int64)])
+        return pos, q, gid, int(stay.sum().item()) + int(r_own.sum().item())
+
+    def _step(self, positions, charges, global_ids, lambdas, n_lambda, sites, n_global, mode):
+        torch = self.torch
+        d = self.cfg.depth
+        pos_l, q_l, gid_l, n_own = self._exchange_particles(positions.contiguous(), charges.contiguous(),
+                                                            global_ids)
+        n_loc = pos_l.shape[0]
         self._ensure_plan(pos_l.cpu().numpy())
         plan = self.plan
         plan.set_count(n_loc)
@@ -352,8 +455,10 @@ class DistributedSolver:
                 self._site_dev = torch.as_tensor(np.asarray(ai, np.int64), device=positions.device)
                 self._site_key = sites
                 self._site_local = None
-            loc = torch.full((positions.shape[0],), -1, dtype=torch.int64, device=positions.device)
-            loc[idx] = torch.arange(n_loc, device=positions.device)
+            if n_global is None:
+                raise ValueError("n_global (the total atom count) is needed with sites")
+            loc = torch.full((int(n_global),), -1, dtype=torch.int64, device=positions.device)
+            loc[gid_l] = torch.arange(n_loc, device=positions.device)
             ai_l = loc[self._site_dev]
             # re-upload the local site tables only when the local indices moved
             if self._site_local is None or not torch.equal(ai_l, self._site_local):
@@ -397,12 +502,21 @@ class DistributedSolver:
         e_solve = float(parts[0] + parts[1] + en[3])
         forces_l = _device_view(ptrs[3], (n_loc, 3), "<f8", torch)[:n_own].clone()
         out = {"energy_solve": e_solve, "near_energy": float(parts[0]), "far_energy": float(parts[1]),
-               "dipole_energy": float(en[3]), "owned": own, "forces": forces_l}
+               "dipole_energy": float(en[3]), "owned": gid_l[:n_own], "owned_positions": pos_l[:n_own],
+               "owned_charges": q_l[:n_own], "forces": forces_l}
         if n_sites:
+            # site-atom potentials and positions from their owners (each site
+            # atom is owned by one rank; the others contribute exact zeros)
             a_tot = int(np.asarray(sites[0])[-1])
             sp = _device_view(ptrs[4], (a_tot,), "<f8", torch)
-            sp.copy_(self.comm.sum_ordered(sp.clone()))
-            plan.dist_hi(site_positions.contiguous(), mode)
+            ai_l = self._site_local
+            mine = (ai_l >= 0) & (ai_l < n_own)
+            sp4 = torch.zeros((a_tot, 4), dtype=torch.float64, device=sp.device)
+            sp4[:, 3] = sp
+            sp4[mine, :3] = pos_l[ai_l[mine]]
+            sp4 = self.comm.sum_ordered(sp4)
+            sp.copy_(sp4[:, 3])
+            plan.dist_hi(sp4[:, :3].contiguous(), mode)
             ptrs, _ = plan.dist_buffers()
             out["lambda_forces"] = _device_view(ptrs[5], (n_sites, 4), "<f8", torch).clone()
             off = float(_device_view(ptrs[6], (1,), "<f8", torch)[0])

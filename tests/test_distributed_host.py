@@ -173,3 +173,52 @@ def test_torch_comm_halo_gloo(world):
             else:
                 assert np.all(buf[x] == -1.0)
         assert list(res[r][1]) == [world - 1, 10, 7]
+
+
+def _particle_worker(rank, world, port, out_q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from paper_2410_01754_b200.distributed import DistributedSolver
+        from paper_2410_01754_b200.fmm.solver import SolverConfig
+
+        depth, box = 3, 3.0
+        rng = np.random.default_rng(0)
+        pos = rng.uniform(-1, 4, size=(3000, 3))
+        moved = pos + rng.uniform(-0.3, 0.3, size=pos.shape)
+        solver = DistributedSolver(box, SolverConfig(p=4, depth=depth), comm=TorchComm())
+        lx = leaf_x(wrap(pos, box), box, depth)
+        own = np.flatnonzero((lx >= solver.x0) & (lx < solver.x1))
+        p_l, q_l, g_l, n_own = solver._exchange_particles(torch.from_numpy(moved[own]),
+                                                          torch.from_numpy(own * 0.5),
+                                                          torch.from_numpy(own.astype(np.int64)))
+        out_q.put((rank, p_l.numpy(), q_l.numpy(), g_l.numpy(), n_own, moved))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 4])
+def test_particle_halo_exchange_gloo(world):
+    """After the exchange each rank holds exactly the atoms select_local
+    picks from the global moved positions: owned = its slab, halo = the
+    leaf planes either side, with their positions, charges and ids."""
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = 31500 + world + (os.getpid() % 1000)
+    procs = [ctx.Process(target=_particle_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = {r: rest for r, *rest in [q.get(timeout=120) for _ in procs]}
+    for p in procs:
+        p.join(timeout=60)
+    depth, box = 3, 3.0
+    _, ranges = slab_partition(depth, world)
+    for r, (x0, x1) in enumerate(ranges):
+        p_l, q_l, g_l, n_own, moved = res[r]
+        lx = leaf_x(wrap(moved, box), box, depth)
+        own, halo = select_local(lx, x0, x1, depth)
+        assert sorted(g_l[:n_own]) == sorted(own)
+        assert sorted(g_l[n_own:]) == sorted(halo)
+        assert np.array_equal(p_l, moved[g_l])
+        assert np.array_equal(q_l, g_l * 0.5)

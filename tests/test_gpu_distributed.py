@@ -118,3 +118,75 @@ def test_multipole_halo_exchange_reads_only_the_halo(wb, precision, world, monke
     assert relerr(fd, f1) <= tol
     for o in outs:
         assert relerr(o["lambda_forces"].cpu().numpy(), lf1) <= tol
+
+
+@pytest.mark.parametrize("world", [2, 4])
+def test_step_owned_hands_over_migrated_atoms(wb, world):
+    """Each rank starts from the atoms it owned before the atoms moved (up to
+    0.2 nm, less than a leaf edge); atoms that crossed into a neighbour's
+    slab are handed over in the halo exchange and the step equals the
+    single-GPU step on the moved positions."""
+    import torch
+
+    from paper_2410_01754_b200.distributed import leaf_x, slab_partition, wrap
+
+    system, lam = wb
+    cfg = SolverConfig(p=10, depth=4, precision="double")
+    rng = np.random.default_rng(5)
+    moved = system.positions + rng.uniform(-0.2, 0.2, size=system.positions.shape)
+    lx_old = leaf_x(wrap(system.positions, system.box_length), system.box_length, 4)
+    lx_new = leaf_x(wrap(moved, system.box_length), system.box_length, 4)
+    _, ranges = slab_partition(4, world)
+    assert any(((lx_old >= a) & (lx_old < b)).sum() != ((lx_new >= a) & (lx_new < b)).sum() for a, b in ranges)
+    import copy
+
+    msys = copy.copy(system)
+    msys.positions = moved
+    e1, f1, lf1 = _single(msys, lam.values, cfg)
+
+    dev = torch.device("cuda", 0)
+    lam_t, nl = lambda_table(system, lam.values)
+    d_lam = torch.from_numpy(lam_t).to(dev)
+    d_nl = torch.from_numpy(nl).to(dev)
+    tables = site_tables(system)
+    shared = LocalComm(world)
+    outs = [None] * world
+    errs = []
+
+    def run(rank):
+        try:
+            torch.cuda.set_device(0)
+            a, b = ranges[rank]
+            own = np.flatnonzero((lx_old >= a) & (lx_old < b))
+            solver = DistributedSolver(system.box_length, cfg, comm=shared.for_rank(rank))
+            outs[rank] = solver.step_owned(torch.from_numpy(moved[own]).to(dev),
+                                           torch.from_numpy(system.charges[own]).to(dev),
+                                           torch.from_numpy(own).to(dev), d_lam, d_nl, sites=tables,
+                                           n_global=system.num_particles)
+            torch.cuda.synchronize()
+        except Exception as e:  # surfaced below
+            errs.append(e)
+            shared.barrier.abort()
+
+    threads = [threading.Thread(target=run, args=(r,)) for r in range(world)]
+    for t in threads:
+        t.start()
+    for t in threads:
+        t.join(timeout=600)
+    if errs:
+        raise errs[0]
+    n = system.num_particles
+    forces = np.zeros((n, 3))
+    count = np.zeros(n, int)
+    for r, o in enumerate(outs):
+        idx = o["owned"].cpu().numpy()
+        a, b = ranges[r]
+        assert np.all((lx_new[idx] >= a) & (lx_new[idx] < b)), "owned atoms lie in the rank's slab after the step"
+        assert np.array_equal(o["owned_positions"].cpu().numpy(), moved[idx])
+        forces[idx] = o["forces"].cpu().numpy()
+        count[idx] += 1
+    assert np.all(count == 1)
+    assert abs(outs[0]["energy"] - e1) <= 1e-10 * abs(e1)
+    assert relerr(forces, f1) <= 1e-10
+    for o in outs:
+        assert relerr(o["lambda_forces"].cpu().numpy(), lf1) <= 1e-10
