@@ -442,8 +442,8 @@ def run_ours(args):
     ms_reuse = max_over_ranks(sum(t_reuse) / len(t_reuse))
 
     # e2e through the C-ABI with pinned host buffers
-    h_pos = torch.from_numpy(np.ascontiguousarray(system.positions[own])).pin_memory()
-    h_q = torch.from_numpy(np.ascontiguousarray(system.charges[own])).pin_memory()
+    h_pos = torch.from_numpy(np.ascontiguousarray(system.positions)).pin_memory()
+    h_q = torch.from_numpy(np.ascontiguousarray(system.charges)).pin_memory()
     h_lam = torch.from_numpy(np.ascontiguousarray(lam)).pin_memory()
     h_nl = torch.from_numpy(np.ascontiguousarray(nl)).pin_memory()
     h_e = torch.empty(1, dtype=torch.float64).pin_memory()

@@ -602,7 +602,7 @@ struct lfmm_plan {
   DevBuf ops_tc, up_part, up_cnt, counters;
   DevBuf ops16, hm_inv_r, hm_inv_c, hm_jobs, hm_level_max, mult16;
   int64_t m16_off[DMAX + 2] = {0};
-  int hm_njobs = 0, hm_rw_cap = 0, hm_lsplit = 1, hm_nbig = 0;
+  int hm_njobs = 0, hm_rw_cap = 0, hm_lsplit = 1, hm_nbig = 0, hm_stagger = 12;
   DevBuf mult, loc, partial, ops_m2l, ops_m2m, ops_l2l, ops_lat, lat64t;
   std::vector<double2> lat_unit;  // unit-box complex lattice operator (nc x nc)
   // solve work
@@ -1216,6 +1216,7 @@ struct lfmm_plan {
     ha.inv_r = hm_inv_r.as<float>();
     ha.inv_c = hm_inv_c.as<float>();
     ha.rw_cap = hm_rw_cap;
+    ha.stagger = hm_stagger;
     ha.mult16 = mult16.as<unsigned char>();
     for (int l = 0; l <= depth; ++l) {
       ha.level_off[l] = level_off[l];
@@ -1405,6 +1406,7 @@ struct lfmm_plan {
         ha.inv_r = hm_inv_r.as<float>();
         ha.inv_c = hm_inv_c.as<float>();
         ha.rw_cap = hm_rw_cap;
+        ha.stagger = hm_stagger;
         ha.lvl0 = 1;
         ha.mult16 = mult16.as<unsigned char>();
         for (int l = 0; l <= depth; ++l) {
@@ -1831,6 +1833,8 @@ int lfmm_plan_create(const double* positions, int64_t n, double box_length, int 
       pl->p2p_scalar = penv && std::string(penv) == "scalar";
       const char* fenv = std::getenv("LFMM_FAR");
       pl->far_serial = fenv && std::string(fenv) == "serial";
+      const char* senv = std::getenv("LFMM_HM_STAGGER");
+      if (senv) pl->hm_stagger = std::min(16, std::max(0, std::atoi(senv)));  // <= 19 (the shortest term list)
     }
     pl->nleaf = 1 << (3 * depth);
     pl->size = box_length / double(1 << depth);

@@ -78,7 +78,18 @@ struct HaloArgs {
   int rw_cap;                        // rows per window the buffers were sized for
   int lvl0;                          // first level of a k_level_absmax / k_pack_mult16 launch (grid.y = levels)
   int own_x0, own_x1, own_depth;     // k_level_absmax over one rank's leaf x-slab (own_x1 == 0: whole level)
+  int stagger;                       // terms issuer 1 runs behind issuer 0 (A-ring order, see hm_aseq)
 };
+
+// A-ring slot sequence of issuer par's u-th term (u counts its terms over all
+// its iterations; both issuers own T terms).  The loader walks steps s = 0,
+// 1, ...: issuer 0's term s, then issuer 1's term s - D.  Issuer 1 thus runs
+// D terms behind issuer 0, so the two never finish an iteration together
+// (an iteration's end waits for its next halo window, and in phase both
+// issuers would wait at once and leave the tensor core idle).
+__device__ __forceinline__ int hm_aseq(int par, int u, int D, int T) {
+  return par == 0 ? u + min(max(u - D, 0), T) : min(u + D + 1, T) + u;
+}
 
 __host__ __device__ inline int hm_rw(int N, int Z) { return N + 2 * Z + 2; }
 __host__ __device__ inline size_t hm_buf_bytes(int rw) { return (size_t)192 * rw; }  // 2 parts x 2 kgroups x 3 windows x 16 B
@@ -370,7 +381,9 @@ __global__ void __launch_bounds__(HM_THREADS, 1) k_m2l_halo(HaloArgs g) {
       // descriptors are advanced by adding (bytes >> 4) to the start-address
       // field (shared addresses < 256 KB: no carry out of its 14 bits)
       const uint64_t a_desc0 = hm_desc(smem_u32(abase), 128, 256);
-      int seq = 0;  // ring sequence number of this pair's first tile
+      const int T = (HM_NKC / 2) * (s_nt[0] + (nsc > 1 ? s_nt[1] : 0));
+      const int D = min(g.stagger, T);
+      int u = 0;  // this issuer's terms so far
       for (int it0 = 0; it0 < niter; it0 += 2) {
         const int k = it0 / HM_NKC;
         const int nt = s_nt[k];
@@ -391,7 +404,7 @@ __global__ void __launch_bounds__(HM_THREADS, 1) k_m2l_halo(HaloArgs g) {
         const uint32_t dacc = tmem + (uint32_t)((it & 1) * 256);
         uint32_t boff = s_boff[k][0];
         for (int t = 0; t < nt; ++t) {
-          const int sq = seq + 2 * t + par;
+          const int sq = hm_aseq(par, u + t, D, T);
           const int stage = sq % HM_ASTAGES;
           const uint64_t dbh = b_desc0 + boff;
           if (t + 1 < nt) boff = s_boff[k][t + 1];
@@ -412,7 +425,7 @@ __global__ void __launch_bounds__(HM_THREADS, 1) k_m2l_halo(HaloArgs g) {
         }
         tc_commit(smem_u32(&acc_full[it & 1]));
         tc_commit(smem_u32(&halo_empty[it & 1]));
-        seq += 2 * nt;
+        u += nt;
       }
 #ifdef LFMM_HM_PROF
       unsigned long long te;
@@ -424,20 +437,28 @@ __global__ void __launch_bounds__(HM_THREADS, 1) k_m2l_halo(HaloArgs g) {
   } else if (warp == 10) {
     // ================================================= A loader ========
     if (lane == 0) {
+      const int T = (HM_NKC / 2) * (s_nt[0] + (nsc > 1 ? s_nt[1] : 0));
+      const int D = min(g.stagger, T);
+      // one cursor per issuer: (iteration pair it0, term t)
+      int c_it0[2] = {0, 0}, c_t[2] = {0, 0};
       int seq = 0;
-      for (int it0 = 0; it0 < niter; it0 += 2) {
-        const int k = it0 / HM_NKC;
-        const int nt = s_nt[k];
-        for (int t = 0; t < nt; ++t) {
-          const int row = s_orow[k][t];
+      for (int s = 0; s < T + D; ++s) {
 #pragma unroll
-          for (int par = 0; par < 2; ++par, ++seq) {
-            const int kc = (it0 + par) % HM_NKC;
-            const int stage = seq % HM_ASTAGES, use = seq / HM_ASTAGES;
-            if (use >= 1) mbar_wait(smem_u32(&a_empty[stage]), (use - 1) & 1);
-            bulk_load(smem_u32(abase + stage * HM_ATILE), g.ops16 + ((size_t)row * HM_NKC + kc) * HM_ATILE, HM_ATILE,
-                      smem_u32(&a_full[stage]));
+        for (int par = 0; par < 2; ++par) {
+          const int u = s - par * D;
+          if (u < 0 || u >= T) continue;
+          const int k = c_it0[par] / HM_NKC;
+          const int row = s_orow[k][c_t[par]];
+          const int kc = (c_it0[par] + par) % HM_NKC;
+          if (++c_t[par] == s_nt[k]) {
+            c_t[par] = 0;
+            c_it0[par] += 2;
           }
+          const int stage = seq % HM_ASTAGES, use = seq / HM_ASTAGES;
+          if (use >= 1) mbar_wait(smem_u32(&a_empty[stage]), (use - 1) & 1);
+          bulk_load(smem_u32(abase + stage * HM_ATILE), g.ops16 + ((size_t)row * HM_NKC + kc) * HM_ATILE, HM_ATILE,
+                    smem_u32(&a_full[stage]));
+          ++seq;
         }
       }
     }
