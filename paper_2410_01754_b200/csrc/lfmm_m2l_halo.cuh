@@ -110,6 +110,21 @@ __device__ __forceinline__ uint64_t hm_desc(uint32_t saddr, uint32_t lbo, uint32
   d |= (uint64_t)1 << 46;
   return d;
 }
+// warp-wide issue: every lane of the issuer warp runs the loop (operands are
+// warp-uniform), one elected lane issues the instruction
+__device__ __forceinline__ void hm_mma_w(uint32_t dtmem, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
+                                         uint32_t acc) {
+  asm volatile(
+      "{\n\t.reg .pred p, e;\n\tsetp.ne.b32 p, %4, 0;\n\telect.sync _|e, 0xffffffff;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(dtmem),
+      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(acc));
+}
+__device__ __forceinline__ void hm_commit_w(uint32_t bar) {
+  asm volatile(
+      "{\n\t.reg .pred e;\n\telect.sync _|e, 0xffffffff;\n\t"
+      "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n\t}" ::"r"(bar)
+      : "memory");
+}
 __device__ __forceinline__ uint32_t hm_idesc(int N) {
   // kind::f16: D f32, A/B f16, K-major both, N, M = 128
   return (1u << 4) | ((uint32_t)(N >> 3) << 17) | ((uint32_t)(128 >> 4) << 24);
@@ -252,7 +267,8 @@ __global__ void k_pack_mult16(HaloArgs g) {
 // wait acc_empty, wait a_full, terms, MMA issue end, smid}
 __device__ unsigned long long g_hm_prof[8192][8];
 #define HM_T0() const unsigned long long _t0 = clock64()
-#define HM_ACC(slot) atomicAdd(&g_hm_prof[blockIdx.x][slot], clock64() - _t0)
+#define HM_ACC(slot) \
+  if ((threadIdx.x & 31) == 0) atomicAdd(&g_hm_prof[blockIdx.x][slot], clock64() - _t0)
 #else
 #define HM_T0()
 #define HM_ACC(slot)
@@ -374,8 +390,9 @@ __global__ void __launch_bounds__(HM_THREADS, 1) k_m2l_halo(HaloArgs g) {
     }
   } else if (warp == 8 || warp == 9) {
     // ================================================= MMA issuers =====
-    if (lane == 0) {
-      const int par = warp - 8;
+    // (whole warp; hm_mma_w / hm_commit_w elect one lane)
+    {
+      const int par = __shfl_sync(0xffffffffu, warp - 8, 0);
       const uint32_t idesc = hm_idesc(N);
       const uint32_t lbo = 3u * rw * 16u;
       // descriptors are advanced by adding (bytes >> 4) to the start-address
@@ -415,16 +432,16 @@ __global__ void __launch_bounds__(HM_THREADS, 1) k_m2l_halo(HaloArgs g) {
             HM_ACC(4);
           }
 #ifdef LFMM_HM_PROF
-          atomicAdd(&g_hm_prof[blockIdx.x][5], 1ull);
+          if (lane == 0) atomicAdd(&g_hm_prof[blockIdx.x][5], 1ull);
 #endif
           asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-          hm_mma(dacc, dah, dbh, idesc, t > 0 ? 1u : 0u);
-          hm_mma(dacc, dah, dbh + b_lo, idesc, 1u);
-          hm_mma(dacc, dah + (4096 >> 4), dbh, idesc, 1u);
-          tc_commit(smem_u32(&a_empty[stage]));
+          hm_mma_w(dacc, dah, dbh, idesc, t > 0 ? 1u : 0u);
+          hm_mma_w(dacc, dah, dbh + b_lo, idesc, 1u);
+          hm_mma_w(dacc, dah + (4096 >> 4), dbh, idesc, 1u);
+          hm_commit_w(smem_u32(&a_empty[stage]));
         }
-        tc_commit(smem_u32(&acc_full[it & 1]));
-        tc_commit(smem_u32(&halo_empty[it & 1]));
+        hm_commit_w(smem_u32(&acc_full[it & 1]));
+        hm_commit_w(smem_u32(&halo_empty[it & 1]));
         u += nt;
       }
 #ifdef LFMM_HM_PROF
