@@ -524,19 +524,35 @@ inline unsigned nblk(int64_t n, int t) { return (unsigned)((n + t - 1) / t); }
 // plans with different halo tiles (e.g. ranks of a slab decomposition driven
 // from threads of one process) must not lower it under each other: set it
 // once to the device's opt-in maximum.
-void halo_smem_attr(size_t need) {
+// Returns the A-ring depth (k_m2l_halo<AS>) whose shared memory fits:
+// 14 stages, or 10 when the halo windows of a depth-6 level need the room.
+int halo_smem_attr(int rw_cap) {
   static std::once_flag once;
   static int max_optin = 0;
   std::call_once(once, [] {
     int dev = 0;
     LFMM_CUDA(cudaGetDevice(&dev));
     LFMM_CUDA(cudaDeviceGetAttribute(&max_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev));
-    cudaFuncAttributes fa{};
-    LFMM_CUDA(cudaFuncGetAttributes(&fa, k_m2l_halo));
-    max_optin -= (int)fa.sharedSizeBytes;  // static shared memory counts against the same limit
-    LFMM_CUDA(cudaFuncSetAttribute(k_m2l_halo, cudaFuncAttributeMaxDynamicSharedMemorySize, max_optin));
+    cudaFuncAttributes fa{}, fb{};
+    LFMM_CUDA(cudaFuncGetAttributes(&fa, k_m2l_halo<HM_ASTAGES>));
+    LFMM_CUDA(cudaFuncGetAttributes(&fb, k_m2l_halo<HM_ASTAGES_SMALL>));
+    // static shared memory counts against the same limit
+    max_optin -= (int)std::max(fa.sharedSizeBytes, fb.sharedSizeBytes);
+    LFMM_CUDA(cudaFuncSetAttribute(k_m2l_halo<HM_ASTAGES>, cudaFuncAttributeMaxDynamicSharedMemorySize, max_optin));
+    LFMM_CUDA(
+        cudaFuncSetAttribute(k_m2l_halo<HM_ASTAGES_SMALL>, cudaFuncAttributeMaxDynamicSharedMemorySize, max_optin));
   });
-  LFMM_REQUIRE(need <= (size_t)max_optin, "halo M2L tile needs more shared memory than the device offers");
+  if (hm_smem_bytes(rw_cap, HM_ASTAGES) <= (size_t)max_optin) return HM_ASTAGES;
+  LFMM_REQUIRE(hm_smem_bytes(rw_cap, HM_ASTAGES_SMALL) <= (size_t)max_optin,
+               "halo M2L tile needs more shared memory than the device offers");
+  return HM_ASTAGES_SMALL;
+}
+
+void launch_m2l_halo(const HaloArgs& ha, int njobs, int astages, cudaStream_t st) {
+  if (astages == HM_ASTAGES)
+    k_m2l_halo<HM_ASTAGES><<<njobs, HM_THREADS, hm_smem_bytes(ha.rw_cap, HM_ASTAGES), st>>>(ha);
+  else
+    k_m2l_halo<HM_ASTAGES_SMALL><<<njobs, HM_THREADS, hm_smem_bytes(ha.rw_cap, HM_ASTAGES_SMALL), st>>>(ha);
 }
 
 }  // namespace
@@ -602,7 +618,7 @@ struct lfmm_plan {
   DevBuf ops_tc, up_part, up_cnt, counters;
   DevBuf ops16, hm_inv_r, hm_inv_c, hm_jobs, hm_level_max, mult16;
   int64_t m16_off[DMAX + 2] = {0};
-  int hm_njobs = 0, hm_rw_cap = 0, hm_lsplit = 1, hm_nbig = 0, hm_stagger = 12;
+  int hm_njobs = 0, hm_rw_cap = 0, hm_lsplit = 1, hm_nbig = 0, hm_stagger = 8, hm_astages = HM_ASTAGES;
   DevBuf mult, loc, partial, ops_m2l, ops_m2m, ops_l2l, ops_lat, lat64t;
   std::vector<double2> lat_unit;  // unit-box complex lattice operator (nc x nc)
   // solve work
@@ -983,7 +999,7 @@ struct lfmm_plan {
     });
     LFMM_CUDA(cudaStreamSynchronize(stream));
     hm_level_max.ensure(sizeof(unsigned int) * (DMAX + 2));
-    halo_smem_attr(hm_smem_bytes(hm_rw_cap));
+    hm_astages = halo_smem_attr(hm_rw_cap);
   }
 
   // Halo M2L jobs: (level, target class, 256-row tile of the padded linear
@@ -1189,7 +1205,7 @@ struct lfmm_plan {
     launch(ST_PACK, [&] {
       k_pack_mult16<<<dim3((unsigned)((8 * hm_plane_rows(l1) + 255) / 256), nl, 8), 256, 0, st>>>(ha);
     });
-    launch(ST_DOWN, [&] { k_m2l_halo<<<njobs, HM_THREADS, hm_smem_bytes(hm_rw_cap), st>>>(ha); });
+    launch(ST_DOWN, [&] { launch_m2l_halo(ha, njobs, hm_astages, st); });
   }
   void far_overlapped() {
     const int ls = hm_lsplit;
@@ -1434,7 +1450,7 @@ struct lfmm_plan {
           k_pack_mult16<<<dim3((unsigned)((8 * hm_plane_rows(depth) + 255) / 256), depth, 8), 256, 0, stream>>>(ha);
         });
         launch(ST_DOWN, [&] {
-          k_m2l_halo<<<hm_njobs, HM_THREADS, hm_smem_bytes(hm_rw_cap), stream>>>(ha);
+          launch_m2l_halo(ha, hm_njobs, hm_astages, stream);
         });
       } else if (use_tc && sizeof(T) == 4) {
         TcArgs ta{};
@@ -2413,7 +2429,7 @@ int lfmm_dist_configure(lfmm_plan* plan, int x0, int x1, int lg) {
     plan->dist_lg = lg;
     if (plan->use_halo) {
       plan->plan_halo_jobs();
-      halo_smem_attr(hm_smem_bytes(plan->hm_rw_cap));
+      plan->hm_astages = halo_smem_attr(plan->hm_rw_cap);
     }
   });
 }

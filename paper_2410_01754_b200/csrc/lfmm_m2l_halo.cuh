@@ -54,7 +54,8 @@ constexpr int HM_NMAX = 256;       // target rows per job (MMA N)
 constexpr int HM_KC = 16;          // coefficients per iteration (one f16 MMA K)
 constexpr int HM_NKC = 8;          // 128 / 16
 constexpr int HM_ATILE = 8192;     // one operator chunk: hi 4 KB | lo 4 KB
-constexpr int HM_ASTAGES = 14;
+constexpr int HM_ASTAGES = 14;   // A-ring stages (10 when the level-6 halo windows need the room)
+constexpr int HM_ASTAGES_SMALL = 10;
 constexpr int HM_THREADS = 384;
 constexpr int HM_WORKERS = 256;
 
@@ -86,14 +87,17 @@ struct HaloArgs {
 // 1, ...: issuer 0's term s, then issuer 1's term s - D.  Issuer 1 thus runs
 // D terms behind issuer 0, so the two never finish an iteration together
 // (an iteration's end waits for its next halo window, and in phase both
-// issuers would wait at once and leave the tensor core idle).
+// issuers would wait at once and leave the tensor core idle).  D is capped at
+// AS - 6: lags of AS + 2 terms and more hung the kernel (AS = 10 and 14).
 __device__ __forceinline__ int hm_aseq(int par, int u, int D, int T) {
   return par == 0 ? u + min(max(u - D, 0), T) : min(u + D + 1, T) + u;
 }
 
 __host__ __device__ inline int hm_rw(int N, int Z) { return N + 2 * Z + 2; }
 __host__ __device__ inline size_t hm_buf_bytes(int rw) { return (size_t)192 * rw; }  // 2 parts x 2 kgroups x 3 windows x 16 B
-__host__ inline size_t hm_smem_bytes(int rw_cap) { return 2 * hm_buf_bytes(rw_cap) + HM_ASTAGES * HM_ATILE + 1024; }
+__host__ inline size_t hm_smem_bytes(int rw_cap, int astages = HM_ASTAGES) {
+  return 2 * hm_buf_bytes(rw_cap) + (size_t)astages * HM_ATILE + 1024;
+}
 
 // group g of G: relative parities (tc ^ sc) it covers
 __device__ __forceinline__ int hm_group_rel(int G, int g, int k) {
@@ -274,6 +278,7 @@ __device__ unsigned long long g_hm_prof[8192][8];
 #define HM_ACC(slot)
 #endif
 
+template <int AS>
 __global__ void __launch_bounds__(HM_THREADS, 1) k_m2l_halo(HaloArgs g) {
 #ifdef LFMM_HM_PROF
   unsigned long long _tstart = 0;
@@ -289,7 +294,7 @@ __global__ void __launch_bounds__(HM_THREADS, 1) k_m2l_halo(HaloArgs g) {
   extern __shared__ __align__(1024) unsigned char hm_smem_raw[];
   unsigned char* smem = reinterpret_cast<unsigned char*>(((uintptr_t)hm_smem_raw + 1023) & ~(uintptr_t)1023);
   __shared__ __align__(8) uint64_t halo_full[2], halo_empty[2], acc_full[2], acc_empty[2];
-  __shared__ __align__(8) uint64_t a_full[HM_ASTAGES], a_empty[HM_ASTAGES];
+  __shared__ __align__(8) uint64_t a_full[AS], a_empty[AS];
   __shared__ uint32_t tmem_base_sh;
   // the job's (tc, sc) term lists: B row offset (16-B units) and operator row
   __shared__ uint32_t s_boff[2][27];
@@ -314,7 +319,7 @@ __global__ void __launch_bounds__(HM_THREADS, 1) k_m2l_halo(HaloArgs g) {
       mbar_init(smem_u32(&acc_full[s]), 1);
       mbar_init(smem_u32(&acc_empty[s]), HM_WORKERS);
     }
-    for (int s = 0; s < HM_ASTAGES; ++s) {
+    for (int s = 0; s < AS; ++s) {
       mbar_init(smem_u32(&a_full[s]), 1);
       mbar_init(smem_u32(&a_empty[s]), 1);
     }
@@ -399,7 +404,7 @@ __global__ void __launch_bounds__(HM_THREADS, 1) k_m2l_halo(HaloArgs g) {
       // field (shared addresses < 256 KB: no carry out of its 14 bits)
       const uint64_t a_desc0 = hm_desc(smem_u32(abase), 128, 256);
       const int T = (HM_NKC / 2) * (s_nt[0] + (nsc > 1 ? s_nt[1] : 0));
-      const int D = min(g.stagger, T);
+      const int D = min(min(g.stagger, AS - 6), T);  // D >= AS + 2 was seen to deadlock
       int u = 0;  // this issuer's terms so far
       for (int it0 = 0; it0 < niter; it0 += 2) {
         const int k = it0 / HM_NKC;
@@ -422,13 +427,13 @@ __global__ void __launch_bounds__(HM_THREADS, 1) k_m2l_halo(HaloArgs g) {
         uint32_t boff = s_boff[k][0];
         for (int t = 0; t < nt; ++t) {
           const int sq = hm_aseq(par, u + t, D, T);
-          const int stage = sq % HM_ASTAGES;
+          const int stage = sq % AS;
           const uint64_t dbh = b_desc0 + boff;
           if (t + 1 < nt) boff = s_boff[k][t + 1];
           const uint64_t dah = a_desc0 + (uint64_t)(stage * (HM_ATILE >> 4));
           {
             HM_T0();
-            mbar_wait(smem_u32(&a_full[stage]), (sq / HM_ASTAGES) & 1);
+            mbar_wait(smem_u32(&a_full[stage]), (sq / AS) & 1);
             HM_ACC(4);
           }
 #ifdef LFMM_HM_PROF
@@ -455,7 +460,7 @@ __global__ void __launch_bounds__(HM_THREADS, 1) k_m2l_halo(HaloArgs g) {
     // ================================================= A loader ========
     if (lane == 0) {
       const int T = (HM_NKC / 2) * (s_nt[0] + (nsc > 1 ? s_nt[1] : 0));
-      const int D = min(g.stagger, T);
+      const int D = min(min(g.stagger, AS - 6), T);  // D >= AS + 2 was seen to deadlock
       // one cursor per issuer: (iteration pair it0, term t)
       int c_it0[2] = {0, 0}, c_t[2] = {0, 0};
       int seq = 0;
@@ -471,7 +476,7 @@ __global__ void __launch_bounds__(HM_THREADS, 1) k_m2l_halo(HaloArgs g) {
             c_t[par] = 0;
             c_it0[par] += 2;
           }
-          const int stage = seq % HM_ASTAGES, use = seq / HM_ASTAGES;
+          const int stage = seq % AS, use = seq / AS;
           if (use >= 1) mbar_wait(smem_u32(&a_empty[stage]), (use - 1) & 1);
           bulk_load(smem_u32(abase + stage * HM_ATILE), g.ops16 + ((size_t)row * HM_NKC + kc) * HM_ATILE, HM_ATILE,
                     smem_u32(&a_full[stage]));

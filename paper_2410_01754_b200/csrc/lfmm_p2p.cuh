@@ -117,6 +117,9 @@ __global__ void __launch_bounds__(P2P_WARPS * 32) k_p2p(const vec4_t<T>* __restr
 #ifndef LFMM_P2P2_WARPS
 #define LFMM_P2P2_WARPS 4
 #endif
+#ifndef LFMM_P2P2_MINB
+#define LFMM_P2P2_MINB 1
+#endif
 #ifndef LFMM_P2P2_SMAX
 #define LFMM_P2P2_SMAX 512
 #endif
@@ -174,7 +177,7 @@ __device__ __forceinline__ void kahan_fold(uint64_t& v2, uint64_t& c2, uint64_t 
 }
 
 template <bool GRAD>
-__global__ void __launch_bounds__(P2P2_WARPS * 32) k_p2p2(const float4* __restrict__ xq,
+__global__ void __launch_bounds__(P2P2_WARPS * 32, LFMM_P2P2_MINB) k_p2p2(const float4* __restrict__ xq,
                                                           const float4* __restrict__ pair_a,
                                                           const float4* __restrict__ pair_b,
                                                           const int* __restrict__ leaf_start, int depth,

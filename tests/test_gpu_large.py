@@ -101,3 +101,15 @@ def test_c3_fp64_near_field_matches_oracle_sample(c3):
     ref = v[idx, 0]
     got = r64.near_potentials[tree["perm"][idx]]
     assert relerr(got, ref) <= 1e-9
+
+
+def test_depth6_fp32_matches_fp64():
+    """Depth 6 (C5's tree; level-6 halo windows run the 10-stage A ring of
+    k_m2l_halo): the fp32 step against the fp64 device solve."""
+    system, _, _ = generate_water_box(300_000, 0, seed=6)
+    _, r64, f64 = _solve(system, 10, 6, "double")
+    _, r32, f32 = _solve(system, 10, 6, "single")
+    assert relerr(r32.potentials, r64.potentials) <= 1e-4
+    assert relerr(r32.far_potentials, r64.far_potentials) <= 1e-4
+    assert relerr(r32.energy, r64.energy) <= 1e-4
+    assert relerr(f32, f64) <= 1e-4

@@ -1,6 +1,7 @@
 """Secondary measurements of SURVEY.md §8d (single GPU), beside bench.py's
 headline: C2 (100k atoms, 64 sites, depth 4) in fp32 and fp64, C3 in fp64,
-C3 with the tree frozen (plan reuse), C4 (4096 sites), and the reference's
+C3 with the tree frozen (plan reuse), C4 (4096 sites), C3 at depth 4, C5's
+8M-atom box (depth 6) on one GPU, and the reference's
 HI-overhead definition t_corr / t_solve.  Device-resident inputs, L2 flushed
 between steps, CUDA events on the plan's stream, mean of K steps after W
 warm-ups.  Prints one JSON object."""
@@ -78,7 +79,8 @@ def measure(atoms, sites, depth, precision, steps=10, warmup=3, seed=0, reuse=Fa
     return {"atoms": n, "sites": s, "depth": depth, "precision": precision, "tree_frozen": reuse,
             "ms_per_step": round(ms_full, 4), "plain_fmm_ms": round(ms_plain, 4),
             "hi_overhead_pct": round(100 * (ms_full / ms_plain - 1), 2),
-            "hi_overhead_ref_def_pct": round(100 * t_corr / t_solve, 2), "generate_s": round(gen_s, 1)}
+            "hi_overhead_ref_def_pct": round(100 * t_corr / t_solve, 2), "generate_s": round(gen_s, 1),
+            "stages_ms": {k: round(v[0] / 5, 4) for k, v in st.items() if v[1]}}
 
 
 def main():
@@ -88,7 +90,9 @@ def main():
                dict(atoms=100_000, sites=64, depth=4, precision="double"),
                dict(atoms=1_000_000, sites=512, depth=5, precision="single", reuse=True),
                dict(atoms=1_000_000, sites=512, depth=5, precision="double"),
-               dict(atoms=1_000_000, sites=4096, depth=5, precision="single"))
+               dict(atoms=1_000_000, sites=4096, depth=5, precision="single"),
+               dict(atoms=1_000_000, sites=512, depth=4, precision="single"),
+               dict(atoms=8_000_000, sites=512, depth=6, precision="single"))
     for i, kw in enumerate(runs):
         if only and str(i) not in only:
             continue
