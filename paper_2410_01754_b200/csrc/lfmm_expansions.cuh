@@ -645,8 +645,13 @@ __device__ __forceinline__ int parity_box(int level, int par, int q) {
 template <class T>
 __global__ void __launch_bounds__(G_THREADS) k_gemm_gather(GemmArgs g) {
   constexpr int BK = GemmTile<T>::BK, AK = GemmTile<T>::AK, BKT = GemmTile<T>::BKT;
-  __shared__ __align__(16) T As[2][BK][GB_M];
-  __shared__ __align__(16) T Bs[2][BK][GB_N];
+  // fp64 runs on the DMMA pipe (mma.sync m8n8k4): rows padded by 8 doubles so
+  // a fragment load (4 k-rows x 8 consecutive elements) touches every bank
+  // exactly twice
+  constexpr bool DMMA = sizeof(T) == 8;
+  constexpr int APAD = DMMA ? 8 : 0;
+  __shared__ __align__(16) T As[2][BK][GB_M + APAD];
+  __shared__ __align__(16) T Bs[2][BK][GB_N + APAD];
   __shared__ int col_dst[GB_N];
   const int tid = threadIdx.x;
   const int ncp = g.ncp;
@@ -697,11 +702,15 @@ __global__ void __launch_bounds__(G_THREADS) k_gemm_gather(GemmArgs g) {
   // compute mapping: 16 x 16 threads, 8 rows (two groups of 4) x 4 columns
   const int ty = tid >> 4, tx = tid & 15;
 
+  // SIMT (fp32): acc[i][j] = D[row i of the thread's 8][col tx*4+j].  DMMA
+  // (fp64): warp w owns rows (w & 3)*32.., cols (w >> 2)*32..; acc[2*mt +
+  // (nt >> 1)][2*(nt & 1) + e] = D[mt*8 + lane/4][nt*8 + 2*(lane%4) + e]
   T acc[8][4];
 #pragma unroll
   for (int i = 0; i < 8; ++i)
 #pragma unroll
     for (int j = 0; j < 4; ++j) acc[i][j] = T(0);
+  const int lane = tid & 31, wm = (tid >> 5) & 3, wn = tid >> 7;
 
   T ra[AK], rb[BKT];
   const T* Ab = nullptr;
@@ -784,6 +793,27 @@ __global__ void __launch_bounds__(G_THREADS) k_gemm_gather(GemmArgs g) {
   for (int it = 0; it < niter; ++it) {
     const int buf = it & 1;
     if (it + 1 < niter) load_regs(it + 1);
+    if constexpr (DMMA) {
+#pragma unroll
+      for (int ks = 0; ks < BK; ks += 4) {
+        double af[4], bf[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          af[u] = As[buf][ks + (lane & 3)][wm * 32 + u * 8 + (lane >> 2)];
+          bf[u] = Bs[buf][ks + (lane & 3)][wn * 32 + u * 8 + (lane >> 2)];
+        }
+#pragma unroll
+        for (int mt = 0; mt < 4; ++mt)
+#pragma unroll
+          for (int nt = 0; nt < 4; ++nt) {
+            double& d0 = reinterpret_cast<double&>(acc[2 * mt + (nt >> 1)][2 * (nt & 1)]);
+            double& d1 = reinterpret_cast<double&>(acc[2 * mt + (nt >> 1)][2 * (nt & 1) + 1]);
+            asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0, %1}, {%2}, {%3}, {%0, %1};"
+                         : "+d"(d0), "+d"(d1)
+                         : "d"(af[mt]), "d"(bf[nt]));
+          }
+      }
+    } else {
 #pragma unroll
     for (int k = 0; k < BK; ++k) {
       T a[8], bv[4];
@@ -797,6 +827,7 @@ __global__ void __launch_bounds__(G_THREADS) k_gemm_gather(GemmArgs g) {
       for (int i = 0; i < 8; ++i)
 #pragma unroll
         for (int j = 0; j < 4; ++j) acc[i][j] = fma(a[i], bv[j], acc[i][j]);
+    }
     }
     if (it + 1 < niter) store_smem(buf ^ 1);
     __syncthreads();
@@ -826,6 +857,17 @@ __global__ void __launch_bounds__(G_THREADS) k_gemm_gather(GemmArgs g) {
   constexpr int CC = (2 * BK * GB_M) / GB_M;  // columns per pass
 #pragma unroll 1
   for (int c0 = 0; c0 < GB_N; c0 += CC) {
+    if constexpr (DMMA) {
+#pragma unroll
+      for (int i = 0; i < 8; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          const int mt = i >> 1, nt = 2 * (i & 1) + (j >> 1), e = j & 1;
+          const int col = wn * 32 + nt * 8 + 2 * (lane & 3) + e - c0;
+          const int r = wm * 32 + mt * 8 + (lane >> 2);
+          if (col >= 0 && col < CC) stage[col * GB_M + r] = acc[i][j];
+        }
+    } else {
 #pragma unroll
     for (int j = 0; j < 4; ++j) {
       const int col = tx * 4 + j - c0;
@@ -835,6 +877,7 @@ __global__ void __launch_bounds__(G_THREADS) k_gemm_gather(GemmArgs g) {
         const int r = (i < 4 ? ty * 4 + i : 64 + ty * 4 + (i - 4));
         stage[col * GB_M + r] = acc[i][j];
       }
+    }
     }
     __syncthreads();
     for (int e = tid; e < CC * GB_M; e += G_THREADS) {
