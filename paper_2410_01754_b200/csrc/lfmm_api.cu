@@ -1182,6 +1182,16 @@ struct lfmm_plan {
     ta.cnt = tr_cnt.as<int>();
     launch(ST_M2M, [&] { tr_launch<float>(ta, 1 << (3 * l), 8, st); });
   }
+  // parent columns of level pl this rank computes: its x-slab when a slab
+  // decomposition owns the level (pl >= dist_lg), else the whole level
+  void owned_parents(int pl, int& p0, int& pend) const {
+    p0 = 0;
+    pend = 1 << (3 * pl);
+    if (dist_lg > 0 && pl >= dist_lg) {
+      p0 = (own_x0 >> (depth - pl)) << (2 * pl);
+      pend = (own_x1 >> (depth - pl)) << (2 * pl);
+    }
+  }
   void tr_l2l(int l, cudaStream_t st) {
     TrArgs ta{};
     ta.mode = 1;
@@ -1192,7 +1202,8 @@ struct lfmm_plan {
     ta.dst = loc.as<float>() + level_off[l] * ncp;
     ta.partial = static_cast<const char*>(partial.p) + sizeof(float) * (size_t)part_off[l] * ncp;
     ta.nsplit = nsplit[l];
-    launch(ST_L2L, [&] { tr_launch<float>(ta, 1 << (3 * (l - 1)), 8, st); });
+    owned_parents(l - 1, ta.p0, ta.pend);
+    launch(ST_L2L, [&] { tr_launch<float>(ta, ta.pend - ta.p0, 8, st); });
   }
   void halo_levels(HaloArgs ha, int l0, int l1, int job0, int njobs, cudaStream_t st) {
     ha.lvl0 = l0;
@@ -1285,7 +1296,8 @@ struct lfmm_plan {
         ta.dst = M + level_off[l] * ncp;
         ta.slots = up_part.p;
         ta.cnt = tr_cnt.as<int>();
-        launch(ST_M2M, [&] { tr_launch<T>(ta, 1 << (3 * l), 8, stream); });
+        owned_parents(l, ta.p0, ta.pend);
+        launch(ST_M2M, [&] { tr_launch<T>(ta, ta.pend - ta.p0, 8, stream); });
         return;
       }
       ga.mode = GEMM_UP;
@@ -1447,7 +1459,22 @@ struct lfmm_plan {
           });
         }
         launch(ST_PACK, [&] {
-          k_pack_mult16<<<dim3((unsigned)((8 * hm_plane_rows(depth) + 255) / 256), depth, 8), 256, 0, stream>>>(ha);
+          // owned levels of a slab decomposition: padded class x-rows
+          // [xl0/2, (xl1+1)/2 + 2) hold every source window of the owned
+          // targets (class positions [ia, ib) of plan_halo_jobs, +-1 plane)
+          int prows = 0;
+          for (int l = 1; l <= depth; ++l) {
+            const int Z = (1 << (l - 1)) + 2;
+            ha.pk_r0[l] = 0;
+            ha.pk_r1[l] = hm_plane_rows(l);
+            if (dist_lg > 0 && l >= dist_lg) {
+              const int xl0 = own_x0 >> (depth - l), xl1 = own_x1 >> (depth - l);
+              ha.pk_r0[l] = (xl0 >> 1) * Z * Z;
+              ha.pk_r1[l] = std::min(hm_plane_rows(l), (((xl1 + 1) >> 1) + 2) * Z * Z);
+            }
+            prows = std::max(prows, ha.pk_r1[l] - ha.pk_r0[l]);
+          }
+          k_pack_mult16<<<dim3((unsigned)((8 * prows + 255) / 256), depth, 8), 256, 0, stream>>>(ha);
         });
         launch(ST_DOWN, [&] {
           launch_m2l_halo(ha, hm_njobs, hm_astages, stream);
@@ -1482,7 +1509,8 @@ struct lfmm_plan {
           ta.dst = Lc + level_off[l] * ncp;
           ta.partial = static_cast<const char*>(partial.p) + tsz() * (size_t)part_off[l] * ncp;
           ta.nsplit = nsplit[l];
-          launch(ST_L2L, [&] { tr_launch<T>(ta, 1 << (3 * (l - 1)), 8, stream); });
+          owned_parents(l - 1, ta.p0, ta.pend);
+          launch(ST_L2L, [&] { tr_launch<T>(ta, ta.pend - ta.p0, 8, stream); });
           continue;
         }
         ga.mode = GEMM_L2L;

@@ -949,6 +949,8 @@ struct TrArgs {
   int* cnt;            // UP: one counter per tile
   const void* partial; // DOWN: M2L partial slots of the child level ([nsplit][nchild][ncp])
   int nsplit;
+  int p0, pend;        // UP/DOWN: parent columns [p0, pend) (pend == 0: the whole level; a
+                       // slab decomposition restricts the owned levels to its x-slab)
 };
 
 template <class T>
@@ -972,11 +974,11 @@ __global__ void __launch_bounds__(TR_THREADS) k_translate(TrArgs g) {
   const int pl = g.mode == 0 ? g.level : g.level - 1;  // parent level
   const int np = 1 << (3 * pl), pn = 1 << pl, cn = 2 * pn;
   if (tid < PT) {
-    const int p = tile * PT + tid;
+    const int p = g.p0 + tile * PT + tid;
     int s = -1, d = -1;
     if (g.mode == 2) {
       if (p < g.ncols) s = d = p;
-    } else if (p < np) {
+    } else if (p < (g.pend ? g.pend : np)) {
       const int px = p >> (2 * pl), py = (p >> pl) & (pn - 1), pz = p & (pn - 1);
       const int c = ((((2 * px + ((o >> 2) & 1)) * cn) + 2 * py + ((o >> 1) & 1)) * cn) + 2 * pz + (o & 1);
       if (g.mode == 0) {

@@ -80,6 +80,7 @@ struct HaloArgs {
   int lvl0;                          // first level of a k_level_absmax / k_pack_mult16 launch (grid.y = levels)
   int own_x0, own_x1, own_depth;     // k_level_absmax over one rank's leaf x-slab (own_x1 == 0: whole level)
   int stagger;                       // terms issuer 1 runs behind issuer 0 (A-ring order, see hm_aseq)
+  int pk_r0[DMAX + 2], pk_r1[DMAX + 2];  // k_pack_mult16: padded rows [r0, r1) per level (r1 == 0: all)
 };
 
 // A-ring slot sequence of issuer par's u-th term (u counts its terms over all
@@ -224,8 +225,9 @@ __global__ void k_pack_mult16(HaloArgs g) {
   const int level = blockIdx.y + g.lvl0, sc = blockIdx.z;
   const int prow = hm_plane_rows(level);
   const int t = blockIdx.x * blockDim.x + threadIdx.x;
-  const int r = t >> 3, kc = t & 7;
-  if (r >= prow) return;
+  // a slab decomposition packs only the x-rows its owned targets' windows read
+  const int r = (t >> 3) + g.pk_r0[level], kc = t & 7;
+  if (r >= (g.pk_r1[level] ? g.pk_r1[level] : prow)) return;
   const int h = 1 << (level - 1), Z = h + 2, YZ = Z * Z;
   const int x = ((r / YZ - 1) + h) & (h - 1), y = (((r / Z) % Z - 1) + h) & (h - 1), z = ((r % Z - 1) + h) & (h - 1);
   const int box = ((((2 * x + ((sc >> 2) & 1)) << level) | (2 * y + ((sc >> 1) & 1))) << level) |
