@@ -1182,6 +1182,11 @@ struct lfmm_plan {
     ta.cnt = tr_cnt.as<int>();
     launch(ST_M2M, [&] { tr_launch<float>(ta, 1 << (3 * l), 8, st); });
   }
+  // leaves of this rank's slab (all of them without a decomposition); the
+  // leaf kernels start their grid at leaf plane own_x0
+  int64_t own_leaves() const {
+    return (int64_t)(std::min(own_x1, 1 << depth) - own_x0) << (2 * depth);
+  }
   // parent columns of level pl this rank computes: its x-slab when a slab
   // decomposition owns the level (pl >= dist_lg), else the whole level
   void owned_parents(int pl, int& p0, int& pend) const {
@@ -1318,7 +1323,7 @@ struct lfmm_plan {
                                                      p2p_scalar ? nullptr : pair_b());
     });
     const int periodic = (flags & LFMM_F_PERIODIC_NEAR) ? 1 : 0;
-    const unsigned lb = nblk(nleaf, P2P_WARPS);
+    const unsigned lb = nblk(own_leaves(), P2P_WARPS);
     const bool side = !profiling;
     if (side && !near_stream) {
       int lo = 0, hi = 0;
@@ -1336,7 +1341,7 @@ struct lfmm_plan {
     launch(ST_P2P, [&] {
       cudaStream_t stream = pst;
       if (sizeof(T) == 4 && !p2p_scalar) {
-        const unsigned lb2 = nblk(nleaf, P2P2_WARPS);
+        const unsigned lb2 = nblk(own_leaves(), P2P2_WARPS);
         if (grad)
           k_p2p2<true><<<lb2, P2P2_WARPS * 32, P2P2_SMEM, stream>>>(reinterpret_cast<const float4*>(xq.p), pair_a(), pair_b(), leaf_start.as<int>(),
                                                                       depth, (float)size, periodic, vnear.as<float>(),
@@ -1360,12 +1365,14 @@ struct lfmm_plan {
     }
     launch(ST_P2M, [&] {
       if (p == 10) {
-        k_p2m_c<T, 10><<<nblk(nleaf, EXP_WARPS), EXP_WARPS * 32, 0, stream>>>(
-            xq.as<vec4_t<T>>(), leaf_start.as<int>(), depth, (T)(1.0 / size), ncp, M + level_off[depth] * ncp);
+        k_p2m_c<T, 10><<<nblk(own_leaves(), EXP_WARPS), EXP_WARPS * 32, 0, stream>>>(
+            xq.as<vec4_t<T>>(), leaf_start.as<int>(), depth, (T)(1.0 / size), ncp, M + level_off[depth] * ncp,
+            own_x0);
         return;
       }
-      k_p2m<T><<<nblk(nleaf, EXP_WARPS), EXP_WARPS * 32, 0, stream>>>(
-          xq.as<vec4_t<T>>(), leaf_start.as<int>(), depth, p, (T)(1.0 / size), ncp, M + level_off[depth] * ncp);
+      k_p2m<T><<<nblk(own_leaves(), EXP_WARPS), EXP_WARPS * 32, 0, stream>>>(
+          xq.as<vec4_t<T>>(), leaf_start.as<int>(), depth, p, (T)(1.0 / size), ncp, M + level_off[depth] * ncp,
+          own_x0);
     });
     if (sizeof(T) == 4 && far_overlap()) {
       far_done = true;
@@ -1527,32 +1534,32 @@ struct lfmm_plan {
       launch(ST_L2P, [&] {
         if (p == 10 && sizeof(T) == 4) {
           if (grad)
-            k_l2p_f2<true, 10><<<nblk(nleaf, EXP_WARPS), EXP_WARPS * 32, 0, stream>>>(
+            k_l2p_f2<true, 10><<<nblk(own_leaves(), EXP_WARPS), EXP_WARPS * 32, 0, stream>>>(
                 reinterpret_cast<const float4*>(xq.p), leaf_start.as<int>(), depth, (float)size, ncp,
                 reinterpret_cast<const float*>(Lc + level_off[depth] * ncp), vfar.as<float>(), gfar.as<float>(), own_x0, own_x1);
           else
-            k_l2p_f2<false, 10><<<nblk(nleaf, EXP_WARPS), EXP_WARPS * 32, 0, stream>>>(
+            k_l2p_f2<false, 10><<<nblk(own_leaves(), EXP_WARPS), EXP_WARPS * 32, 0, stream>>>(
                 reinterpret_cast<const float4*>(xq.p), leaf_start.as<int>(), depth, (float)size, ncp,
                 reinterpret_cast<const float*>(Lc + level_off[depth] * ncp), vfar.as<float>(), gfar.as<float>(), own_x0, own_x1);
           return;
         }
         if (p == 10) {
           if (grad)
-            k_l2p_c<T, true, 10><<<nblk(nleaf, EXP_WARPS), EXP_WARPS * 32, 0, stream>>>(
+            k_l2p_c<T, true, 10><<<nblk(own_leaves(), EXP_WARPS), EXP_WARPS * 32, 0, stream>>>(
                 xq.as<vec4_t<T>>(), leaf_start.as<int>(), depth, tsize, ncp, Lc + level_off[depth] * ncp,
                 vfar.as<T>(), gfar.as<T>(), own_x0, own_x1);
           else
-            k_l2p_c<T, false, 10><<<nblk(nleaf, EXP_WARPS), EXP_WARPS * 32, 0, stream>>>(
+            k_l2p_c<T, false, 10><<<nblk(own_leaves(), EXP_WARPS), EXP_WARPS * 32, 0, stream>>>(
                 xq.as<vec4_t<T>>(), leaf_start.as<int>(), depth, tsize, ncp, Lc + level_off[depth] * ncp,
                 vfar.as<T>(), gfar.as<T>(), own_x0, own_x1);
           return;
         }
         if (grad)
-          k_l2p<T, true><<<nblk(nleaf, warps), warps * 32, smem, stream>>>(
+          k_l2p<T, true><<<nblk(own_leaves(), warps), warps * 32, smem, stream>>>(
               xq.as<vec4_t<T>>(), leaf_start.as<int>(), depth, p, tsize, ncp, Lc + level_off[depth] * ncp,
               vfar.as<T>(), gfar.as<T>(), own_x0, own_x1);
         else
-          k_l2p<T, false><<<nblk(nleaf, warps), warps * 32, smem, stream>>>(
+          k_l2p<T, false><<<nblk(own_leaves(), warps), warps * 32, smem, stream>>>(
               xq.as<vec4_t<T>>(), leaf_start.as<int>(), depth, p, tsize, ncp, Lc + level_off[depth] * ncp,
               vfar.as<T>(), gfar.as<T>(), own_x0, own_x1);
       });

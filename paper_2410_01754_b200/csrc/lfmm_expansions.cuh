@@ -23,10 +23,10 @@ template <class T>
 __global__ void __launch_bounds__(EXP_WARPS * 32) k_p2m(const vec4_t<T>* __restrict__ xq,
                                                         const int* __restrict__ leaf_start, int depth,
                                                         int p, T inv_size, int ncp,
-                                                        T* __restrict__ mult) {
+                                                        T* __restrict__ mult, int x0) {
   __shared__ T buf[EXP_WARPS][32][33];
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-  const int b = blockIdx.x * EXP_WARPS + w;
+  const int b = (x0 << (2 * depth)) + blockIdx.x * EXP_WARPS + w;  // grid from the rank's first leaf plane
   const int nleaf = 1 << (3 * depth);
   if (b >= nleaf) return;
   T* out = mult + (size_t)b * ncp;
@@ -81,13 +81,13 @@ __global__ void __launch_bounds__(EXP_WARPS * 32) k_p2m(const vec4_t<T>* __restr
 template <class T, int P>
 __global__ void __launch_bounds__(EXP_WARPS * 32) k_p2m_c(const vec4_t<T>* __restrict__ xq,
                                                           const int* __restrict__ leaf_start, int depth,
-                                                          T inv_size, int ncp, T* __restrict__ mult) {
+                                                          T inv_size, int ncp, T* __restrict__ mult, int x0) {
   constexpr int NC = (P + 1) * (P + 1);
   constexpr int NF = (NC + 31) / 32;  // flushes of 32 coefficients
   constexpr int TBS = sizeof(T) == 4 ? 36 : 33;  // row stride: 16-B rows (LDS.128) for fp32
   __shared__ __align__(16) T buf[EXP_WARPS][32][TBS];
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-  const int b = blockIdx.x * EXP_WARPS + w;
+  const int b = (x0 << (2 * depth)) + blockIdx.x * EXP_WARPS + w;  // grid from the rank's first leaf plane
   const int nleaf = 1 << (3 * depth);
   if (b >= nleaf) return;
   T* out = mult + (size_t)b * ncp;
@@ -186,7 +186,7 @@ __global__ void __launch_bounds__(EXP_WARPS * 32) k_l2p(const vec4_t<T>* __restr
   T* Gx = Lh + nc;
   T* Gy = Gx + ng;
   T* Gz = Gy + ng;
-  const int b = blockIdx.x * (blockDim.x >> 5) + w;
+  const int b = (x0 << (2 * depth)) + blockIdx.x * (blockDim.x >> 5) + w;  // grid from the rank's first leaf plane
   const int nleaf = 1 << (3 * depth);
   if (b >= nleaf) return;
   if ((b >> (2 * depth)) < x0 || (b >> (2 * depth)) >= x1) return;  // leaf outside this rank's slab
@@ -272,7 +272,7 @@ __global__ void __launch_bounds__(EXP_WARPS * 32) k_l2p_c(const vec4_t<T>* __res
   T* Gx = Lh + NC;
   T* Gy = Gx + NG;
   T* Gz = Gy + NG;
-  const int b = blockIdx.x * (blockDim.x >> 5) + w;
+  const int b = (x0 << (2 * depth)) + blockIdx.x * (blockDim.x >> 5) + w;  // grid from the rank's first leaf plane
   const int nleaf = 1 << (3 * depth);
   if (b >= nleaf) return;
   if ((b >> (2 * depth)) < x0 || (b >> (2 * depth)) >= x1) return;  // leaf outside this rank's slab
@@ -358,7 +358,7 @@ __global__ void __launch_bounds__(EXP_WARPS * 32) k_l2p_f2(const float4* __restr
   __shared__ float s0[EXP_WARPS][4][P + 1];                      // m = 0: L, Gx, Gy, Gz
   __shared__ float2 sc[EXP_WARPS][NCC + 3 * NQC];                // m > 0: L | Gx | Gy | Gz
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-  const int b = blockIdx.x * (blockDim.x >> 5) + w;
+  const int b = (x0 << (2 * depth)) + blockIdx.x * (blockDim.x >> 5) + w;  // grid from the rank's first leaf plane
   const int nleaf = 1 << (3 * depth);
   if (b >= nleaf) return;
   if ((b >> (2 * depth)) < x0 || (b >> (2 * depth)) >= x1) return;  // leaf outside this rank's slab

@@ -46,7 +46,7 @@ __global__ void __launch_bounds__(P2P_WARPS * 32) k_p2p(const vec4_t<T>* __restr
                                                         T* __restrict__ gout, int x0, int x1) {
   __shared__ vec4_t<T> tiles[P2P_WARPS][32];
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-  const int b = blockIdx.x * P2P_WARPS + w;
+  const int b = (x0 << (2 * depth)) + blockIdx.x * P2P_WARPS + w;  // grid from the rank's first leaf plane
   const int nleaf = 1 << (3 * depth);
   if (b >= nleaf) return;
   if ((b >> (2 * depth)) < x0 || (b >> (2 * depth)) >= x1) return;  // leaf outside this rank's slab
@@ -188,7 +188,7 @@ __global__ void __launch_bounds__(P2P2_WARPS * 32, LFMM_P2P2_MINB) k_p2p2(const 
   __shared__ int2 s_img[P2P2_WARPS][28];  // {first staged pair, pair count}; sentinel at nimg
   __shared__ float4 s_shift[P2P2_WARPS][27];
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-  const int b = blockIdx.x * P2P2_WARPS + w;
+  const int b = (x0 << (2 * depth)) + blockIdx.x * P2P2_WARPS + w;  // grid from the rank's first leaf plane
   const int nleaf = 1 << (3 * depth);
   if (b >= nleaf) return;
   if ((b >> (2 * depth)) < x0 || (b >> (2 * depth)) >= x1) return;  // leaf outside this rank's slab
