@@ -445,7 +445,8 @@ class DistributedSolver:
         pos_l, q_l, gid_l, n_own = self._exchange_particles(positions.contiguous(), charges.contiguous(),
                                                             global_ids)
         n_loc = pos_l.shape[0]
-        self._ensure_plan(pos_l.cpu().numpy())
+        if self.plan is None:  # positions reach the host once, for the plan's setup
+            self._ensure_plan(pos_l.cpu().numpy())
         plan = self.plan
         plan.set_count(n_loc)
         n_sites = 0
