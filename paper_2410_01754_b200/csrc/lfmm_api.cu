@@ -619,6 +619,8 @@ struct lfmm_plan {
   DevBuf ops16, hm_inv_r, hm_inv_c, hm_jobs, hm_level_max, mult16;
   int64_t m16_off[DMAX + 2] = {0};
   int hm_njobs = 0, hm_rw_cap = 0, hm_lsplit = 1, hm_nbig = 0, hm_stagger = 8, hm_astages = HM_ASTAGES;
+  int hm_groups_big = 2;    // M2L jobs (partial slots) per tile at levels >= 4: 4 or 2 (LFMM_HM_GROUPS)
+  int hm_groups_small = 8;  // ... at levels < 4: 8, 4 or 2 (LFMM_HM_GROUPS_SMALL)
   DevBuf mult, loc, partial, ops_m2l, ops_m2m, ops_l2l, ops_lat, lat64t;
   std::vector<double2> lat_unit;  // unit-box complex lattice operator (nc x nc)
   // solve work
@@ -1011,7 +1013,7 @@ struct lfmm_plan {
     std::vector<int4> jobs;
     int64_t off = 0;
     hm_rw_cap = 0;
-    for (int l = depth; l >= 1; --l) nsplit[l] = (l >= 4) ? 4 : 8;
+    for (int l = depth; l >= 1; --l) nsplit[l] = (l >= 4) ? hm_groups_big : hm_groups_small;
     for (int l = 1; l <= depth; ++l) {
       part_off[l] = off;
       off += (int64_t)nsplit[l] << (3 * l);
@@ -1884,6 +1886,11 @@ int lfmm_plan_create(const double* positions, int64_t n, double box_length, int 
       pl->p2p_scalar = penv && std::string(penv) == "scalar";
       const char* fenv = std::getenv("LFMM_FAR");
       pl->far_serial = fenv && std::string(fenv) == "serial";
+      const char* genv = std::getenv("LFMM_HM_GROUPS");
+      if (genv && (std::atoi(genv) == 2 || std::atoi(genv) == 4)) pl->hm_groups_big = std::atoi(genv);
+      const char* gsenv = std::getenv("LFMM_HM_GROUPS_SMALL");
+      if (gsenv && (std::atoi(gsenv) == 2 || std::atoi(gsenv) == 4 || std::atoi(gsenv) == 8))
+        pl->hm_groups_small = std::atoi(gsenv);
       const char* senv = std::getenv("LFMM_HM_STAGGER");
       if (senv) pl->hm_stagger = std::min(16, std::max(0, std::atoi(senv)));  // <= 19 (the shortest term list)
     }

@@ -101,10 +101,13 @@ __host__ inline size_t hm_smem_bytes(int rw_cap, int astages = HM_ASTAGES) {
 }
 
 // group g of G: relative parities (tc ^ sc) it covers
+// (G = 8: one class per job; 4: the pairs (0,7) (1,6) (2,5) (4,3); 2: two
+// pairs per job)
 __device__ __forceinline__ int hm_group_rel(int G, int g, int k) {
   if (G == 8) return g;
-  const int r = (g == 3) ? 4 : g;  // pairs (0,7) (1,6) (2,5) (4,3)
-  return k == 0 ? r : (r ^ 7);
+  const int pi = (G == 4) ? g : 2 * g + (k >> 1);
+  const int r = (pi == 3) ? 4 : pi;
+  return (k & 1) == 0 ? r : (r ^ 7);
 }
 
 __device__ __forceinline__ uint64_t hm_desc(uint32_t saddr, uint32_t lbo, uint32_t sbo) {
@@ -299,9 +302,9 @@ __global__ void __launch_bounds__(HM_THREADS, 1) k_m2l_halo(HaloArgs g) {
   __shared__ __align__(8) uint64_t a_full[AS], a_empty[AS];
   __shared__ uint32_t tmem_base_sh;
   // the job's (tc, sc) term lists: B row offset (16-B units) and operator row
-  __shared__ uint32_t s_boff[2][27];
-  __shared__ int s_orow[2][27];
-  __shared__ int s_nt[2];
+  __shared__ uint32_t s_boff[4][27];
+  __shared__ int s_orow[4][27];
+  __shared__ int s_nt[4];
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int4 job = g.jobs[blockIdx.x];
@@ -309,7 +312,7 @@ __global__ void __launch_bounds__(HM_THREADS, 1) k_m2l_halo(HaloArgs g) {
   const int t0 = job.y, N = job.z;
   const int h = 1 << (level - 1), Z = h + 2, YZ = Z * Z;
   const int rw = hm_rw(N, Z);
-  const int nsc = (G == 8) ? 1 : 2;
+  const int nsc = 8 / G;  // source classes per job
   const int niter = nsc * HM_NKC;
   const size_t bufb = hm_buf_bytes(g.rw_cap);
   unsigned char* abase = smem + 2 * bufb;
@@ -327,7 +330,7 @@ __global__ void __launch_bounds__(HM_THREADS, 1) k_m2l_halo(HaloArgs g) {
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
-  if (tid >= 64 && tid < 64 + 2 * 27) {
+  if (tid >= 64 && tid < 64 + 4 * 27) {
     const int k = (tid - 64) / 27, t = (tid - 64) % 27;
     if (k < nsc) {
       const int sc = tc ^ hm_group_rel(G, grp, k);
@@ -405,7 +408,8 @@ __global__ void __launch_bounds__(HM_THREADS, 1) k_m2l_halo(HaloArgs g) {
       // descriptors are advanced by adding (bytes >> 4) to the start-address
       // field (shared addresses < 256 KB: no carry out of its 14 bits)
       const uint64_t a_desc0 = hm_desc(smem_u32(abase), 128, 256);
-      const int T = (HM_NKC / 2) * (s_nt[0] + (nsc > 1 ? s_nt[1] : 0));
+      int T = 0;
+      for (int k = 0; k < nsc; ++k) T += (HM_NKC / 2) * s_nt[k];
       const int D = min(min(g.stagger, AS - 6), T);  // D >= AS + 2 was seen to deadlock
       int u = 0;  // this issuer's terms so far
       for (int it0 = 0; it0 < niter; it0 += 2) {
@@ -461,7 +465,8 @@ __global__ void __launch_bounds__(HM_THREADS, 1) k_m2l_halo(HaloArgs g) {
   } else if (warp == 10) {
     // ================================================= A loader ========
     if (lane == 0) {
-      const int T = (HM_NKC / 2) * (s_nt[0] + (nsc > 1 ? s_nt[1] : 0));
+      int T = 0;
+      for (int k = 0; k < nsc; ++k) T += (HM_NKC / 2) * s_nt[k];
       const int D = min(min(g.stagger, AS - 6), T);  // D >= AS + 2 was seen to deadlock
       // one cursor per issuer: (iteration pair it0, term t)
       int c_it0[2] = {0, 0}, c_t[2] = {0, 0};
