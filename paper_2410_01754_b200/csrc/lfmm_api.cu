@@ -2352,7 +2352,9 @@ int lfmm_step(lfmm_plan* plan, const double* positions, const double* charges, c
       if (!plan->hi_stream) {
         int lo = 0, hi = 0;
         LFMM_CUDA(cudaDeviceGetStreamPriorityRange(&lo, &hi));
-        LFMM_CUDA(cudaStreamCreateWithPriority(&plan->hi_stream, cudaStreamNonBlocking, lo));
+        const char* henv = std::getenv("LFMM_HI_PRIO");
+        LFMM_CUDA(cudaStreamCreateWithPriority(&plan->hi_stream, cudaStreamNonBlocking,
+                                               (henv && std::string(henv) == "high") ? hi : lo));
         LFMM_CUDA(cudaEventCreateWithFlags(&plan->ev_hi_in, cudaEventDisableTiming));
         LFMM_CUDA(cudaEventCreateWithFlags(&plan->ev_hi_out, cudaEventDisableTiming));
       }
