@@ -616,11 +616,12 @@ struct lfmm_plan {
   // solve, 1 up to the owned multipoles, 2 the rest.
   int own_x0 = 0, own_x1 = 1 << 30, dist_lg = 0, dist_phase = 0;
   DevBuf ops_tc, up_part, up_cnt, counters;
-  DevBuf ops16, hm_inv_r, hm_inv_c, hm_jobs, hm_level_max, mult16;
+  DevBuf ops16, hm_inv_r, hm_inv_c, hm_jobs, hm_level_max, mult16, ops_m2l_t;
   int64_t m16_off[DMAX + 2] = {0};
   int hm_njobs = 0, hm_rw_cap = 0, hm_lsplit = 1, hm_nbig = 0, hm_stagger = 8, hm_astages = HM_ASTAGES;
   int hm_groups_big = 2;    // M2L jobs (partial slots) per tile at levels >= 4: 4 or 2 (LFMM_HM_GROUPS)
   int hm_groups_small = 8;  // ... at levels < 4: 8, 4 or 2 (LFMM_HM_GROUPS_SMALL)
+  bool m2l_f64_simt = false;  // fp64 M2L on k_gemm_gather instead of k_m2l_f64 (LFMM_M2L64=gather)
   DevBuf mult, loc, partial, ops_m2l, ops_m2m, ops_l2l, ops_lat, lat64t;
   std::vector<double2> lat_unit;  // unit-box complex lattice operator (nc x nc)
   // solve work
@@ -865,6 +866,17 @@ struct lfmm_plan {
                                                              vals.as<double2>());
       });
       realify<T>(OP_M2L, NOFF, vals.as<double2>(), nc2, 1.0, 0, 1.0, ops_m2l.as<T>());
+      if (sizeof(T) == 8 && ncp == 128) {  // [k][row] copy for k_m2l_f64
+        ops_m2l_t.ensure(opb * NOFF);
+        launch(ST_SETUP, [&] {
+          k_transpose_ops<T><<<nblk((int64_t)NOFF * ncp * ncp, 256), 256, 0, stream>>>(ops_m2l.as<T>(),
+                                                                                  ops_m2l_t.as<T>(), ncp, NOFF);
+        });
+        static std::once_flag f64_once;
+        std::call_once(f64_once, [] {
+          LFMM_CUDA(cudaFuncSetAttribute(k_m2l_f64, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)F64_SMEM));
+        });
+      }
       LFMM_CUDA(cudaStreamSynchronize(stream));
     }
     // M2M (parent edge 1, child 1/2): A(d) = gather R(-d), d = (0.5-oct)/2;
@@ -1504,8 +1516,13 @@ struct lfmm_plan {
       } else {
         ga.mode = GEMM_M2L;
         ga.level = 0;
-        dim3 grid(ga.job_start[depth + 1], rowb);
-        launch(ST_DOWN, [&] { k_gemm_gather<T><<<grid, G_THREADS, 0, stream>>>(ga); });
+        if (sizeof(T) == 8 && ncp == 128 && !m2l_f64_simt) {
+          ga.ops_m2l_t = ops_m2l_t.p;
+          launch(ST_DOWN, [&] { k_m2l_f64<<<ga.job_start[depth + 1], G_THREADS, F64_SMEM, stream>>>(ga); });
+        } else {
+          dim3 grid(ga.job_start[depth + 1], rowb);
+          launch(ST_DOWN, [&] { k_gemm_gather<T><<<grid, G_THREADS, 0, stream>>>(ga); });
+        }
       }
       for (int l = 1; l <= depth; ++l) {
         if (use_tr) {
@@ -1886,6 +1903,8 @@ int lfmm_plan_create(const double* positions, int64_t n, double box_length, int 
       pl->p2p_scalar = penv && std::string(penv) == "scalar";
       const char* fenv = std::getenv("LFMM_FAR");
       pl->far_serial = fenv && std::string(fenv) == "serial";
+      const char* m64 = std::getenv("LFMM_M2L64");
+      pl->m2l_f64_simt = m64 && std::string(m64) == "gather";
       const char* genv = std::getenv("LFMM_HM_GROUPS");
       if (genv && (std::atoi(genv) == 2 || std::atoi(genv) == 4)) pl->hm_groups_big = std::atoi(genv);
       const char* gsenv = std::getenv("LFMM_HM_GROUPS_SMALL");

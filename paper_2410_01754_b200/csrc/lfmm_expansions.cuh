@@ -548,6 +548,7 @@ struct GemmArgs {
   void* loc;          // all levels
   void* partial;      // M2L partial slots
   const void* ops_m2l;   // [316][ncp][ncp]
+  const void* ops_m2l_t; // fp64, ncp == 128: [316][k][row] (k_m2l_f64)
   const void* ops_m2m;   // [8]
   const void* ops_l2l;   // [8]
   const void* ops_lat;   // [1]
@@ -915,6 +916,131 @@ __global__ void __launch_bounds__(G_THREADS) k_gemm_gather(GemmArgs g) {
       }
       if (tid == 0) g.up_cnt[tile * gridDim.y + blockIdx.y] = 0;
     }
+  }
+}
+
+// fp64 M2L (ncp == 128) on the DMMA pipe with a cp.async ring: the same jobs
+// as k_gemm_gather's GEMM_M2L (a tile of 64 same-parity targets x a slice of
+// the 189 terms, one partial slot), K streamed in 16-deep chunks through a
+// 4-stage ring so three chunks are in flight while one is multiplied.
+// A = the term's operator, stored transposed ([k][row]) so a chunk is 16
+// contiguous 1-KB rows; B = the 64 targets' source multipoles, one 128-B run
+// per column (zero-filled for padding columns).  Warp tiles 32 x 32 of
+// mma.sync m8n8k4.f64; every output is one thread's fixed-order sum.
+constexpr int F64_BK = 16, F64_S = 4, F64_AP = GB_M + 8, F64_BP = F64_BK + 4;
+constexpr int F64_STAGE = F64_BK * F64_AP + GB_N * F64_BP;  // doubles per stage
+constexpr size_t F64_SMEM = (size_t)F64_S * F64_STAGE * sizeof(double);
+
+__device__ __forceinline__ void cp16_zfill(uint32_t dst, const void* src, bool valid) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(dst), "l"(src), "r"(valid ? 16 : 0)
+               : "memory");
+}
+
+__global__ void __launch_bounds__(G_THREADS, 2) k_m2l_f64(GemmArgs g) {
+  extern __shared__ __align__(16) double f64_smem[];
+  __shared__ int col_dst[GB_N];
+  const int tid = threadIdx.x, lane = tid & 31, wm = (tid >> 5) & 3, wn = tid >> 7;
+  int level = 1;
+  while (level < g.depth && (int)blockIdx.x >= g.job_start[level + 1]) ++level;
+  const int j = blockIdx.x - g.job_start[level];
+  const int ns = g.nsplit[level];
+  const int tpp = tiles_per_parity(level);
+  const int slot = j % ns, tile = j / ns;
+  const int par = tile / tpp, q0 = (tile % tpp) * GB_N;
+  const int sub = 1 << (level - 1);
+  if (tid < GB_N) col_dst[tid] = (q0 + tid < sub * sub * sub) ? parity_box(level, par, q0 + tid) : -1;
+  const int t0 = (NM2L * slot) / ns, t1 = (NM2L * (slot + 1)) / ns;
+  __syncthreads();
+  const int msk = (1 << level) - 1;
+  const int nk = 128 / F64_BK;
+  const int niter = (t1 - t0) * nk;
+  const double* mult = reinterpret_cast<const double*>(g.mult) + g.level_off[level] * 128;
+  const double* ops_t = reinterpret_cast<const double*>(g.ops_m2l_t);
+  // this thread's two B pieces: column n = c >> 3, 16-B piece u = c & 7
+  int bt[2];
+#pragma unroll
+  for (int h = 0; h < 2; ++h) bt[h] = col_dst[(tid + h * G_THREADS) >> 3];
+  const uint32_t sbase = (uint32_t)__cvta_generic_to_shared(f64_smem);
+
+  auto load = [&](int it, int st) {
+    const int term = t0 + it / nk, k0 = (it % nk) * F64_BK;
+    const char4 o = c_m2l_off[par * NM2L + term];
+    const int row = c_m2l_row[par * NM2L + term];
+    const double* A = ops_t + ((size_t)row * 128 + k0) * 128;
+    const uint32_t sa = sbase + (uint32_t)(st * F64_STAGE) * 8u;
+    const uint32_t sb = sa + (uint32_t)(F64_BK * F64_AP) * 8u;
+#pragma unroll
+    for (int h = 0; h < 4; ++h) {  // A: 16 k-rows x 64 pieces
+      const int c = tid + h * G_THREADS, kr = c >> 6, pc = c & 63;
+      cp16_zfill(sa + (uint32_t)(kr * F64_AP + 2 * pc) * 8u, A + kr * 128 + 2 * pc, true);
+    }
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {  // B: 64 columns x 8 pieces
+      const int c = tid + h * G_THREADS, n = c >> 3, u = c & 7;
+      const int t = bt[h];
+      int src = 0;
+      if (t >= 0) {
+        const int gx = t >> (2 * level), gy = (t >> level) & msk, gz = t & msk;
+        src = ((((gx + o.x) & msk) << level | ((gy + o.y) & msk)) << level) | ((gz + o.z) & msk);
+      }
+      cp16_zfill(sb + (uint32_t)(n * F64_BP + 2 * u) * 8u, mult + (size_t)src * 128 + k0 + 2 * u, t >= 0);
+    }
+  };
+
+  double acc[4][4][2];
+#pragma unroll
+  for (int a = 0; a < 4; ++a)
+#pragma unroll
+    for (int b = 0; b < 4; ++b) acc[a][b][0] = acc[a][b][1] = 0.0;
+#pragma unroll
+  for (int s = 0; s < F64_S - 1; ++s) {
+    if (s < niter) load(s, s);
+    asm volatile("cp.async.commit_group;" ::: "memory");
+  }
+  for (int it = 0; it < niter; ++it) {
+    asm volatile("cp.async.wait_group %0;" ::"n"(F64_S - 2) : "memory");
+    __syncthreads();
+    const double* As = f64_smem + (size_t)(it % F64_S) * F64_STAGE;
+    const double* Bs = As + F64_BK * F64_AP;
+#pragma unroll
+    for (int ks = 0; ks < F64_BK; ks += 4) {
+      double af[4], bf[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        af[u] = As[(ks + (lane & 3)) * F64_AP + wm * 32 + u * 8 + (lane >> 2)];
+        bf[u] = Bs[(wn * 32 + u * 8 + (lane >> 2)) * F64_BP + ks + (lane & 3)];
+      }
+#pragma unroll
+      for (int mt = 0; mt < 4; ++mt)
+#pragma unroll
+        for (int nt = 0; nt < 4; ++nt)
+          asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0, %1}, {%2}, {%3}, {%0, %1};"
+                       : "+d"(acc[mt][nt][0]), "+d"(acc[mt][nt][1])
+                       : "d"(af[mt]), "d"(bf[nt]));
+    }
+    if (it + F64_S - 1 < niter) load(it + F64_S - 1, (it + F64_S - 1) % F64_S);
+    asm volatile("cp.async.commit_group;" ::: "memory");
+  }
+  asm volatile("cp.async.wait_group 0;" ::: "memory");
+  __syncthreads();
+  // ---- epilogue: stage D column-major through shared memory, then every
+  // partial-slot write is a coalesced run along the coefficients ----
+  double* stage = f64_smem;  // 64 x 128 doubles = 64 KB < F64_SMEM
+#pragma unroll
+  for (int mt = 0; mt < 4; ++mt)
+#pragma unroll
+    for (int nt = 0; nt < 4; ++nt)
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        const int col = wn * 32 + nt * 8 + 2 * (lane & 3) + e, r = wm * 32 + mt * 8 + (lane >> 2);
+        stage[col * GB_M + r] = acc[mt][nt][e];
+      }
+  __syncthreads();
+  const size_t nbox_l = (size_t)1 << (3 * level);
+  double* out = reinterpret_cast<double*>(g.partial) + ((size_t)g.part_off[level] + (size_t)slot * nbox_l) * 128;
+  for (int e = tid; e < GB_N * GB_M; e += G_THREADS) {
+    const int box = col_dst[e / GB_M];
+    if (box >= 0) out[(size_t)box * 128 + (e % GB_M)] = stage[e];
   }
 }
 
