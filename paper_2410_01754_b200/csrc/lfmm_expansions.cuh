@@ -927,7 +927,16 @@ __global__ void __launch_bounds__(G_THREADS) k_gemm_gather(GemmArgs g) {
 // contiguous 1-KB rows; B = the 64 targets' source multipoles, one 128-B run
 // per column (zero-filled for padding columns).  Warp tiles 32 x 32 of
 // mma.sync m8n8k4.f64; every output is one thread's fixed-order sum.
-constexpr int F64_BK = 16, F64_S = 4, F64_AP = GB_M + 8, F64_BP = F64_BK + 4;
+#ifndef LFMM_F64_BK
+#define LFMM_F64_BK 16
+#endif
+#ifndef LFMM_F64_S
+#define LFMM_F64_S 4
+#endif
+#ifndef LFMM_F64_MINB
+#define LFMM_F64_MINB 2
+#endif
+constexpr int F64_BK = LFMM_F64_BK, F64_S = LFMM_F64_S, F64_AP = GB_M + 8, F64_BP = F64_BK + 4;
 constexpr int F64_STAGE = F64_BK * F64_AP + GB_N * F64_BP;  // doubles per stage
 constexpr size_t F64_SMEM = (size_t)F64_S * F64_STAGE * sizeof(double);
 
@@ -936,7 +945,7 @@ __device__ __forceinline__ void cp16_zfill(uint32_t dst, const void* src, bool v
                : "memory");
 }
 
-__global__ void __launch_bounds__(G_THREADS, 2) k_m2l_f64(GemmArgs g) {
+__global__ void __launch_bounds__(G_THREADS, LFMM_F64_MINB) k_m2l_f64(GemmArgs g) {
   extern __shared__ __align__(16) double f64_smem[];
   __shared__ int col_dst[GB_N];
   const int tid = threadIdx.x, lane = tid & 31, wm = (tid >> 5) & 3, wn = tid >> 7;
@@ -956,10 +965,10 @@ __global__ void __launch_bounds__(G_THREADS, 2) k_m2l_f64(GemmArgs g) {
   const int niter = (t1 - t0) * nk;
   const double* mult = reinterpret_cast<const double*>(g.mult) + g.level_off[level] * 128;
   const double* ops_t = reinterpret_cast<const double*>(g.ops_m2l_t);
-  // this thread's two B pieces: column n = c >> 3, 16-B piece u = c & 7
-  int bt[2];
+  // this thread's B pieces: column n = c / (BK / 2), 16-B piece u = c % (BK / 2)
+  int bt[F64_BK / 8];
 #pragma unroll
-  for (int h = 0; h < 2; ++h) bt[h] = col_dst[(tid + h * G_THREADS) >> 3];
+  for (int h = 0; h < F64_BK / 8; ++h) bt[h] = col_dst[(tid + h * G_THREADS) / (F64_BK / 2)];
   const uint32_t sbase = (uint32_t)__cvta_generic_to_shared(f64_smem);
 
   auto load = [&](int it, int st) {
@@ -970,13 +979,13 @@ __global__ void __launch_bounds__(G_THREADS, 2) k_m2l_f64(GemmArgs g) {
     const uint32_t sa = sbase + (uint32_t)(st * F64_STAGE) * 8u;
     const uint32_t sb = sa + (uint32_t)(F64_BK * F64_AP) * 8u;
 #pragma unroll
-    for (int h = 0; h < 4; ++h) {  // A: 16 k-rows x 64 pieces
+    for (int h = 0; h < F64_BK / 4; ++h) {  // A: F64_BK k-rows x 64 pieces
       const int c = tid + h * G_THREADS, kr = c >> 6, pc = c & 63;
       cp16_zfill(sa + (uint32_t)(kr * F64_AP + 2 * pc) * 8u, A + kr * 128 + 2 * pc, true);
     }
 #pragma unroll
-    for (int h = 0; h < 2; ++h) {  // B: 64 columns x 8 pieces
-      const int c = tid + h * G_THREADS, n = c >> 3, u = c & 7;
+    for (int h = 0; h < F64_BK / 8; ++h) {  // B: 64 columns x F64_BK / 2 pieces
+      const int c = tid + h * G_THREADS, n = c / (F64_BK / 2), u = c % (F64_BK / 2);
       const int t = bt[h];
       int src = 0;
       if (t >= 0) {
