@@ -274,7 +274,7 @@ __global__ void k_finalize(int64_t n, int K, int c, const int* __restrict__ perm
     const double gam = 2.0 * 3.14159265358979323846 / (3.0 * box * box * box);
     const double h = 0.5 * box;
     double vd = 0.0;
-    if (dipole)
+    if (dipole && (out_pot || out_dip))  // the step path outputs forces only: no position reads
       vd = 2.0 * DIPOLE_ETA * gam *
            ((pos_sorted[3 * k] - h) * scal[0] + (pos_sorted[3 * k + 1] - h) * scal[1] +
             (pos_sorted[3 * k + 2] - h) * scal[2]);
