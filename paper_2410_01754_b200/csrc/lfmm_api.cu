@@ -2336,12 +2336,20 @@ int lfmm_step(lfmm_plan* plan, const double* positions, const double* charges, c
   return guarded([&] {
     const int64_t N = plan->N;
     LFMM_REQUIRE(mode == LFMM_MODE_HI || mode == LFMM_MODE_QI, "unknown mode");
-    if (positions) {
+    // device-resident inputs: charges, scale_charges and the HI side work are
+    // issued before the tree build, so the HI kernels (site geometry, lambdas
+    // and blended site charges only) overlap the latency-bound tree kernels;
+    // host inputs keep the positions upload first (the charges upload hides
+    // the tree build)
+    const bool early = io_on_device && positions && !plain && plan->n_sites > 0 && !plan->profiling &&
+                       potentials == nullptr;
+    auto tree = [&] {
       if (plan->fp32)
         plan->build_tree<float>(positions, io_on_device != 0);
       else
         plan->build_tree<double>(positions, io_on_device != 0);
-    }
+    };
+    if (positions && !early) tree();
     plan->ensure_solve_buffers(1, true);
     plan->q_tmp.ensure(sizeof(double) * std::max<int64_t>(N, 1));
     const auto kind = io_on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice;
@@ -2382,7 +2390,15 @@ int lfmm_step(lfmm_plan* plan, const double* positions, const double* charges, c
       cudaStream_t main = plan->stream;
       plan->stream = plan->hi_stream;
       try {
-        gather_site_positions(plan, nullptr, 0);
+        if (early) {  // site atoms straight from the caller's positions (pos_in is filled by the tree build)
+          if (plan->n_site_atoms > 0)
+            plan->launch(ST_HI, [&] {
+              k_gather_site_pos<<<nblk(plan->n_site_atoms, 128), 128, 0, plan->stream>>>(
+                  positions, plan->atom_idx.as<int>(), (int)plan->n_site_atoms, plan->site_pos.as<double>());
+            });
+        } else {
+          gather_site_positions(plan, nullptr, 0);
+        }
         run_hi(plan, mode, nullptr, nullptr);  // C_rho, blend energies, offsets
       } catch (...) {
         plan->stream = main;
@@ -2391,6 +2407,7 @@ int lfmm_step(lfmm_plan* plan, const double* positions, const double* charges, c
       plan->stream = main;
       LFMM_CUDA(cudaEventRecord(plan->ev_hi_out, plan->hi_stream));
     }
+    if (early) tree();
     plan->step_mode = potentials == nullptr;
     plan->run_solve(1, true);
     const bool step_mode = plan->step_mode;
