@@ -1788,8 +1788,17 @@ void run_hi(lfmm_plan* pl, int mode, const double* pot_dev, const double* pot_si
       ta.src = g.rscratch;
       ta.dst = g.uscratch;
       static std::once_flag attr_once;  // process-wide function attribute
-      std::call_once(attr_once, [&] { tr_set_attrs<double>(g.ncp); });
-      pl->launch(ST_HI, [&] { tr_launch<double>(ta, na, 1, pl->stream); });
+      std::call_once(attr_once, [&] {
+        tr_set_attrs<double>(g.ncp);
+        LFMM_CUDA(cudaFuncSetAttribute(k_cols_f64, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)F64_SMEM));
+      });
+      if (pl->m2l_f64_simt)  // LFMM_M2L64=gather: the SIMT translate kernel here too
+        pl->launch(ST_HI, [&] { tr_launch<double>(ta, na, 1, pl->stream); });
+      else
+        pl->launch(ST_HI, [&] {
+          k_cols_f64<<<(unsigned)((na + GB_N - 1) / GB_N), G_THREADS, F64_SMEM, pl->stream>>>(
+              g.lat_t, g.rscratch, g.uscratch, na);
+        });
     } else {
       pl->launch(ST_HI, [&] {
         k_hi_umat<<<nblk((int64_t)na * g.ncp, 128), 128, 0, pl->stream>>>(g.lat_t, g.rscratch, na, ncoef(g.p), g.ncp,

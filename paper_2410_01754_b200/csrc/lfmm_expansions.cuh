@@ -1053,6 +1053,86 @@ __global__ void __launch_bounds__(G_THREADS, LFMM_F64_MINB) k_m2l_f64(GemmArgs g
   }
 }
 
+// dst[:, j] = A src[:, j] for ncols contiguous 128-double columns, fp64 on
+// the DMMA pipe (the HI lattice product U = T1 R over all site atoms): the
+// k_m2l_f64 tile and ring with one operator (A transposed, [k][row]).
+__global__ void __launch_bounds__(G_THREADS, LFMM_F64_MINB) k_cols_f64(const double* __restrict__ ops_t,
+                                                                      const double* __restrict__ src,
+                                                                      double* __restrict__ dst, int ncols) {
+  extern __shared__ __align__(16) double f64_smem[];
+  const int tid = threadIdx.x, lane = tid & 31, wm = (tid >> 5) & 3, wn = tid >> 7;
+  const int c0 = blockIdx.x * GB_N;
+  const int nk = 128 / F64_BK;
+  const uint32_t sbase = (uint32_t)__cvta_generic_to_shared(f64_smem);
+  auto load = [&](int it, int st) {
+    const int k0 = it * F64_BK;
+    const uint32_t sa = sbase + (uint32_t)(st * F64_STAGE) * 8u;
+    const uint32_t sb = sa + (uint32_t)(F64_BK * F64_AP) * 8u;
+#pragma unroll
+    for (int h = 0; h < F64_BK / 4; ++h) {
+      const int c = tid + h * G_THREADS, kr = c >> 6, pc = c & 63;
+      cp16_zfill(sa + (uint32_t)(kr * F64_AP + 2 * pc) * 8u, ops_t + (size_t)(k0 + kr) * 128 + 2 * pc, true);
+    }
+#pragma unroll
+    for (int h = 0; h < F64_BK / 8; ++h) {
+      const int c = tid + h * G_THREADS, n = c / (F64_BK / 2), u = c % (F64_BK / 2);
+      const bool ok = c0 + n < ncols;
+      cp16_zfill(sb + (uint32_t)(n * F64_BP + 2 * u) * 8u, src + (size_t)(ok ? c0 + n : 0) * 128 + k0 + 2 * u, ok);
+    }
+  };
+  double acc[4][4][2];
+#pragma unroll
+  for (int a = 0; a < 4; ++a)
+#pragma unroll
+    for (int b = 0; b < 4; ++b) acc[a][b][0] = acc[a][b][1] = 0.0;
+#pragma unroll
+  for (int s = 0; s < F64_S - 1; ++s) {
+    if (s < nk) load(s, s);
+    asm volatile("cp.async.commit_group;" ::: "memory");
+  }
+  for (int it = 0; it < nk; ++it) {
+    asm volatile("cp.async.wait_group %0;" ::"n"(F64_S - 2) : "memory");
+    __syncthreads();
+    const double* As = f64_smem + (size_t)(it % F64_S) * F64_STAGE;
+    const double* Bs = As + F64_BK * F64_AP;
+#pragma unroll
+    for (int ks = 0; ks < F64_BK; ks += 4) {
+      double af[4], bf[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        af[u] = As[(ks + (lane & 3)) * F64_AP + wm * 32 + u * 8 + (lane >> 2)];
+        bf[u] = Bs[(wn * 32 + u * 8 + (lane >> 2)) * F64_BP + ks + (lane & 3)];
+      }
+#pragma unroll
+      for (int mt = 0; mt < 4; ++mt)
+#pragma unroll
+        for (int nt = 0; nt < 4; ++nt)
+          asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0, %1}, {%2}, {%3}, {%0, %1};"
+                       : "+d"(acc[mt][nt][0]), "+d"(acc[mt][nt][1])
+                       : "d"(af[mt]), "d"(bf[nt]));
+    }
+    if (it + F64_S - 1 < nk) load(it + F64_S - 1, (it + F64_S - 1) % F64_S);
+    asm volatile("cp.async.commit_group;" ::: "memory");
+  }
+  asm volatile("cp.async.wait_group 0;" ::: "memory");
+  __syncthreads();
+  double* stage = f64_smem;
+#pragma unroll
+  for (int mt = 0; mt < 4; ++mt)
+#pragma unroll
+    for (int nt = 0; nt < 4; ++nt)
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        const int col = wn * 32 + nt * 8 + 2 * (lane & 3) + e, r = wm * 32 + mt * 8 + (lane >> 2);
+        stage[col * GB_M + r] = acc[mt][nt][e];
+      }
+  __syncthreads();
+  for (int e = tid; e < GB_N * GB_M; e += G_THREADS) {
+    const int col = c0 + e / GB_M;
+    if (col < ncols) dst[(size_t)col * 128 + (e % GB_M)] = stage[e];
+  }
+}
+
 }  // namespace lfmm
 
 namespace lfmm {
