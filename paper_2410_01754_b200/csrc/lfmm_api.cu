@@ -1809,7 +1809,7 @@ void run_hi(lfmm_plan* pl, int mode, const double* pot_dev, const double* pot_si
   const int ns = pl->ns_max;
   const bool lat_smem = mode == LFMM_MODE_HI && g.images_full && g.lat_t;
   const size_t smem = sizeof(double) * ((size_t)ns + 2 * (size_t)ns * ns + 3 * (size_t)ns +
-                                        (lat_smem ? 2 * (size_t)ns * g.ncp : 0));
+                                        (lat_smem ? 2 * (size_t)ns * (g.ncp + 1) : 0));
   if (smem > 48 * 1024) {  // raise only (process-wide attribute, see halo_smem_attr)
     static std::mutex mu;
     static size_t cur = 48 * 1024;

@@ -141,43 +141,47 @@ __global__ void __launch_bounds__(HI_THREADS) k_hi_site(HiArgs g) {
     // site atoms (k_hi_rvec + one batched GEMM, k_translate mode 2); staged
     // in shared memory, G_st = (1/L) <R_s, U_t>_packed, thread per pair ----
     if (lattice) {
-      double* Rs = pos + 3 * ns;         // ns x ncp
-      double* Us = Rs + (size_t)ns * ncp;  // ns x ncp
+      // rows padded to ncp + 1 doubles: the lanes of a warp read different
+      // atoms' rows at the same coefficient, which then fall in different banks
+      const int rs = ncp + 1;
+      double* Rs = pos + 3 * ns;              // ns x rs
+      double* Us = Rs + (size_t)ns * rs;      // ns x rs
       const double* R = g.rscratch + (size_t)a0 * ncp;
       const double* U = g.uscratch + (size_t)a0 * ncp;
-      {  // every load in flight at once (16-B vectors, unrolled)
-        const int nv = ns * ncp / 2;
-        const double2* R2 = reinterpret_cast<const double2*>(R);
-        const double2* U2 = reinterpret_cast<const double2*>(U);
-        double2* Rs2 = reinterpret_cast<double2*>(Rs);
-        double2* Us2 = reinterpret_cast<double2*>(Us);
-        for (int e0 = tid; e0 < nv; e0 += 8 * HI_THREADS) {
-          double2 a[8], b[8];
+      const int nv = ns * ncp;
+      for (int e0 = tid; e0 < nv; e0 += 4 * HI_THREADS) {  // four loads of each in flight
+        double a[4], b[4];
 #pragma unroll
-          for (int u = 0; u < 8; ++u)
-            if (e0 + u * HI_THREADS < nv) {
-              a[u] = R2[e0 + u * HI_THREADS];
-              b[u] = U2[e0 + u * HI_THREADS];
-            }
+        for (int u = 0; u < 4; ++u)
+          if (e0 + u * HI_THREADS < nv) {
+            a[u] = R[e0 + u * HI_THREADS];
+            b[u] = U[e0 + u * HI_THREADS];
+          }
 #pragma unroll
-          for (int u = 0; u < 8; ++u)
-            if (e0 + u * HI_THREADS < nv) {
-              Rs2[e0 + u * HI_THREADS] = a[u];
-              Us2[e0 + u * HI_THREADS] = b[u];
-            }
-        }
+        for (int u = 0; u < 4; ++u)
+          if (e0 + u * HI_THREADS < nv) {
+            const int e = e0 + u * HI_THREADS, row = e / ncp, col = e - row * ncp;
+            Rs[row * rs + col] = a[u];
+            Us[row * rs + col] = b[u];
+          }
       }
       __syncthreads();
       const double invL = 1.0 / L;
       for (int e = tid; e < ns * ns; e += blockDim.x) {
         const int i = e / ns, j = e % ns;
-        const double* a = Rs + (size_t)i * ncp;
-        const double* b = Us + (size_t)j * ncp;
+        const double* a = Rs + (size_t)i * rs;
+        const double* b = Us + (size_t)j * rs;
         double v = 0.0;
         for (int c = 0; c <= p; ++c) v = fma(a[c], b[c], v);  // m = 0 block
-        double w2 = 0.0;
-        for (int c = p + 1; c < nc; c += 2) w2 = fma(a[c], b[c], fma(-a[c + 1], b[c + 1], w2));
-        GG[e] = (v + 2.0 * w2) * invL;
+        // m > 0 pairs: two interleaved chains, combined in a fixed order
+        double w0 = 0.0, w1 = 0.0;
+        int c = p + 1;
+        for (; c + 3 < nc; c += 4) {
+          w0 = fma(a[c], b[c], fma(-a[c + 1], b[c + 1], w0));
+          w1 = fma(a[c + 2], b[c + 2], fma(-a[c + 3], b[c + 3], w1));
+        }
+        for (; c < nc; c += 2) w0 = fma(a[c], b[c], fma(-a[c + 1], b[c + 1], w0));
+        GG[e] = (v + 2.0 * (w0 + w1)) * invL;
       }
     }
   }
