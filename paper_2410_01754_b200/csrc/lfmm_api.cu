@@ -597,7 +597,7 @@ struct lfmm_plan {
   int64_t stage_launch[ST_COUNT] = {0};
 
   // tree
-  DevBuf pos_in, pos_wrap, leaf_of, counts, cursor, leaf_start, bucket, perm, inv_perm, pos_sorted, leaf_sorted, xq;
+  DevBuf pos_in, pos_wrap, leaf_of, slot_of, counts, cursor, leaf_start, bucket, perm, inv_perm, pos_sorted, leaf_sorted, xq;
   // fp32 near-field source pairs (k_p2p2): [pair_cap] float4 x/y halves, then [pair_cap] z/q halves
   DevBuf pairs;
   int64_t pair_cap = 0;
@@ -695,9 +695,9 @@ struct lfmm_plan {
       cudaEventDestroy(e.b);
     }
     for (auto e : free_events) cudaEventDestroy(e);
-    DevBuf* hbufs[] = {&ops16, &hm_inv_r, &hm_inv_c, &hm_jobs, &hm_level_max, &mult16, &boxq, &site_pot, &ops_m2m_t, &ops_l2l_t, &ops_lat_t, &tr_cnt};
+    DevBuf* hbufs[] = {&ops16, &hm_inv_r, &hm_inv_c, &hm_jobs, &hm_level_max, &mult16, &boxq, &site_pot, &ops_m2m_t, &ops_l2l_t, &ops_lat_t, &tr_cnt, &ops_m2l_t};
     for (auto* b : hbufs) b->release();
-    DevBuf* bufs[] = {&pos_in, &pos_wrap, &leaf_of, &counts, &cursor, &leaf_start, &bucket, &perm,
+    DevBuf* bufs[] = {&pos_in, &pos_wrap, &leaf_of, &slot_of, &counts, &cursor, &leaf_start, &bucket, &perm,
                       &inv_perm, &pos_sorted, &leaf_sorted, &xq, &mult, &loc, &partial, &ops_tc, &up_part, &up_cnt, &counters, &ops_m2l, &ops_m2m,
                       &ops_l2l, &ops_lat, &lat64t, &q_in, &qs, &vnear, &vfar, &gnear, &gfar, &part,
                       &scal, &epart, &roots, &out_pot, &out_near, &out_far, &out_dip, &out_forces, &energies,
@@ -1137,11 +1137,11 @@ struct lfmm_plan {
     else
       LFMM_CUDA(cudaMemcpyAsync(pos_in.p, positions, sizeof(double) * 3 * N, cudaMemcpyHostToDevice, stream));
     LFMM_CUDA(cudaMemsetAsync(counts.p, 0, sizeof(int) * nleaf, stream));
-    LFMM_CUDA(cudaMemsetAsync(cursor.p, 0, sizeof(int) * nleaf, stream));
     if (N > 0) {
       launch(ST_TREE, [&] {
         k_wrap_cell<<<nblk(N, 256), 256, 0, stream>>>(pos_in.as<double>(), N, L, size, depth,
-                                                       pos_wrap.as<double>(), leaf_of.as<int>(), counts.as<int>());
+                                                       pos_wrap.as<double>(), leaf_of.as<int>(), counts.as<int>(),
+                                                       slot_of.as<int>());
       });
     }
     {
@@ -1157,7 +1157,7 @@ struct lfmm_plan {
     if (N > 0) {
       launch(ST_TREE, [&] {
         k_scatter_leaf<<<nblk(N, 256), 256, 0, stream>>>(leaf_of.as<int>(), N, leaf_start.as<int>(),
-                                                          cursor.as<int>(), bucket.as<int>());
+                                                          slot_of.as<int>(), bucket.as<int>());
       });
       launch(ST_TREE, [&] {
         k_leaf_rank<T><<<nblk((int64_t)nleaf * 32, RANK_WARPS * 32), RANK_WARPS * 32, 0, stream>>>(
@@ -1937,6 +1937,7 @@ int lfmm_plan_create(const double* positions, int64_t n, double box_length, int 
     pl->pos_in.ensure(sizeof(double) * 3 * nn);
     pl->pos_wrap.ensure(sizeof(double) * 3 * nn);
     pl->leaf_of.ensure(sizeof(int) * nn);
+    pl->slot_of.ensure(sizeof(int) * nn);
     pl->counts.ensure(sizeof(int) * pl->nleaf);
     pl->cursor.ensure(sizeof(int) * (pl->nleaf + pl->nleaf / 1024 + 2));
     pl->leaf_start.ensure(sizeof(int) * (pl->nleaf + 1));
@@ -2495,6 +2496,7 @@ int lfmm_plan_set_count(lfmm_plan* plan, int64_t n) {
     plan->pos_in.ensure(sizeof(double) * 3 * nn);
     plan->pos_wrap.ensure(sizeof(double) * 3 * nn);
     plan->leaf_of.ensure(sizeof(int) * nn);
+    plan->slot_of.ensure(sizeof(int) * nn);
     plan->bucket.ensure(sizeof(int) * nn);
     plan->perm.ensure(sizeof(int) * nn);
     plan->inv_perm.ensure(sizeof(int) * nn);

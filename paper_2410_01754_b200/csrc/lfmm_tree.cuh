@@ -27,7 +27,7 @@ __device__ __forceinline__ double np_mod(double a, double b) {
 
 __global__ void k_wrap_cell(const double* __restrict__ pos_in, int64_t n, double box, double size,
                             int depth, double* __restrict__ pos_wrap, int* __restrict__ leaf_of,
-                            int* __restrict__ counts) {
+                            int* __restrict__ counts, int* __restrict__ slot_of) {
   const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (i >= n) return;
   const int nside = 1 << depth;
@@ -44,7 +44,9 @@ __global__ void k_wrap_cell(const double* __restrict__ pos_in, int64_t n, double
   }
   const int leaf = (cell[0] * nside + cell[1]) * nside + cell[2];
   leaf_of[i] = leaf;
-  atomicAdd(&counts[leaf], 1);
+  // the counter's old value is the atom's slot in its leaf bucket (bucket
+  // order is arbitrary: k_leaf_rank orders each leaf by the exact key)
+  slot_of[i] = atomicAdd(&counts[leaf], 1);
 }
 
 // Exclusive scan of counts[0..n) into start[0..n] in three passes:
@@ -108,12 +110,10 @@ __global__ void k_scan_add(int* __restrict__ start, int n, const int* __restrict
 }
 
 __global__ void k_scatter_leaf(const int* __restrict__ leaf_of, int64_t n, const int* __restrict__ start,
-                               int* __restrict__ cursor, int* __restrict__ bucket) {
+                               const int* __restrict__ slot_of, int* __restrict__ bucket) {
   const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (i >= n) return;
-  const int leaf = leaf_of[i];
-  const int slot = atomicAdd(&cursor[leaf], 1);
-  bucket[start[leaf] + slot] = (int)i;
+  bucket[start[leaf_of[i]] + slot_of[i]] = (int)i;
 }
 
 __device__ __forceinline__ bool key_less(double ax, double ay, double az, int ai, double bx, double by,
