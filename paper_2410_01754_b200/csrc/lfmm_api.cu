@@ -1342,7 +1342,9 @@ struct lfmm_plan {
     if (side && !near_stream) {
       int lo = 0, hi = 0;
       LFMM_CUDA(cudaDeviceGetStreamPriorityRange(&lo, &hi));
-      LFMM_CUDA(cudaStreamCreateWithPriority(&near_stream, cudaStreamNonBlocking, lo));
+      const char* nenv = std::getenv("LFMM_P2P_PRIO");  // A/B: the near field at high priority
+      LFMM_CUDA(cudaStreamCreateWithPriority(&near_stream, cudaStreamNonBlocking,
+                                             (nenv && std::string(nenv) == "high") ? hi : lo));
       LFMM_CUDA(cudaEventCreateWithFlags(&ev_near_in, cudaEventDisableTiming));
       LFMM_CUDA(cudaEventCreateWithFlags(&ev_near_out, cudaEventDisableTiming));
     }
