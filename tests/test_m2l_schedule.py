@@ -1,0 +1,63 @@
+"""Host restatement of the tcgen05 M2L job schedule (lfmm_m2l_halo.cuh):
+the A-ring sequence numbers the two MMA issuers compute (hm_aseq) must be
+exactly the order the A loader fills the ring in, and the source-class groups
+of a tile (hm_group_rel) must cover every relative parity once, for every
+group count the plan uses."""
+
+import pytest
+
+HM_NKC = 8
+
+
+def hm_aseq(par, u, D, T):
+    """lfmm_m2l_halo.cuh hm_aseq."""
+    return u + min(max(u - D, 0), T) if par == 0 else min(u + D + 1, T) + u
+
+
+def loader_order(T, D):
+    """The A loader's fill order: step s loads issuer 0's term s, then issuer
+    1's term s - D (k_m2l_halo, A loader warp)."""
+    order = []
+    for s in range(T + D):
+        for par in (0, 1):
+            u = s - par * D
+            if 0 <= u < T:
+                order.append((par, u))
+    return order
+
+
+def hm_group_rel(G, g, k):
+    """lfmm_m2l_halo.cuh hm_group_rel."""
+    if G == 8:
+        return g
+    pi = g if G == 4 else 2 * g + (k >> 1)
+    r = 4 if pi == 3 else pi
+    return r if (k & 1) == 0 else r ^ 7
+
+
+@pytest.mark.parametrize("nts", [(26,), (19, 26), (25, 23), (19,), (23, 19, 26, 25)])
+@pytest.mark.parametrize("D", [0, 4, 8, 12])
+def test_issuer_sequence_matches_loader_order(nts, D):
+    T = (HM_NKC // 2) * sum(nts)
+    D = min(D, T)
+    order = loader_order(T, D)
+    assert len(order) == 2 * T
+    for seq, (par, u) in enumerate(order):
+        assert hm_aseq(par, u, D, T) == seq
+
+
+@pytest.mark.parametrize("G", [8, 4, 2])
+def test_groups_cover_every_source_class_once(G):
+    nsc = 8 // G
+    for tc in range(8):
+        seen = [tc ^ hm_group_rel(G, g, k) for g in range(G) for k in range(nsc)]
+        assert sorted(seen) == list(range(8))
+
+
+def test_stagger_cap_leaves_ring_room():
+    """The kernel caps the lag at AS - 6 (k_m2l_halo<AS>): with the 14- and
+    10-stage rings that is 8 and 4 terms, below the shortest term list (19)."""
+    for AS, default in ((14, 8), (10, 8)):
+        D = min(default, AS - 6)
+        assert D <= 19
+        assert D <= AS - 6
