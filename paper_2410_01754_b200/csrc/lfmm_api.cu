@@ -1778,8 +1778,9 @@ void run_hi(lfmm_plan* pl, int mode, const double* pot_dev, const double* pot_si
     // lattice pair kernel inputs for all site atoms at once: R_t, U_t = T1 R_t
     const int na = (int)pl->n_site_atoms;
     pl->launch(ST_HI, [&] {
-      k_hi_rvec<<<nblk((int64_t)na * (g.p + 1), 128), 128, 0, pl->stream>>>(g.site_pos, na, g.box, g.p, g.ncp,
-                                                                             g.rscratch);
+      const int apb = std::max(1, 128 / (g.p + 1));
+      k_hi_rvec<<<(unsigned)((na + apb - 1) / apb), apb * (g.p + 1), sizeof(double) * apb * g.ncp, pl->stream>>>(
+          g.site_pos, na, g.box, g.p, g.ncp, g.rscratch);
     });
     if (g.ncp == 128) {
       TrArgs ta{};

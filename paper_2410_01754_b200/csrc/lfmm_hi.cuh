@@ -280,15 +280,22 @@ __global__ void __launch_bounds__(HI_THREADS) k_hi_site(HiArgs g) {
 __global__ void k_hi_rvec(const double* __restrict__ site_pos, int n_atoms, double box, int p, int ncp,
                           double* __restrict__ rscratch) {
   // thread per (site atom, order m): the diagonal R_m^m by m complex steps,
-  // then the m column (harmonics.py:62-76), written to its packed slots
-  const int e = blockIdx.x * blockDim.x + threadIdx.x;
-  const int a = e / (p + 1), m = e % (p + 1);
-  if (a >= n_atoms) return;
+  // then the m column (harmonics.py:62-76), written to its packed slots of
+  // the block's rows in shared memory; the block's consecutive atoms' rows
+  // then leave as one coalesced run.  Block = (atoms per block) x (p + 1).
+  extern __shared__ double rv_rows[];  // [atoms per block][ncp]
+  const int apb = blockDim.x / (p + 1);
+  const int la = threadIdx.x / (p + 1), m = threadIdx.x % (p + 1);
+  const int a0 = blockIdx.x * apb, a = a0 + la;
+  const int na_blk = min(apb, n_atoms - a0);
+  for (int c = threadIdx.x; c < na_blk * ncp; c += blockDim.x) rv_rows[c] = 0.0;  // padding slots stay zero
+  __syncthreads();
+  if (la < na_blk) {
   const double invL = 1.0 / box;
   const double x = (site_pos[3 * a] - 0.5 * box) * invL, y = (site_pos[3 * a + 1] - 0.5 * box) * invL,
                z = (site_pos[3 * a + 2] - 0.5 * box) * invL;
   const double r2 = x * x + y * y + z * z;
-  double* Rt = rscratch + (size_t)a * ncp;
+  double* Rt = rv_rows + (size_t)la * ncp;
   double mr = 1.0, mi = 0.0;
   for (int k = 1; k <= m; ++k) {
     const double c = 1.0 / (2.0 * k);
@@ -319,8 +326,10 @@ __global__ void k_hi_rvec(const double* __restrict__ site_pos, int n_atoms, doub
       put(l, nr, ni);
     }
   }
-  if (m == 0)
-    for (int c = (p + 1) * (p + 1); c < ncp; ++c) Rt[c] = 0.0;
+  }
+  __syncthreads();
+  double* out = rscratch + (size_t)a0 * ncp;
+  for (int c = threadIdx.x; c < na_blk * ncp; c += blockDim.x) out[c] = rv_rows[c];
 }
 
 // generic U_t = T1 R_t (any ncp): thread per (site atom, output row)
