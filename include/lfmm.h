@@ -130,6 +130,15 @@ int lfmm_hi(lfmm_plan* plan, const double* lambdas, const int32_t* n_lambda,
             double* c_dipole, double* blend_energy, double* lambda_forces,
             double* energy_offset);
 
+/* HI spatial forces of the site atoms (no reference counterpart: the
+ * reference's only spatial forces are spatial_forces(q~), solver.py:407-427;
+ * SURVEY.md §0.2 and §8c).  out (A,3) f64 in site-table atom order:
+ * -grad_r Delta E_site, Delta E_site = e(q~) - sum_rho w_rho C_rho
+ * (corrections.py:141-143, :179-183) from the last HI-mode lfmm_hi /
+ * lfmm_step call.  The HI-consistent force on a site atom is
+ * spatial_forces(q~) + this term; lfmm_step in HI mode returns the sum. */
+int lfmm_hi_site_forces(lfmm_plan* plan, int io_on_device, double* out);
+
 /* assemble_lambda_forces (corrections.py:221-238) without a plan:
  * S_rho = Q_rho . V[site] (s_values :196-198) and
  * F_k = -sum_rho dw_rho/dlambda_k (S_rho - C_rho)  (k_terms :201-218).
@@ -178,7 +187,9 @@ int lfmm_scale_charges(lfmm_plan* plan, const double* charges,
  * potentials + spatial forces -> HI corrections -> lambda forces.
  * plain != 0 runs the fixed-protonation baseline instead (same positions,
  * `charges` used as is, no lambda machinery).
- * Outputs: energy (1) = E_solve + offset; forces (N,3); lambda_forces (S,4);
+ * Outputs: energy (1) = E_solve + offset; forces (N,3) = -grad E of the
+ * returned energy (spatial_forces(q~) plus, in HI mode, -grad Delta E_site on
+ * the site atoms, see lfmm_hi_site_forces); lambda_forces (S,4);
  * potentials (N) optional. */
 int lfmm_step(lfmm_plan* plan, const double* positions, const double* charges,
               const double* lambdas, const int32_t* n_lambda, int mode,
@@ -227,10 +238,12 @@ int lfmm_dist_phase(lfmm_plan* plan, int phase, const double* positions, const d
  * float bits, DMAX + 2 entries; after phase 1 it holds this rank's slab of the
  * levels >= lg, which the caller max-reduces across ranks before phase 2).
  * ptrs holds 9 entries; level_off (8 entries): first box of each level. */
-int lfmm_dist_buffers(lfmm_plan* plan, void** ptrs, int64_t* level_off);
+int lfmm_dist_buffers(lfmm_plan* plan, void** ptrs, int64_t* level_off, int64_t* ncp);
 
 /* HI corrections + lambda forces for every site from the gathered site-atom
- * potentials (ptrs[4]); site_positions (A x 3, device) caller-supplied. */
+ * potentials (ptrs[4]); site_positions (A x 3, device) caller-supplied.  In
+ * HI mode also adds -grad Delta E_site to the local force rows (ptrs[3]) of
+ * the site atoms this rank holds (lfmm_hi_site_forces). */
 int lfmm_dist_hi(lfmm_plan* plan, const double* site_positions, int mode);
 
 #ifdef __cplusplus

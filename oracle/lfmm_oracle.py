@@ -594,6 +594,55 @@ def hi(positions, charges, box, sites, lam_values, cfg, mode="hi", potentials=No
     return out
 
 
+def hi_site_forces(positions, box, sites, lam_values, cfg, lat):
+    """-grad_r Delta E_site of every site atom (A, 3), site-table order.
+
+    Delta E_site = e(q~) - sum_rho w_rho C_rho (corrections.py:141-143,
+    :179-183) with C_rho = Q_rho (K + G)(q~ - Q_rho/2) + c_dip_rho
+    (:157-193) is a function of the site's own atom positions only; the
+    reference has no spatial gradient of it (its spatial forces are
+    spatial_forces(q~), solver.py:407-427).  Analytic gradient of the same
+    pieces: near_kernel (:46-70), lattice_kernel (:73-77) through
+    harmonics.regular_grad (harmonics.py:119-130), c_dipole (:112-124).
+    Pinned against the reference by central differences of its per-site
+    pieces (tests/golden/make_golden_large.py sitef)."""
+    gam = 2.0 * math.pi / (3.0 * box ** 3)
+    full = cfg["intra_site_images"] == "full"
+    out = []
+    for (idx, forms), lams in zip(sites, lam_values):
+        w = weights(lams)
+        sp = np.asarray(positions, np.float64)[idx]
+        qt = w @ forms
+        # Delta E = sum_st W_st (K + G)_st + eta gamma sum_rho w_rho |D_rho|^2
+        wm = 0.5 * (np.einsum("r,rs,rt->st", w, forms, forms) - np.outer(qt, qt))
+        g = np.zeros_like(sp)
+        disp = sp[:, None, :] - sp[None, :, :]
+        if full:
+            for nvec in image_vectors(0, 1):
+                d = disp + nvec * box
+                r = np.sqrt((d * d).sum(-1))
+                if not nvec.any():
+                    np.fill_diagonal(r, np.inf)
+                g += 2.0 * np.einsum("it,itx->ix", wm, -d / r[..., None] ** 3)
+        else:
+            d = disp - box * np.round(disp / box)
+            r = np.sqrt((d * d).sum(-1))
+            np.fill_diagonal(r, np.inf)
+            g += 2.0 * np.einsum("it,itx->ix", wm, -d / r[..., None] ** 3)
+        if full and lat is not None:
+            rv = regular(sp - 0.5 * box, cfg["p"])
+            dr = regular_grad(sp - 0.5 * box, cfg["p"])
+            # d/dr_i sum_st W_st Re(R_s T R_t): both slots
+            g += np.real(np.einsum("inx,nm,tm,it->ix", dr, lat, rv, wm))
+            g += np.real(np.einsum("sn,nm,imx,si->ix", rv, lat, dr, wm))
+        if full and cfg["dipole"]:
+            dev = qt[None, :] - forms
+            dd = dev @ (sp - 0.5 * box)
+            g += 2.0 * DIPOLE_ETA * gam * np.einsum("r,ri,rx->ix", w, dev, dd)
+        out.append(-g)
+    return np.concatenate(out) if out else np.zeros((0, 3))
+
+
 # ------------------------------------------------------ direct sums ----
 def direct_potentials(positions, charges, box, shell_cap=0):
     """Brute-force image sum |n|_inf <= shell_cap (oracle.py:33-51)."""

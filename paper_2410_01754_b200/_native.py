@@ -63,9 +63,10 @@ def _declare(lib):
         "lfmm_plan_set_count": (_i32, [_vp, _i64]),
         "lfmm_dist_configure": (_i32, [_vp, _i32, _i32, _i32]),
         "lfmm_dist_phase": (_i32, [_vp, _i32, _vp, _vp, _vp, _vp, _i32]),
-        "lfmm_dist_buffers": (_i32, [_vp, _vp, _vp]),
+        "lfmm_dist_buffers": (_i32, [_vp, _vp, _vp, _vp]),
         "lfmm_dist_hi": (_i32, [_vp, _vp, _i32]),
         "lfmm_site_gram": (_i32, [_vp, _vp, _vp, _vp, _vp]),
+        "lfmm_hi_site_forces": (_i32, [_vp, _i32, _vp]),
         "lfmm_lambda_baoab": (_i32, [_vp, _i64, _vp, _vp, _vp, _vp, _vp, _vp, _i32, _dbl, _dbl, _dbl, _dbl, _dbl,
                                      _c.c_uint64, _c.c_uint64]),
         "lfmm_lambda_record": (_i32, [_vp, _i64, _vp, _vp, _vp, _vp, _vp, _vp, _dbl, _i64, _vp, _vp, _vp, _vp,
@@ -86,7 +87,7 @@ def exported_symbols():
         "lfmm_assemble", "lfmm_scale_charges", "lfmm_step", "lfmm_profile_enable",
         "lfmm_stage_count", "lfmm_stage_name", "lfmm_stage_times", "lfmm_launch_count",
         "lfmm_plan_set_count", "lfmm_dist_configure", "lfmm_dist_phase", "lfmm_dist_buffers", "lfmm_dist_hi",
-        "lfmm_site_gram", "lfmm_lambda_baoab", "lfmm_lambda_record",
+        "lfmm_site_gram", "lfmm_lambda_baoab", "lfmm_lambda_record", "lfmm_hi_site_forces",
     ]
 
 
@@ -240,6 +241,7 @@ class Plan:
         check(lib().lfmm_sites_set(self.h, len(nf), ptr(ao), ptr(ai), ptr(nf), ptr(fo), ptr(fq)))
         self.sites_key = key
         self.n_sites = len(nf)
+        self.n_site_atoms = int(ao[-1]) if len(ao) else 0
         self.n_form_slots = int(nf.sum())
         self.form_slot_offsets = np.concatenate([[0], np.cumsum(nf)]).astype(np.int64)
 
@@ -257,6 +259,12 @@ class Plan:
         check(lib().lfmm_hi(self.h, ptr(lam), ptr(nl), int(mode), ptr(sp), ptr(pot), 0, ptr(cp), ptr(cl),
                             ptr(cd), ptr(eb), ptr(lf), ptr(off)))
         return dict(c_p2p=cp, c_lattice=cl, c_dipole=cd, blend=eb, forces=lf, offset=float(off[0]))
+
+    def hi_site_forces(self):
+        """(A, 3) -grad Delta E_site of the last HI-mode correction pass."""
+        out = np.empty((self.n_site_atoms, 3))
+        check(lib().lfmm_hi_site_forces(self.h, 0, ptr(out)))
+        return out
 
     def scale_charges(self, charges, lambdas, n_lambda):
         q = f64(charges, (self.n,))
@@ -320,7 +328,9 @@ class Plan:
     def dist_buffers(self):
         ptrs = (ctypes.c_void_p * 9)()
         offs = np.zeros(8, np.int64)
-        check(lib().lfmm_dist_buffers(self.h, ptrs, ptr(offs)))
+        ncp = np.zeros(1, np.int64)
+        check(lib().lfmm_dist_buffers(self.h, ptrs, ptr(offs), ptr(ncp)))
+        self.ncp = int(ncp[0])
         return [p if p is not None else 0 for p in ptrs], offs
 
     def dist_hi(self, site_positions, mode=MODE_HI):

@@ -73,6 +73,10 @@ class InterpolationResult:
     mode: str
     solve: object
     corrections: object
+    # (N, 3) -grad_r of `energy` when requested (not in the reference, whose
+    # only spatial forces are spatial_forces(q~), solver.py:407-427): in HI
+    # mode spatial_forces(q~) plus -grad Delta E_site on the site atoms
+    spatial_forces: np.ndarray = None
 
 
 def _fingerprint(lam_values):
@@ -143,11 +147,15 @@ def assemble_lambda_forces(system, lam_values, corrections, potentials):
     return _split_forces(system, lam, nl, out)
 
 
-def hi_energy_and_forces(system, lam_state, config=None, solver=None, mode="hi"):
+def hi_energy_and_forces(system, lam_state, config=None, solver=None, mode="hi", *, spatial_forces=False):
     """One charge-scaled solve plus the fused HI correction (corrections.py:252-274).
 
     Charge scaling, the solve and the correction/assembly all run on the
     device; the potentials never leave device memory between them.
+    ``spatial_forces=True`` (an extension; the reference signature is
+    unchanged) also returns -grad_r of the returned energy from the same
+    pass: spatial_forces(q~) (solver.py:407-427) on every atom plus, in HI
+    mode, -grad Delta E_site on the site atoms (csrc/lfmm_hi.cuh).
     """
     if mode not in ("hi", "qi"):
         raise ValueError(f"unknown mode {mode!r}")
@@ -159,12 +167,20 @@ def hi_energy_and_forces(system, lam_state, config=None, solver=None, mode="hi")
     plan = solver.plan
     qt = plan.scale_charges(np.asarray(system.charges, dtype=np.float64), lam, nl) if system.sites else \
         np.asarray(system.charges, dtype=np.float64)
-    res = solver.solve(qt)
+    if spatial_forces:
+        res, frc = solver.solve_with_forces(qt)
+    else:
+        res, frc = solver.solve(qt), None
     m = _native.MODE_QI if mode == "qi" else _native.MODE_HI
     out = plan.hi(lam, nl, m, site_positions=_site_positions(system), potentials=None, want_forces=True)
     forces = _split_forces(system, lam, nl, out["forces"])
     if mode == "qi":
-        return InterpolationResult(energy=float(res.energy), forces=forces, mode=mode, solve=res, corrections=None)
+        return InterpolationResult(energy=float(res.energy), forces=forces, mode=mode, solve=res, corrections=None,
+                                   spatial_forces=frc)
+    if frc is not None and system.sites:
+        idx = np.concatenate([s.particle_indices for s in system.sites])
+        frc[idx] += plan.hi_site_forces()
     corr = _correction_set(system, lam_values, out, plan)
     energy = float(res.energy) + corr.energy_offset()
-    return InterpolationResult(energy=energy, forces=forces, mode=mode, solve=res, corrections=corr)
+    return InterpolationResult(energy=energy, forces=forces, mode=mode, solve=res, corrections=corr,
+                               spatial_forces=frc)

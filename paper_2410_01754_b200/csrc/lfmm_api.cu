@@ -638,6 +638,8 @@ struct lfmm_plan {
   std::vector<int> h_atom_off, h_atom_idx, h_nforms, h_fslot_off;
   DevBuf atom_off, atom_idx, nforms, form_off, fslot_off, form_q, site_pos, lambdas, nlam, rscr, uscr;
   DevBuf c_p2p, c_lat, c_dip, blend, lam_forces, offsets, offset_total, pot_tmp, q_tmp;
+  DevBuf site_force;  // A x 3: -grad Delta E_site of the last HI-mode correction pass
+  bool site_force_valid = false;
   DevBuf finite_flag;
 
   size_t tsz() const { return fp32 ? sizeof(float) : sizeof(double); }
@@ -703,7 +705,7 @@ struct lfmm_plan {
                       &scal, &epart, &roots, &out_pot, &out_near, &out_far, &out_dip, &out_forces, &energies,
                       &dvec, &qtot, &atom_off, &atom_idx, &nforms, &form_off, &fslot_off, &form_q,
                       &site_pos, &lambdas, &nlam, &rscr, &uscr, &c_p2p, &c_lat, &c_dip, &blend,
-                      &lam_forces, &offsets, &offset_total, &pot_tmp, &q_tmp, &finite_flag};
+                      &lam_forces, &offsets, &offset_total, &pot_tmp, &q_tmp, &finite_flag, &site_force};
     for (auto* b : bufs) b->release();
     if (own_stream) cudaStreamDestroy(own_stream);
     if (io_stream) cudaStreamDestroy(io_stream);
@@ -1774,6 +1776,8 @@ void run_hi(lfmm_plan* pl, int mode, const double* pot_dev, const double* pot_si
   g.forces = pl->lam_forces.as<double>();
   g.offset = pl->offsets.as<double>();
   g.gram = gram;
+  g.site_force = mode == LFMM_MODE_HI ? pl->site_force.as<double>() : nullptr;
+  pl->site_force_valid = mode == LFMM_MODE_HI;
   if (mode == LFMM_MODE_HI && g.images_full && g.lat_t) {
     // lattice pair kernel inputs for all site atoms at once: R_t, U_t = T1 R_t
     const int na = (int)pl->n_site_atoms;
@@ -1811,7 +1815,7 @@ void run_hi(lfmm_plan* pl, int mode, const double* pot_dev, const double* pot_si
   }
   const int ns = pl->ns_max;
   const bool lat_smem = mode == LFMM_MODE_HI && g.images_full && g.lat_t;
-  const size_t smem = sizeof(double) * ((size_t)ns + 2 * (size_t)ns * ns + 3 * (size_t)ns +
+  const size_t smem = sizeof(double) * ((size_t)ns + 3 * (size_t)ns * ns + 3 * (size_t)ns +
                                         (lat_smem ? 2 * (size_t)ns * (g.ncp + 1) : 0));
   if (smem > 48 * 1024) {  // raise only (process-wide attribute, see halo_smem_attr)
     static std::mutex mu;
@@ -1826,6 +1830,14 @@ void run_hi(lfmm_plan* pl, int mode, const double* pot_dev, const double* pot_si
   pl->launch(ST_HI, [&] {
     k_sum_offsets<<<1, 256, 0, pl->stream>>>(pl->offsets.as<double>(), (int)pl->n_sites,
                                              pl->offset_total.as<double>());
+  });
+}
+
+void add_site_forces(lfmm_plan* pl) {
+  if (pl->n_site_atoms == 0) return;
+  pl->launch(ST_HI, [&] {
+    k_add_site_forces<<<nblk(3 * pl->n_site_atoms, 128), 128, 0, pl->stream>>>(
+        pl->out_forces.as<double>(), pl->atom_idx.as<int>(), (int)pl->n_site_atoms, pl->site_force.as<double>());
   });
 }
 
@@ -2147,6 +2159,20 @@ int lfmm_sites_set(lfmm_plan* plan, int64_t n_sites, const int64_t* atom_offsets
                    "site particle index out of range");
       aidx[a] = (int)atom_index[a];
     }
+    {
+      // sites never share particles (system.validate_system, system.py:135-143);
+      // the HI spatial forces rely on it (one writer per force row)
+      std::vector<int> owner((size_t)std::max<int64_t>(plan->N, 1), -1);
+      for (int64_t s = 0; s < S; ++s)
+        for (int a = aoff[s]; a < aoff[s + 1]; ++a) {
+          const int i = aidx[a];
+          if (i < 0) continue;
+          LFMM_REQUIRE(owner[i] != (int)s, "site " + std::to_string(s) + ": duplicate particle indices");
+          LFMM_REQUIRE(owner[i] < 0, "site " + std::to_string(s) + ": site overlap on particle indices [" +
+                                         std::to_string(i) + "]");
+          owner[i] = (int)s;
+        }
+    }
     fsl[0] = 0;
     for (int64_t s = 0; s < S; ++s) {
       const int ns = aoff[s + 1] - aoff[s];
@@ -2187,6 +2213,8 @@ int lfmm_sites_set(lfmm_plan* plan, int64_t n_sites, const int64_t* atom_offsets
     plan->blend.ensure(sizeof(double) * std::max<int64_t>(S, 1));
     plan->lam_forces.ensure(sizeof(double) * 4 * std::max<int64_t>(S, 1));
     plan->offsets.ensure(sizeof(double) * std::max<int64_t>(S, 1));
+    plan->site_force.ensure(sizeof(double) * 3 * std::max<int64_t>(A, 1));
+    plan->site_force_valid = false;
     LFMM_CUDA(cudaStreamSynchronize(plan->stream));
   });
 }
@@ -2217,6 +2245,16 @@ int lfmm_hi(lfmm_plan* plan, const double* lambdas, const int32_t* n_lambda, int
     copy_out(plan, blend_energy, plan->blend, sizeof(double) * S, io_on_device);
     copy_out(plan, lambda_forces, plan->lam_forces, sizeof(double) * 4 * S, io_on_device);
     copy_out(plan, energy_offset, plan->offset_total, sizeof(double), io_on_device);
+    if (!io_on_device) LFMM_CUDA(cudaStreamSynchronize(plan->stream));
+  });
+}
+
+int lfmm_hi_site_forces(lfmm_plan* plan, int io_on_device, double* out) {
+  if (!plan) return fail(Error{LFMM_EINVAL, "plan is NULL"});
+  return guarded([&] {
+    LFMM_REQUIRE(out != nullptr || plan->n_site_atoms == 0, "out is NULL");
+    LFMM_REQUIRE(plan->site_force_valid, "no HI-mode correction pass to take site forces from");
+    copy_out(plan, out, plan->site_force, sizeof(double) * 3 * plan->n_site_atoms, io_on_device);
     if (!io_on_device) LFMM_CUDA(cudaStreamSynchronize(plan->stream));
   });
 }
@@ -2425,6 +2463,13 @@ int lfmm_step(lfmm_plan* plan, const double* positions, const double* charges, c
     plan->run_solve(1, true);
     const bool step_mode = plan->step_mode;
     plan->step_mode = false;
+    // HI spatial forces: -grad Delta E_site on the site atoms (k_hi_site,
+    // issued on the HI side stream before the solve)
+    const bool site_forces = !plain && plan->n_sites > 0 && mode == LFMM_MODE_HI;
+    if (site_forces && hi_side) {
+      LFMM_CUDA(cudaStreamWaitEvent(plan->stream, plan->ev_hi_out, 0));
+      add_site_forces(plan);
+    }
     if (overlap && forces) {
       // the forces download overlaps the HI corrections
       LFMM_CUDA(cudaEventRecord(plan->ev_f, plan->stream));
@@ -2469,6 +2514,7 @@ int lfmm_step(lfmm_plan* plan, const double* positions, const double* charges, c
       } else {
         run_hi(plan, mode, plan->out_pot.as<double>());
       }
+      if (site_forces && !hi_side) add_site_forces(plan);
     }
     // energy = E_solve + sum of site offsets (hi_energy_and_forces :273)
     const bool add_off = !plain && plan->n_sites > 0 && mode == LFMM_MODE_HI;
@@ -2597,9 +2643,10 @@ int lfmm_dist_phase(lfmm_plan* plan, int phase, const double* positions, const d
 // [6] HI energy offset (1), [7] stream, [8] per-level max |M^/c| of the fp16
 // M2L (uint32 float bits, DMAX + 2 entries; NULL unless the fp32 tensor-core
 // M2L runs); level_off[l] = first box of level l
-int lfmm_dist_buffers(lfmm_plan* plan, void** ptrs, int64_t* level_off) {
+int lfmm_dist_buffers(lfmm_plan* plan, void** ptrs, int64_t* level_off, int64_t* ncp) {
   if (!plan) return fail(Error{LFMM_EINVAL, "plan is NULL"});
   return guarded([&] {
+    if (ncp) *ncp = plan->ncp;
     ptrs[0] = plan->mult.p;
     ptrs[1] = plan->scal.p;
     ptrs[2] = plan->energies.p;
@@ -2622,6 +2669,9 @@ int lfmm_dist_hi(lfmm_plan* plan, const double* site_positions, int mode) {
     if (plan->n_sites == 0) return;
     gather_site_positions(plan, site_positions, 1);
     run_hi(plan, mode, nullptr, plan->site_pot.as<double>());
+    // HI spatial forces into the local force rows (remote site atoms carry
+    // index -1 and are skipped)
+    if (mode == LFMM_MODE_HI) add_site_forces(plan);
   });
 }
 

@@ -16,6 +16,24 @@
 //   S_rho = Q_rho . V[site]                          (s_values :196-198)
 //   F_k   = -sum_rho dw_rho/dlambda_k (S_rho - C_rho) (assemble :221-238)
 // QI mode: F_k = -sum_rho dw_rho/dlambda_k S_rho, no offset.
+//
+// HI spatial forces on site atoms.  The reference has spatial forces only as
+// spatial_forces(q~) (solver.py:407-427); the HI energy adds
+//   Delta E_site = e(q~) - sum_rho w_rho C_rho
+//                = sum_st W_st (K + G)_st + eta gamma sum_rho w_rho |D_rho|^2,
+//   W_st = 1/2 (sum_rho w_rho Q_rho,s Q_rho,t - q~_s q~_t),
+//   D_rho = sum_s (q~_s - Q_rho,s)(r_s - L/2)   (c_dipole :112-124),
+// which depends on the site's own atom positions only, so
+// the HI-consistent force on site atom i is spatial_forces(q~)_i - grad_i
+// Delta E_site with
+//   grad_i sum W K = 2 sum_{t != i} W_it sum_n -(d_n / |d_n|^3),
+//                    d_n = r_i - r_t + n L      (27 images or minimum image)
+//   grad_i sum W G = (2 / L^2) Re< grad_x R(x_i), sum_t W_it U_t >,
+//                    x = (r - L/2) / L, U_t = T1 R(x_t), gradient ladder
+//                    harmonics.py:119-130 (dx R_l^m = (R_{l-1}^{m-1} -
+//                    R_{l-1}^{m+1})/2, dy = i (R_{l-1}^{m-1} + R_{l-1}^{m+1})/2,
+//                    dz = R_{l-1}^m)
+//   grad_i eta gamma sum w |D|^2 = 2 eta gamma sum_rho w_rho (q~_i - Q_rho,i) D_rho.
 #pragma once
 #include "lfmm_common.cuh"
 
@@ -53,7 +71,24 @@ struct HiArgs {
   double* forces;      // S x 4
   double* offset;      // S
   double* gram;        // optional: S x HI_MAXF x HI_MAXF, Q (K + G) Q^T (dynamics.py FrozenLambdaForceField)
+  double* site_force;  // optional: A x 3, -grad Delta E_site per site atom (HI mode)
 };
+
+// R_l^m of a packed conj-symmetric vector, any m (X_l^-m = (-1)^m conj X_l^m,
+// harmonics.py:3-8), zero outside |m| <= l
+__device__ inline double2 pk_get(const double* a, int p, int l, int m) {
+  if (l < 0 || m > l || -m > l) return make_double2(0.0, 0.0);
+  if (m == 0) return make_double2(a[l], 0.0);
+  const int mm = m < 0 ? -m : m;
+  const int c = pk_index(p, l, mm, 0);
+  double re = a[c], im = a[c + 1];
+  if (m < 0) {
+    const double sg = (mm & 1) ? -1.0 : 1.0;
+    re *= sg;
+    im *= -sg;
+  }
+  return make_double2(re, im);
+}
 
 __device__ inline double hi_weight(const double* lam, int nl, int rho) {
   double w = 1.0;
@@ -87,6 +122,103 @@ __device__ inline double packed_pair(const double* a, const double* b, int p, in
   return s;
 }
 
+// -grad Delta E_site of every atom of one site (see the header); called by the
+// whole CTA of k_hi_site once K, G, R_t/U_t (shared memory) and D_rho are in
+// place.  Warp per atom, fixed-order lane sums: reruns are bit-identical.
+__device__ __noinline__ void hi_site_force(const HiArgs& g, int s, int a0, int ns, int nf, const double* Q,
+                                           const double* qt, const double* w, const double* pos, double* Wm,
+                                           const double* Dv, bool lattice, double gamma) {
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  const double L = g.box;
+  const int p = g.p, ncp = g.ncp, nc = ncoef(p);
+  for (int e = tid; e < ns * ns; e += blockDim.x) {
+    const int i = e / ns, j = e % ns;
+    double acc = 0.0;
+    for (int r = 0; r < nf; ++r) acc += w[r] * Q[r * ns + i] * Q[r * ns + j];
+    Wm[e] = 0.5 * (acc - qt[i] * qt[j]);
+  }
+  __syncthreads();
+  const int rs = ncp + 1;
+  const double* Rs = Wm + ns * ns;
+  const double* Us = Rs + (size_t)ns * rs;
+  const bool dip = g.images_full && g.dipole;
+  for (int i = wid; i < ns; i += blockDim.x / 32) {
+    double gx = 0.0, gy = 0.0, gz = 0.0;
+    // near kernel: lanes over (partner, image)
+    const int nimg = g.images_full ? 27 : 1;
+    for (int e = lane; e < ns * nimg; e += 32) {
+      const int t = e / nimg, n = e - t * nimg;
+      if (t == i) continue;
+      double dx = pos[3 * i] - pos[3 * t], dy = pos[3 * i + 1] - pos[3 * t + 1], dz = pos[3 * i + 2] - pos[3 * t + 2];
+      if (g.images_full) {
+        dx += (n / 9 - 1) * L;
+        dy += ((n / 3) % 3 - 1) * L;
+        dz += (n % 3 - 1) * L;
+      } else {
+        dx -= L * rint(dx / L);
+        dy -= L * rint(dy / L);
+        dz -= L * rint(dz / L);
+      }
+      const double ir = 1.0 / sqrt(dx * dx + dy * dy + dz * dz);
+      const double c = -2.0 * Wm[i * ns + t] * ir * ir * ir;
+      gx = fma(c, dx, gx);
+      gy = fma(c, dy, gy);
+      gz = fma(c, dz, gz);
+    }
+    // lattice kernel: V = sum_t W_it U_t, contracted with grad_x R(x_i)
+    if (lattice) {
+      const double* Ri = Rs + (size_t)i * rs;
+      double hx = 0.0, hy = 0.0, hz = 0.0;
+      for (int c = lane; c < nc; c += 32) {
+        double v = 0.0;
+        for (int t = 0; t < ns; ++t) v = fma(Wm[i * ns + t], Us[(size_t)t * rs + c], v);
+        int l, m, part;
+        pk_decode(p, c, l, m, part);
+        if (l == 0) continue;
+        const double2 A = pk_get(Ri, p, l - 1, m - 1), B = pk_get(Ri, p, l - 1, m + 1), C = pk_get(Ri, p, l - 1, m);
+        double dxv, dyv, dzv;
+        if (part == 0) {
+          dxv = 0.5 * (A.x - B.x);
+          dyv = -0.5 * (A.y + B.y);
+          dzv = C.x;
+        } else {
+          dxv = 0.5 * (A.y - B.y);
+          dyv = 0.5 * (A.x + B.x);
+          dzv = C.y;
+        }
+        // packed pairing Re sum_full a b: m = 0 once, m > 0 twice, imaginary parts negated
+        const double wgt = (m == 0) ? v : (part == 0 ? 2.0 * v : -2.0 * v);
+        hx = fma(dxv, wgt, hx);
+        hy = fma(dyv, wgt, hy);
+        hz = fma(dzv, wgt, hz);
+      }
+      const double sc = 2.0 / (L * L);
+      gx = fma(sc, hx, gx);
+      gy = fma(sc, hy, gy);
+      gz = fma(sc, hz, gz);
+    }
+    for (int off = 16; off > 0; off >>= 1) {
+      gx += __shfl_down_sync(0xffffffffu, gx, off);
+      gy += __shfl_down_sync(0xffffffffu, gy, off);
+      gz += __shfl_down_sync(0xffffffffu, gz, off);
+    }
+    if (lane == 0) {
+      if (dip) {
+        for (int r = 0; r < nf; ++r) {
+          const double c = 2.0 * DIPOLE_ETA * gamma * w[r] * (qt[i] - Q[r * ns + i]);
+          gx = fma(c, Dv[3 * r], gx);
+          gy = fma(c, Dv[3 * r + 1], gy);
+          gz = fma(c, Dv[3 * r + 2], gz);
+        }
+      }
+      double* f = g.site_force + 3 * (size_t)(a0 + i);
+      f[0] = -gx;
+      f[1] = -gy;
+      f[2] = -gz;
+    }
+  }
+}
+
 __global__ void __launch_bounds__(HI_THREADS) k_hi_site(HiArgs g) {
   const int s = blockIdx.x;
   if (s >= g.n_sites) return;
@@ -102,7 +234,8 @@ __global__ void __launch_bounds__(HI_THREADS) k_hi_site(HiArgs g) {
   double* KG = qt + ns;          // ns*ns (K)
   double* GG = KG + ns * ns;     // ns*ns (G)
   double* pos = GG + ns * ns;    // ns*3
-  __shared__ double lam[4], w[HI_MAXF], Cv[HI_MAXF], Sv[HI_MAXF];
+  double* Wm = pos + 3 * ns;     // ns*ns: W_st of the site-force gradient
+  __shared__ double lam[4], w[HI_MAXF], Cv[HI_MAXF], Sv[HI_MAXF], Dv[3 * HI_MAXF];
 
   if (tid < 4) lam[tid] = g.lambdas[4 * s + tid];
   for (int i = tid; i < 3 * ns; i += blockDim.x) pos[i] = g.site_pos[3 * a0 + i];
@@ -144,7 +277,7 @@ __global__ void __launch_bounds__(HI_THREADS) k_hi_site(HiArgs g) {
       // rows padded to ncp + 1 doubles: the lanes of a warp read different
       // atoms' rows at the same coefficient, which then fall in different banks
       const int rs = ncp + 1;
-      double* Rs = pos + 3 * ns;              // ns x rs
+      double* Rs = Wm + ns * ns;              // ns x rs
       double* Us = Rs + (size_t)ns * rs;      // ns x rs
       const double* R = g.rscratch + (size_t)a0 * ncp;
       const double* U = g.uscratch + (size_t)a0 * ncp;
@@ -244,9 +377,13 @@ __global__ void __launch_bounds__(HI_THREADS) k_hi_site(HiArgs g) {
       if (g.c_dip) g.c_dip[slot] = cd;
       Cv[r] = cp + cl + cd;
       Sv[r] = sv;
+      Dv[3 * r] = ddx;
+      Dv[3 * r + 1] = ddy;
+      Dv[3 * r + 2] = ddz;
     }
   }
   __syncthreads();
+  if (g.site_force && !qi) hi_site_force(g, s, a0, ns, nf, Q, qt, w, pos, Wm, Dv, lattice, gamma);
   // ---- blend energy, offset, lambda forces (warp 0) ----
   if (wid == 0) {
     double eb = 0.0;
@@ -369,6 +506,18 @@ __global__ void k_hi_lambda_forces(HiArgs g) {
   }
   if (lane == 0)
     for (int k = 0; k < 4; ++k) g.forces[4 * s + k] = k < nl ? -f[k] : 0.0;
+}
+
+// HI spatial forces: spatial_forces(q~) plus -grad Delta E_site on the site
+// atoms (sites never share atoms, system.py:139-143, so no two threads add
+// to the same row)
+__global__ void k_add_site_forces(double* __restrict__ forces, const int* __restrict__ atom_idx, int n_atoms,
+                                  const double* __restrict__ site_force) {
+  const int e = blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= 3 * n_atoms) return;
+  const int a = e / 3, k = e - 3 * a;
+  const int i = atom_idx[a];
+  if (i >= 0) forces[3 * (size_t)i + k] += site_force[e];
 }
 
 // fixed-order sum of per-site offsets (CorrectionSet.energy_offset, :153-154)

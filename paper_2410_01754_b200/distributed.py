@@ -421,6 +421,12 @@ class DistributedSolver:
         if bool((~(stay | (lx == xl) | (lx == xr))).any()):
             raise ValueError("an atom moved more than one leaf plane out of its rank's slab; "
                              "re-partition from global positions (DistributedSolver.step)")
+        if x1 - x0 < 2 and self.world > 2 and bool((~stay).any()):
+            # with one plane per rank a migrant into plane x1 (x0-1) is also
+            # the halo of rank r+2 (r-2), which this one-hop exchange never
+            # reaches: those pairs would silently drop out of the P2P
+            raise ValueError("atoms migrated between ranks that own a single leaf plane each; "
+                             "re-partition from global positions (DistributedSolver.step) or use a deeper tree")
         rows = torch.cat([positions, charges[:, None], global_ids.to(torch.float64)[:, None]], 1)
         left, right = (self.rank - 1) % self.world, (self.rank + 1) % self.world
         if left == right:
@@ -451,6 +457,8 @@ class DistributedSolver:
         plan.set_count(n_loc)
         n_sites = 0
         if sites is not None:
+            if lambdas is None or n_lambda is None:
+                raise ValueError("sites need lambdas and n_lambda (the HI step scales the site charges)")
             ao, ai, nf, fo, fq = sites
             if self._site_dev is None or self._site_key is not sites:
                 self._site_dev = torch.as_tensor(np.asarray(ai, np.int64), device=positions.device)
@@ -469,7 +477,7 @@ class DistributedSolver:
         plan.dist_phase(1, pos_l, q_l, lambdas if n_sites else None, n_lambda if n_sites else None, grad=True)
         ptrs, loff = plan.dist_buffers()
         # ---- exchange 1: owned multipoles of levels >= lg, dipole / charge ----
-        ncp = self._ncp()
+        ncp = plan.ncp  # the plan's padded coefficient count (lfmm_dist_buffers)
         tdt = "<f4" if self.tsize == 4 else "<f8"
         for lvl in range(self.lg, d + 1) if self.world > 1 else ():
             nbox = 1 << (3 * lvl)
@@ -501,10 +509,9 @@ class DistributedSolver:
             print("rank", self.rank, "energies", en.cpu().numpy(), "scal", _device_view(ptrs[1], (4,), "<f8", torch).cpu().numpy(), flush=True)
         parts = self.comm.sum_ordered(en[1:3].clone())
         e_solve = float(parts[0] + parts[1] + en[3])
-        forces_l = _device_view(ptrs[3], (n_loc, 3), "<f8", torch)[:n_own].clone()
         out = {"energy_solve": e_solve, "near_energy": float(parts[0]), "far_energy": float(parts[1]),
                "dipole_energy": float(en[3]), "owned": gid_l[:n_own], "owned_positions": pos_l[:n_own],
-               "owned_charges": q_l[:n_own], "forces": forces_l}
+               "owned_charges": q_l[:n_own]}
         if n_sites:
             # site-atom potentials and positions from their owners (each site
             # atom is owned by one rank; the others contribute exact zeros)
@@ -524,6 +531,8 @@ class DistributedSolver:
             out["energy"] = e_solve + (off if mode == _native.MODE_HI else 0.0)
         else:
             out["energy"] = e_solve
+        # after dist_hi: in HI mode the site atoms' rows carry -grad Delta E_site
+        out["forces"] = _device_view(ptrs[3], (n_loc, 3), "<f8", torch)[:n_own].clone()
         return out
 
     def _poison(self, ptrs, loff, ncp, tdt):
@@ -543,7 +552,3 @@ class DistributedSolver:
                 if x not in keep:
                     view[x].fill_(float("nan"))
 
-    def _ncp(self):
-        nc = (self.cfg.p + 1) ** 2
-        use_tc = self.cfg.precision == "single" and 64 < nc <= 128
-        return 128 if use_tc else (nc + 15) // 16 * 16

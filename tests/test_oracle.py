@@ -169,3 +169,26 @@ def test_oracle_matches_reference_c2(golden):
         assert np.abs(r[key][idx] - g[ref]).max() / float(g[amax]) <= 1e-11, key
     for k in ("energy", "near_energy", "far_energy", "dipole_energy"):
         assert abs(r[k] - float(g[k])) <= 1e-11 * abs(float(g[k])), k
+
+
+def test_oracle_hi_site_forces_match_reference():
+    """The oracle's analytic -grad Delta E_site (HI spatial forces on site
+    atoms) against the reference's own per-site correction
+    pieces differentiated by 4-point central differences
+    (tests/golden/make_golden_large.py sitef)."""
+    import os
+
+    from paper_2410_01754_b200.waterbox import generate_water_box
+
+    g = np.load(os.path.join(os.path.dirname(__file__), "golden", "ref_site_forces.npz"))
+    system, lam, _ = generate_water_box(3000, 4, seed=0)
+    sites = [(s.particle_indices, s.form_charges) for s in system.sites]
+    for images, key in (("full", "c1"), ("minimum", "c1_minimum")):
+        np.testing.assert_allclose(g[key + "_checksum"][:4], [system.positions.sum(), (system.positions ** 2).sum(),
+                                                              system.charges.sum(), np.abs(system.charges).sum()],
+                                   rtol=1e-13)
+        cfg = orc.default_config(p=8, depth=3, intra_site_images=images)
+        lat = orc.lattice_matrix(cfg, system.box_length)
+        f = orc.hi_site_forces(system.positions, system.box_length, sites, lam.values, cfg, lat)
+        ref = g[key + "_dforce"]
+        assert np.abs(f - ref).max() <= 1e-10 * np.abs(ref).max()
