@@ -24,7 +24,6 @@
 #include "lfmm_expansions.cuh"
 #include "lfmm_hi.cuh"
 #include "lfmm_m2l_halo.cuh"
-#include "lfmm_m2l_tc.cuh"
 #include "lfmm_p2p.cuh"
 #include "lfmm_setup.cuh"
 #include "lfmm_tree.cuh"
@@ -348,23 +347,6 @@ __global__ void k_site_pot(const int* __restrict__ atom_idx, int n, const int* _
   out[a] = v;
 }
 
-// energies (4,K) rows total/near/far/dip; dipole (3,K); qtot (K)
-__global__ void k_energies(const double* __restrict__ scal, const double* __restrict__ epart, int K, int c,
-                           int dipole, double box, double* __restrict__ energies,
-                           double* __restrict__ dvec, double* __restrict__ qtot) {
-  const double gam = 2.0 * 3.14159265358979323846 / (3.0 * box * box * box);
-  const double en = 0.5 * epart[0], ef = 0.5 * epart[1];
-  const double ed = dipole ? DIPOLE_ETA * gam * (scal[0] * scal[0] + scal[1] * scal[1] + scal[2] * scal[2]) : 0.0;
-  energies[0 * K + c] = en + ef + ed;
-  energies[1 * K + c] = en;
-  energies[2 * K + c] = ef;
-  energies[3 * K + c] = ed;
-  dvec[0 * K + c] = scal[0];
-  dvec[1 * K + c] = scal[1];
-  dvec[2 * K + c] = scal[2];
-  qtot[c] = scal[3];
-}
-
 // warp per site: S_rho and lambda forces from given potentials and C_rho
 __global__ void k_assemble(int S, const int* __restrict__ atom_off, const int* __restrict__ atom_idx,
                            const int* __restrict__ nforms, const int* __restrict__ form_off,
@@ -398,11 +380,6 @@ __global__ void k_step_energy(const double* __restrict__ energies, const double*
 __global__ void k_i32_to_i64(const int* __restrict__ in, int64_t n, int64_t* __restrict__ out) {
   const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (i < n) out[i] = in[i];
-}
-
-__global__ void k_check_finite(const double* __restrict__ v, int64_t n, int* __restrict__ flag) {
-  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (i < n && !isfinite(v[i])) atomicOr(flag, 1);
 }
 
 // ------------------------------------------------------ host helpers ----
@@ -605,8 +582,7 @@ struct lfmm_plan {
   float4* pair_a() { return fp32 ? reinterpret_cast<float4*>(pairs.p) : nullptr; }
   float4* pair_b() { return fp32 ? reinterpret_cast<float4*>(pairs.p) + pair_cap : nullptr; }
   // expansions / operators
-  bool use_tc = false;    // M2L on tcgen05 (fp32, (p+1)^2 <= 128)
-  bool use_halo = false;  // ... as shifted-window fp16x3 GEMMs (lfmm_m2l_halo.cuh)
+  bool use_halo = false;  // fp32 M2L on tcgen05 as shifted-window fp16x3 GEMMs (lfmm_m2l_halo.cuh)
   bool p2p_scalar = false;  // fp32 P2P on the scalar kernel (LFMM_P2P=scalar, A/B checks)
   bool far_serial = false;  // no far_overlapped() (LFMM_FAR=serial, A/B checks and tools/hm_prof.py)
   bool step_mode = false;   // lfmm_step: skip the input-order potential arrays
@@ -615,12 +591,13 @@ struct lfmm_plan {
   // computed redundantly from the gathered level dist_lg.  dist_phase: 0 whole
   // solve, 1 up to the owned multipoles, 2 the rest.
   int own_x0 = 0, own_x1 = 1 << 30, dist_lg = 0, dist_phase = 0;
-  DevBuf ops_tc, up_part, up_cnt, counters;
+  DevBuf up_part, up_cnt, counters;
   DevBuf ops16, hm_inv_r, hm_inv_c, hm_jobs, hm_level_max, mult16, ops_m2l_t;
   int64_t m16_off[DMAX + 2] = {0};
-  int hm_njobs = 0, hm_rw_cap = 0, hm_lsplit = 1, hm_nbig = 0, hm_stagger = 8, hm_astages = HM_ASTAGES;
-  int hm_groups_big = 2;    // M2L jobs (partial slots) per tile at levels >= 4: 4 or 2 (LFMM_HM_GROUPS)
-  int hm_groups_small = 8;  // ... at levels < 4: 8, 4 or 2 (LFMM_HM_GROUPS_SMALL)
+  int hm_njobs = 0, hm_rw_cap = 0, hm_lsplit = 1, hm_nbig = 0, hm_astages = HM_ASTAGES;
+  static constexpr int hm_stagger = 8;       // terms issuer 1 lags issuer 0 (capped at AS - 6 in the kernel)
+  static constexpr int hm_groups_big = 2;    // M2L jobs (partial slots) per tile at levels >= 4
+  static constexpr int hm_groups_small = 8;  // ... at levels < 4 (one source class per job)
   bool m2l_f64_simt = false;  // fp64 M2L on k_gemm_gather instead of k_m2l_f64 (LFMM_M2L64=gather)
   DevBuf mult, loc, partial, ops_m2l, ops_m2m, ops_l2l, ops_lat, lat64t;
   std::vector<double2> lat_unit;  // unit-box complex lattice operator (nc x nc)
@@ -640,7 +617,6 @@ struct lfmm_plan {
   DevBuf c_p2p, c_lat, c_dip, blend, lam_forces, offsets, offset_total, pot_tmp, q_tmp;
   DevBuf site_force;  // A x 3: -grad Delta E_site of the last HI-mode correction pass
   bool site_force_valid = false;
-  DevBuf finite_flag;
 
   size_t tsz() const { return fp32 ? sizeof(float) : sizeof(double); }
   // leaf b's pairs start at (leaf_start[b] + b + 1) / 2 (lfmm_p2p.cuh)
@@ -700,12 +676,12 @@ struct lfmm_plan {
     DevBuf* hbufs[] = {&ops16, &hm_inv_r, &hm_inv_c, &hm_jobs, &hm_level_max, &mult16, &boxq, &site_pot, &ops_m2m_t, &ops_l2l_t, &ops_lat_t, &tr_cnt, &ops_m2l_t};
     for (auto* b : hbufs) b->release();
     DevBuf* bufs[] = {&pos_in, &pos_wrap, &leaf_of, &slot_of, &counts, &cursor, &leaf_start, &bucket, &perm,
-                      &inv_perm, &pos_sorted, &leaf_sorted, &xq, &mult, &loc, &partial, &ops_tc, &up_part, &up_cnt, &counters, &ops_m2l, &ops_m2m,
+                      &inv_perm, &pos_sorted, &leaf_sorted, &xq, &mult, &loc, &partial, &up_part, &up_cnt, &counters, &ops_m2l, &ops_m2m,
                       &ops_l2l, &ops_lat, &lat64t, &q_in, &qs, &vnear, &vfar, &gnear, &gfar, &part,
                       &scal, &epart, &roots, &out_pot, &out_near, &out_far, &out_dip, &out_forces, &energies,
                       &dvec, &qtot, &atom_off, &atom_idx, &nforms, &form_off, &fslot_off, &form_q,
                       &site_pos, &lambdas, &nlam, &rscr, &uscr, &c_p2p, &c_lat, &c_dip, &blend,
-                      &lam_forces, &offsets, &offset_total, &pot_tmp, &q_tmp, &finite_flag, &site_force};
+                      &lam_forces, &offsets, &offset_total, &pot_tmp, &q_tmp, &site_force};
     for (auto* b : bufs) b->release();
     if (own_stream) cudaStreamDestroy(own_stream);
     if (io_stream) cudaStreamDestroy(io_stream);
@@ -950,14 +926,6 @@ struct lfmm_plan {
       l64.release();
     }
     if (use_halo) build_halo_operators();
-    if (use_tc && !use_halo) {
-      ops_tc.ensure((size_t)NOFF * TC_NCHUNK * TC_STAGE);
-      const int64_t total = (int64_t)NOFF * TC_M * TC_M;
-      launch(ST_SETUP, [&] {
-        k_tc_arrange_ops<<<nblk(total, 256), 256, 0, stream>>>(ops_m2l.as<float>(), ops_tc.as<float>(), NOFF);
-      });
-      LFMM_CUDA(cudaFuncSetAttribute(k_m2l_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, TC_SMEM_WS));
-    }
     if (fp32) {
       LFMM_CUDA(cudaFuncSetAttribute(k_p2p2<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, P2P2_SMEM));
       LFMM_CUDA(cudaFuncSetAttribute(k_p2p2<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, P2P2_SMEM));
@@ -1085,11 +1053,11 @@ struct lfmm_plan {
   int64_t part_off[DMAX + 2] = {0};
   int job_start[DMAX + 3] = {0};
   void plan_m2l_split() {
-    const int target_jobs = use_tc ? 4 * 148 : 4 * 148 * 2;
+    const int target_jobs = 4 * 148 * 2;
     int64_t off = 0;
     int jobs = 0;
     for (int l = 1; l <= depth; ++l) {
-      const int tiles = 8 * (use_tc ? tc_tiles_per_parity(l) : tiles_per_parity(l));
+      const int tiles = 8 * tiles_per_parity(l);
       int ns = (target_jobs + tiles - 1) / tiles;
       ns = std::max(1, std::min(MAX_SPLIT, ns));
       nsplit[l] = ns;
@@ -1344,9 +1312,7 @@ struct lfmm_plan {
     if (side && !near_stream) {
       int lo = 0, hi = 0;
       LFMM_CUDA(cudaDeviceGetStreamPriorityRange(&lo, &hi));
-      const char* nenv = std::getenv("LFMM_P2P_PRIO");  // A/B: the near field at high priority
-      LFMM_CUDA(cudaStreamCreateWithPriority(&near_stream, cudaStreamNonBlocking,
-                                             (nenv && std::string(nenv) == "high") ? hi : lo));
+      LFMM_CUDA(cudaStreamCreateWithPriority(&near_stream, cudaStreamNonBlocking, lo));
       LFMM_CUDA(cudaEventCreateWithFlags(&ev_near_in, cudaEventDisableTiming));
       LFMM_CUDA(cudaEventCreateWithFlags(&ev_near_out, cudaEventDisableTiming));
     }
@@ -1504,19 +1470,6 @@ struct lfmm_plan {
         launch(ST_DOWN, [&] {
           launch_m2l_halo(ha, hm_njobs, hm_astages, stream);
         });
-      } else if (use_tc && sizeof(T) == 4) {
-        TcArgs ta{};
-        ta.mult = reinterpret_cast<const float*>(mult.p);
-        ta.partial = reinterpret_cast<float*>(partial.p);
-        ta.ops_tc = ops_tc.as<float>();
-        ta.depth = depth;
-        for (int l = 0; l <= depth; ++l) {
-          ta.level_off[l] = level_off[l];
-          ta.part_off[l] = part_off[l];
-          ta.nsplit[l] = nsplit[l];
-        }
-        for (int l = 0; l <= depth + 1; ++l) ta.job_start[l] = job_start[l];
-        launch(ST_DOWN, [&] { k_m2l_tc<<<job_start[depth + 1], TC_THREADS, TC_SMEM_WS, stream>>>(ta); });
       } else {
         ga.mode = GEMM_M2L;
         ga.level = 0;
@@ -1710,14 +1663,14 @@ void copy_out(lfmm_plan* pl, double* dst, const DevBuf& src, size_t bytes, int o
                             pl->stream));
 }
 
-void check_finite(lfmm_plan* pl, const DevBuf& buf, int64_t n, const char* what) {
-  pl->finite_flag.ensure(sizeof(int));
-  LFMM_CUDA(cudaMemsetAsync(pl->finite_flag.p, 0, sizeof(int), pl->stream));
-  if (n > 0) k_check_finite<<<nblk(n, 256), 256, 0, pl->stream>>>(buf.as<double>(), n, pl->finite_flag.as<int>());
-  int h = 0;
-  LFMM_CUDA(cudaMemcpyAsync(&h, pl->finite_flag.p, sizeof(int), cudaMemcpyDeviceToHost, pl->stream));
-  LFMM_CUDA(cudaStreamSynchronize(pl->stream));
-  if (h) throw Error{LFMM_ENONFINITE, std::string("non-finite values in ") + what};
+// NumericalFailure (status 3, the reference CLI's _require_finite /
+// NumericalFailure, cli.py:24-25, :107-112): the host copies of the energies
+// and lambda forces are scanned after the call's final synchronisation
+// (device-resident outputs are left to the caller: no extra host sync).
+void require_finite(const double* v, int64_t n, const char* what) {
+  if (!v) return;
+  for (int64_t i = 0; i < n; ++i)
+    if (!std::isfinite(v[i])) throw Error{LFMM_ENONFINITE, std::string("non-finite values in ") + what};
 }
 
 void hi_args(lfmm_plan* pl, HiArgs& g) {
@@ -1918,24 +1871,20 @@ int lfmm_plan_create(const double* positions, int64_t n, double box_length, int 
     pl->nc = ncoef(p);
     pl->ncp = ncpad(p);
     {
-      const char* env = std::getenv("LFMM_M2L");
-      const bool force_simt = env && std::string(env) == "simt";
-      pl->use_tc = pl->fp32 && depth >= 1 && pl->nc > 64 && pl->nc <= 128 && !force_simt;
-      if (pl->use_tc) pl->ncp = 128;
-      pl->use_halo = pl->use_tc && !(env && std::string(env) == "gather");
-      const char* penv = std::getenv("LFMM_P2P");
-      pl->p2p_scalar = penv && std::string(penv) == "scalar";
-      const char* fenv = std::getenv("LFMM_FAR");
-      pl->far_serial = fenv && std::string(fenv) == "serial";
-      const char* m64 = std::getenv("LFMM_M2L64");
-      pl->m2l_f64_simt = m64 && std::string(m64) == "gather";
-      const char* genv = std::getenv("LFMM_HM_GROUPS");
-      if (genv && (std::atoi(genv) == 2 || std::atoi(genv) == 4)) pl->hm_groups_big = std::atoi(genv);
-      const char* gsenv = std::getenv("LFMM_HM_GROUPS_SMALL");
-      if (gsenv && (std::atoi(gsenv) == 2 || std::atoi(gsenv) == 4 || std::atoi(gsenv) == 8))
-        pl->hm_groups_small = std::atoi(gsenv);
-      const char* senv = std::getenv("LFMM_HM_STAGGER");
-      if (senv) pl->hm_stagger = std::min(16, std::max(0, std::atoi(senv)));  // <= 19 (the shortest term list)
+      // A/B switches, each exercised by tests/test_gpu_variants.py:
+      //   LFMM_M2L=simt    fp32 M2L on the SIMT gather kernel (no tensor cores)
+      //   LFMM_P2P=scalar  fp32 P2P on the scalar kernel k_p2p
+      //   LFMM_FAR=serial  far field on one stream (no far_overlapped())
+      //   LFMM_M2L64=gather fp64 M2L on the SIMT gather kernel (no DMMA)
+      auto env_is = [](const char* name, const char* val) {
+        const char* e = std::getenv(name);
+        return e && std::string(e) == val;
+      };
+      pl->use_halo = pl->fp32 && depth >= 1 && pl->nc > 64 && pl->nc <= 128 && !env_is("LFMM_M2L", "simt");
+      if (pl->use_halo) pl->ncp = 128;
+      pl->p2p_scalar = env_is("LFMM_P2P", "scalar");
+      pl->far_serial = env_is("LFMM_FAR", "serial");
+      pl->m2l_f64_simt = env_is("LFMM_M2L64", "gather");
     }
     pl->nleaf = 1 << (3 * depth);
     pl->size = box_length / double(1 << depth);
@@ -2135,7 +2084,10 @@ int lfmm_solve(lfmm_plan* plan, const double* charges, int64_t k, int io_on_devi
       LFMM_REQUIRE(!io_on_device, "root_multipole is returned to host memory only");
       for (int64_t c = 0; c < k; ++c) plan->root_multipole_host(k, c, root_multipole);
     }
-    if (!io_on_device) LFMM_CUDA(cudaStreamSynchronize(plan->stream));
+    if (!io_on_device) {
+      LFMM_CUDA(cudaStreamSynchronize(plan->stream));
+      require_finite(energies, 4 * k, "the solve energies");
+    }
   });
 }
 
@@ -2245,7 +2197,11 @@ int lfmm_hi(lfmm_plan* plan, const double* lambdas, const int32_t* n_lambda, int
     copy_out(plan, blend_energy, plan->blend, sizeof(double) * S, io_on_device);
     copy_out(plan, lambda_forces, plan->lam_forces, sizeof(double) * 4 * S, io_on_device);
     copy_out(plan, energy_offset, plan->offset_total, sizeof(double), io_on_device);
-    if (!io_on_device) LFMM_CUDA(cudaStreamSynchronize(plan->stream));
+    if (!io_on_device) {
+      LFMM_CUDA(cudaStreamSynchronize(plan->stream));
+      require_finite(lambda_forces, 4 * plan->n_sites, "the lambda forces");
+      require_finite(energy_offset, 1, "the HI energy offset");
+    }
   });
 }
 
@@ -2430,9 +2386,7 @@ int lfmm_step(lfmm_plan* plan, const double* positions, const double* charges, c
       if (!plan->hi_stream) {
         int lo = 0, hi = 0;
         LFMM_CUDA(cudaDeviceGetStreamPriorityRange(&lo, &hi));
-        const char* henv = std::getenv("LFMM_HI_PRIO");
-        LFMM_CUDA(cudaStreamCreateWithPriority(&plan->hi_stream, cudaStreamNonBlocking,
-                                               (henv && std::string(henv) == "high") ? hi : lo));
+        LFMM_CUDA(cudaStreamCreateWithPriority(&plan->hi_stream, cudaStreamNonBlocking, lo));
         LFMM_CUDA(cudaEventCreateWithFlags(&plan->ev_hi_in, cudaEventDisableTiming));
         LFMM_CUDA(cudaEventCreateWithFlags(&plan->ev_hi_out, cudaEventDisableTiming));
       }
@@ -2531,6 +2485,8 @@ int lfmm_step(lfmm_plan* plan, const double* positions, const double* charges, c
     if (!io_on_device) {
       LFMM_CUDA(cudaStreamSynchronize(plan->stream));
       LFMM_CUDA(cudaStreamSynchronize(plan->io_stream));
+      require_finite(energy, 1, "the step energy");
+      if (!plain) require_finite(lambda_forces, 4 * plan->n_sites, "the lambda forces");
     }
   });
 }

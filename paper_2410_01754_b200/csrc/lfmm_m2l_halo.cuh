@@ -46,7 +46,7 @@
 #include <cstdint>
 
 #include "lfmm_common.cuh"
-#include "lfmm_m2l_tc.cuh"
+#include "lfmm_sm100.cuh"
 
 namespace lfmm {
 
@@ -89,7 +89,7 @@ struct HaloArgs {
 // D terms behind issuer 0, so the two never finish an iteration together
 // (an iteration's end waits for its next halo window, and in phase both
 // issuers would wait at once and leave the tensor core idle).  D is capped at
-// AS - 6: lags of AS + 2 terms and more hung the kernel (AS = 10 and 14).
+// AS - 6; soundness needs D + 1 < AS (the ring invariant in k_m2l_halo).
 __device__ __forceinline__ int hm_aseq(int par, int u, int D, int T) {
   return par == 0 ? u + min(max(u - D, 0), T) : min(u + D + 1, T) + u;
 }
@@ -410,7 +410,15 @@ __global__ void __launch_bounds__(HM_THREADS, 1) k_m2l_halo(HaloArgs g) {
       const uint64_t a_desc0 = hm_desc(smem_u32(abase), 128, 256);
       int T = 0;
       for (int k = 0; k < nsc; ++k) T += (HM_NKC / 2) * s_nt[k];
-      const int D = min(min(g.stagger, AS - 6), T);  // D >= AS + 2 was seen to deadlock
+      // Ring invariant: an issuer's wait on sequence j (stage j % AS, parity
+      // (j / AS) & 1) is only sound if fill j - AS of that stage has completed
+      // (else the parity test sees the phase two behind and passes early).
+      // Fills complete in issue order and an issuer's consumed sequence m
+      // orders every fill <= m before it, so the largest jump between an
+      // issuer's consecutive sequence numbers must stay <= AS; issuer 1
+      // starts at j = D + 1, so D + 1 < AS (tests/test_m2l_schedule.py
+      // checks it over every term count).  The cap keeps 4 stages spare.
+      const int D = min(min(g.stagger, AS - 6), T);
       int u = 0;  // this issuer's terms so far
       for (int it0 = 0; it0 < niter; it0 += 2) {
         const int k = it0 / HM_NKC;
@@ -467,7 +475,7 @@ __global__ void __launch_bounds__(HM_THREADS, 1) k_m2l_halo(HaloArgs g) {
     if (lane == 0) {
       int T = 0;
       for (int k = 0; k < nsc; ++k) T += (HM_NKC / 2) * s_nt[k];
-      const int D = min(min(g.stagger, AS - 6), T);  // D >= AS + 2 was seen to deadlock
+      const int D = min(min(g.stagger, AS - 6), T);  // same lag as the issuers (ring invariant above)
       // one cursor per issuer: (iteration pair it0, term t)
       int c_it0[2] = {0, 0}, c_t[2] = {0, 0};
       int seq = 0;

@@ -12,6 +12,7 @@
 // pair (same box, zero shift, j == i) is skipped exactly like :182-189.
 #pragma once
 #include "lfmm_common.cuh"
+#include "lfmm_sm100.cuh"
 #include "lfmm_tree.cuh"
 
 namespace lfmm {

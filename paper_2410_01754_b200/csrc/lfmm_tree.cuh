@@ -228,34 +228,6 @@ __global__ void __launch_bounds__(RANK_WARPS * 32) k_leaf_rank(const double* __r
   }
 }
 
-// Canonical-order arrays: fp64 sorted positions and leaf-relative coordinates
-// (x - c_leaf with c_leaf = (grid + 0.5) * size, octree.py:65-66) in T.
-template <class T>
-__global__ void k_sorted_arrays(const double* __restrict__ pos_wrap, const int* __restrict__ perm,
-                                const int* __restrict__ leaf_of, int64_t n, int depth, double size,
-                                double* __restrict__ pos_sorted, vec4_t<T>* __restrict__ xq,
-                                int* __restrict__ leaf_sorted) {
-  const int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (k >= n) return;
-  const int i = perm[k];
-  const int leaf = leaf_of[i];
-  const int nside = 1 << depth, msk = nside - 1;
-  const int g[3] = {leaf >> (2 * depth), (leaf >> depth) & msk, leaf & msk};
-  double r[3];
-#pragma unroll
-  for (int a = 0; a < 3; ++a) {
-    r[a] = pos_wrap[3 * i + a];
-    pos_sorted[3 * k + a] = r[a];
-  }
-  vec4_t<T> v;
-  v.x = (T)(r[0] - (g[0] + 0.5) * size);
-  v.y = (T)(r[1] - (g[1] + 0.5) * size);
-  v.z = (T)(r[2] - (g[2] + 0.5) * size);
-  v.w = T(0);
-  xq[k] = v;
-  leaf_sorted[k] = leaf;
-}
-
 // Neighbour enumeration shared by P2P and the list export (octree.py:136-139):
 // row t of NEIGHBOR_OFFSETS is ((t/9)-1, (t/3)%3-1, t%3-1).
 __host__ __device__ inline void neighbor(int b, int t, int depth, int& nb, int& shx, int& shy, int& shz) {

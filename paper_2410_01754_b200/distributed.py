@@ -447,6 +447,8 @@ class DistributedSolver:
 
     def _step(self, positions, charges, global_ids, lambdas, n_lambda, sites, n_global, mode):
         torch = self.torch
+        if sites is not None and (lambdas is None or n_lambda is None):
+            raise ValueError("sites need lambdas and n_lambda (the HI step scales the site charges)")
         d = self.cfg.depth
         pos_l, q_l, gid_l, n_own = self._exchange_particles(positions.contiguous(), charges.contiguous(),
                                                             global_ids)
@@ -457,8 +459,6 @@ class DistributedSolver:
         plan.set_count(n_loc)
         n_sites = 0
         if sites is not None:
-            if lambdas is None or n_lambda is None:
-                raise ValueError("sites need lambdas and n_lambda (the HI step scales the site charges)")
             ao, ai, nf, fo, fq = sites
             if self._site_dev is None or self._site_key is not sites:
                 self._site_dev = torch.as_tensor(np.asarray(ai, np.int64), device=positions.device)

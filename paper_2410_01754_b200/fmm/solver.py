@@ -84,6 +84,8 @@ class PeriodicSolver:
         self._plan = _native.Plan(pos, self.box_length, cfg.p, cfg.depth, _native.LFMM_LATTICE[cfg.lattice_mode],
                                   cfg.shell_cap, cfg.flags())
         self._n = pos.shape[0]
+        self._positions = pos
+        self._plan64 = None  # fp64 plan of spatial_forces under precision="single"
         self.lattice_matrix = None
         if cfg.lattice_mode != "off":
             lm = self._plan.lattice_matrix()
@@ -148,6 +150,21 @@ class PeriodicSolver:
         return self._result(out, True), out["forces"]
 
     def spatial_forces(self, charges):
-        """Forces -q grad V on every particle, (N, 3) (solver.py:407-427)."""
+        """Forces -q grad V on every particle, (N, 3) (solver.py:407-427).
+
+        The reference evaluates spatial forces in full fp64 whatever the
+        precision knob (its single-precision rounder only touches solve,
+        solver.py:357-371, :407-427), so with precision="single" this runs
+        on a lazily created fp64 plan over the same positions.  The fused
+        fp32 step path (solve_with_forces, lfmm_step) keeps the plan's
+        precision."""
+        if self.config.precision == "single":
+            if self._plan64 is None:
+                cfg = self.config
+                self._plan64 = _native.Plan(self._positions, self.box_length, cfg.p, cfg.depth,
+                                            _native.LFMM_LATTICE[cfg.lattice_mode], cfg.shell_cap,
+                                            cfg.flags() & ~_native.F_FP32)
+            q2, _ = self._charges(np.asarray(charges, dtype=np.float64).reshape(-1))
+            return self._plan64.solve(q2, forces=True)["forces"]
         _, f = self.solve_with_forces(charges)
         return f

@@ -176,6 +176,17 @@ def make_site_forces():
     print("wrote ref_site_forces.npz")
 
 
+def make_site_forces_c4():
+    """The C4 box (4096 sites): -dDelta E_site/dr of every site atom."""
+    t0 = time.time()
+    system, lam, _ = generate_water_box(1_000_000, 4096, seed=5)
+    solver = PeriodicSolver(system.positions[:1], system.box_length, SolverConfig(p=10, depth=5))
+    idx, f = site_force_corrections(system, lam.values, solver, range(len(system.sites)))
+    np.savez_compressed(os.path.join(OUT, "ref_site_forces_c4.npz"), c4_checksum=checksum(system), c4_idx=idx,
+                        c4_dforce=f)
+    print("c4 site forces in %.1f s" % (time.time() - t0))
+
+
 def main():
     which = sys.argv[1:] or ["c2", "c3"]
     if "c2" in which:
@@ -189,6 +200,8 @@ def main():
     if "c4" in which:
         # the HI site-count stress box
         make("ref_c4_d5.npz", 1_000_000, 4096, 5, 5)
+    if "sitef4" in which:
+        make_site_forces_c4()
     if "c3d6" in which:
         # the C3 box at the reference's depth cap (solver.py:62-64), ~3.8 atoms/leaf
         make("ref_c3_d6.npz", 1_000_000, 512, 4, 6)

@@ -222,3 +222,37 @@ def test_particle_halo_exchange_gloo(world):
         assert sorted(g_l[n_own:]) == sorted(halo)
         assert np.array_equal(p_l, moved[g_l])
         assert np.array_equal(q_l, g_l * 0.5)
+
+
+def test_single_plane_slabs_reject_migrants():
+    """with one leaf plane per rank (depth 2, world 4) a migrant
+    into plane x1 is also rank r+2's halo, which the one-hop exchange never
+    reaches; step_owned must refuse instead of dropping P2P pairs."""
+    import torch
+
+    from paper_2410_01754_b200.distributed import DistributedSolver, LocalComm
+    from paper_2410_01754_b200.fmm.solver import SolverConfig
+
+    box, depth, world = 4.0, 2, 4
+    solver = DistributedSolver(box, SolverConfig(p=4, depth=depth), comm=LocalComm(world).for_rank(1))
+    assert (solver.x0, solver.x1) == (1, 2)
+    pos = torch.tensor([[1.5, 0.3, 0.3], [1.2, 2.0, 1.0], [0.5, 1.0, 1.0]], dtype=torch.float64)  # last: plane 0
+    q = torch.zeros(3, dtype=torch.float64)
+    gid = torch.arange(3)
+    with pytest.raises(ValueError, match="single leaf plane"):
+        solver._exchange_particles(pos, q, gid)
+
+
+def test_sites_without_lambdas_rejected():
+    """sites given without lambdas would run the HI kernel on
+    never-uploaded lambdas; the step refuses before any device work."""
+    import torch
+
+    from paper_2410_01754_b200.distributed import DistributedSolver, LocalComm
+    from paper_2410_01754_b200.fmm.solver import SolverConfig
+
+    solver = DistributedSolver(4.0, SolverConfig(p=4, depth=2), comm=LocalComm(1).for_rank(0))
+    pos = torch.rand(8, 3, dtype=torch.float64) * 4.0
+    tables = (np.array([0, 2]), np.array([0, 1]), np.array([2], np.int32), np.array([0, 4]), np.zeros(4))
+    with pytest.raises(ValueError, match="lambdas"):
+        solver._step(pos, torch.zeros(8, dtype=torch.float64), torch.arange(8), None, None, tables, 8, 0)

@@ -97,3 +97,36 @@ def test_replica_rng_streams_differ_and_reproduce():
     a = dyn.replica_rng(7, 0).standard_normal(4)
     assert_allclose(a, dyn.replica_rng(7, 0).standard_normal(4), rtol=0, atol=0)
     assert not np.allclose(a, dyn.replica_rng(7, 1).standard_normal(4))
+
+
+class CoupledSprings:
+    """tests/golden/make_golden_dynamics.py CoupledSprings (same formula)."""
+
+    def lambda_forces(self, lam_values):
+        flat = np.concatenate([np.asarray(v, float) for v in lam_values])
+        k, g = 80.0 / COULOMB_KJ_PER_MOL, 15.0 / COULOMB_KJ_PER_MOL
+        centre = np.linspace(0.35, 0.65, flat.size)
+        f = -k * (flat - centre) - g * (flat.sum() - flat)
+        e = 0.5 * k * float(((flat - centre) ** 2).sum())
+        out, o = [], 0
+        for v in lam_values:
+            out.append(f[o:o + len(v)])
+            o += len(v)
+        return e, out
+
+
+def test_thermostatted_trajectory_matches_reference_run():
+    """The reference's own run_trajectory (dynamics.py:214-285) on a coupled
+    spring field, thermostatted, two sites, sample_every=7: same samples to
+    round-off, same final state (tests/golden/dyn_spring.npz)."""
+    import os
+
+    g = np.load(os.path.join(os.path.dirname(__file__), "golden", "dyn_spring.npz"))
+    lam = LambdaState(values=[np.array([0.3]), np.array([0.6, 0.2])], velocities=[np.array([0.1]), np.zeros(2)],
+                      masses=[5.0, 3.0])
+    t = dyn.run_trajectory(CoupledSprings(), lam, 400, dt=0.002, temperature=300.0, friction=5.0,
+                           bias=dyn.BiasPotential(4.0), rng=np.random.default_rng(9), sample_every=7)
+    for key in ("times", "lambdas", "velocities", "forces", "energies"):
+        assert_allclose(getattr(t, key), g[key], rtol=1e-12, atol=1e-12, err_msg=key)
+    assert_allclose(np.concatenate(lam.values), g["final_values"], rtol=1e-12, atol=1e-12)
+    assert_allclose(np.concatenate(lam.velocities), g["final_velocities"], rtol=1e-12, atol=1e-12)

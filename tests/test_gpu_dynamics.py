@@ -103,3 +103,25 @@ def test_device_noise_variance_is_kt_over_m():
     sd = np.sqrt(BOLTZMANN_KJ_PER_MOL_K * 300.0 / m)
     assert abs(v.mean()) < 4 * sd / np.sqrt(v.size)
     assert abs(np.var(v) / sd ** 2 - 1.0) < 0.25
+
+
+def test_frozen_field_trajectory_matches_reference_run():
+    """The reference's run_trajectory over its FrozenLambdaForceField
+    (dynamics.py:88-171, :214-285) on a small periodic system, HI mode, p=8,
+    depth 1, thermostatted: this package's frozen field (device basis solve +
+    device site Gram) under the host BAOAB reproduces every sample
+    (tests/golden/dyn_frozen.npz)."""
+    import os
+
+    g = np.load(os.path.join(os.path.dirname(__file__), "golden", "dyn_frozen.npz"))
+    sites = [TitratableSite(g["site0_idx"], g["site0_forms"]), TitratableSite(g["site1_idx"], g["site1_forms"])]
+    system = ParticleSystem(float(g["box"]), g["positions"], g["charges"], sites)
+    lam = LambdaState(values=[np.array([0.4]), np.array([0.7, 0.25])], velocities=[np.zeros(1), np.zeros(2)],
+                      masses=[5.0, 5.0])
+    field = dyn.FrozenLambdaForceField(system, config=SolverConfig(p=8, depth=1))
+    t = dyn.run_trajectory(field, lam, 150, dt=0.002, temperature=300.0, friction=5.0,
+                           rng=np.random.default_rng(21), sample_every=3)
+    for key in ("times", "lambdas", "velocities"):
+        assert_allclose(getattr(t, key), g[key], rtol=0, atol=1e-9, err_msg=key)
+    assert_allclose(t.forces, g["forces"], rtol=0, atol=1e-9 * np.abs(g["forces"]).max())
+    assert_allclose(t.energies, g["energies"], rtol=1e-11)

@@ -26,7 +26,7 @@ from paper_2410_01754_b200 import (  # noqa: E402
 from paper_2410_01754_b200.waterbox import generate_water_box  # noqa: E402
 
 GOLDEN = os.path.join(os.path.dirname(__file__), "golden")
-CASES = {"c2": "ref_c2_d4.npz", "c3": "ref_c3_d5.npz"}
+CASES = {"c2": "ref_c2_d4.npz", "c3": "ref_c3_d5.npz", "c4": "ref_c4_d5.npz", "c3d6": "ref_c3_d6.npz"}
 _systems = {}
 
 
@@ -49,7 +49,7 @@ def _err(got, ref, absmax):
 
 
 @pytest.mark.parametrize("precision", ["double", "single"])
-@pytest.mark.parametrize("case", ["c2", "c3"])
+@pytest.mark.parametrize("case", ["c2", "c3", "c4", "c3d6"])
 def test_matches_reference(case, precision):
     g, system, lam = _load(case)
     tol = 1e-6 if precision == "double" else 1e-4

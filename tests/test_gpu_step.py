@@ -101,7 +101,7 @@ def lambda_rows(system, lam_values, lf):
 
 
 def site_force_fixture(tag):
-    g = np.load(os.path.join(GOLDEN, "ref_site_forces.npz"))
+    g = np.load(os.path.join(GOLDEN, "ref_site_forces_c4.npz" if tag == "c4" else "ref_site_forces.npz"))
     return g[tag + "_idx"], g[tag + "_dforce"], g[tag + "_checksum"]
 
 
@@ -151,9 +151,12 @@ def test_step_qi_mode_forces_are_charge_scaled():
 # --------------------------------------------------- C2 / C3, reference ----
 @pytest.mark.slow
 @pytest.mark.parametrize("precision", ["double", "single"])
-@pytest.mark.parametrize("case", ["c2", "c3"])
+@pytest.mark.parametrize("case", ["c2", "c3", "c4", "c3d6"])
 def test_step_matches_reference(case, precision):
-    name = {"c2": "ref_c2_d4.npz", "c3": "ref_c3_d5.npz"}[case]
+    """C2 (100k, 64 sites, d=4), C3 (1M, 512 sites, d=5), C4 (1M, 4096
+    sites, d=5: the HI site-count stress box) and the C3 box at the
+    reference's depth cap d=6 (solver.py:62-64)."""
+    name = {"c2": "ref_c2_d4.npz", "c3": "ref_c3_d5.npz", "c4": "ref_c4_d5.npz", "c3d6": "ref_c3_d6.npz"}[case]
     g = np.load(os.path.join(GOLDEN, name))
     system, lam = water(int(g["n_atoms"]), int(g["n_sites"]), int(g["seed"]))
     np.testing.assert_allclose(checksum(system), g["checksum"], rtol=1e-13)
@@ -163,7 +166,7 @@ def test_step_matches_reference(case, precision):
         e, f, lf = st.step(system.positions)
     tol = TOL[precision]
     idx = g["idx"]
-    sidx, dforce, _ = site_force_fixture(case)
+    sidx, dforce, _ = site_force_fixture("c3" if case == "c3d6" else case)
     f_ref = g["forces"].copy()
     pos_in_sample = {int(a): k for k, a in enumerate(idx)}
     hit = 0

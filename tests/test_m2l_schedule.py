@@ -54,10 +54,31 @@ def test_groups_cover_every_source_class_once(G):
         assert sorted(seen) == list(range(8))
 
 
-def test_stagger_cap_leaves_ring_room():
-    """The kernel caps the lag at AS - 6 (k_m2l_halo<AS>): with the 14- and
-    10-stage rings that is 8 and 4 terms, below the shortest term list (19)."""
-    for AS, default in ((14, 8), (10, 8)):
-        D = min(default, AS - 6)
-        assert D <= 19
-        assert D <= AS - 6
+def test_stagger_keeps_every_wait_sound():
+    """The mbarrier parity wait of sequence j on stage j % AS is only sound
+    when fill j - AS of that stage completed before it (otherwise the wait
+    sees the phase two behind and passes).  Fills complete in issue order and
+    an issuer's consumed sequence m orders every fill <= m before its next
+    wait, so j - AS <= m_last must hold for every term of both issuers, with
+    the kernel's lag cap D = min(stagger, AS - 6) (k_m2l_halo<AS>: 14- and
+    10-stage rings) and every term count the job lists produce."""
+    for AS in (14, 10):
+        for stagger in range(0, 17):
+            for nts in ((19,), (26,), (19, 26), (25, 23), (23, 19, 26, 25)):
+                T = (HM_NKC // 2) * sum(nts)
+                D = min(stagger, AS - 6, T)
+                assert D + 1 < AS
+                for par in (0, 1):
+                    last = -1
+                    for u in range(T):
+                        j = hm_aseq(par, u, D, T)
+                        assert j - AS <= last, (AS, stagger, nts, par, u)
+                        last = j
+
+
+def test_stagger_bound_is_tight():
+    """With D = AS - 1 issuer 1's first wait (j = AS) would read the parity
+    of a stage whose first fill nobody has ordered: the invariant fails."""
+    AS, T = 14, 76
+    D = AS - 1
+    assert hm_aseq(1, 0, D, T) - AS > -1

@@ -133,7 +133,8 @@ def main():
               (level, np.abs(Mh).max(), np.abs(Ms).max(), np.abs(Ms[Ms != 0]).min()))
         gl = 2.0 ** (12 - np.ceil(np.log2(np.abs(Ms).max())))
         pairs = orc.m2l_pairs(level)
-        variants = {"exact": None, "fp32": None, "tf32x3": None, "fp16x3": None, "fp16x1": None}
+        variants = {"exact": None, "fp32": None, "tf32x3": None, "fp16x3": None, "fp16x2a": None,
+                    "fp16x2b": None, "fp16x1": None}
         locs = {}
         for name in variants:
             Lh = np.zeros_like(Mh)
@@ -150,6 +151,14 @@ def main():
                     ah, al = split(Bs[row], "fp16")
                     bh, bl = split(Ms[:, s] * gl, "fp16")
                     Lh[:, t] += ((ah @ bh + ah @ bl + al @ bh) / r[:, None]) / gl
+                elif name == "fp16x2a":  # operator hi/lo, multipoles one fp16
+                    ah, al = split(Bs[row], "fp16")
+                    bh = np.asarray(Ms[:, s] * gl, np.float16).astype(np.float64)
+                    Lh[:, t] += ((ah @ bh + al @ bh) / r[:, None]) / gl
+                elif name == "fp16x2b":  # operator one fp16, multipoles hi/lo
+                    ah = np.asarray(Bs[row], np.float16).astype(np.float64)
+                    bh, bl = split(Ms[:, s] * gl, "fp16")
+                    Lh[:, t] += ((ah @ bh + ah @ bl) / r[:, None]) / gl
                 elif name == "fp16x1":
                     ah = np.asarray(Bs[row], np.float16).astype(np.float64)
                     bh = np.asarray(Ms[:, s] * gl, np.float16).astype(np.float64)
