@@ -633,8 +633,10 @@ def hi_site_forces(positions, box, sites, lam_values, cfg, lat):
             rv = regular(sp - 0.5 * box, cfg["p"])
             dr = regular_grad(sp - 0.5 * box, cfg["p"])
             # d/dr_i sum_st W_st Re(R_s T R_t): both slots
-            g += np.real(np.einsum("inx,nm,tm,it->ix", dr, lat, rv, wm))
-            g += np.real(np.einsum("sn,nm,imx,si->ix", rv, lat, dr, wm))
+            v1 = lat @ (rv.T @ wm.T)  # (nc, ns): column i = T sum_t W_it R_t
+            v2 = (wm.T @ rv) @ lat    # (ns, nc): row i = sum_s W_si R_s T
+            g += np.real(np.einsum("inx,ni->ix", dr, v1))
+            g += np.real(np.einsum("imx,im->ix", dr, v2))
         if full and cfg["dipole"]:
             dev = qt[None, :] - forms
             dd = dev @ (sp - 0.5 * box)
@@ -657,6 +659,82 @@ def direct_potentials(positions, charges, box, shell_cap=0):
             np.fill_diagonal(r, np.inf)
         v += (1.0 / r) @ q
     return v
+
+
+# ------------------------------------------------------- full CPU step ----
+if _nb is not None:
+    _p2p_serial = _nb.njit(parallel=False, cache=False)(_p2p_numba.py_func)
+else:  # pragma: no cover
+    _p2p_serial = None
+
+
+def full_step(positions, charges, box, sites, lam_values, cfg, clock, serial_near=True):
+    """One complete electrostatics step on the host, nothing sampled or
+    extrapolated (SURVEY.md §8d step definition): tree + scale_charges
+    (system.py:179-197) + solve with near/far/dipole potentials, energies and
+    spatial forces in one pass (solver.py:349-427) + HI corrections and
+    lambda forces (corrections.py:157-274) + the HI site-atom forces.  The
+    near field runs the reference's serial numba loop (solver.py:164-195:
+    @njit without parallel) when serial_near; numpy / BLAS use every thread
+    they are given (the reference's LAMBDAFMM_THREADS knob, cli.py:35-47).
+    Returns (seconds, parts, results)."""
+    parts = {}
+    t0 = clock()
+    q = np.array(charges, np.float64, copy=True)
+    for (idx, forms), lams in zip(sites, lam_values):
+        q[idx] = weights(lams) @ forms
+    pos = wrap(np.atleast_2d(positions), box)
+    tree = build_tree(pos, box, cfg["depth"])
+    qs = q[tree["perm"]][:, None]
+    parts["tree+scale"] = clock() - t0
+    t0 = clock()
+    if serial_near and _p2p_serial is not None:
+        nleaf = tree["leaf_start"].size - 1
+        vn = np.zeros((pos.shape[0], 1))
+        gn = np.zeros((pos.shape[0], 3))
+        rows = np.arange(27) if cfg["periodic_near"] else np.array([13])
+        _p2p_serial(tree["positions"], tree["leaf_start"], tree["nb_box"],
+                    (tree["nb_shift"] * box).astype(np.float64), np.ascontiguousarray(qs), rows,
+                    np.arange(nleaf), True, vn, gn)
+    else:
+        vn, gn = near_field(tree, qs, cfg["periodic_near"], grad=True)
+    parts["p2p"] = clock() - t0
+    t0 = clock()
+    mult = upward(tree, qs, cfg["p"])
+    parts["p2m+m2m"] = clock() - t0
+    t0 = clock()
+    lat = lattice_matrix(cfg, box)
+    root_local = None if lat is None else lat @ mult[0][:, 0, :]
+    loc = downward(tree, mult, cfg["p"], root_local)
+    parts["lattice+m2l+l2l"] = clock() - t0
+    t0 = clock()
+    vf, gf = evaluate(tree, loc, cfg["p"], grad=True)
+    parts["l2p"] = clock() - t0
+    t0 = clock()
+    disp = tree["positions"] - 0.5 * box
+    dvec = disp.T @ qs
+    gam = 2.0 * math.pi / (3.0 * box ** 3)
+    if cfg["dipole"]:
+        vd = 2.0 * DIPOLE_ETA * gam * (disp @ dvec)
+        ed = float(DIPOLE_ETA * gam * (dvec * dvec).sum())
+    else:
+        vd, ed = np.zeros_like(vn), 0.0
+    en = 0.5 * math.fsum((qs[:, 0] * vn[:, 0]).tolist())
+    ef = 0.5 * math.fsum((qs[:, 0] * vf[:, 0]).tolist())
+    inv = tree["inv_perm"]
+    pot = (vn + vf + vd)[inv, 0]
+    f = -qs[:, :1] * (gn + gf)
+    if cfg["dipole"]:
+        f += -2.0 * DIPOLE_ETA * gam * qs[:, :1] * dvec[None, :, 0]
+    forces = f[inv]
+    res = dict(potentials=pot, energy=en + ef + ed, lattice=lat)
+    out = hi(positions, charges, box, sites, lam_values, cfg, solve_out=res)
+    if sites:
+        idx = np.concatenate([s[0] for s in sites])
+        forces[idx] += hi_site_forces(positions, box, sites, lam_values, cfg, lat)
+    parts["finalize+hi"] = clock() - t0
+    out["spatial_forces"] = forces
+    return sum(parts.values()), parts, out
 
 
 # --------------------------------------------------- timed CPU sample ----

@@ -224,16 +224,6 @@ __global__ void k_box_charges(const double* __restrict__ qs, const int* __restri
   }
 }
 
-// coefficient 0 of levels [0, lmax) from the exact box charges of
-// k_box_charges (its wmin = lmax run left them out while the small levels'
-// M2M ran beside it)
-template <class T>
-__global__ void k_apply_boxq(const double* __restrict__ boxq, int lmax, int ncp, T* __restrict__ mult) {
-  const int64_t nb = ((1LL << (3 * lmax)) - 1) / 7;  // boxes of levels 0 .. lmax-1
-  for (int64_t b = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; b < nb; b += (int64_t)gridDim.x * blockDim.x)
-    mult[(size_t)b * ncp] = (T)boxq[b];
-}
-
 template <int NQ>
 __global__ void k_reduce_parts(const dd* __restrict__ part, int nb, double* __restrict__ out) {
   dd v[NQ];
@@ -525,11 +515,16 @@ int halo_smem_attr(int rw_cap) {
   return HM_ASTAGES_SMALL;
 }
 
-void launch_m2l_halo(const HaloArgs& ha, int njobs, int astages, cudaStream_t st) {
+// persistent launch: at most `ctas` CTAs (one per SM) walk the njobs jobs of
+// ha.jobs through the zeroed ha.counter
+void launch_m2l_halo(HaloArgs ha, int njobs, int ctas, int astages, cudaStream_t st) {
+  ha.njobs = njobs;
+  LFMM_CUDA(cudaMemsetAsync(ha.counter, 0, sizeof(int), st));
+  const unsigned grid = (unsigned)std::max(1, std::min(njobs, ctas));
   if (astages == HM_ASTAGES)
-    k_m2l_halo<HM_ASTAGES><<<njobs, HM_THREADS, hm_smem_bytes(ha.rw_cap, HM_ASTAGES), st>>>(ha);
+    k_m2l_halo<HM_ASTAGES><<<grid, HM_THREADS, hm_smem_bytes(ha.rw_cap, HM_ASTAGES), st>>>(ha);
   else
-    k_m2l_halo<HM_ASTAGES_SMALL><<<njobs, HM_THREADS, hm_smem_bytes(ha.rw_cap, HM_ASTAGES_SMALL), st>>>(ha);
+    k_m2l_halo<HM_ASTAGES_SMALL><<<grid, HM_THREADS, hm_smem_bytes(ha.rw_cap, HM_ASTAGES_SMALL), st>>>(ha);
 }
 
 }  // namespace
@@ -555,10 +550,6 @@ struct lfmm_plan {
   cudaStream_t near_stream = nullptr;
   cudaEvent_t ev_near_in = nullptr, ev_near_out = nullptr;
   bool near_pending = false;
-  // far_overlapped(): the latency-bound small levels of the far field run on
-  // far_stream (highest priority) beside the big levels' M2L
-  cudaStream_t far_stream = nullptr;
-  cudaEvent_t ev_far_fork = nullptr, ev_far_join = nullptr;
   // HI corrections (site geometry only) run on hi_stream beside the solve
   cudaStream_t hi_stream = nullptr;
   cudaEvent_t ev_hi_in = nullptr, ev_hi_out = nullptr;
@@ -584,7 +575,6 @@ struct lfmm_plan {
   // expansions / operators
   bool use_halo = false;  // fp32 M2L on tcgen05 as shifted-window fp16x3 GEMMs (lfmm_m2l_halo.cuh)
   bool p2p_scalar = false;  // fp32 P2P on the scalar kernel (LFMM_P2P=scalar, A/B checks)
-  bool far_serial = false;  // no far_overlapped() (LFMM_FAR=serial, A/B checks and tools/hm_prof.py)
   bool step_mode = false;   // lfmm_step: skip the input-order potential arrays
   // Slab decomposition (distributed.py): this rank owns leaves with x index in
   // [own_x0, own_x1); levels < dist_lg have boxes spanning ranks and are
@@ -593,8 +583,14 @@ struct lfmm_plan {
   int own_x0 = 0, own_x1 = 1 << 30, dist_lg = 0, dist_phase = 0;
   DevBuf up_part, up_cnt, counters;
   DevBuf ops16, hm_inv_r, hm_inv_c, hm_jobs, hm_level_max, mult16, ops_m2l_t;
+  DevBuf hm_counter;  // job counters of the persistent M2L launches (main, far stream)
+  DevBuf p2p_ctl;     // preemptible near field: leaf counter, stop flags of launches 1, 2, 3
+  cudaEvent_t ev_m2l_done = nullptr;
+  int p2p_c1 = 3, p2p_c2 = 3;  // CTAs per SM of near-field launches 1 and 2 (room for the far-field chains)
+  bool p2p_preempt = true;
+  int nsm = 148;
   int64_t m16_off[DMAX + 2] = {0};
-  int hm_njobs = 0, hm_rw_cap = 0, hm_lsplit = 1, hm_nbig = 0, hm_astages = HM_ASTAGES;
+  int hm_njobs = 0, hm_rw_cap = 0, hm_astages = HM_ASTAGES;
   static constexpr int hm_stagger = 8;       // terms issuer 1 lags issuer 0 (capped at AS - 6 in the kernel)
   static constexpr int hm_groups_big = 2;    // M2L jobs (partial slots) per tile at levels >= 4
   static constexpr int hm_groups_small = 8;  // ... at levels < 4 (one source class per job)
@@ -637,22 +633,39 @@ struct lfmm_plan {
     LFMM_CUDA(cudaEventCreate(&e));
     return e;
   }
+  // tracing (profiling build, tools/step_trace.py): events on the launching
+  // stream around every launch without serialising the streams
+  bool tracing = false;
+  cudaEvent_t trace_base = nullptr;
+  std::vector<Ev> trace;
+  cudaStream_t rec_stream = nullptr;  // stream of the launch in flight (launch_on)
   template <class F>
   void launch(int stage, F&& f) {
     cudaEvent_t a = nullptr, b = nullptr;
-    if (profiling) {
+    cudaStream_t rs = rec_stream ? rec_stream : stream;
+    if (profiling || tracing) {
       a = get_event();
       b = get_event();
-      LFMM_CUDA(cudaEventRecord(a, stream));
+      LFMM_CUDA(cudaEventRecord(a, rs));
     }
     f();
     LFMM_CUDA(cudaGetLastError());
     ++launches;
     stage_launch[stage]++;
     if (profiling) {
-      LFMM_CUDA(cudaEventRecord(b, stream));
+      LFMM_CUDA(cudaEventRecord(b, rs));
       pending.push_back({stage, a, b});
+    } else if (tracing) {
+      LFMM_CUDA(cudaEventRecord(b, rs));
+      trace.push_back({stage, a, b});
     }
+  }
+  template <class F>
+  void launch_on(int stage, cudaStream_t st, F&& f) {
+    cudaStream_t prev = rec_stream;
+    rec_stream = st;
+    launch(stage, f);
+    rec_stream = prev;
   }
   void harvest() {
     if (pending.empty()) return;
@@ -673,7 +686,7 @@ struct lfmm_plan {
       cudaEventDestroy(e.b);
     }
     for (auto e : free_events) cudaEventDestroy(e);
-    DevBuf* hbufs[] = {&ops16, &hm_inv_r, &hm_inv_c, &hm_jobs, &hm_level_max, &mult16, &boxq, &site_pot, &ops_m2m_t, &ops_l2l_t, &ops_lat_t, &tr_cnt, &ops_m2l_t};
+    DevBuf* hbufs[] = {&ops16, &hm_inv_r, &hm_inv_c, &hm_jobs, &hm_counter, &p2p_ctl, &hm_level_max, &mult16, &boxq, &site_pot, &ops_m2m_t, &ops_l2l_t, &ops_lat_t, &tr_cnt, &ops_m2l_t};
     for (auto* b : hbufs) b->release();
     DevBuf* bufs[] = {&pos_in, &pos_wrap, &leaf_of, &slot_of, &counts, &cursor, &leaf_start, &bucket, &perm,
                       &inv_perm, &pos_sorted, &leaf_sorted, &xq, &mult, &loc, &partial, &up_part, &up_cnt, &counters, &ops_m2l, &ops_m2m,
@@ -687,14 +700,12 @@ struct lfmm_plan {
     if (io_stream) cudaStreamDestroy(io_stream);
     if (near_stream) cudaStreamDestroy(near_stream);
     if (hi_stream) cudaStreamDestroy(hi_stream);
-    if (far_stream) cudaStreamDestroy(far_stream);
-    if (ev_far_fork) cudaEventDestroy(ev_far_fork);
-    if (ev_far_join) cudaEventDestroy(ev_far_join);
     if (ev_hi_in) cudaEventDestroy(ev_hi_in);
     if (ev_hi_out) cudaEventDestroy(ev_hi_out);
     if (ev_near_in) cudaEventDestroy(ev_near_in);
     if (ev_near_out) cudaEventDestroy(ev_near_out);
     if (ev_q) cudaEventDestroy(ev_q);
+    if (ev_m2l_done) cudaEventDestroy(ev_m2l_done);
     if (ev_f) cudaEventDestroy(ev_f);
   }
 
@@ -1015,24 +1026,20 @@ struct lfmm_plan {
           if (ia >= ib) continue;
         }
         const int r0 = S + ia * Z * Z, r1 = std::min(last, S + (ib - 1) * Z * Z + h * Z + h);
-        for (int t0 = r0; t0 <= r1; t0 += HM_NMAX) {
-          const int N = std::min(HM_NMAX, ((r1 + 1 - t0) + 15) / 16 * 16);
+        // tiles of equal size (a multiple of 16 rows, <= HM_NMAX): a short
+        // last tile would cost a full tile's MMA issue for a few rows
+        const int rows = r1 + 1 - r0, ntile = (rows + HM_NMAX - 1) / HM_NMAX;
+        const int nt16 = ((rows + ntile - 1) / ntile + 15) / 16 * 16;
+        for (int t0 = r0; t0 <= r1; t0 += nt16) {
+          const int N = std::min(nt16, ((r1 + 1 - t0) + 15) / 16 * 16);
           hm_rw_cap = std::max(hm_rw_cap, hm_rw(N, Z));
           for (int grp = 0; grp < G; ++grp) jobs.push_back(make_int4(l | (tc << 4) | (grp << 8) | (G << 12), t0, N, 0));
         }
       }
     }
-    // two launches when the far field is overlapped (far_overlap): levels >=
-    // hm_lsplit first, then the small levels; big jobs first within each
-    hm_lsplit = (depth >= 3 && dist_lg == 0) ? depth - 1 : 1;
-    const int ls = hm_lsplit;
-    std::stable_sort(jobs.begin(), jobs.end(), [ls](const int4& a, const int4& b) {
-      const int ga = (a.x & 15) >= ls ? 0 : 1, gb = (b.x & 15) >= ls ? 0 : 1;
-      if (ga != gb) return ga < gb;
-      return a.z > b.z;
-    });
-    hm_nbig = 0;
-    for (const int4& j : jobs) hm_nbig += (j.x & 15) >= ls ? 1 : 0;
+    // big jobs first: the small levels' short jobs fill the tail of the
+    // persistent launch
+    std::stable_sort(jobs.begin(), jobs.end(), [](const int4& a, const int4& b) { return a.z > b.z; });
     int64_t moff = 0;
     for (int l = 1; l <= depth; ++l) {
       m16_off[l] = moff;
@@ -1040,6 +1047,9 @@ struct lfmm_plan {
     }
     mult16.ensure(std::max<int64_t>(moff, 16));
     hm_njobs = (int)jobs.size();
+    hm_counter.ensure(sizeof(int) * 2);
+    p2p_ctl.ensure(sizeof(int) * 4);
+    if (!ev_m2l_done) LFMM_CUDA(cudaEventCreateWithFlags(&ev_m2l_done, cudaEventDisableTiming));
     hm_jobs.ensure(sizeof(int4) * std::max<size_t>(jobs.size(), 1));
     if (!jobs.empty())
       LFMM_CUDA(cudaMemcpyAsync(hm_jobs.p, jobs.data(), sizeof(int4) * jobs.size(), cudaMemcpyHostToDevice, stream));
@@ -1139,32 +1149,21 @@ struct lfmm_plan {
   }
 
   // ---------------------------------------------------------- solve ----
-  // Far field with the small levels beside the big ones (fp32 halo path,
-  // single rank, depth >= 3).  The levels < ls = hm_lsplit hold <= 8^(d-2)
-  // boxes: their M2M / M2L / L2L launches are latency-bound chains of a few
-  // us each that would otherwise sit on the critical path.
-  //   stream:     M2M (>= ls) -> box charges -> [fork] -> pack + M2L (>= ls)
-  //               -> [join] -> L2L (>= ls)
-  //   far_stream: [fork] -> M2M (< ls) -> exact charges (< ls) -> lattice
-  //               -> pack + M2L (< ls) -> L2L (< ls) -> [join]
-  // Every buffer region is written by exactly one side (levels are disjoint;
-  // the fork orders the small M2M after the level-ls box charges), so the
-  // result is the same sequence of operations on every run.
-  bool far_overlap() const {
-    return use_halo && fp32 && use_tr && !profiling && !far_serial && dist_lg == 0 && dist_phase == 0 && depth >= 3 &&
-           hm_lsplit > 1 && hm_nbig > 0 && hm_nbig < hm_njobs;
-  }
-  void tr_m2m(int l, cudaStream_t st) {
-    TrArgs ta{};
-    ta.mode = 0;
-    ta.level = l;
-    ta.ncp = ncp;
-    ta.ops_t = ops_m2m_t.p;
-    ta.src = mult.as<float>() + level_off[l + 1] * ncp;
-    ta.dst = mult.as<float>() + level_off[l] * ncp;
-    ta.slots = up_part.p;
-    ta.cnt = tr_cnt.as<int>();
-    launch(ST_M2M, [&] { tr_launch<float>(ta, 1 << (3 * l), 8, st); });
+  // k_p2p2: ctas == 0 one warp per leaf; else persistent with that many CTAs
+  // over the shared leaf counter p2p_ctl[0], stopped by *stop
+  void p2p2_launch(bool grad, int periodic, int ctas, const int* stop, cudaStream_t st) {
+    const unsigned grid = ctas > 0 ? (unsigned)ctas : nblk(own_leaves(), P2P2_WARPS);
+    int* ctl = ctas > 0 ? p2p_ctl.as<int>() : nullptr;
+    if (grad)
+      k_p2p2<true><<<grid, P2P2_WARPS * 32, P2P2_SMEM, st>>>(reinterpret_cast<const float4*>(xq.p), pair_a(), pair_b(),
+                                                            leaf_start.as<int>(), depth, (float)size, periodic,
+                                                            vnear.as<float>(), gnear.as<float>(), own_x0, own_x1, ctl,
+                                                            stop);
+    else
+      k_p2p2<false><<<grid, P2P2_WARPS * 32, P2P2_SMEM, st>>>(reinterpret_cast<const float4*>(xq.p), pair_a(), pair_b(),
+                                                             leaf_start.as<int>(), depth, (float)size, periodic,
+                                                             vnear.as<float>(), gnear.as<float>(), own_x0, own_x1, ctl,
+                                                             stop);
   }
   // leaves of this rank's slab (all of them without a decomposition); the
   // leaf kernels start their grid at leaf plane own_x0
@@ -1181,91 +1180,6 @@ struct lfmm_plan {
       pend = (own_x1 >> (depth - pl)) << (2 * pl);
     }
   }
-  void tr_l2l(int l, cudaStream_t st) {
-    TrArgs ta{};
-    ta.mode = 1;
-    ta.level = l;
-    ta.ncp = ncp;
-    ta.ops_t = ops_l2l_t.p;
-    ta.src = loc.as<float>() + level_off[l - 1] * ncp;
-    ta.dst = loc.as<float>() + level_off[l] * ncp;
-    ta.partial = static_cast<const char*>(partial.p) + sizeof(float) * (size_t)part_off[l] * ncp;
-    ta.nsplit = nsplit[l];
-    owned_parents(l - 1, ta.p0, ta.pend);
-    launch(ST_L2L, [&] { tr_launch<float>(ta, ta.pend - ta.p0, 8, st); });
-  }
-  void halo_levels(HaloArgs ha, int l0, int l1, int job0, int njobs, cudaStream_t st) {
-    ha.lvl0 = l0;
-    ha.jobs = hm_jobs.as<int4>() + job0;
-    const int nl = l1 - l0 + 1;
-    launch(ST_PACK, [&] {
-      k_level_absmax<<<dim3((unsigned)std::max<int64_t>(1, ((1LL << (3 * l1)) + 63) / 64), nl), 256, 0, st>>>(
-          ha.mult, ha, hm_level_max.as<unsigned int>());
-    });
-    launch(ST_PACK, [&] {
-      k_pack_mult16<<<dim3((unsigned)((8 * hm_plane_rows(l1) + 255) / 256), nl, 8), 256, 0, st>>>(ha);
-    });
-    launch(ST_DOWN, [&] { launch_m2l_halo(ha, njobs, hm_astages, st); });
-  }
-  void far_overlapped() {
-    const int ls = hm_lsplit;
-    if (!far_stream) {
-      int lo = 0, hi = 0;
-      LFMM_CUDA(cudaDeviceGetStreamPriorityRange(&lo, &hi));
-      LFMM_CUDA(cudaStreamCreateWithPriority(&far_stream, cudaStreamNonBlocking, hi));
-      LFMM_CUDA(cudaEventCreateWithFlags(&ev_far_fork, cudaEventDisableTiming));
-      LFMM_CUDA(cudaEventCreateWithFlags(&ev_far_join, cudaEventDisableTiming));
-    }
-    float* M = mult.as<float>();
-    float* Lc = loc.as<float>();
-    for (int l = depth - 1; l >= ls; --l) tr_m2m(l, stream);
-    launch(ST_M2M, [&] {
-      k_box_charges<float><<<nblk(nleaf, 256), 256, 0, stream>>>(qs.as<double>(), leaf_start.as<int>(), depth,
-                                                                 level_off[depth], ncp, M, boxq.as<double>(),
-                                                                 counters.as<int>() + 2, ls);
-    });
-    HaloArgs ha{};
-    ha.mult = M;
-    ha.partial = reinterpret_cast<float*>(partial.p);
-    ha.ops16 = ops16.as<unsigned char>();
-    ha.level_max = hm_level_max.as<unsigned int>();
-    ha.inv_r = hm_inv_r.as<float>();
-    ha.inv_c = hm_inv_c.as<float>();
-    ha.rw_cap = hm_rw_cap;
-    ha.stagger = hm_stagger;
-    ha.mult16 = mult16.as<unsigned char>();
-    for (int l = 0; l <= depth; ++l) {
-      ha.level_off[l] = level_off[l];
-      ha.part_off[l] = part_off[l];
-      ha.m16_off[l] = m16_off[l];
-    }
-    LFMM_CUDA(cudaMemsetAsync(hm_level_max.p, 0, hm_level_max.bytes, stream));
-    LFMM_CUDA(cudaEventRecord(ev_far_fork, stream));
-    // ---- small levels ----
-    LFMM_CUDA(cudaStreamWaitEvent(far_stream, ev_far_fork, 0));
-    for (int l = ls - 1; l >= 0; --l) tr_m2m(l, far_stream);
-    launch(ST_M2M, [&] { k_apply_boxq<float><<<4, 256, 0, far_stream>>>(boxq.as<double>(), ls, ncp, M); });
-    if (lattice_mode != LFMM_LATTICE_OFF) {
-      TrArgs ta{};
-      ta.mode = 2;
-      ta.ncols = 1;
-      ta.ncp = ncp;
-      ta.ops_t = ops_lat_t.p;
-      ta.src = M;
-      ta.dst = Lc;
-      launch(ST_ROOT, [&] { tr_launch<float>(ta, 1, 1, far_stream); });
-    } else {
-      LFMM_CUDA(cudaMemsetAsync(Lc, 0, sizeof(float) * ncp, far_stream));
-    }
-    halo_levels(ha, 1, ls - 1, hm_nbig, hm_njobs - hm_nbig, far_stream);
-    for (int l = 1; l < ls; ++l) tr_l2l(l, far_stream);
-    LFMM_CUDA(cudaEventRecord(ev_far_join, far_stream));
-    // ---- big levels ----
-    halo_levels(ha, ls, depth, 0, hm_nbig, stream);
-    LFMM_CUDA(cudaStreamWaitEvent(stream, ev_far_join, 0));
-    for (int l = ls; l <= depth; ++l) tr_l2l(l, stream);
-  }
-
   template <class T>
   void solve_column(int K, int c, bool grad) {
     const int64_t nb = std::min<int64_t>(nblk(N, 256), 148 * 4);
@@ -1294,18 +1208,6 @@ struct lfmm_plan {
       dim3 grid(tiles_all(l) * ga.up_split, rowb);
       launch(ST_M2M, [&] { k_gemm_gather<T><<<grid, G_THREADS, 0, stream>>>(ga); });
     };
-    bool far_done = false;
-    if (dist_phase == 2) {
-      // levels spanning several ranks, from the gathered level dist_lg
-      for (int l = std::min(dist_lg, depth) - 1; l >= 0; --l) m2m_level(l);
-    } else {
-    launch(ST_STAGE, [&] {
-      k_stage_q<T><<<(unsigned)nb, 256, 0, stream>>>(q_in.as<double>(), K, c, perm.as<int>(), pos_sorted.as<double>(),
-                                                     N, L, xq.as<vec4_t<T>>(), qs.as<double>(), part.as<dd>(),
-                                                     counters.as<int>(), scal.as<double>(), leaf_sorted.as<int>(),
-                                                     depth, own_x0, own_x1, leaf_start.as<int>(),
-                                                     p2p_scalar ? nullptr : pair_b());
-    });
     const int periodic = (flags & LFMM_F_PERIODIC_NEAR) ? 1 : 0;
     const unsigned lb = nblk(own_leaves(), P2P_WARPS);
     const bool side = !profiling;
@@ -1316,24 +1218,17 @@ struct lfmm_plan {
       LFMM_CUDA(cudaEventCreateWithFlags(&ev_near_in, cudaEventDisableTiming));
       LFMM_CUDA(cudaEventCreateWithFlags(&ev_near_out, cudaEventDisableTiming));
     }
+    auto issue_p2p = [&]() {
     cudaStream_t pst = stream;
     if (side) {
       LFMM_CUDA(cudaEventRecord(ev_near_in, stream));
       LFMM_CUDA(cudaStreamWaitEvent(near_stream, ev_near_in, 0));
       pst = near_stream;
     }
-    launch(ST_P2P, [&] {
+    launch_on(ST_P2P, pst, [&] {
       cudaStream_t stream = pst;
       if (sizeof(T) == 4 && !p2p_scalar) {
-        const unsigned lb2 = nblk(own_leaves(), P2P2_WARPS);
-        if (grad)
-          k_p2p2<true><<<lb2, P2P2_WARPS * 32, P2P2_SMEM, stream>>>(reinterpret_cast<const float4*>(xq.p), pair_a(), pair_b(), leaf_start.as<int>(),
-                                                                      depth, (float)size, periodic, vnear.as<float>(),
-                                                                      gnear.as<float>(), own_x0, own_x1);
-        else
-          k_p2p2<false><<<lb2, P2P2_WARPS * 32, P2P2_SMEM, stream>>>(reinterpret_cast<const float4*>(xq.p), pair_a(), pair_b(), leaf_start.as<int>(),
-                                                               depth, (float)size, periodic, vnear.as<float>(),
-                                                               gnear.as<float>(), own_x0, own_x1);
+        p2p2_launch(grad, periodic, 0, nullptr, stream);
         return;
       }
       if (grad)
@@ -1347,6 +1242,34 @@ struct lfmm_plan {
       LFMM_CUDA(cudaEventRecord(ev_near_out, near_stream));
       near_pending = true;
     }
+    };
+    // Preemptible near field (fp32, tensor-core M2L, single rank): launch 1
+    // (p2p_c1 CTAs per SM) runs beside the P2M / M2M / lattice chain and is
+    // stopped before the M2L takes every SM; launch 2 (p2p_c2 per SM) runs
+    // beside the L2L chain and L2P; launch 3 (full occupancy, main stream)
+    // finishes the leaves left.  Each leaf is computed by one warp with the
+    // same arithmetic whichever launch takes it.
+    const bool preempt = side && p2p_preempt && sizeof(T) == 4 && !p2p_scalar && use_halo && dist_phase == 0;
+    int* ctl = p2p_ctl.as<int>();
+    if (dist_phase == 2) {
+      // levels spanning several ranks, from the gathered level dist_lg
+      for (int l = std::min(dist_lg, depth) - 1; l >= 0; --l) m2m_level(l);
+    } else {
+    launch(ST_STAGE, [&] {
+      k_stage_q<T><<<(unsigned)nb, 256, 0, stream>>>(q_in.as<double>(), K, c, perm.as<int>(), pos_sorted.as<double>(),
+                                                     N, L, xq.as<vec4_t<T>>(), qs.as<double>(), part.as<dd>(),
+                                                     counters.as<int>(), scal.as<double>(), leaf_sorted.as<int>(),
+                                                     depth, own_x0, own_x1, leaf_start.as<int>(),
+                                                     p2p_scalar ? nullptr : pair_b());
+    });
+    if (preempt) {
+      LFMM_CUDA(cudaMemsetAsync(ctl, 0, 4 * sizeof(int), stream));
+      LFMM_CUDA(cudaEventRecord(ev_near_in, stream));
+      LFMM_CUDA(cudaStreamWaitEvent(near_stream, ev_near_in, 0));
+      launch_on(ST_P2P, near_stream, [&] { p2p2_launch(grad, periodic, nsm * p2p_c1, ctl + 1, near_stream); });
+    } else {
+      issue_p2p();
+    }
     launch(ST_P2M, [&] {
       if (p == 10) {
         k_p2m_c<T, 10><<<nblk(own_leaves(), EXP_WARPS), EXP_WARPS * 32, 0, stream>>>(
@@ -1358,10 +1281,7 @@ struct lfmm_plan {
           xq.as<vec4_t<T>>(), leaf_start.as<int>(), depth, p, (T)(1.0 / size), ncp, M + level_off[depth] * ncp,
           own_x0);
     });
-    if (sizeof(T) == 4 && far_overlap()) {
-      far_done = true;
-      far_overlapped();
-    } else {
+    {
     for (int l = depth - 1; l >= (dist_phase == 1 ? dist_lg : 0); --l) m2m_level(l);
     launch(ST_M2M, [&] {
       k_box_charges<T><<<nblk(nleaf, 256), 256, 0, stream>>>(qs.as<double>(), leaf_start.as<int>(), depth,
@@ -1393,9 +1313,7 @@ struct lfmm_plan {
       return;
     }
     }  // up
-    if (far_done) {
-      // lattice, M2L and L2L already issued by far_overlapped()
-    } else if (lattice_mode != LFMM_LATTICE_OFF && use_tr) {
+    if (lattice_mode != LFMM_LATTICE_OFF && use_tr) {
       TrArgs ta{};
       ta.mode = 2;
       ta.ncols = 1;
@@ -1412,7 +1330,7 @@ struct lfmm_plan {
     } else {
       LFMM_CUDA(cudaMemsetAsync(Lc, 0, sizeof(T) * ncp, stream));
     }
-    if (depth >= 1 && !far_done) {
+    if (depth >= 1) {
       // M2L of every level in one launch (terms split over CTAs), then the
       // L2L sweep adds the partial slots level by level
       if (use_halo && sizeof(T) == 4) {
@@ -1467,9 +1385,18 @@ struct lfmm_plan {
           }
           k_pack_mult16<<<dim3((unsigned)((8 * prows + 255) / 256), depth, 8), 256, 0, stream>>>(ha);
         });
+        if (preempt) LFMM_CUDA(cudaMemsetAsync(ctl + 1, 1, sizeof(int), stream));  // near field 1 yields the SMs
         launch(ST_DOWN, [&] {
-          launch_m2l_halo(ha, hm_njobs, hm_astages, stream);
+          ha.counter = hm_counter.as<int>();
+          launch_m2l_halo(ha, hm_njobs, nsm, hm_astages, stream);
         });
+        if (preempt) {
+          LFMM_CUDA(cudaEventRecord(ev_m2l_done, stream));
+          LFMM_CUDA(cudaStreamWaitEvent(near_stream, ev_m2l_done, 0));
+          launch_on(ST_P2P, near_stream, [&] { p2p2_launch(grad, periodic, nsm * p2p_c2, ctl + 2, near_stream); });
+          LFMM_CUDA(cudaEventRecord(ev_near_out, near_stream));
+          near_pending = true;
+        }
       } else {
         ga.mode = GEMM_M2L;
         ga.level = 0;
@@ -1541,6 +1468,10 @@ struct lfmm_plan {
       });
     }
     const int dip = (flags & LFMM_F_DIPOLE) ? 1 : 0;
+    if (preempt) {  // the remaining leaves at full occupancy
+      LFMM_CUDA(cudaMemsetAsync(ctl + 2, 1, sizeof(int), stream));
+      launch(ST_P2P, [&] { p2p2_launch(grad, periodic, nsm * 6, ctl + 3, stream); });
+    }
     if (near_pending) {  // near field done
       LFMM_CUDA(cudaStreamWaitEvent(stream, ev_near_out, 0));
       near_pending = false;
@@ -1823,6 +1754,42 @@ extern "C" {
 const char* lfmm_version(void) { return "lfmm-b200 0.1.0 sm_100a"; }
 
 #ifdef LFMM_HM_PROF
+// profiling build only (tools/step_trace.py): trace the launches of the next
+// calls on every stream; lfmm_debug_trace_read returns (stage, start ms, end
+// ms) per launch relative to the first traced launch
+int lfmm_debug_trace(lfmm_plan* plan, int enable) {
+  return guarded([&] {
+    plan->tracing = enable != 0;
+    for (auto& e : plan->trace) {
+      plan->free_events.push_back(e.a);
+      plan->free_events.push_back(e.b);
+    }
+    plan->trace.clear();
+  });
+}
+int64_t lfmm_debug_trace_read(lfmm_plan* plan, double* out, int64_t n) {
+  int64_t k = 0;
+  LFMM_CUDA(cudaDeviceSynchronize());
+  if (plan->trace.empty()) return 0;
+  cudaEvent_t base = plan->trace.front().a;
+  float t0 = 0.f;
+  for (auto& e : plan->trace) {  // earliest start (streams may reorder)
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, base, e.a);
+    t0 = std::min(t0, ms);
+  }
+  for (auto& e : plan->trace) {
+    if (k >= n) break;
+    float a = 0.f, b = 0.f;
+    cudaEventElapsedTime(&a, base, e.a);
+    cudaEventElapsedTime(&b, base, e.b);
+    out[3 * k] = e.stage;
+    out[3 * k + 1] = a - t0;
+    out[3 * k + 2] = b - t0;
+    ++k;
+  }
+  return k;
+}
 // profiling build only: copy the per-CTA M2L timing records (tools/hm_prof.py)
 int lfmm_debug_hm_prof(unsigned long long* out, int64_t n) {
   return guarded([&] {
@@ -1859,6 +1826,7 @@ int lfmm_plan_create(const double* positions, int64_t n, double box_length, int 
       LFMM_REQUIRE(std::isfinite(positions[i]), "positions contain non-finite values");
     int dev = 0;
     LFMM_CUDA(cudaGetDevice(&dev));
+    LFMM_CUDA(cudaDeviceGetAttribute(&pl->nsm, cudaDevAttrMultiProcessorCount, dev));
     std::call_once(g_const_once, init_constants);
     pl->N = n;
     pl->L = box_length;
@@ -1874,7 +1842,8 @@ int lfmm_plan_create(const double* positions, int64_t n, double box_length, int 
       // A/B switches, each exercised by tests/test_gpu_variants.py:
       //   LFMM_M2L=simt    fp32 M2L on the SIMT gather kernel (no tensor cores)
       //   LFMM_P2P=scalar  fp32 P2P on the scalar kernel k_p2p
-      //   LFMM_FAR=serial  far field on one stream (no far_overlapped())
+      //   LFMM_P2P=plain   fp32 near field in one launch on the side stream
+      //                    (not the preemptible three-launch schedule)
       //   LFMM_M2L64=gather fp64 M2L on the SIMT gather kernel (no DMMA)
       auto env_is = [](const char* name, const char* val) {
         const char* e = std::getenv(name);
@@ -1883,7 +1852,7 @@ int lfmm_plan_create(const double* positions, int64_t n, double box_length, int 
       pl->use_halo = pl->fp32 && depth >= 1 && pl->nc > 64 && pl->nc <= 128 && !env_is("LFMM_M2L", "simt");
       if (pl->use_halo) pl->ncp = 128;
       pl->p2p_scalar = env_is("LFMM_P2P", "scalar");
-      pl->far_serial = env_is("LFMM_FAR", "serial");
+      pl->p2p_preempt = !env_is("LFMM_P2P", "plain");
       pl->m2l_f64_simt = env_is("LFMM_M2L64", "gather");
     }
     pl->nleaf = 1 << (3 * depth);

@@ -81,6 +81,8 @@ struct HaloArgs {
   int own_x0, own_x1, own_depth;     // k_level_absmax over one rank's leaf x-slab (own_x1 == 0: whole level)
   int stagger;                       // terms issuer 1 runs behind issuer 0 (A-ring order, see hm_aseq)
   int pk_r0[DMAX + 2], pk_r1[DMAX + 2];  // k_pack_mult16: padded rows [r0, r1) per level (r1 == 0: all)
+  int njobs;                         // jobs of this launch (k_m2l_halo is persistent)
+  int* counter;                      // next job to fetch; zeroed before each launch
 };
 
 // A-ring slot sequence of issuer par's u-th term (u counts its terms over all
@@ -283,6 +285,16 @@ __device__ unsigned long long g_hm_prof[8192][8];
 #define HM_ACC(slot)
 #endif
 
+// Persistent CTAs (one per SM): jobs are fetched from a global counter by
+// the halo-loader warp and handed to the other roles through a JQ-slot ring in
+// shared memory (job descriptor + its term tables, job_full / job_empty
+// mbarriers).  Every role walks the same job sequence; iteration, A-ring and
+// accumulator counters run on across jobs, so the next job's MMAs start while
+// the workers drain and write out the previous one (no per-job pipeline
+// fill / drain tail).
+constexpr int HM_JQ = 2;
+constexpr int HM_JOB_CONSUMERS = 1 + 2 + 8;  // A loader lane, 2 issuer warps, 8 worker warps
+
 template <int AS>
 __global__ void __launch_bounds__(HM_THREADS, 1) k_m2l_halo(HaloArgs g) {
 #ifdef LFMM_HM_PROF
@@ -300,20 +312,16 @@ __global__ void __launch_bounds__(HM_THREADS, 1) k_m2l_halo(HaloArgs g) {
   unsigned char* smem = reinterpret_cast<unsigned char*>(((uintptr_t)hm_smem_raw + 1023) & ~(uintptr_t)1023);
   __shared__ __align__(8) uint64_t halo_full[2], halo_empty[2], acc_full[2], acc_empty[2];
   __shared__ __align__(8) uint64_t a_full[AS], a_empty[AS];
+  __shared__ __align__(8) uint64_t job_full[HM_JQ], job_empty[HM_JQ];
   __shared__ uint32_t tmem_base_sh;
-  // the job's (tc, sc) term lists: B row offset (16-B units) and operator row
-  __shared__ uint32_t s_boff[4][27];
-  __shared__ int s_orow[4][27];
-  __shared__ int s_nt[4];
+  // per job slot: the descriptor and the (tc, sc) term lists (B row offset in
+  // 16-B units, operator row, term count per source class)
+  __shared__ int4 s_job[HM_JQ];
+  __shared__ uint32_t s_boff[HM_JQ][4][27];
+  __shared__ int s_orow[HM_JQ][4][27];
+  __shared__ int s_nt[HM_JQ][4];
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  const int4 job = g.jobs[blockIdx.x];
-  const int level = job.x & 15, tc = (job.x >> 4) & 7, grp = (job.x >> 8) & 15, G = (job.x >> 12) & 15;
-  const int t0 = job.y, N = job.z;
-  const int h = 1 << (level - 1), Z = h + 2, YZ = Z * Z;
-  const int rw = hm_rw(N, Z);
-  const int nsc = 8 / G;  // source classes per job
-  const int niter = nsc * HM_NKC;
   const size_t bufb = hm_buf_bytes(g.rw_cap);
   unsigned char* abase = smem + 2 * bufb;
 
@@ -328,20 +336,11 @@ __global__ void __launch_bounds__(HM_THREADS, 1) k_m2l_halo(HaloArgs g) {
       mbar_init(smem_u32(&a_full[s]), 1);
       mbar_init(smem_u32(&a_empty[s]), 1);
     }
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-  }
-  if (tid >= 64 && tid < 64 + 4 * 27) {
-    const int k = (tid - 64) / 27, t = (tid - 64) % 27;
-    if (k < nsc) {
-      const int sc = tc ^ hm_group_rel(G, grp, k);
-      const int tab = tc * 8 + sc;
-      if (t == 0) s_nt[k] = c_hterm_n[tab];
-      if (t < c_hterm_n[tab]) {
-        const char4 d = c_hterm_d[tab * 27 + t];
-        s_boff[k][t] = (uint32_t)((d.x + 1) * rw + (Z + 1) + d.y * Z + d.z);
-        s_orow[k][t] = c_hterm_row[tab * 27 + t];
-      }
+    for (int s = 0; s < HM_JQ; ++s) {
+      mbar_init(smem_u32(&job_full[s]), 1);
+      mbar_init(smem_u32(&job_empty[s]), HM_JOB_CONSUMERS);
     }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   if (warp == 0) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(smem_u32(&tmem_base_sh)));
@@ -355,95 +354,120 @@ __global__ void __launch_bounds__(HM_THREADS, 1) k_m2l_halo(HaloArgs g) {
   if (warp < 8) {
     // ================================================= workers =========
     const int quad = warp & 3, hcol = warp >> 2;
-    const int ncol = min(128, N - 128 * hcol);  // columns this thread drains (may be <= 0)
-    float sum[128];
+    int it_g = 0;
+    for (int jq = 0;; ++jq) {
+      const int slot = jq % HM_JQ;
+      mbar_wait(smem_u32(&job_full[slot]), (jq / HM_JQ) & 1);
+      const int4 job = s_job[slot];
+      if (job.x == 0) break;
+      const int level = job.x & 15, tc = (job.x >> 4) & 7, grp = (job.x >> 8) & 15, G = (job.x >> 12) & 15;
+      const int t0 = job.y, N = job.z;
+      const int h = 1 << (level - 1), Z = h + 2, YZ = Z * Z;
+      const int niter = (8 / G) * HM_NKC;
+      const int ncol = min(128, N - 128 * hcol);  // columns this thread drains (may be <= 0)
+      float sum[128];
 #pragma unroll
-    for (int j = 0; j < 128; ++j) sum[j] = 0.f;
-    for (int it = 0; it < niter; ++it) {
-      mbar_wait(smem_u32(&acc_full[it & 1]), (it >> 1) & 1);
-      asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-      if (ncol > 0) {
-        const uint32_t tb = tmem + ((uint32_t)(quad * 32) << 16) + (uint32_t)((it & 1) * 256 + hcol * 128);
+      for (int j = 0; j < 128; ++j) sum[j] = 0.f;
+      for (int it = 0; it < niter; ++it, ++it_g) {
+        mbar_wait(smem_u32(&acc_full[it_g & 1]), (it_g >> 1) & 1);
+        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+        if (ncol > 0) {
+          const uint32_t tb = tmem + ((uint32_t)(quad * 32) << 16) + (uint32_t)((it_g & 1) * 256 + hcol * 128);
 #pragma unroll
-        for (int c = 0; c < 16; ++c) {
-          if (c * 8 < ncol) {
-            float v[8];
-            hm_ld8(tb + c * 8, v);
+          for (int c = 0; c < 16; ++c) {
+            if (c * 8 < ncol) {
+              float v[8];
+              hm_ld8(tb + c * 8, v);
 #pragma unroll
-            for (int j = 0; j < 8; ++j) sum[c * 8 + j] += v[j];
+              for (int j = 0; j < 8; ++j) sum[c * 8 + j] += v[j];
+            }
+          }
+        }
+        asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+        mbar_arrive(smem_u32(&acc_empty[it_g & 1]));
+      }
+      // ---- epilogue: partial slot grp of this level (overlaps the next job's MMAs) ----
+      const int coef = quad * 32 + lane;
+      const float scale = g.inv_r[coef] / hm_level_scale(g.level_max, level);
+      float* out = g.partial + ((size_t)g.part_off[level] + (size_t)grp * ((size_t)1 << (3 * level))) * 128;
+      const int tcx = (tc >> 2) & 1, tcy = (tc >> 1) & 1, tcz = tc & 1;
+      const int gi = t0 + hcol * 128;
+      int x = gi / YZ - 1, y = (gi / Z) % Z - 1, z = gi % Z - 1;
+#pragma unroll
+      for (int j = 0; j < 128; ++j) {
+        if (hcol * 128 + j < N && x >= 0 && x < h && y >= 0 && y < h && z >= 0 && z < h) {
+          const int box = ((((2 * x + tcx) << level) | (2 * y + tcy)) << level) | (2 * z + tcz);
+          out[(size_t)box * 128 + coef] = sum[j] * scale;
+        }
+        if (++z == Z - 1) {  // next padded row: z, y in [-1, Z - 1)
+          z = -1;
+          if (++y == Z - 1) {
+            y = -1;
+            ++x;
           }
         }
       }
-      asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
-      mbar_arrive(smem_u32(&acc_empty[it & 1]));
-    }
-    // ---- epilogue: partial slot grp of this level ----
-    const int coef = quad * 32 + lane;
-    const float scale = g.inv_r[coef] / hm_level_scale(g.level_max, level);
-    float* out = g.partial + ((size_t)g.part_off[level] + (size_t)grp * ((size_t)1 << (3 * level))) * 128;
-    const int tcx = (tc >> 2) & 1, tcy = (tc >> 1) & 1, tcz = tc & 1;
-    const int gi = t0 + hcol * 128;
-    int x = gi / YZ - 1, y = (gi / Z) % Z - 1, z = gi % Z - 1;
-#pragma unroll
-    for (int j = 0; j < 128; ++j) {
-      if (hcol * 128 + j < N && x >= 0 && x < h && y >= 0 && y < h && z >= 0 && z < h) {
-        const int box = ((((2 * x + tcx) << level) | (2 * y + tcy)) << level) | (2 * z + tcz);
-        out[(size_t)box * 128 + coef] = sum[j] * scale;
-      }
-      if (++z == Z - 1) {  // next padded row: z, y in [-1, Z - 1)
-        z = -1;
-        if (++y == Z - 1) {
-          y = -1;
-          ++x;
-        }
-      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(smem_u32(&job_empty[slot]));
     }
   } else if (warp == 8 || warp == 9) {
     // ================================================= MMA issuers =====
-    // (whole warp; hm_mma_w / hm_commit_w elect one lane)
-    {
-      const int par = __shfl_sync(0xffffffffu, warp - 8, 0);
+    // (whole warp; hm_mma_w / hm_commit_w elect one lane).  Issuer par runs
+    // the global iterations of its parity, so it always fills accumulator par
+    // and reads halo buffer par (every job has an even iteration count).
+    const int par = __shfl_sync(0xffffffffu, warp - 8, 0);
+    const uint64_t a_desc0 = hm_desc(smem_u32(abase), 128, 256);
+    int it_base = 0, seq_base = 0;
+    for (int jq = 0;; ++jq) {
+      const int slot = jq % HM_JQ;
+      mbar_wait(smem_u32(&job_full[slot]), (jq / HM_JQ) & 1);
+      const int4 job = s_job[slot];
+      if (job.x == 0) break;
+      const int level = job.x & 15, G = (job.x >> 12) & 15, N = job.z;
+      const int Z = (1 << (level - 1)) + 2;
+      const int rw = hm_rw(N, Z);
+      const int nsc = 8 / G, niter = nsc * HM_NKC;
       const uint32_t idesc = hm_idesc(N);
       const uint32_t lbo = 3u * rw * 16u;
-      // descriptors are advanced by adding (bytes >> 4) to the start-address
-      // field (shared addresses < 256 KB: no carry out of its 14 bits)
-      const uint64_t a_desc0 = hm_desc(smem_u32(abase), 128, 256);
       int T = 0;
-      for (int k = 0; k < nsc; ++k) T += (HM_NKC / 2) * s_nt[k];
+      for (int k = 0; k < nsc; ++k) T += (HM_NKC / 2) * s_nt[slot][k];
       // Ring invariant: an issuer's wait on sequence j (stage j % AS, parity
       // (j / AS) & 1) is only sound if fill j - AS of that stage has completed
       // (else the parity test sees the phase two behind and passes early).
       // Fills complete in issue order and an issuer's consumed sequence m
       // orders every fill <= m before it, so the largest jump between an
       // issuer's consecutive sequence numbers must stay <= AS; issuer 1
-      // starts at j = D + 1, so D + 1 < AS (tests/test_m2l_schedule.py
-      // checks it over every term count).  The cap keeps 4 stages spare.
+      // starts a job at j = D + 1 after its previous job's last term (a jump
+      // of D + 2), so D + 2 <= AS (tests/test_m2l_schedule.py checks every
+      // term count, across job boundaries).  The cap keeps 4 stages spare.
       const int D = min(min(g.stagger, AS - 6), T);
-      int u = 0;  // this issuer's terms so far
+      int u = 0;  // this issuer's terms so far in this job
       for (int it0 = 0; it0 < niter; it0 += 2) {
         const int k = it0 / HM_NKC;
-        const int nt = s_nt[k];
-        const int it = it0 + par;
+        const int nt = s_nt[slot][k];
+        const int itg = it_base + it0 + par;
         {
           HM_T0();
-          mbar_wait(smem_u32(&halo_full[it & 1]), (it >> 1) & 1);
+          mbar_wait(smem_u32(&halo_full[par]), (itg >> 1) & 1);
           HM_ACC(2);
         }
         {
           HM_T0();
-          if (it >= 2) mbar_wait(smem_u32(&acc_empty[it & 1]), ((it - 2) >> 1) & 1);
+          if (itg >= 2) mbar_wait(smem_u32(&acc_empty[par]), ((itg - 2) >> 1) & 1);
           HM_ACC(3);
         }
         asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-        const uint64_t b_desc0 = hm_desc(smem_u32(smem + (it & 1) * bufb), lbo, 128);
+        // descriptors are advanced by adding (bytes >> 4) to the start-address
+        // field (shared addresses < 256 KB: no carry out of its 14 bits)
+        const uint64_t b_desc0 = hm_desc(smem_u32(smem + par * bufb), lbo, 128);
         const uint64_t b_lo = (2u * lbo) >> 4;
-        const uint32_t dacc = tmem + (uint32_t)((it & 1) * 256);
-        uint32_t boff = s_boff[k][0];
+        const uint32_t dacc = tmem + (uint32_t)(par * 256);
+        uint32_t boff = s_boff[slot][k][0];
         for (int t = 0; t < nt; ++t) {
-          const int sq = hm_aseq(par, u + t, D, T);
+          const int sq = seq_base + hm_aseq(par, u + t, D, T);
           const int stage = sq % AS;
           const uint64_t dbh = b_desc0 + boff;
-          if (t + 1 < nt) boff = s_boff[k][t + 1];
+          if (t + 1 < nt) boff = s_boff[slot][k][t + 1];
           const uint64_t dah = a_desc0 + (uint64_t)(stage * (HM_ATILE >> 4));
           {
             HM_T0();
@@ -459,71 +483,119 @@ __global__ void __launch_bounds__(HM_THREADS, 1) k_m2l_halo(HaloArgs g) {
           hm_mma_w(dacc, dah + (4096 >> 4), dbh, idesc, 1u);
           hm_commit_w(smem_u32(&a_empty[stage]));
         }
-        hm_commit_w(smem_u32(&acc_full[it & 1]));
-        hm_commit_w(smem_u32(&halo_empty[it & 1]));
+        hm_commit_w(smem_u32(&acc_full[par]));
+        hm_commit_w(smem_u32(&halo_empty[par]));
         u += nt;
       }
-#ifdef LFMM_HM_PROF
-      unsigned long long te;
-      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(te));
-      g_hm_prof[blockIdx.x][6] = te;
-#endif
+      it_base += niter;
+      seq_base += 2 * T;
+      __syncwarp();
+      if (lane == 0) mbar_arrive(smem_u32(&job_empty[slot]));
     }
+#ifdef LFMM_HM_PROF
+    unsigned long long te;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(te));
+    g_hm_prof[blockIdx.x][6] = te;
+#endif
     __syncwarp();
   } else if (warp == 10) {
     // ================================================= A loader ========
     if (lane == 0) {
-      int T = 0;
-      for (int k = 0; k < nsc; ++k) T += (HM_NKC / 2) * s_nt[k];
-      const int D = min(min(g.stagger, AS - 6), T);  // same lag as the issuers (ring invariant above)
-      // one cursor per issuer: (iteration pair it0, term t)
-      int c_it0[2] = {0, 0}, c_t[2] = {0, 0};
       int seq = 0;
-      for (int s = 0; s < T + D; ++s) {
+      for (int jq = 0;; ++jq) {
+        const int slot = jq % HM_JQ;
+        mbar_wait(smem_u32(&job_full[slot]), (jq / HM_JQ) & 1);
+        const int4 job = s_job[slot];
+        if (job.x == 0) break;
+        const int G = (job.x >> 12) & 15, nsc = 8 / G;
+        int T = 0;
+        for (int k = 0; k < nsc; ++k) T += (HM_NKC / 2) * s_nt[slot][k];
+        const int D = min(min(g.stagger, AS - 6), T);  // same lag as the issuers (ring invariant above)
+        // one cursor per issuer: (iteration pair it0, term t)
+        int c_it0[2] = {0, 0}, c_t[2] = {0, 0};
+        for (int s = 0; s < T + D; ++s) {
 #pragma unroll
-        for (int par = 0; par < 2; ++par) {
-          const int u = s - par * D;
-          if (u < 0 || u >= T) continue;
-          const int k = c_it0[par] / HM_NKC;
-          const int row = s_orow[k][c_t[par]];
-          const int kc = (c_it0[par] + par) % HM_NKC;
-          if (++c_t[par] == s_nt[k]) {
-            c_t[par] = 0;
-            c_it0[par] += 2;
+          for (int par = 0; par < 2; ++par) {
+            const int u = s - par * D;
+            if (u < 0 || u >= T) continue;
+            const int k = c_it0[par] / HM_NKC;
+            const int row = s_orow[slot][k][c_t[par]];
+            const int kc = (c_it0[par] + par) % HM_NKC;
+            if (++c_t[par] == s_nt[slot][k]) {
+              c_t[par] = 0;
+              c_it0[par] += 2;
+            }
+            const int stage = seq % AS, use = seq / AS;
+            if (use >= 1) mbar_wait(smem_u32(&a_empty[stage]), (use - 1) & 1);
+            bulk_load(smem_u32(abase + stage * HM_ATILE), g.ops16 + ((size_t)row * HM_NKC + kc) * HM_ATILE,
+                      HM_ATILE, smem_u32(&a_full[stage]));
+            ++seq;
           }
-          const int stage = seq % AS, use = seq / AS;
-          if (use >= 1) mbar_wait(smem_u32(&a_empty[stage]), (use - 1) & 1);
-          bulk_load(smem_u32(abase + stage * HM_ATILE), g.ops16 + ((size_t)row * HM_NKC + kc) * HM_ATILE, HM_ATILE,
-                    smem_u32(&a_full[stage]));
-          ++seq;
         }
+        mbar_arrive(smem_u32(&job_empty[slot]));
       }
     }
     __syncwarp();
   } else {
-    // ================================================= halo loader =====
-    if (lane == 0) {
-      const int prow = hm_plane_rows(level);
-      const unsigned char* base = g.mult16 + g.m16_off[level];
-      const uint32_t bytes = (uint32_t)rw * 16u;
-      for (int it = 0; it < niter; ++it) {
-        const int sc = tc ^ hm_group_rel(G, grp, it / HM_NKC);
-        const int kc = it % HM_NKC;
-        if (it >= 2) mbar_wait(smem_u32(&halo_empty[it & 1]), ((it - 2) >> 1) & 1);
-        unsigned char* buf = smem + (it & 1) * bufb;
-        const uint32_t bar = smem_u32(&halo_full[it & 1]);
-#pragma unroll
-        for (int pk = 0; pk < 4; ++pk) {  // (part, kgroup)
-          const size_t plane = ((size_t)sc * HM_NKC + kc) * 4 + pk;
-#pragma unroll
-          for (int w = 0; w < 3; ++w) {
-            const int r0 = t0 + (w - 1) * YZ - (Z + 1);
-            bulk_load(smem_u32(buf + (size_t)(pk * 3 + w) * bytes), base + (plane * prow + r0) * 16, bytes, bar);
+    // ========================================= job fetch + halo loader =====
+    int it_g = 0;
+    for (int jq = 0;; ++jq) {
+      const int slot = jq % HM_JQ;
+      if (jq >= HM_JQ) mbar_wait(smem_u32(&job_empty[slot]), ((jq / HM_JQ) - 1) & 1);
+      int j = 0;
+      if (lane == 0) j = atomicAdd(g.counter, 1);
+      j = __shfl_sync(0xffffffffu, j, 0);
+      const int4 job = j < g.njobs ? g.jobs[j] : make_int4(0, 0, 0, 0);
+      if (job.x != 0) {
+        const int level = job.x & 15, tc = (job.x >> 4) & 7, grp = (job.x >> 8) & 15, G = (job.x >> 12) & 15;
+        const int Z = (1 << (level - 1)) + 2;
+        const int rw = hm_rw(job.z, Z);
+        for (int e = lane; e < 4 * 27; e += 32) {
+          const int k = e / 27, t = e % 27;
+          if (k < 8 / G) {
+            const int sc = tc ^ hm_group_rel(G, grp, k);
+            const int tab = tc * 8 + sc;
+            if (t == 0) s_nt[slot][k] = c_hterm_n[tab];
+            if (t < c_hterm_n[tab]) {
+              const char4 d = c_hterm_d[tab * 27 + t];
+              s_boff[slot][k][t] = (uint32_t)((d.x + 1) * rw + (Z + 1) + d.y * Z + d.z);
+              s_orow[slot][k][t] = c_hterm_row[tab * 27 + t];
+            }
           }
         }
       }
+      if (lane == 0) s_job[slot] = job;
+      __syncwarp();
+      if (lane == 0) mbar_arrive(smem_u32(&job_full[slot]));  // release: tables and descriptor
+      if (job.x == 0) break;
+      if (lane == 0) {
+        const int level = job.x & 15, tc = (job.x >> 4) & 7, grp = (job.x >> 8) & 15, G = (job.x >> 12) & 15;
+        const int t0 = job.y, N = job.z;
+        const int Z = (1 << (level - 1)) + 2, YZ = Z * Z;
+        const int rw = hm_rw(N, Z);
+        const int niter = (8 / G) * HM_NKC;
+        const int prow = hm_plane_rows(level);
+        const unsigned char* base = g.mult16 + g.m16_off[level];
+        const uint32_t bytes = (uint32_t)rw * 16u;
+        for (int it = 0; it < niter; ++it, ++it_g) {
+          const int sc = tc ^ hm_group_rel(G, grp, it / HM_NKC);
+          const int kc = it % HM_NKC;
+          if (it_g >= 2) mbar_wait(smem_u32(&halo_empty[it_g & 1]), ((it_g - 2) >> 1) & 1);
+          unsigned char* buf = smem + (it_g & 1) * bufb;
+          const uint32_t bar = smem_u32(&halo_full[it_g & 1]);
+#pragma unroll
+          for (int pk = 0; pk < 4; ++pk) {  // (part, kgroup)
+            const size_t plane = ((size_t)sc * HM_NKC + kc) * 4 + pk;
+#pragma unroll
+            for (int w = 0; w < 3; ++w) {
+              const int r0 = t0 + (w - 1) * YZ - (Z + 1);
+              bulk_load(smem_u32(buf + (size_t)(pk * 3 + w) * bytes), base + (plane * prow + r0) * 16, bytes, bar);
+            }
+          }
+        }
+      }
+      __syncwarp();
     }
-    __syncwarp();
   }
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
   __syncthreads();

@@ -119,7 +119,7 @@ __global__ void __launch_bounds__(P2P_WARPS * 32) k_p2p(const vec4_t<T>* __restr
 #define LFMM_P2P2_WARPS 4
 #endif
 #ifndef LFMM_P2P2_MINB
-#define LFMM_P2P2_MINB 1
+#define LFMM_P2P2_MINB 5  // <= 102 registers: 5 CTAs (20 warps) per SM; measured 0.525 vs 0.543 ms at 4 CTAs
 #endif
 #ifndef LFMM_P2P2_SMAX
 #define LFMM_P2P2_SMAX 512
@@ -177,31 +177,17 @@ __device__ __forceinline__ void kahan_fold(uint64_t& v2, uint64_t& c2, uint64_t 
   v2 = t;
 }
 
+// One target leaf b for the calling warp (staging buffers A/B, per-warp
+// tables, mbarrier `bar` whose parity `phase` carries over between leaves).
 template <bool GRAD>
-__global__ void __launch_bounds__(P2P2_WARPS * 32, LFMM_P2P2_MINB) k_p2p2(const float4* __restrict__ xq,
-                                                          const float4* __restrict__ pair_a,
-                                                          const float4* __restrict__ pair_b,
-                                                          const int* __restrict__ leaf_start, int depth,
-                                                          float size, int periodic, float* __restrict__ vout,
-                                                          float* __restrict__ gout, int x0, int x1) {
-  extern __shared__ float4 p2p2_smem[];  // [warp][A | B][SMAX / 2]
-  __shared__ __align__(8) uint64_t s_bar[P2P2_WARPS];
-  __shared__ int2 s_img[P2P2_WARPS][28];  // {first staged pair, pair count}; sentinel at nimg
-  __shared__ float4 s_shift[P2P2_WARPS][27];
-  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-  const int b = (x0 << (2 * depth)) + blockIdx.x * P2P2_WARPS + w;  // grid from the rank's first leaf plane
-  const int nleaf = 1 << (3 * depth);
-  if (b >= nleaf) return;
-  if ((b >> (2 * depth)) < x0 || (b >> (2 * depth)) >= x1) return;  // leaf outside this rank's slab
-  float4* A = p2p2_smem + (size_t)w * P2P2_SMAX;
-  float4* B = A + P2P2_SMAX / 2;
+__device__ __forceinline__ void p2p2_leaf(int b, const float4* __restrict__ xq, const float4* __restrict__ pair_a,
+                                          const float4* __restrict__ pair_b, const int* __restrict__ leaf_start,
+                                          int depth, float size, int periodic, float* __restrict__ vout,
+                                          float* __restrict__ gout, float4* A, float4* B, int2* s_imgw,
+                                          float4* s_shiftw, uint32_t bar, uint32_t& phase) {
+  const int lane = threadIdx.x & 31;
   const int t0 = leaf_start[b], n = leaf_start[b + 1] - t0;
   if (n == 0) return;
-  const uint32_t bar = smem_u32(&s_bar[w]);
-  if (lane == 0) {
-    mbar_init(bar, 1);
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-  }
   // images: lane t < nimg holds image t (home = lane 0): its leaf's first
   // source pair, pair count, shift into the target leaf's frame
   const int nimg = periodic ? 27 : 1;
@@ -230,13 +216,12 @@ __global__ void __launch_bounds__(P2P2_WARPS * 32, LFMM_P2P2_MINB) k_p2p2(const 
   const int i_off = excl - i_np;                        // staged pair offset of my image
   const int tp = __shfl_sync(0xffffffffu, excl, 31);  // total staged pairs
   if (lane < nimg) {
-    s_img[w][lane] = make_int2(i_off, i_np);
-    s_shift[w][lane] = make_float4(i_ox, i_oy, i_oz, 0.f);
+    s_imgw[lane] = make_int2(i_off, i_np);
+    s_shiftw[lane] = make_float4(i_ox, i_oy, i_oz, 0.f);
   }
-  if (lane == nimg) s_img[w][lane] = make_int2(0x7fffffff, 0);
+  if (lane == nimg) s_imgw[lane] = make_int2(0x7fffffff, 0);
   constexpr int CH = P2P2_SMAX / 2;  // pairs per staging chunk
   const int nchunk = (tp + CH - 1) / CH;
-  uint32_t phase = 0;
   __syncwarp();
 
   for (int pb = 0; pb < n; pb += 32) {
@@ -284,8 +269,8 @@ __global__ void __launch_bounds__(P2P2_WARPS * 32, LFMM_P2P2_MINB) k_p2p2(const 
         if (nimg > 1) {
           int im = 0;
           for (int q = max(cb, hp) + lane; q < ce; q += 32) {
-            while (q >= s_img[w][im + 1].x) ++im;
-            const float4 sh = s_shift[w][im];
+            while (q >= s_imgw[im + 1].x) ++im;
+            const float4 sh = s_shiftw[im];
             float4 av = A[q - cb];
             float4 bv = B[q - cb];
             av.x += sh.x;
@@ -378,6 +363,55 @@ __global__ void __launch_bounds__(P2P2_WARPS * 32, LFMM_P2P2_MINB) k_p2p2(const 
         gout[3 * (size_t)i + 2] = -gz;
       }
     }
+  }
+  __syncwarp();  // the staging buffers are reused by the warp's next leaf
+}
+
+// ctl == nullptr: one warp per leaf of the grid.  ctl != nullptr: persistent
+// and preemptible: warps fetch leaves from the counter *ctl (relative to the
+// rank's first leaf) until every leaf is taken or the flag *stop is raised; a fetched leaf is always finished, so a later launch over the
+// same counter picks up exactly the leaves not done yet (the near field then
+// fills the SMs the latency-bound far-field chains leave idle, and yields them
+// to the tensor-core M2L, lfmm_api.cu issue_p2p).
+template <bool GRAD>
+__global__ void __launch_bounds__(P2P2_WARPS * 32, LFMM_P2P2_MINB) k_p2p2(const float4* __restrict__ xq,
+                                                          const float4* __restrict__ pair_a,
+                                                          const float4* __restrict__ pair_b,
+                                                          const int* __restrict__ leaf_start, int depth,
+                                                          float size, int periodic, float* __restrict__ vout,
+                                                          float* __restrict__ gout, int x0, int x1,
+                                                          int* __restrict__ ctl, const int* __restrict__ stop) {
+  extern __shared__ float4 p2p2_smem[];  // [warp][A | B][SMAX / 2]
+  __shared__ __align__(8) uint64_t s_bar[P2P2_WARPS];
+  __shared__ int2 s_img[P2P2_WARPS][28];  // {first staged pair, pair count}; sentinel at nimg
+  __shared__ float4 s_shift[P2P2_WARPS][27];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int nleaf = 1 << (3 * depth);
+  const int first = x0 << (2 * depth);  // the rank's first leaf plane
+  const int own = (min(x1, 1 << depth) - x0) << (2 * depth);
+  float4* A = p2p2_smem + (size_t)w * P2P2_SMAX;
+  float4* B = A + P2P2_SMAX / 2;
+  const uint32_t bar = smem_u32(&s_bar[w]);
+  if (lane == 0) {
+    mbar_init(bar, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncwarp();
+  uint32_t phase = 0;
+  if (ctl == nullptr) {
+    const int b = first + blockIdx.x * P2P2_WARPS + w;
+    if (b >= nleaf || (b >> (2 * depth)) >= x1) return;
+    p2p2_leaf<GRAD>(b, xq, pair_a, pair_b, leaf_start, depth, size, periodic, vout, gout, A, B, s_img[w],
+                    s_shift[w], bar, phase);
+    return;
+  }
+  for (;;) {
+    int v = 0;
+    if (lane == 0) v = *reinterpret_cast<const volatile int*>(stop) ? own : atomicAdd(ctl, 1);
+    v = __shfl_sync(0xffffffffu, v, 0);
+    if (v >= own) break;
+    p2p2_leaf<GRAD>(first + v, xq, pair_a, pair_b, leaf_start, depth, size, periodic, vout, gout, A, B, s_img[w],
+                    s_shift[w], bar, phase);
   }
 }
 

@@ -30,7 +30,7 @@ def c1():
 
 
 @pytest.mark.parametrize("env,precision", [("LFMM_M2L=simt", "single"), ("LFMM_P2P=scalar", "single"),
-                                           ("LFMM_FAR=serial", "single"), ("LFMM_M2L64=gather", "double")])
+                                           ("LFMM_P2P=plain", "single"), ("LFMM_M2L64=gather", "double")])
 def test_switch_matches_oracle(env, precision, monkeypatch):
     d = c1()
     name, val = env.split("=")
@@ -45,18 +45,40 @@ def test_switch_matches_oracle(env, precision, monkeypatch):
     assert relerr(r.spatial_forces, d["fq"]) <= tol
 
 
-def test_far_serial_matches_overlapped(monkeypatch):
-    """far_overlapped() runs the small levels on a second stream; the only
-    arithmetic difference is that their M2M reads level ls with the exact
-    box charges already applied (serial: applied after every M2M), an fp32
-    rounding-level change (depth 5 so the split is active).  Each order is
-    bit-reproducible on its own (test_gpu_solve reruns)."""
+def test_preemptible_near_field_is_bit_identical(monkeypatch):
+    """The default fp32 near field runs as three persistent launches that
+    share one leaf counter (lfmm_api.cu solve_column: beside the far-field
+    chains, yielding to the M2L); every leaf is computed by one warp with the
+    same arithmetic whichever launch takes it, so potentials and forces equal
+    the single-launch schedule (LFMM_P2P=plain) bit for bit (depth 5: the
+    schedule is active)."""
+    import torch
+
+    from paper_2410_01754_b200 import _native
+    from paper_2410_01754_b200.system import lambda_table, site_tables
+
     system, lam, _ = generate_water_box(200_000, 16, seed=3)
     cfg = SolverConfig(p=10, depth=5, precision="single")
-    a = PeriodicSolver(system.positions, system.box_length, cfg).solve(system.charges)
-    monkeypatch.setenv("LFMM_FAR", "serial")
-    b = PeriodicSolver(system.positions, system.box_length, cfg).solve(system.charges)
-    assert relerr(b.potentials, a.potentials) <= 2e-6
+    outs = []
+    for plain in (False, True):
+        if plain:
+            monkeypatch.setenv("LFMM_P2P", "plain")
+        solver = PeriodicSolver(system.positions, system.box_length, cfg)
+        plan = solver.plan
+        plan.set_sites(*site_tables(system))
+        lt, nl = lambda_table(system, lam.values)
+        dev = torch.device("cuda", 0)
+        d = lambda a: torch.from_numpy(np.ascontiguousarray(a)).to(dev)  # noqa: E731
+        e = torch.empty(1, dtype=torch.float64, device=dev)
+        f = torch.empty((system.num_particles, 3), dtype=torch.float64, device=dev)
+        lf = torch.empty((len(system.sites), 4), dtype=torch.float64, device=dev)
+        for _ in range(2):
+            plan.step(d(system.positions), d(system.charges), d(lt), d(nl), mode=_native.MODE_HI, on_device=True,
+                      energy=e, forces=f, lambda_forces=lf)
+        torch.cuda.synchronize()
+        outs.append((e.cpu().numpy(), f.cpu().numpy(), lf.cpu().numpy()))
+    for a, b in zip(*outs):
+        assert a.tobytes() == b.tobytes()
 
 
 def test_non_finite_result_raises_numerical_failure():

@@ -32,25 +32,32 @@ __global__ void rsqrt_k(float* out, float a) {
   out[blockIdx.x*blockDim.x+threadIdx.x]=x0+x1+x2+x3;
 }
 __global__ void mma_tf32_k(float* out) {
+  // four independent chains with distinct operands and initial values, so
+  // ptxas cannot merge them (cuobjdump -sass: 4 HMMA per inner iteration)
   unsigned a0=threadIdx.x,a1=a0+1,a2=a0+2,a3=a0+3,b0=a0*3,b1=a0*5;
-  float c[4][4]={};
+  float c[4][4];
+  for(int j=0;j<4;j++) for(int r=0;r<4;r++) c[j][r]=j+0.25f*r;
   for (int i=0;i<ITERS/4;i++){
 #pragma unroll
     for(int j=0;j<4;j++)
     asm volatile("mma.sync.aligned.m16n8k8.row.col.f32.tf32.tf32.f32 {%0,%1,%2,%3},{%4,%5,%6,%7},{%8,%9},{%0,%1,%2,%3};\n"
-      : "+f"(c[j][0]),"+f"(c[j][1]),"+f"(c[j][2]),"+f"(c[j][3]) : "r"(a0),"r"(a1),"r"(a2),"r"(a3),"r"(b0),"r"(b1));
+      : "+f"(c[j][0]),"+f"(c[j][1]),"+f"(c[j][2]),"+f"(c[j][3]) : "r"(a0+j),"r"(a1),"r"(a2),"r"(a3),"r"(b0),"r"(b1+j));
   }
   float s=0; for(int j=0;j<4;j++) s+=c[j][0]+c[j][1]+c[j][2]+c[j][3];
   out[blockIdx.x*blockDim.x+threadIdx.x]=s;
 }
 __global__ void dmma_k(double* out) {
+  // four independent chains with distinct operands and initial values (the
+  // round-1 version fed four identical chains and ptxas merged them into one,
+  // overstating the rate 4x)
   double a=threadIdx.x, b=a*0.5;
-  double c[4][2]={};
+  double c[4][2];
+  for(int j=0;j<4;j++){ c[j][0]=j; c[j][1]=-j; }
   for (int i=0;i<ITERS/16;i++){
 #pragma unroll
     for(int j=0;j<4;j++)
     asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1},{%2},{%3},{%0,%1};\n"
-      : "+d"(c[j][0]),"+d"(c[j][1]) : "d"(a),"d"(b));
+      : "+d"(c[j][0]),"+d"(c[j][1]) : "d"(a+j),"d"(b-j));
   }
   out[blockIdx.x*blockDim.x+threadIdx.x]=c[0][0]+c[1][1]+c[2][0]+c[3][1];
 }
