@@ -525,6 +525,34 @@ def run_ours(args):
                     "frac": round(p2p_tf / fp32_pipe, 4),
                     "algorithmic": "20 flop per ordered pair (potential + gradient), exact pair count"}
 
+    # the precision-matched (fp64, the reference's complex128 arithmetic) step
+    # on the same system and call, with its own clock record
+    fp64 = None
+    if args.precision == "single":
+        s64 = PeriodicSolver(system.positions, system.box_length,
+                             SolverConfig(p=args.p, depth=args.depth, precision="double"))
+        p64 = s64.plan
+        p64.set_sites(*tables)
+        p64.set_stream(stream.cuda_stream)
+
+        def step64():
+            p64.step(d_pos, d_q, d_lam, d_nl, mode=_native.MODE_HI, plain=False, on_device=True, energy=d_e,
+                     forces=d_f, lambda_forces=d_lf)
+
+        for _ in range(max(3, args.warmup)):
+            step64()
+        torch.cuda.synchronize()
+        barrier()
+        clk64 = ClockSampler(local).__enter__()
+        t64 = timed(step64, args.steps)
+        clk64.__exit__(None, None, None)
+        ms64 = max_over_ranks(sum(t64) / len(t64))
+        fp64 = {"value": round(world * 1000.0 / ms64, 3), "unit": "steps/s", "ms_per_step": round(ms64, 4),
+                "dtype": "f64", "clocks": clk64.summary(),
+                "what": "the same full step (tree rebuild + scale + solve + forces + HI + lambda forces) on fp64 "
+                        "kernels (M2L on DMMA), device-resident inputs, L2 flushed between steps"}
+        del s64, p64
+
     cpu = None
     if rank == 0 and not args.no_cpu_baseline and world == 1:
         cpu = cpu_sample(system, lam_state, args)
@@ -552,6 +580,7 @@ def run_ours(args):
         "stages": stage_rows,
         "p2p_pairs": pairs,
         "cpu_baseline": cpu,
+        "fp64_step": fp64,
     }
     if rank == 0:
         print(json.dumps(line), flush=True)

@@ -588,6 +588,7 @@ struct lfmm_plan {
   cudaEvent_t ev_m2l_done = nullptr;
   int p2p_c1 = 3, p2p_c2 = 3;  // CTAs per SM of near-field launches 1 and 2 (room for the far-field chains)
   bool p2p_preempt = true;
+  bool near_after_hi = false;  // lfmm_step without a tree rebuild (set per call)
   int nsm = 148;
   int64_t m16_off[DMAX + 2] = {0};
   int hm_njobs = 0, hm_rw_cap = 0, hm_astages = HM_ASTAGES;
@@ -1266,6 +1267,10 @@ struct lfmm_plan {
       LFMM_CUDA(cudaMemsetAsync(ctl, 0, 4 * sizeof(int), stream));
       LFMM_CUDA(cudaEventRecord(ev_near_in, stream));
       LFMM_CUDA(cudaStreamWaitEvent(near_stream, ev_near_in, 0));
+      // HI side work issued together with the solve (no tree build to hide
+      // behind): let it finish before the near field holds the SMs, or its
+      // large-smem kernels wait behind the M2L
+      if (near_after_hi) LFMM_CUDA(cudaStreamWaitEvent(near_stream, ev_hi_out, 0));
       launch_on(ST_P2P, near_stream, [&] { p2p2_launch(grad, periodic, nsm * p2p_c1, ctl + 1, near_stream); });
     } else {
       issue_p2p();
@@ -2383,7 +2388,9 @@ int lfmm_step(lfmm_plan* plan, const double* positions, const double* charges, c
     }
     if (early) tree();
     plan->step_mode = potentials == nullptr;
+    plan->near_after_hi = hi_side && !early;
     plan->run_solve(1, true);
+    plan->near_after_hi = false;
     const bool step_mode = plan->step_mode;
     plan->step_mode = false;
     // HI spatial forces: -grad Delta E_site on the site atoms (k_hi_site,

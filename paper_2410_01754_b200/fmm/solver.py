@@ -46,16 +46,24 @@ class SolverConfig:
         return self
 
     def flags(self):
-        f = 0
-        if self.dipole:
-            f |= _native.F_DIPOLE
-        if self.periodic_near:
-            f |= _native.F_PERIODIC_NEAR
-        if self.precision == "single":
-            f |= _native.F_FP32
-        if self.intra_site_images == "minimum":
-            f |= _native.F_INTRA_MINIMUM
-        return f
+        return config_flags(self)
+
+
+def config_flags(cfg):
+    """C-ABI flag bits of a solver configuration.  Duck-typed: the
+    reference's own SolverConfig objects (solver.py:36-75) are accepted as
+    they are, so callers that build configs from lambdafmm (its bench, CLI
+    and tests) work unchanged."""
+    f = 0
+    if cfg.dipole:
+        f |= _native.F_DIPOLE
+    if cfg.periodic_near:
+        f |= _native.F_PERIODIC_NEAR
+    if cfg.precision == "single":
+        f |= _native.F_FP32
+    if cfg.intra_site_images == "minimum":
+        f |= _native.F_INTRA_MINIMUM
+    return f
 
 
 @dataclass
@@ -82,7 +90,7 @@ class PeriodicSolver:
         cfg = self.config
         pos = np.atleast_2d(np.asarray(positions, dtype=np.float64))
         self._plan = _native.Plan(pos, self.box_length, cfg.p, cfg.depth, _native.LFMM_LATTICE[cfg.lattice_mode],
-                                  cfg.shell_cap, cfg.flags())
+                                  cfg.shell_cap, config_flags(cfg))
         self._n = pos.shape[0]
         self._positions = pos
         self._plan64 = None  # fp64 plan of spatial_forces under precision="single"
@@ -163,7 +171,7 @@ class PeriodicSolver:
                 cfg = self.config
                 self._plan64 = _native.Plan(self._positions, self.box_length, cfg.p, cfg.depth,
                                             _native.LFMM_LATTICE[cfg.lattice_mode], cfg.shell_cap,
-                                            cfg.flags() & ~_native.F_FP32)
+                                            config_flags(cfg) & ~_native.F_FP32)
             q2, _ = self._charges(np.asarray(charges, dtype=np.float64).reshape(-1))
             return self._plan64.solve(q2, forces=True)["forces"]
         _, f = self.solve_with_forces(charges)
