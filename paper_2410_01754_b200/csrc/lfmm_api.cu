@@ -14,6 +14,7 @@
 #include <cstring>
 #include <map>
 #include <memory>
+#include <atomic>
 #include <mutex>
 #include <string>
 #include <tuple>
@@ -373,6 +374,10 @@ __global__ void k_i32_to_i64(const int* __restrict__ in, int64_t n, int64_t* __r
 }
 
 // ------------------------------------------------------ host helpers ----
+// bumped by every device (re)allocation: a captured step graph holds raw
+// buffer addresses and is re-captured when this moves
+std::atomic<uint64_t> g_alloc_gen{0};
+
 struct DevBuf {
   void* p = nullptr;
   size_t bytes = 0;
@@ -392,9 +397,13 @@ struct DevBuf {
     if (b == 0) return;
     LFMM_CUDA(cudaMalloc(&p, b));
     bytes = b;
+    g_alloc_gen.fetch_add(1);
   }
   void release() {
-    if (p) cudaFree(p);
+    if (p) {
+      cudaFree(p);
+      g_alloc_gen.fetch_add(1);
+    }
     p = nullptr;
     bytes = 0;
   }
@@ -588,6 +597,19 @@ struct lfmm_plan {
   cudaEvent_t ev_m2l_done = nullptr;
   int p2p_c1 = 3, p2p_c2 = 3;  // CTAs per SM of near-field launches 1 and 2 (room for the far-field chains)
   bool p2p_preempt = true;
+  // lfmm_step with device-resident inputs as one CUDA graph: captured on the
+  // second call with the same arguments, replayed while the arguments, the
+  // stream and every device allocation stay the same (LFMM_GRAPH=0: off)
+  bool graphs = true;
+  struct StepGraph {
+    std::array<const void*, 10> ptrs{};
+    int mode = -1, plain = -1;
+    cudaStream_t stream = nullptr;
+    uint64_t gen = 0;
+    bool warm = false;
+    cudaGraphExec_t exec = nullptr;
+    int64_t nlaunch = 0;
+  } step_graph;
   bool near_after_hi = false;  // lfmm_step without a tree rebuild (set per call)
   int nsm = 148;
   int64_t m16_off[DMAX + 2] = {0};
@@ -707,6 +729,7 @@ struct lfmm_plan {
     if (ev_near_out) cudaEventDestroy(ev_near_out);
     if (ev_q) cudaEventDestroy(ev_q);
     if (ev_m2l_done) cudaEventDestroy(ev_m2l_done);
+    if (step_graph.exec) cudaGraphExecDestroy(step_graph.exec);
     if (ev_f) cudaEventDestroy(ev_f);
   }
 
@@ -1125,16 +1148,7 @@ struct lfmm_plan {
                                                        slot_of.as<int>());
       });
     }
-    {
-      const int nb = (nleaf + 1023) / 1024;
-      int* bt = cursor.as<int>() + nleaf;  // scratch after the cursors
-      launch(ST_TREE, [&] {
-        k_scan_blocks<<<nb, 1024, 0, stream>>>(counts.as<int>(), nleaf, leaf_start.as<int>(), bt);
-      });
-      launch(ST_TREE, [&] { k_scan_totals<<<1, 1024, 0, stream>>>(bt, nb, leaf_start.as<int>(), nleaf); });
-      if (nb > 1)
-        launch(ST_TREE, [&] { k_scan_add<<<nb, 1024, 0, stream>>>(leaf_start.as<int>(), nleaf, bt); });
-    }
+    launch(ST_TREE, [&] { k_scan_single<<<1, 1024, 0, stream>>>(counts.as<int>(), nleaf, leaf_start.as<int>()); });
     if (N > 0) {
       launch(ST_TREE, [&] {
         k_scatter_leaf<<<nblk(N, 256), 256, 0, stream>>>(leaf_of.as<int>(), N, leaf_start.as<int>(),
@@ -1858,6 +1872,7 @@ int lfmm_plan_create(const double* positions, int64_t n, double box_length, int 
       if (pl->use_halo) pl->ncp = 128;
       pl->p2p_scalar = env_is("LFMM_P2P", "scalar");
       pl->p2p_preempt = !env_is("LFMM_P2P", "plain");
+      pl->graphs = !env_is("LFMM_GRAPH", "0");
       pl->m2l_f64_simt = env_is("LFMM_M2L64", "gather");
     }
     pl->nleaf = 1 << (3 * depth);
@@ -2310,11 +2325,13 @@ int lfmm_scale_charges(lfmm_plan* plan, const double* charges, const double* lam
   });
 }
 
-int lfmm_step(lfmm_plan* plan, const double* positions, const double* charges, const double* lambdas,
-              const int32_t* n_lambda, int mode, int plain, int io_on_device, double* energy, double* forces,
-              double* lambda_forces, double* potentials) {
-  if (!plan) return fail(Error{LFMM_EINVAL, "plan is NULL"});
-  return guarded([&] {
+}  // extern "C"
+
+namespace {
+void step_body(lfmm_plan* plan, const double* positions, const double* charges, const double* lambdas,
+               const int32_t* n_lambda, int mode, int plain, int io_on_device, double* energy, double* forces,
+               double* lambda_forces, double* potentials) {
+  {
     const int64_t N = plan->N;
     LFMM_REQUIRE(mode == LFMM_MODE_HI || mode == LFMM_MODE_QI, "unknown mode");
     // device-resident inputs: charges, scale_charges and the HI side work are
@@ -2464,6 +2481,90 @@ int lfmm_step(lfmm_plan* plan, const double* positions, const double* charges, c
       require_finite(energy, 1, "the step energy");
       if (!plain) require_finite(lambda_forces, 4 * plan->n_sites, "the lambda forces");
     }
+  }
+}
+
+// Device-resident step through the plan's step graph (see lfmm_plan::graphs).
+// Returns false when the call has to run uncaptured.
+bool step_graph_launch(lfmm_plan* plan, const double* positions, const double* charges, const double* lambdas,
+                       const int32_t* n_lambda, int mode, int plain, double* energy, double* forces,
+                       double* lambda_forces, double* potentials) {
+  auto& g = plan->step_graph;
+  const std::array<const void*, 10> ptrs{positions, charges, lambdas, n_lambda, energy, forces, lambda_forces,
+                                         potentials, nullptr, nullptr};
+  const bool same = g.ptrs == ptrs && g.mode == mode && g.plain == plain && g.stream == plan->stream;
+  if (g.exec && same && g.gen == g_alloc_gen.load()) {
+    LFMM_CUDA(cudaGraphLaunch(g.exec, plan->stream));
+    plan->launches += g.nlaunch;
+    return true;
+  }
+  if (g.exec) {
+    LFMM_CUDA(cudaGraphExecDestroy(g.exec));
+    g.exec = nullptr;
+  }
+  if (!same || !g.warm) {  // first call with these arguments: run it (allocates), capture on the next
+    g.ptrs = ptrs;
+    g.mode = mode;
+    g.plain = plain;
+    g.stream = plan->stream;
+    g.warm = true;
+    return false;
+  }
+  const uint64_t gen0 = g_alloc_gen.load();
+  const int64_t l0 = plan->launches;
+  LFMM_CUDA(cudaStreamBeginCapture(plan->stream, cudaStreamCaptureModeThreadLocal));
+  cudaGraph_t graph = nullptr;
+  try {
+    step_body(plan, positions, charges, lambdas, n_lambda, mode, plain, 1, energy, forces, lambda_forces,
+              potentials);
+  } catch (...) {
+    cudaStreamEndCapture(plan->stream, &graph);
+    if (graph) cudaGraphDestroy(graph);
+    cudaGetLastError();
+    plan->launches = l0;
+    plan->graphs = false;  // something in the step cannot be captured: stay uncaptured
+    return false;
+  }
+  const cudaError_t ec = cudaStreamEndCapture(plan->stream, &graph);
+  if (ec != cudaSuccess || !graph || g_alloc_gen.load() != gen0) {
+    if (graph) cudaGraphDestroy(graph);
+    cudaGetLastError();
+    plan->launches = l0;
+    plan->graphs = false;
+    return false;
+  }
+  const cudaError_t ei = cudaGraphInstantiate(&g.exec, graph, 0);
+  cudaGraphDestroy(graph);
+  if (ei != cudaSuccess) {
+    cudaGetLastError();
+    g.exec = nullptr;
+    plan->launches = l0;
+    plan->graphs = false;
+    return false;
+  }
+  g.nlaunch = plan->launches - l0;
+  g.gen = gen0;
+  plan->launches = l0;
+  LFMM_CUDA(cudaGraphLaunch(g.exec, plan->stream));
+  plan->launches += g.nlaunch;
+  return true;
+}
+}  // namespace
+
+extern "C" {
+
+int lfmm_step(lfmm_plan* plan, const double* positions, const double* charges, const double* lambdas,
+              const int32_t* n_lambda, int mode, int plain, int io_on_device, double* energy, double* forces,
+              double* lambda_forces, double* potentials) {
+  if (!plan) return fail(Error{LFMM_EINVAL, "plan is NULL"});
+  return guarded([&] {
+    LFMM_REQUIRE(mode == LFMM_MODE_HI || mode == LFMM_MODE_QI, "unknown mode");
+    if (io_on_device && plan->graphs && !plan->profiling && !plan->tracing &&
+        step_graph_launch(plan, positions, charges, lambdas, n_lambda, mode, plain, energy, forces,
+                          lambda_forces, potentials))
+      return;
+    step_body(plan, positions, charges, lambdas, n_lambda, mode, plain, io_on_device, energy, forces,
+              lambda_forces, potentials);
   });
 }
 

@@ -49,9 +49,7 @@ __global__ void k_wrap_cell(const double* __restrict__ pos_in, int64_t n, double
   slot_of[i] = atomicAdd(&counts[leaf], 1);
 }
 
-// Exclusive scan of counts[0..n) into start[0..n] in three passes:
-// per-1024 block scans (warp shuffles), a scan of the block totals, and the
-// block-offset add.
+// Exclusive scan of one block's values (warp shuffles, then the warp totals).
 __device__ __forceinline__ int block_scan_excl(int v, int* warp_tot, int& total) {
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = blockDim.x >> 5;
   int x = v;
@@ -77,36 +75,54 @@ __device__ __forceinline__ int block_scan_excl(int v, int* warp_tot, int& total)
   return base + x - v;
 }
 
-__global__ void k_scan_blocks(const int* __restrict__ counts, int n, int* __restrict__ start,
-                              int* __restrict__ block_tot) {
+// One block (1024 threads) scans all n leaf counts in tiles of 8 x 1024:
+// each thread loads 8 consecutive counts (two int4, coalesced across the
+// warp), the block scans the per-thread sums, and a running carry links the
+// tiles (one launch instead of block scans + total scan + add; n = 32,768 at
+// depth 5: 4 tiles, 262,144 at depth 6: 32 tiles).  n is a multiple of 8.
+__global__ void __launch_bounds__(1024) k_scan_single(const int* __restrict__ counts, int n,
+                                                      int* __restrict__ start) {
   __shared__ int wt[32];
-  const int i = blockIdx.x * blockDim.x + threadIdx.x;
-  const int v = i < n ? counts[i] : 0;
-  int total;
-  const int ex = block_scan_excl(v, wt, total);
-  if (i < n) start[i] = ex;
-  if (threadIdx.x == 0) block_tot[blockIdx.x] = total;
-}
-
-__global__ void k_scan_totals(int* __restrict__ block_tot, int nb, int* __restrict__ start, int n) {
-  __shared__ int wt[32];
-  int run = 0;
-  for (int b0 = 0; b0 < nb; b0 += blockDim.x) {
-    const int b = b0 + threadIdx.x;
-    const int v = b < nb ? block_tot[b] : 0;
-    int total;
-    const int ex = block_scan_excl(v, wt, total);
-    __syncthreads();
-    if (b < nb) block_tot[b] = run + ex;
-    run += total;
-    __syncthreads();
+  if (n & 7) {  // depth 0: one leaf
+    if (threadIdx.x == 0) {
+      int run = 0;
+      for (int i = 0; i < n; ++i) {
+        start[i] = run;
+        run += counts[i];
+      }
+      start[n] = run;
+    }
+    return;
   }
-  if (threadIdx.x == 0) start[n] = run;
-}
-
-__global__ void k_scan_add(int* __restrict__ start, int n, const int* __restrict__ block_tot) {
-  const int i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i < n) start[i] += block_tot[blockIdx.x];
+  const int tile = blockDim.x * 8;
+  int carry = 0;
+  for (int base = 0; base < n; base += tile) {
+    const int i0 = base + 8 * threadIdx.x;
+    int4 a = make_int4(0, 0, 0, 0), b = make_int4(0, 0, 0, 0);
+    if (i0 < n) {
+      a = reinterpret_cast<const int4*>(counts + i0)[0];
+      b = reinterpret_cast<const int4*>(counts + i0)[1];
+    }
+    const int sum = a.x + a.y + a.z + a.w + b.x + b.y + b.z + b.w;
+    int total;
+    int ex = carry + block_scan_excl(sum, wt, total);
+    if (i0 < n) {
+      int4 oa, ob;
+      oa.x = ex;
+      oa.y = oa.x + a.x;
+      oa.z = oa.y + a.y;
+      oa.w = oa.z + a.z;
+      ob.x = oa.w + a.w;
+      ob.y = ob.x + b.x;
+      ob.z = ob.y + b.y;
+      ob.w = ob.z + b.z;
+      reinterpret_cast<int4*>(start + i0)[0] = oa;
+      reinterpret_cast<int4*>(start + i0)[1] = ob;
+    }
+    carry += total;
+    __syncthreads();  // wt is reused by the next tile's scan
+  }
+  if (threadIdx.x == 0) start[n] = carry;
 }
 
 __global__ void k_scatter_leaf(const int* __restrict__ leaf_of, int64_t n, const int* __restrict__ start,

@@ -30,7 +30,8 @@ def c1():
 
 
 @pytest.mark.parametrize("env,precision", [("LFMM_M2L=simt", "single"), ("LFMM_P2P=scalar", "single"),
-                                           ("LFMM_P2P=plain", "single"), ("LFMM_M2L64=gather", "double")])
+                                           ("LFMM_P2P=plain", "single"), ("LFMM_M2L64=gather", "double"),
+                                           ("LFMM_GRAPH=0", "single")])
 def test_switch_matches_oracle(env, precision, monkeypatch):
     d = c1()
     name, val = env.split("=")
@@ -45,13 +46,14 @@ def test_switch_matches_oracle(env, precision, monkeypatch):
     assert relerr(r.spatial_forces, d["fq"]) <= tol
 
 
-def test_preemptible_near_field_is_bit_identical(monkeypatch):
+def test_preemptible_near_field_and_step_graph_are_bit_identical(monkeypatch):
     """The default fp32 near field runs as three persistent launches that
     share one leaf counter (lfmm_api.cu solve_column: beside the far-field
     chains, yielding to the M2L); every leaf is computed by one warp with the
     same arithmetic whichever launch takes it, so potentials and forces equal
     the single-launch schedule (LFMM_P2P=plain) bit for bit (depth 5: the
-    schedule is active)."""
+    schedule is active); the step replayed from its CUDA graph equals the
+    uncaptured step (LFMM_GRAPH=0) bit for bit."""
     import torch
 
     from paper_2410_01754_b200 import _native
@@ -60,9 +62,12 @@ def test_preemptible_near_field_is_bit_identical(monkeypatch):
     system, lam, _ = generate_water_box(200_000, 16, seed=3)
     cfg = SolverConfig(p=10, depth=5, precision="single")
     outs = []
-    for plain in (False, True):
-        if plain:
+    for plain in (False, True, "nograph"):
+        if plain is True:
             monkeypatch.setenv("LFMM_P2P", "plain")
+        if plain == "nograph":
+            monkeypatch.delenv("LFMM_P2P")
+            monkeypatch.setenv("LFMM_GRAPH", "0")
         solver = PeriodicSolver(system.positions, system.box_length, cfg)
         plan = solver.plan
         plan.set_sites(*site_tables(system))
@@ -72,13 +77,14 @@ def test_preemptible_near_field_is_bit_identical(monkeypatch):
         e = torch.empty(1, dtype=torch.float64, device=dev)
         f = torch.empty((system.num_particles, 3), dtype=torch.float64, device=dev)
         lf = torch.empty((len(system.sites), 4), dtype=torch.float64, device=dev)
-        for _ in range(2):
-            plan.step(d(system.positions), d(system.charges), d(lt), d(nl), mode=_native.MODE_HI, on_device=True,
-                      energy=e, forces=f, lambda_forces=lf)
+        args = (d(system.positions), d(system.charges), d(lt), d(nl))
+        for _ in range(3):  # warm-up, capture + replay, replay (the step graph, unless LFMM_GRAPH=0)
+            plan.step(*args, mode=_native.MODE_HI, on_device=True, energy=e, forces=f, lambda_forces=lf)
         torch.cuda.synchronize()
         outs.append((e.cpu().numpy(), f.cpu().numpy(), lf.cpu().numpy()))
-    for a, b in zip(*outs):
-        assert a.tobytes() == b.tobytes()
+    for other in outs[1:]:
+        for a, b in zip(outs[0], other):
+            assert a.tobytes() == b.tobytes()
 
 
 def test_non_finite_result_raises_numerical_failure():
