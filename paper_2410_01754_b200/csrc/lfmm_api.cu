@@ -502,7 +502,6 @@ inline unsigned nblk(int64_t n, int t) { return (unsigned)((n + t - 1) / t); }
 // once to the device's opt-in maximum.
 // Returns the A-ring depth (k_m2l_halo<AS>) whose shared memory fits:
 // 14 stages, or 10 when the halo windows of a depth-6 level need the room.
-bool g_hm_fused_fits = false;  // set by halo_smem_attr for the plan being built
 int halo_smem_attr(int rw_cap) {
   static std::once_flag once;
   static int max_optin = 0;
@@ -510,19 +509,15 @@ int halo_smem_attr(int rw_cap) {
     int dev = 0;
     LFMM_CUDA(cudaGetDevice(&dev));
     LFMM_CUDA(cudaDeviceGetAttribute(&max_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev));
-    cudaFuncAttributes fa{}, fb{}, fc{};
+    cudaFuncAttributes fa{}, fb{};
     LFMM_CUDA(cudaFuncGetAttributes(&fa, k_m2l_halo<HM_ASTAGES>));
     LFMM_CUDA(cudaFuncGetAttributes(&fb, k_m2l_halo<HM_ASTAGES_SMALL>));
-    LFMM_CUDA(cudaFuncGetAttributes(&fc, k_m2l_halo<HM_ASTAGES_FUSED, 1>));
     // static shared memory counts against the same limit
-    max_optin -= (int)std::max(std::max(fa.sharedSizeBytes, fb.sharedSizeBytes), fc.sharedSizeBytes);
+    max_optin -= (int)std::max(fa.sharedSizeBytes, fb.sharedSizeBytes);
     LFMM_CUDA(cudaFuncSetAttribute(k_m2l_halo<HM_ASTAGES>, cudaFuncAttributeMaxDynamicSharedMemorySize, max_optin));
     LFMM_CUDA(
         cudaFuncSetAttribute(k_m2l_halo<HM_ASTAGES_SMALL>, cudaFuncAttributeMaxDynamicSharedMemorySize, max_optin));
-    LFMM_CUDA(cudaFuncSetAttribute(k_m2l_halo<HM_ASTAGES_FUSED, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                   max_optin));
   });
-  g_hm_fused_fits = hm_smem_bytes(rw_cap, HM_ASTAGES_FUSED, 1) <= (size_t)max_optin;
   if (hm_smem_bytes(rw_cap, HM_ASTAGES) <= (size_t)max_optin) return HM_ASTAGES;
   LFMM_REQUIRE(hm_smem_bytes(rw_cap, HM_ASTAGES_SMALL) <= (size_t)max_optin,
                "halo M2L tile needs more shared memory than the device offers");
@@ -531,13 +526,11 @@ int halo_smem_attr(int rw_cap) {
 
 // persistent launch: at most `ctas` CTAs (one per SM) walk the njobs jobs of
 // ha.jobs through the zeroed ha.counter
-void launch_m2l_halo(HaloArgs ha, int njobs, int ctas, int astages, cudaStream_t st, bool fused_p2p = false) {
+void launch_m2l_halo(HaloArgs ha, int njobs, int ctas, int astages, cudaStream_t st) {
   ha.njobs = njobs;
   LFMM_CUDA(cudaMemsetAsync(ha.counter, 0, sizeof(int), st));
   const unsigned grid = (unsigned)std::max(1, std::min(njobs, ctas));
-  if (fused_p2p)
-    k_m2l_halo<HM_ASTAGES_FUSED, 1><<<grid, HM_THREADS_FUSED, hm_smem_bytes(ha.rw_cap, HM_ASTAGES_FUSED, 1), st>>>(ha);
-  else if (astages == HM_ASTAGES)
+  if (astages == HM_ASTAGES)
     k_m2l_halo<HM_ASTAGES><<<grid, HM_THREADS, hm_smem_bytes(ha.rw_cap, HM_ASTAGES), st>>>(ha);
   else
     k_m2l_halo<HM_ASTAGES_SMALL><<<grid, HM_THREADS, hm_smem_bytes(ha.rw_cap, HM_ASTAGES_SMALL), st>>>(ha);
@@ -604,9 +597,6 @@ struct lfmm_plan {
   cudaEvent_t ev_m2l_done = nullptr;
   int p2p_c1 = 3, p2p_c2 = 3;  // CTAs per SM of near-field launches 1 and 2 (room for the far-field chains)
   bool p2p_preempt = true;
-  double p2p_q1 = 0.4;  // share of the leaves near-field launch 1 may take when the M2L carries near-field warps
-  bool m2l_p2p = true;       // near-field warps inside the M2L launch (k_m2l_halo<9, 1>; LFMM_M2L_P2P=0: off)
-  bool hm_fused_ok = false;  // ... when its shared memory fits this plan's halo windows
   // lfmm_step with device-resident inputs as one CUDA graph: captured on the
   // second call with the same arguments, replayed while the arguments, the
   // stream and every device allocation stay the same (LFMM_GRAPH=0: off)
@@ -1029,7 +1019,6 @@ struct lfmm_plan {
     LFMM_CUDA(cudaStreamSynchronize(stream));
     hm_level_max.ensure(sizeof(unsigned int) * (DMAX + 2));
     hm_astages = halo_smem_attr(hm_rw_cap);
-    hm_fused_ok = g_hm_fused_fits;
   }
 
   // Halo M2L jobs: (level, target class, 256-row tile of the padded linear
@@ -1177,19 +1166,19 @@ struct lfmm_plan {
   // ---------------------------------------------------------- solve ----
   // k_p2p2: ctas == 0 one warp per leaf; else persistent with that many CTAs
   // over the shared leaf counter p2p_ctl[0], stopped by *stop
-  void p2p2_launch(bool grad, int periodic, int ctas, const int* stop, cudaStream_t st, int limit = 1 << 30) {
+  void p2p2_launch(bool grad, int periodic, int ctas, const int* stop, cudaStream_t st) {
     const unsigned grid = ctas > 0 ? (unsigned)ctas : nblk(own_leaves(), P2P2_WARPS);
     int* ctl = ctas > 0 ? p2p_ctl.as<int>() : nullptr;
     if (grad)
       k_p2p2<true><<<grid, P2P2_WARPS * 32, P2P2_SMEM, st>>>(reinterpret_cast<const float4*>(xq.p), pair_a(), pair_b(),
                                                             leaf_start.as<int>(), depth, (float)size, periodic,
                                                             vnear.as<float>(), gnear.as<float>(), own_x0, own_x1, ctl,
-                                                            stop, limit);
+                                                            stop);
     else
       k_p2p2<false><<<grid, P2P2_WARPS * 32, P2P2_SMEM, st>>>(reinterpret_cast<const float4*>(xq.p), pair_a(), pair_b(),
                                                              leaf_start.as<int>(), depth, (float)size, periodic,
                                                              vnear.as<float>(), gnear.as<float>(), own_x0, own_x1, ctl,
-                                                             stop, limit);
+                                                             stop);
   }
   // leaves of this rank's slab (all of them without a decomposition); the
   // leaf kernels start their grid at leaf plane own_x0
@@ -1296,9 +1285,7 @@ struct lfmm_plan {
       // behind): let it finish before the near field holds the SMs, or its
       // large-smem kernels wait behind the M2L
       if (near_after_hi) LFMM_CUDA(cudaStreamWaitEvent(near_stream, ev_hi_out, 0));
-      // with near-field warps in the M2L launch, launch 1 leaves them a share
-      const int quota = (m2l_p2p && hm_fused_ok) ? (int)(p2p_q1 * (double)own_leaves()) : (1 << 30);
-      launch_on(ST_P2P, near_stream, [&] { p2p2_launch(grad, periodic, nsm * p2p_c1, ctl + 1, near_stream, quota); });
+      launch_on(ST_P2P, near_stream, [&] { p2p2_launch(grad, periodic, nsm * p2p_c1, ctl + 1, near_stream); });
     } else {
       issue_p2p();
     }
@@ -1418,25 +1405,9 @@ struct lfmm_plan {
           k_pack_mult16<<<dim3((unsigned)((8 * prows + 255) / 256), depth, 8), 256, 0, stream>>>(ha);
         });
         if (preempt) LFMM_CUDA(cudaMemsetAsync(ctl + 1, 1, sizeof(int), stream));  // near field 1 yields the SMs
-        const bool fused = preempt && m2l_p2p && hm_fused_ok;
-        if (fused) {  // the near field continues inside the M2L launch
-          ha.p2p_xq = reinterpret_cast<const float4*>(xq.p);
-          ha.p2p_pair_a = pair_a();
-          ha.p2p_pair_b = pair_b();
-          ha.p2p_leaf_start = leaf_start.as<int>();
-          ha.p2p_depth = depth;
-          ha.p2p_periodic = (flags & LFMM_F_PERIODIC_NEAR) ? 1 : 0;
-          ha.p2p_grad = grad ? 1 : 0;
-          ha.p2p_x0 = own_x0;
-          ha.p2p_x1 = own_x1;
-          ha.p2p_size = (float)size;
-          ha.p2p_vnear = vnear.as<float>();
-          ha.p2p_gnear = gnear.as<float>();
-          ha.p2p_ctl = ctl;
-        }
         launch(ST_DOWN, [&] {
           ha.counter = hm_counter.as<int>();
-          launch_m2l_halo(ha, hm_njobs, nsm, hm_astages, stream, fused);
+          launch_m2l_halo(ha, hm_njobs, nsm, hm_astages, stream);
         });
         if (preempt) {
           LFMM_CUDA(cudaEventRecord(ev_m2l_done, stream));
@@ -1902,7 +1873,6 @@ int lfmm_plan_create(const double* positions, int64_t n, double box_length, int 
       pl->p2p_scalar = env_is("LFMM_P2P", "scalar");
       pl->p2p_preempt = !env_is("LFMM_P2P", "plain");
       pl->graphs = !env_is("LFMM_GRAPH", "0");
-      pl->m2l_p2p = !env_is("LFMM_M2L_P2P", "0");
       pl->m2l_f64_simt = env_is("LFMM_M2L64", "gather");
     }
     pl->nleaf = 1 << (3 * depth);

@@ -46,7 +46,6 @@
 #include <cstdint>
 
 #include "lfmm_common.cuh"
-#include "lfmm_p2p.cuh"
 #include "lfmm_sm100.cuh"
 
 namespace lfmm {
@@ -57,14 +56,8 @@ constexpr int HM_NKC = 8;          // 128 / 16
 constexpr int HM_ATILE = 8192;     // one operator chunk: hi 4 KB | lo 4 KB
 constexpr int HM_ASTAGES = 14;   // A-ring stages (10 when the level-6 halo windows need the room)
 constexpr int HM_ASTAGES_SMALL = 10;
-constexpr int HM_ASTAGES_FUSED = 9;  // k_m2l_halo<9, 1>: the near-field staging takes the rest
 constexpr int HM_THREADS = 384;
 constexpr int HM_WORKERS = 256;
-// k_m2l_halo<AS, 1>: a fourth warpgroup runs the near field (k_p2p2's leaf
-// loop) on the CUDA cores the tensor-core roles leave idle (the M2L issues
-// from ~18 % of the issue slots and 7 % of the FMA pipe, ncu r02)
-constexpr int HM_P2P_WARPS = 4;
-constexpr int HM_THREADS_FUSED = HM_THREADS + 32 * HM_P2P_WARPS;
 
 // (tc, sc) term tables: count and {operator row, dx, dy, dz}
 __constant__ int c_hterm_n[64];
@@ -90,17 +83,6 @@ struct HaloArgs {
   int pk_r0[DMAX + 2], pk_r1[DMAX + 2];  // k_pack_mult16: padded rows [r0, r1) per level (r1 == 0: all)
   int njobs;                         // jobs of this launch (k_m2l_halo is persistent)
   int* counter;                      // next job to fetch; zeroed before each launch
-  // k_m2l_halo<AS, 1>: near-field warps beside the tensor-core roles (the
-  // preemptible k_p2p2 leaf loop on the same leaf counter)
-  const float4* p2p_xq;
-  const float4* p2p_pair_a;
-  const float4* p2p_pair_b;
-  const int* p2p_leaf_start;
-  int p2p_depth, p2p_periodic, p2p_grad, p2p_x0, p2p_x1;
-  float p2p_size;
-  float* p2p_vnear;
-  float* p2p_gnear;
-  int* p2p_ctl;
 };
 
 // A-ring slot sequence of issuer par's u-th term (u counts its terms over all
@@ -116,9 +98,8 @@ __device__ __forceinline__ int hm_aseq(int par, int u, int D, int T) {
 
 __host__ __device__ inline int hm_rw(int N, int Z) { return N + 2 * Z + 2; }
 __host__ __device__ inline size_t hm_buf_bytes(int rw) { return (size_t)192 * rw; }  // 2 parts x 2 kgroups x 3 windows x 16 B
-__host__ inline size_t hm_smem_bytes(int rw_cap, int astages = HM_ASTAGES, int fused_p2p = 0) {
-  return 2 * hm_buf_bytes(rw_cap) + (size_t)astages * HM_ATILE + 1024 +
-         (fused_p2p ? (size_t)HM_P2P_WARPS * P2P2_SMAX * 16 : 0);
+__host__ inline size_t hm_smem_bytes(int rw_cap, int astages = HM_ASTAGES) {
+  return 2 * hm_buf_bytes(rw_cap) + (size_t)astages * HM_ATILE + 1024;
 }
 
 // group g of G: relative parities (tc ^ sc) it covers
@@ -314,8 +295,8 @@ __device__ unsigned long long g_hm_prof[8192][8];
 constexpr int HM_JQ = 2;
 constexpr int HM_JOB_CONSUMERS = 1 + 2 + 8;  // A loader lane, 2 issuer warps, 8 worker warps
 
-template <int AS, int FP = 0>
-__global__ void __launch_bounds__(FP ? HM_THREADS_FUSED : HM_THREADS, 1) k_m2l_halo(HaloArgs g) {
+template <int AS>
+__global__ void __launch_bounds__(HM_THREADS, 1) k_m2l_halo(HaloArgs g) {
 #ifdef LFMM_HM_PROF
   unsigned long long _tstart = 0;
   if (threadIdx.x == 0) {
@@ -339,12 +320,6 @@ __global__ void __launch_bounds__(FP ? HM_THREADS_FUSED : HM_THREADS, 1) k_m2l_h
   __shared__ uint32_t s_boff[HM_JQ][4][27];
   __shared__ int s_orow[HM_JQ][4][27];
   __shared__ int s_nt[HM_JQ][4];
-  // fused near field (FP): per-warp staging barrier and image tables, and the
-  // flag that ends it once the M2L work of this CTA is done
-  __shared__ __align__(8) uint64_t s_pbar[HM_P2P_WARPS];
-  __shared__ int2 s_pimg[HM_P2P_WARPS][28];
-  __shared__ float4 s_pshift[HM_P2P_WARPS][27];
-  __shared__ int s_m2l_done;
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const size_t bufb = hm_buf_bytes(g.rw_cap);
@@ -365,10 +340,6 @@ __global__ void __launch_bounds__(FP ? HM_THREADS_FUSED : HM_THREADS, 1) k_m2l_h
       mbar_init(smem_u32(&job_full[s]), 1);
       mbar_init(smem_u32(&job_empty[s]), HM_JOB_CONSUMERS);
     }
-    if (FP) {
-      for (int s = 0; s < HM_P2P_WARPS; ++s) mbar_init(smem_u32(&s_pbar[s]), 1);
-      s_m2l_done = 0;
-    }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   if (warp == 0) {
@@ -379,18 +350,6 @@ __global__ void __launch_bounds__(FP ? HM_THREADS_FUSED : HM_THREADS, 1) k_m2l_h
   __syncthreads();
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
   const uint32_t tmem = tmem_base_sh;
-  if (FP) {
-    // 65536 registers over 512 threads (128 each at launch): the drain warps
-    // hold 128 fp32 sums, the issue / copy warps 88, the near field 104 (no
-    // spills at 160 / 88 / 104; 256 x 160 + 128 x 88 + 128 x 104 = 65536)
-    const int wg = warp >> 2;
-    if (wg < 2)
-      asm volatile("setmaxnreg.inc.sync.aligned.u32 152;");
-    else if (wg == 2)
-      asm volatile("setmaxnreg.dec.sync.aligned.u32 88;");
-    else
-      asm volatile("setmaxnreg.dec.sync.aligned.u32 120;");
-  }
 
   if (warp < 8) {
     // ================================================= workers =========
@@ -451,7 +410,6 @@ __global__ void __launch_bounds__(FP ? HM_THREADS_FUSED : HM_THREADS, 1) k_m2l_h
       __syncwarp();
       if (lane == 0) mbar_arrive(smem_u32(&job_empty[slot]));
     }
-    if (FP && warp == 0 && lane == 0) *reinterpret_cast<volatile int*>(&s_m2l_done) = 1;  // near field: no new leaves
   } else if (warp == 8 || warp == 9) {
     // ================================================= MMA issuers =====
     // (whole warp; hm_mma_w / hm_commit_w elect one lane).  Issuer par runs
@@ -578,7 +536,7 @@ __global__ void __launch_bounds__(FP ? HM_THREADS_FUSED : HM_THREADS, 1) k_m2l_h
       }
     }
     __syncwarp();
-  } else if (warp == 11) {
+  } else {
     // ========================================= job fetch + halo loader =====
     int it_g = 0;
     for (int jq = 0;; ++jq) {
@@ -637,32 +595,6 @@ __global__ void __launch_bounds__(FP ? HM_THREADS_FUSED : HM_THREADS, 1) k_m2l_h
         }
       }
       __syncwarp();
-    }
-  } else if (FP) {
-    // ============================================== near field (FP) =====
-    // k_p2p2's persistent leaf loop on the shared counter until the CTA's
-    // M2L work is done; the leaves left go to the next near-field launch
-    const int pw = warp - 12;
-    {
-    float4* A = reinterpret_cast<float4*>(abase + (size_t)AS * HM_ATILE) + (size_t)pw * P2P2_SMAX;
-    float4* B = A + P2P2_SMAX / 2;
-    const uint32_t bar = smem_u32(&s_pbar[pw]);
-    const int first = g.p2p_x0 << (2 * g.p2p_depth);
-    const int own = (min(g.p2p_x1, 1 << g.p2p_depth) - g.p2p_x0) << (2 * g.p2p_depth);
-    uint32_t phase = 0;
-    for (;;) {
-      int v = 0;
-      if (lane == 0) v = *reinterpret_cast<volatile int*>(&s_m2l_done) ? own : atomicAdd(g.p2p_ctl, 1);
-      v = __shfl_sync(0xffffffffu, v, 0);
-      if (v >= own) break;
-      if (g.p2p_grad)
-        p2p2_leaf<true>(first + v, g.p2p_xq, g.p2p_pair_a, g.p2p_pair_b, g.p2p_leaf_start, g.p2p_depth, g.p2p_size,
-                        g.p2p_periodic, g.p2p_vnear, g.p2p_gnear, A, B, s_pimg[pw], s_pshift[pw], bar, phase);
-      else
-        p2p2_leaf<false>(first + v, g.p2p_xq, g.p2p_pair_a, g.p2p_pair_b, g.p2p_leaf_start, g.p2p_depth,
-                         g.p2p_size, g.p2p_periodic, g.p2p_vnear, g.p2p_gnear, A, B, s_pimg[pw], s_pshift[pw], bar,
-                         phase);
-    }
     }
   }
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");

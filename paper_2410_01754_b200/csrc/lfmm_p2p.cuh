@@ -380,8 +380,7 @@ __global__ void __launch_bounds__(P2P2_WARPS * 32, LFMM_P2P2_MINB) k_p2p2(const 
                                                           const int* __restrict__ leaf_start, int depth,
                                                           float size, int periodic, float* __restrict__ vout,
                                                           float* __restrict__ gout, int x0, int x1,
-                                                          int* __restrict__ ctl, const int* __restrict__ stop,
-                                                          int limit) {
+                                                          int* __restrict__ ctl, const int* __restrict__ stop) {
   extern __shared__ float4 p2p2_smem[];  // [warp][A | B][SMAX / 2]
   __shared__ __align__(8) uint64_t s_bar[P2P2_WARPS];
   __shared__ int2 s_img[P2P2_WARPS][28];  // {first staged pair, pair count}; sentinel at nimg
@@ -389,7 +388,7 @@ __global__ void __launch_bounds__(P2P2_WARPS * 32, LFMM_P2P2_MINB) k_p2p2(const 
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   const int nleaf = 1 << (3 * depth);
   const int first = x0 << (2 * depth);  // the rank's first leaf plane
-  const int own = min((min(x1, 1 << depth) - x0) << (2 * depth), limit);
+  const int own = (min(x1, 1 << depth) - x0) << (2 * depth);
   float4* A = p2p2_smem + (size_t)w * P2P2_SMAX;
   float4* B = A + P2P2_SMAX / 2;
   const uint32_t bar = smem_u32(&s_bar[w]);
