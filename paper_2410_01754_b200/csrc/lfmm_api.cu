@@ -601,11 +601,12 @@ struct lfmm_plan {
   // second call with the same arguments, replayed while the arguments, the
   // stream and every device allocation stay the same (LFMM_GRAPH=0: off)
   bool graphs = true;
+  uint64_t epoch = 0;  // bumped by every call that changes sizes or tables a captured step bakes in
   struct StepGraph {
     std::array<const void*, 10> ptrs{};
     int mode = -1, plain = -1;
     cudaStream_t stream = nullptr;
-    uint64_t gen = 0;
+    uint64_t gen = 0, epoch = 0;
     bool warm = false;
     cudaGraphExec_t exec = nullptr;
     int64_t nlaunch = 0;
@@ -2156,6 +2157,7 @@ int lfmm_sites_set(lfmm_plan* plan, int64_t n_sites, const int64_t* atom_offsets
     plan->offsets.ensure(sizeof(double) * std::max<int64_t>(S, 1));
     plan->site_force.ensure(sizeof(double) * 3 * std::max<int64_t>(A, 1));
     plan->site_force_valid = false;
+    ++plan->epoch;
     LFMM_CUDA(cudaStreamSynchronize(plan->stream));
   });
 }
@@ -2492,7 +2494,8 @@ bool step_graph_launch(lfmm_plan* plan, const double* positions, const double* c
   auto& g = plan->step_graph;
   const std::array<const void*, 10> ptrs{positions, charges, lambdas, n_lambda, energy, forces, lambda_forces,
                                          potentials, nullptr, nullptr};
-  const bool same = g.ptrs == ptrs && g.mode == mode && g.plain == plain && g.stream == plan->stream;
+  const bool same = g.ptrs == ptrs && g.mode == mode && g.plain == plain && g.stream == plan->stream &&
+                    g.epoch == plan->epoch;
   if (g.exec && same && g.gen == g_alloc_gen.load()) {
     LFMM_CUDA(cudaGraphLaunch(g.exec, plan->stream));
     plan->launches += g.nlaunch;
@@ -2507,6 +2510,7 @@ bool step_graph_launch(lfmm_plan* plan, const double* positions, const double* c
     g.mode = mode;
     g.plain = plain;
     g.stream = plan->stream;
+    g.epoch = plan->epoch;
     g.warm = true;
     return false;
   }
@@ -2573,6 +2577,7 @@ int lfmm_plan_set_count(lfmm_plan* plan, int64_t n) {
   if (!plan) return fail(Error{LFMM_EINVAL, "plan is NULL"});
   return guarded([&] {
     LFMM_REQUIRE(n >= 0 && n < (1LL << 31), "particle count out of range");
+    ++plan->epoch;
     const int64_t nn = std::max<int64_t>(n, 1);
     const size_t t = plan->tsz();
     plan->pos_in.ensure(sizeof(double) * 3 * nn);
@@ -2597,6 +2602,7 @@ int lfmm_dist_configure(lfmm_plan* plan, int x0, int x1, int lg) {
     const int n = 1 << plan->depth;
     LFMM_REQUIRE(0 <= x0 && x0 < x1 && x1 <= n, "owned leaf x-range outside the grid");
     LFMM_REQUIRE(lg >= 0 && lg <= plan->depth, "bad shared-level count");
+    ++plan->epoch;
     plan->own_x0 = x0;
     plan->own_x1 = x1;
     plan->dist_lg = lg;

@@ -96,3 +96,41 @@ def test_non_finite_result_raises_numerical_failure():
     solver = PeriodicSolver(system.positions, system.box_length, SolverConfig(p=6, depth=2))
     with pytest.raises(NumericalFailure, match="non-finite"):
         solver.solve(q)
+
+
+def test_step_graph_follows_new_site_tables():
+    """A captured step bakes in sizes (site count, grids): replacing the site
+    tables with fewer sites between calls must re-capture, so the step equals
+    a fresh plan's uncaptured step."""
+    import torch
+
+    from paper_2410_01754_b200 import _native
+    from paper_2410_01754_b200.system import ParticleSystem, lambda_table, site_tables
+
+    system, lam, _ = generate_water_box(20_000, 8, seed=5)
+    fewer = ParticleSystem(system.box_length, system.positions, system.charges, system.sites[:3])
+    cfg = SolverConfig(p=8, depth=3, precision="single")
+    dev = torch.device("cuda", 0)
+    d = lambda a: torch.from_numpy(np.ascontiguousarray(a)).to(dev)  # noqa: E731
+
+    def run(plan, sysm, lam_values, reps):
+        lt, nl = lambda_table(sysm, lam_values)
+        e = torch.empty(1, dtype=torch.float64, device=dev)
+        f = torch.empty((sysm.num_particles, 3), dtype=torch.float64, device=dev)
+        lf = torch.empty((8, 4), dtype=torch.float64, device=dev)
+        args = (d(sysm.positions), d(sysm.charges), d(lt), d(nl))
+        for _ in range(reps):
+            plan.step(*args, mode=_native.MODE_HI, on_device=True, energy=e, forces=f, lambda_forces=lf)
+        torch.cuda.synchronize()
+        return float(e.cpu()[0]), f.cpu().numpy(), lf.cpu().numpy()[: len(sysm.sites)]
+
+    solver = PeriodicSolver(system.positions, system.box_length, cfg)
+    solver.plan.set_sites(*site_tables(system))
+    run(solver.plan, system, lam.values, 3)  # captured with 8 sites
+    solver.plan.set_sites(*site_tables(fewer))
+    got = run(solver.plan, fewer, lam.values[:3], 3)
+    fresh = PeriodicSolver(system.positions, system.box_length, cfg)
+    fresh.plan.set_sites(*site_tables(fewer))
+    want = run(fresh.plan, fewer, lam.values[:3], 1)
+    assert got[0] == want[0]
+    assert got[1].tobytes() == want[1].tobytes() and got[2].tobytes() == want[2].tobytes()
