@@ -194,10 +194,11 @@ class TorchComm:
             r.wait()
         out = {}
         ops = []
-        for p in peers:
+        counts = torch.cat([cnt_in[p] for p in peers]).tolist()  # the one host sync of the exchange
+        for p, m in zip(peers, counts):
             t = sends[p]
             src = t.cpu().contiguous() if staged else t.contiguous()
-            out[p] = torch.empty((int(cnt_in[p].item()),) + tuple(t.shape[1:]), dtype=t.dtype, device=cdev)
+            out[p] = torch.empty((int(m),) + tuple(t.shape[1:]), dtype=t.dtype, device=cdev)
             ops.append(dist.P2POp(dist.isend, src, p, self.group))
             ops.append(dist.P2POp(dist.irecv, out[p], p, self.group))
         for r in dist.batch_isend_irecv(ops):
@@ -418,10 +419,13 @@ class DistributedSolver:
         xl, xr = (x0 - 1) % n, x1 % n
         to_left = (lx == x0) | (lx == xl)
         to_right = (lx == x1 - 1) | (lx == xr)
-        if bool((~(stay | (lx == xl) | (lx == xr))).any()):
+        # both migration checks and the kept-atom count in one host sync
+        far, moved, n_stay = torch.stack([(~(stay | (lx == xl) | (lx == xr))).any().to(torch.int64),
+                                          (~stay).any().to(torch.int64), stay.sum()]).tolist()
+        if far:
             raise ValueError("an atom moved more than one leaf plane out of its rank's slab; "
                              "re-partition from global positions (DistributedSolver.step)")
-        if x1 - x0 < 2 and self.world > 2 and bool((~stay).any()):
+        if x1 - x0 < 2 and self.world > 2 and moved:
             # with one plane per rank a migrant into plane x1 (x0-1) is also
             # the halo of rank r+2 (r-2), which this one-hop exchange never
             # reaches: those pairs would silently drop out of the P2P
@@ -443,7 +447,7 @@ class DistributedSolver:
         q = torch.cat([charges[stay], rec[r_own, 3], charges[gone], rec[r_halo, 3]]).contiguous()
         gid = torch.cat([global_ids[stay], rec[r_own, 4].to(torch.int64), global_ids[gone],
                          rec[r_halo, 4].to(torch.int64)])
-        return pos, q, gid, int(stay.sum().item()) + int(r_own.sum().item())
+        return pos, q, gid, int(n_stay) + int(r_own.sum())
 
     def _step(self, positions, charges, global_ids, lambdas, n_lambda, sites, n_global, mode):
         torch = self.torch
