@@ -2492,6 +2492,9 @@ bool step_graph_launch(lfmm_plan* plan, const double* positions, const double* c
                        const int32_t* n_lambda, int mode, int plain, double* energy, double* forces,
                        double* lambda_forces, double* potentials) {
   auto& g = plan->step_graph;
+  cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+  LFMM_CUDA(cudaStreamIsCapturing(plan->stream, &cs));
+  if (cs != cudaStreamCaptureStatusNone) return false;  // the caller is capturing its own graph: record into it
   const std::array<const void*, 10> ptrs{positions, charges, lambdas, n_lambda, energy, forces, lambda_forces,
                                          potentials, nullptr, nullptr};
   const bool same = g.ptrs == ptrs && g.mode == mode && g.plain == plain && g.stream == plan->stream &&
