@@ -311,23 +311,14 @@ __global__ void k_finalize(int64_t n, int K, int c, const int* __restrict__ perm
 // pieces (the step path skips the input-order potential arrays):
 // V = V_near + V_far + 2 eta gamma (r - L/2).D   (solver.py:373-379)
 template <class T>
-__global__ void k_site_pot(const int* __restrict__ atom_idx, int n, const int* __restrict__ inv_perm,
-                           const T* __restrict__ vnear, const T* __restrict__ vfar,
-                           const double* __restrict__ pos_sorted, const double* __restrict__ scal, int dipole,
-                           double box, double* __restrict__ out, const int* __restrict__ leaf_sorted, int depth,
-                           int x0, int x1) {
-  const int a = blockIdx.x * blockDim.x + threadIdx.x;
-  if (a >= n) return;
-  if (atom_idx[a] < 0) {  // site atom held by another rank (distributed.py)
-    out[a] = 0.0;
-    return;
-  }
-  const int k = inv_perm[atom_idx[a]];
+__device__ __forceinline__ double site_pot_at(int i, const int* __restrict__ inv_perm, const T* __restrict__ vnear,
+                                              const T* __restrict__ vfar, const double* __restrict__ pos_sorted,
+                                              const double* __restrict__ scal, int dipole, double box,
+                                              const int* __restrict__ leaf_sorted, int depth, int x0, int x1) {
+  if (i < 0) return 0.0;  // site atom held by another rank (distributed.py)
+  const int k = inv_perm[i];
   const int lx = leaf_sorted[k] >> (2 * depth);
-  if (lx < x0 || lx >= x1) {  // halo atom: its owner supplies the potential
-    out[a] = 0.0;
-    return;
-  }
+  if (lx < x0 || lx >= x1) return 0.0;  // halo atom: its owner supplies the potential
   double v = (double)vnear[k] + (double)vfar[k];
   if (dipole) {
     const double gam = 2.0 * 3.14159265358979323846 / (3.0 * box * box * box), h = 0.5 * box;
@@ -335,7 +326,61 @@ __global__ void k_site_pot(const int* __restrict__ atom_idx, int n, const int* _
          ((pos_sorted[3 * k] - h) * scal[0] + (pos_sorted[3 * k + 1] - h) * scal[1] +
           (pos_sorted[3 * k + 2] - h) * scal[2]);
   }
-  out[a] = v;
+  return v;
+}
+
+template <class T>
+__global__ void k_site_pot(const int* __restrict__ atom_idx, int n, const int* __restrict__ inv_perm,
+                           const T* __restrict__ vnear, const T* __restrict__ vfar,
+                           const double* __restrict__ pos_sorted, const double* __restrict__ scal, int dipole,
+                           double box, double* __restrict__ out, const int* __restrict__ leaf_sorted, int depth,
+                           int x0, int x1) {
+  const int a = blockIdx.x * blockDim.x + threadIdx.x;
+  if (a >= n) return;
+  out[a] = site_pot_at<T>(atom_idx[a], inv_perm, vnear, vfar, pos_sorted, scal, dipole, box, leaf_sorted, depth, x0,
+                          x1);
+}
+
+// The single-GPU step's tail in one launch, warp per site: the site-atom
+// potentials (k_site_pot), the lambda forces (hi_lambda_site, the sums of
+// k_hi_site in its order), the HI spatial forces added into the force rows
+// (k_add_site_forces) and the step energy (k_step_energy).  Every value is
+// the one the four separate kernels produce.
+template <class T>
+struct TailArgs {
+  const int* inv_perm;
+  const T* vnear;
+  const T* vfar;
+  const double* pos_sorted;
+  const double* scal;
+  int dipole;
+  const int* leaf_sorted;
+  int depth, x0, x1;
+  double* pot_site;          // A
+  double* forces;            // N x 3, input order
+  const double* site_force;  // A x 3, or null (QI mode)
+  const double* energies;
+  const double* off;
+  int add_off;
+  double* energy_out;
+};
+
+template <class T>
+__global__ void k_step_tail(HiArgs g, TailArgs<T> t) {
+  if (blockIdx.x == 0 && threadIdx.x == 0) *t.energy_out = t.energies[0] + (t.add_off ? t.off[0] : 0.0);
+  const int s = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  const int lane = threadIdx.x & 31;
+  if (s >= g.n_sites) return;
+  const int a0 = g.atom_off[s], a1 = g.atom_off[s + 1];
+  for (int a = a0 + lane; a < a1; a += 32) {
+    const int i = g.atom_idx[a];
+    t.pot_site[a] = site_pot_at<T>(i, t.inv_perm, t.vnear, t.vfar, t.pos_sorted, t.scal, t.dipole, g.box,
+                                   t.leaf_sorted, t.depth, t.x0, t.x1);
+    if (t.site_force && i >= 0)
+      for (int k = 0; k < 3; ++k) t.forces[3 * (size_t)i + k] += t.site_force[3 * a + k];
+  }
+  __syncwarp();
+  hi_lambda_site(g, s, lane);
 }
 
 // warp per site: S_rho and lambda forces from given potentials and C_rho
@@ -2415,9 +2460,51 @@ void step_body(lfmm_plan* plan, const double* positions, const double* charges, 
     // HI spatial forces: -grad Delta E_site on the site atoms (k_hi_site,
     // issued on the HI side stream before the solve)
     const bool site_forces = !plain && plan->n_sites > 0 && mode == LFMM_MODE_HI;
-    if (site_forces && hi_side) {
+    const bool add_off = !plain && plan->n_sites > 0 && mode == LFMM_MODE_HI;
+    // step mode with the HI side stream: one tail kernel does site
+    // potentials, lambda forces, site forces and the energy
+    const bool fused_tail = !plain && plan->n_sites > 0 && step_mode && hi_side;
+    if (fused_tail) {
       LFMM_CUDA(cudaStreamWaitEvent(plan->stream, plan->ev_hi_out, 0));
-      add_site_forces(plan);
+      plan->site_pot.ensure(sizeof(double) * std::max<int64_t>(plan->n_site_atoms, 1));
+      HiArgs g{};
+      hi_args(plan, g);
+      g.pot_site = plan->site_pot.as<double>();
+      g.mode = mode;
+      g.c_p2p = plan->c_p2p.as<double>();
+      g.c_lat = plan->c_lat.as<double>();
+      g.c_dip = plan->c_dip.as<double>();
+      g.forces = plan->lam_forces.as<double>();
+      auto fill = [&](auto& t, auto* vn, auto* vf) {
+        t.inv_perm = plan->inv_perm.as<int>();
+        t.vnear = vn;
+        t.vfar = vf;
+        t.pos_sorted = plan->pos_sorted.as<double>();
+        t.scal = plan->scal.as<double>();
+        t.dipole = (plan->flags & LFMM_F_DIPOLE) ? 1 : 0;
+        t.leaf_sorted = plan->leaf_sorted.as<int>();
+        t.depth = plan->depth;
+        t.x0 = plan->own_x0;
+        t.x1 = plan->own_x1;
+        t.pot_site = plan->site_pot.as<double>();
+        t.forces = plan->out_forces.as<double>();
+        t.site_force = site_forces ? plan->site_force.as<double>() : nullptr;
+        t.energies = plan->energies.as<double>();
+        t.off = plan->offset_total.as<double>();
+        t.add_off = add_off ? 1 : 0;
+        t.energy_out = plan->scal.as<double>() + 6;
+      };
+      plan->launch(ST_FINAL, [&] {
+        if (plan->fp32) {
+          TailArgs<float> t{};
+          fill(t, plan->vnear.as<float>(), plan->vfar.as<float>());
+          k_step_tail<float><<<nblk(plan->n_sites, 4), 128, 0, plan->stream>>>(g, t);
+        } else {
+          TailArgs<double> t{};
+          fill(t, plan->vnear.as<double>(), plan->vfar.as<double>());
+          k_step_tail<double><<<nblk(plan->n_sites, 4), 128, 0, plan->stream>>>(g, t);
+        }
+      });
     }
     if (overlap && forces) {
       // the forces download overlaps the HI corrections
@@ -2426,8 +2513,8 @@ void step_body(lfmm_plan* plan, const double* positions, const double* charges, 
       LFMM_CUDA(cudaMemcpyAsync(forces, plan->out_forces.p, sizeof(double) * 3 * N, cudaMemcpyDeviceToHost,
                                 plan->io_stream));
     }
-    if (!plain && plan->n_sites > 0) {
-      if (!hi_side) gather_site_positions(plan, nullptr, 0);
+    if (!plain && plan->n_sites > 0 && !fused_tail) {
+      gather_site_positions(plan, nullptr, 0);
       if (step_mode) {
         plan->site_pot.ensure(sizeof(double) * std::max<int64_t>(plan->n_site_atoms, 1));
         const int na = (int)plan->n_site_atoms;
@@ -2444,33 +2531,18 @@ void step_body(lfmm_plan* plan, const double* positions, const double* charges, 
                 plan->vfar.as<double>(), plan->pos_sorted.as<double>(), plan->scal.as<double>(), dip, plan->L,
                 plan->site_pot.as<double>(), plan->leaf_sorted.as<int>(), plan->depth, plan->own_x0, plan->own_x1);
         });
-        if (hi_side) {
-          LFMM_CUDA(cudaStreamWaitEvent(plan->stream, plan->ev_hi_out, 0));
-          HiArgs g{};
-          hi_args(plan, g);
-          g.pot_site = plan->site_pot.as<double>();
-          g.mode = mode;
-          g.c_p2p = plan->c_p2p.as<double>();
-          g.c_lat = plan->c_lat.as<double>();
-          g.c_dip = plan->c_dip.as<double>();
-          g.forces = plan->lam_forces.as<double>();
-          plan->launch(ST_HI, [&] {
-            k_hi_lambda_forces<<<nblk(plan->n_sites, 4), 128, 0, plan->stream>>>(g);
-          });
-        } else {
-          run_hi(plan, mode, nullptr, plan->site_pot.as<double>());
-        }
+        run_hi(plan, mode, nullptr, plan->site_pot.as<double>());
       } else {
         run_hi(plan, mode, plan->out_pot.as<double>());
       }
-      if (site_forces && !hi_side) add_site_forces(plan);
+      if (site_forces) add_site_forces(plan);
     }
     // energy = E_solve + sum of site offsets (hi_energy_and_forces :273)
-    const bool add_off = !plain && plan->n_sites > 0 && mode == LFMM_MODE_HI;
-    plan->launch(ST_FINAL, [&] {
-      k_step_energy<<<1, 1, 0, plan->stream>>>(plan->energies.as<double>(), plan->offset_total.as<double>(),
-                                               add_off ? 1 : 0, plan->scal.as<double>() + 6);
-    });
+    if (!fused_tail)
+      plan->launch(ST_FINAL, [&] {
+        k_step_energy<<<1, 1, 0, plan->stream>>>(plan->energies.as<double>(), plan->offset_total.as<double>(),
+                                                 add_off ? 1 : 0, plan->scal.as<double>() + 6);
+      });
     if (energy)
       LFMM_CUDA(cudaMemcpyAsync(energy, plan->scal.as<double>() + 6, sizeof(double),
                                 io_on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost, plan->stream));

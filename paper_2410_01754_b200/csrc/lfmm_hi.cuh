@@ -486,10 +486,7 @@ __global__ void k_hi_umat(const double* __restrict__ lat_t, const double* __rest
 // corrections-only k_hi_site pass (assemble_lambda_forces, corrections.py:
 // 221-238), warp per site; S_rho and the force sums in exactly k_hi_site's
 // order, so splitting the HI step this way changes no bit.
-__global__ void k_hi_lambda_forces(HiArgs g) {
-  const int s = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
-  const int lane = threadIdx.x & 31;
-  if (s >= g.n_sites) return;
+__device__ __forceinline__ void hi_lambda_site(const HiArgs& g, int s, int lane) {
   const int a0 = g.atom_off[s], ns = g.atom_off[s + 1] - a0;
   const int nf = g.nforms[s], nl = g.nlam[s];
   const double* Q = g.form_q + g.form_off[s];

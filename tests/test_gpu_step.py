@@ -3,10 +3,10 @@ reference and the pinned oracle.
 
 bench.py times ``plan.step(d_pos, d_q, d_lam, d_nl, MODE_HI, on_device=True)``:
 device inputs, positions passed every step (per-step tree rebuild), the HI
-corrections issued on a side stream before the tree, site potentials rebuilt
-from the canonical pieces (k_site_pot), lambda forces by k_hi_lambda_forces,
-the HI site-atom spatial forces added on the main stream, and the step energy
-by k_step_energy.  These tests run exactly that call and compare
+corrections issued on a side stream before the tree, then one tail kernel
+(k_step_tail) that rebuilds the site potentials from the canonical pieces,
+forms the lambda forces, adds the HI site-atom spatial forces into the force
+rows and writes the step energy.  These tests run exactly that call and compare
 
 * energy with the reference's hi_energy_and_forces(...).energy
   (corrections.py:252-274),
