@@ -27,6 +27,7 @@
 #include "lfmm_m2l_halo.cuh"
 #include "lfmm_p2p.cuh"
 #include "lfmm_setup.cuh"
+#include "lfmm_translate_tc.cuh"
 #include "lfmm_tree.cuh"
 
 using namespace lfmm;
@@ -151,6 +152,33 @@ inline void tr_launch(const TrArgs& ta, int ncols_total, int noct, cudaStream_t 
     const unsigned tiles = (unsigned)((ncols_total + 15) / 16);
     k_translate<T, 2, 4><<<dim3(tiles, noct), TR_THREADS, tr_smem_bytes<T, 2, 4>(ta.ncp), st>>>(ta);
   }
+}
+// fp32 M2M / L2L on the tensor cores: 64 columns per CTA on the big levels,
+// 16 on the small ones (more CTAs in flight)
+// fp32 M2M / L2L on the tensor cores: 64 columns per CTA on the big
+// levels, 16 on the small ones (more CTAs in flight)
+inline void tt_launch(const TrArgs& ta, int ncols_total, const void* img, cudaStream_t st) {
+  const auto* im = static_cast<const unsigned char*>(img);
+  if (ncols_total >= 4096)
+    k_translate_tc<64, 2><<<dim3((ncols_total + 63) / 64, 8), TT_THREADS, tt_smem_bytes<64, 2>(), st>>>(ta, im);
+  else
+    k_translate_tc<16, 2><<<dim3((ncols_total + 15) / 16, 8), TT_THREADS, tt_smem_bytes<16, 2>(), st>>>(ta, im);
+}
+// The 81-97 KB CTAs of k_translate_tc run beside the near-field CTAs only if
+// the SMs were configured for the whole shared-memory carveout by the kernels
+// running when the near field lands on them (a resident persistent CTA keeps
+// the SM from being reconfigured): P2M, charge staging, near field.
+inline void tt_set_attrs() {
+  LFMM_CUDA(cudaFuncSetAttribute(k_translate_tc<64, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)tt_smem_bytes<64, 2>()));
+  LFMM_CUDA(cudaFuncSetAttribute(k_translate_tc<16, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)tt_smem_bytes<16, 2>()));
+  LFMM_CUDA(cudaFuncSetAttribute(k_translate_tc<64, 2>, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
+  LFMM_CUDA(cudaFuncSetAttribute(k_translate_tc<16, 2>, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
+  LFMM_CUDA(cudaFuncSetAttribute(k_p2m_c<float, 10>, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
+  LFMM_CUDA(cudaFuncSetAttribute(k_stage_q<float>, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
+  LFMM_CUDA(cudaFuncSetAttribute(k_p2p2<true>, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
+  LFMM_CUDA(cudaFuncSetAttribute(k_p2p2<false>, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
 }
 template <class T>
 inline void tr_set_attrs(int ncp) {
@@ -670,6 +698,9 @@ struct lfmm_plan {
   DevBuf boxq, site_pot;
   DevBuf ops_m2m_t, ops_l2l_t, ops_lat_t, tr_cnt;  // k_translate operators ([k][row]) and tile counters
   bool use_tr = false;                  // M2M / L2L on k_translate (ncp == 128)
+  bool use_tt = false;                  // ... fp32 on k_translate_tc (tensor cores)
+  bool tt_simt = false;                 // LFMM_TRANSLATE=simt: fp32 on k_translate
+  DevBuf tt_m2m, tt_l2l;                // k_translate_tc operator images
   DevBuf q_in, qs, vnear, vfar, gnear, gfar, part, scal, epart, roots;
   DevBuf out_pot, out_near, out_far, out_dip, out_forces, energies, dvec, qtot;
   int64_t last_k = 0;
@@ -755,7 +786,7 @@ struct lfmm_plan {
       cudaEventDestroy(e.b);
     }
     for (auto e : free_events) cudaEventDestroy(e);
-    DevBuf* hbufs[] = {&ops16, &hm_inv_r, &hm_inv_c, &hm_jobs, &hm_counter, &p2p_ctl, &hm_level_max, &mult16, &boxq, &site_pot, &ops_m2m_t, &ops_l2l_t, &ops_lat_t, &tr_cnt, &ops_m2l_t};
+    DevBuf* hbufs[] = {&ops16, &hm_inv_r, &hm_inv_c, &hm_jobs, &hm_counter, &p2p_ctl, &hm_level_max, &mult16, &boxq, &site_pot, &ops_m2m_t, &ops_l2l_t, &ops_lat_t, &tr_cnt, &ops_m2l_t, &tt_m2m, &tt_l2l};
     for (auto* b : hbufs) b->release();
     DevBuf* bufs[] = {&pos_in, &pos_wrap, &leaf_of, &slot_of, &counts, &cursor, &leaf_start, &bucket, &perm,
                       &inv_perm, &pos_sorted, &leaf_sorted, &xq, &mult, &loc, &partial, &up_part, &up_cnt, &counters, &ops_m2l, &ops_m2m,
@@ -978,6 +1009,18 @@ struct lfmm_plan {
       tr_cnt.ensure(sizeof(int) * tiles);
       LFMM_CUDA(cudaMemsetAsync(tr_cnt.p, 0, tr_cnt.bytes, stream));
       tr_set_attrs<T>(ncp);
+      use_tt = sizeof(T) == 4 && !tt_simt;
+      if (use_tt) {
+        tt_m2m.ensure((size_t)8 * TT_OPBYTES);
+        tt_l2l.ensure((size_t)8 * TT_OPBYTES);
+        launch(ST_SETUP, [&] {
+          k_tt_ops<<<nblk(8 * 128 * 128, 256), 256, 0, stream>>>(ops_m2m.as<float>(), tt_m2m.as<unsigned char>());
+        });
+        launch(ST_SETUP, [&] {
+          k_tt_ops<<<nblk(8 * 128 * 128, 256), 256, 0, stream>>>(ops_l2l.as<float>(), tt_l2l.as<unsigned char>());
+        });
+        tt_set_attrs();
+      }
     }
     if (lattice_mode != LFMM_LATTICE_OFF) {
       lat_unit = build_lattice_unit();
@@ -1010,6 +1053,7 @@ struct lfmm_plan {
     if (fp32) {
       LFMM_CUDA(cudaFuncSetAttribute(k_p2p2<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, P2P2_SMEM));
       LFMM_CUDA(cudaFuncSetAttribute(k_p2p2<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, P2P2_SMEM));
+
     }
     LFMM_CUDA(cudaStreamSynchronize(stream));
     vecs.release();
@@ -1261,7 +1305,12 @@ struct lfmm_plan {
         ta.slots = up_part.p;
         ta.cnt = tr_cnt.as<int>();
         owned_parents(l, ta.p0, ta.pend);
-        launch(ST_M2M, [&] { tr_launch<T>(ta, ta.pend - ta.p0, 8, stream); });
+        launch(ST_M2M, [&] {
+          if (use_tt)
+            tt_launch(ta, ta.pend - ta.p0, tt_m2m.p, stream);
+          else
+            tr_launch<T>(ta, ta.pend - ta.p0, 8, stream);
+        });
         return;
       }
       ga.mode = GEMM_UP;
@@ -1485,7 +1534,12 @@ struct lfmm_plan {
           ta.partial = static_cast<const char*>(partial.p) + tsz() * (size_t)part_off[l] * ncp;
           ta.nsplit = nsplit[l];
           owned_parents(l - 1, ta.p0, ta.pend);
-          launch(ST_L2L, [&] { tr_launch<T>(ta, ta.pend - ta.p0, 8, stream); });
+          launch(ST_L2L, [&] {
+            if (use_tt)
+              tt_launch(ta, ta.pend - ta.p0, tt_l2l.p, stream);
+            else
+              tr_launch<T>(ta, ta.pend - ta.p0, 8, stream);
+          });
           continue;
         }
         ga.mode = GEMM_L2L;
@@ -1910,6 +1964,7 @@ int lfmm_plan_create(const double* positions, int64_t n, double box_length, int 
       //   LFMM_P2P=plain   fp32 near field in one launch on the side stream
       //                    (not the preemptible three-launch schedule)
       //   LFMM_M2L64=gather fp64 M2L on the SIMT gather kernel (no DMMA)
+      //   LFMM_TRANSLATE=simt fp32 M2M / L2L on the SIMT kernel k_translate
       auto env_is = [](const char* name, const char* val) {
         const char* e = std::getenv(name);
         return e && std::string(e) == val;
@@ -1920,6 +1975,7 @@ int lfmm_plan_create(const double* positions, int64_t n, double box_length, int 
       pl->p2p_preempt = !env_is("LFMM_P2P", "plain");
       pl->graphs = !env_is("LFMM_GRAPH", "0");
       pl->m2l_f64_simt = env_is("LFMM_M2L64", "gather");
+      pl->tt_simt = env_is("LFMM_TRANSLATE", "simt");
     }
     pl->nleaf = 1 << (3 * depth);
     pl->size = box_length / double(1 << depth);

@@ -48,9 +48,16 @@ def _err(got, ref, absmax):
     return float(np.max(np.abs(np.asarray(got) - np.asarray(ref))) / absmax)
 
 
-@pytest.mark.parametrize("precision", ["double", "single"])
+@pytest.mark.parametrize("precision", ["double", "single", "single-simt"])
 @pytest.mark.parametrize("case", ["c2", "c3", "c4", "c3d6"])
-def test_matches_reference(case, precision):
+def test_matches_reference(case, precision, monkeypatch):
+    """single-simt: the fp32 M2M / L2L on the SIMT k_translate
+    (LFMM_TRANSLATE=simt) instead of the tensor-core k_translate_tc."""
+    if precision == "single-simt":
+        if case not in ("c3", "c3d6"):
+            pytest.skip("the SIMT translation sweeps are checked on the depth-5/6 boxes")
+        monkeypatch.setenv("LFMM_TRANSLATE", "simt")
+        precision = "single"
     g, system, lam = _load(case)
     tol = 1e-6 if precision == "double" else 1e-4
     cfg = SolverConfig(p=int(g["p"]), depth=int(g["depth"]), precision=precision)

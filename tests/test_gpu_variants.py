@@ -31,7 +31,7 @@ def c1():
 
 @pytest.mark.parametrize("env,precision", [("LFMM_M2L=simt", "single"), ("LFMM_P2P=scalar", "single"),
                                            ("LFMM_P2P=plain", "single"), ("LFMM_M2L64=gather", "double"),
-                                           ("LFMM_GRAPH=0", "single")])
+                                           ("LFMM_GRAPH=0", "single"), ("LFMM_TRANSLATE=simt", "single")])
 def test_switch_matches_oracle(env, precision, monkeypatch):
     d = c1()
     name, val = env.split("=")
