@@ -153,8 +153,6 @@ inline void tr_launch(const TrArgs& ta, int ncols_total, int noct, cudaStream_t 
     k_translate<T, 2, 4><<<dim3(tiles, noct), TR_THREADS, tr_smem_bytes<T, 2, 4>(ta.ncp), st>>>(ta);
   }
 }
-// fp32 M2M / L2L on the tensor cores: 64 columns per CTA on the big levels,
-// 16 on the small ones (more CTAs in flight)
 // fp32 M2M / L2L on the tensor cores: 64 columns per CTA on the big
 // levels, 16 on the small ones (more CTAs in flight)
 inline void tt_launch(const TrArgs& ta, int ncols_total, const void* img, cudaStream_t st) {
@@ -1226,16 +1224,14 @@ struct lfmm_plan {
   // ----------------------------------------------------------- tree ----
   template <class T>
   void build_tree(const double* positions, bool on_device) {
-    if (on_device)
-      LFMM_CUDA(cudaMemcpyAsync(pos_in.p, positions, sizeof(double) * 3 * N, cudaMemcpyDeviceToDevice, stream));
-    else
+    if (!on_device)
       LFMM_CUDA(cudaMemcpyAsync(pos_in.p, positions, sizeof(double) * 3 * N, cudaMemcpyHostToDevice, stream));
     LFMM_CUDA(cudaMemsetAsync(counts.p, 0, sizeof(int) * nleaf, stream));
     if (N > 0) {
       launch(ST_TREE, [&] {
-        k_wrap_cell<<<nblk(N, 256), 256, 0, stream>>>(pos_in.as<double>(), N, L, size, depth,
+        k_wrap_cell<<<nblk(N, 256), 256, 0, stream>>>(on_device ? positions : pos_in.as<double>(), N, L, size, depth,
                                                        pos_wrap.as<double>(), leaf_of.as<int>(), counts.as<int>(),
-                                                       slot_of.as<int>());
+                                                       slot_of.as<int>(), on_device ? pos_in.as<double>() : nullptr);
       });
     }
     launch(ST_TREE, [&] { k_scan_single<<<1, 1024, 0, stream>>>(counts.as<int>(), nleaf, leaf_start.as<int>()); });

@@ -25,28 +25,43 @@ __device__ __forceinline__ double np_mod(double a, double b) {
   return m;
 }
 
+// pos_copy (device-resident caller positions): also written to pos_copy,
+// the plan's copy of the raw positions (one pass instead of a memcpy first)
 __global__ void k_wrap_cell(const double* __restrict__ pos_in, int64_t n, double box, double size,
                             int depth, double* __restrict__ pos_wrap, int* __restrict__ leaf_of,
-                            int* __restrict__ counts, int* __restrict__ slot_of) {
+                            int* __restrict__ counts, int* __restrict__ slot_of, double* __restrict__ pos_copy) {
   const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (i >= n) return;
+  const bool ok = i < n;
   const int nside = 1 << depth;
-  int cell[3];
+  int leaf = -1;
+  if (ok) {
+    int cell[3];
 #pragma unroll
-  for (int a = 0; a < 3; ++a) {
-    double w = np_mod(pos_in[3 * i + a], box);
-    if (w >= box) w = 0.0;
-    pos_wrap[3 * i + a] = w;
-    double t = w / size;  // IEEE division, like positions / size
-    long long c = (long long)t;  // astype(int64): truncation
-    c = c < 0 ? 0 : (c > nside - 1 ? nside - 1 : c);
-    cell[a] = (int)c;
+    for (int a = 0; a < 3; ++a) {
+      const double x = pos_in[3 * i + a];
+      if (pos_copy) pos_copy[3 * i + a] = x;
+      double w = np_mod(x, box);
+      if (w >= box) w = 0.0;
+      pos_wrap[3 * i + a] = w;
+      double t = w / size;  // IEEE division, like positions / size
+      long long c = (long long)t;  // astype(int64): truncation
+      c = c < 0 ? 0 : (c > nside - 1 ? nside - 1 : c);
+      cell[a] = (int)c;
+    }
+    leaf = (cell[0] * nside + cell[1]) * nside + cell[2];
+    leaf_of[i] = leaf;
   }
-  const int leaf = (cell[0] * nside + cell[1]) * nside + cell[2];
-  leaf_of[i] = leaf;
   // the counter's old value is the atom's slot in its leaf bucket (bucket
-  // order is arbitrary: k_leaf_rank orders each leaf by the exact key)
-  slot_of[i] = atomicAdd(&counts[leaf], 1);
+  // order is arbitrary: k_leaf_rank orders each leaf by the exact key); one
+  // atomic per distinct leaf of the warp (neighbouring atoms share leaves)
+  const unsigned act = __ballot_sync(0xffffffffu, ok);
+  if (!ok) return;
+  const unsigned peers = __match_any_sync(act, leaf);
+  const int lane = threadIdx.x & 31, leader = __ffs(peers) - 1;
+  int base = 0;
+  if (lane == leader) base = atomicAdd(&counts[leaf], __popc(peers));
+  base = __shfl_sync(peers, base, leader);
+  slot_of[i] = base + __popc(peers & ((1u << lane) - 1u));
 }
 
 // Exclusive scan of one block's values (warp shuffles, then the warp totals).
