@@ -184,7 +184,8 @@ __device__ __forceinline__ void p2p2_leaf(int b, const float4* __restrict__ xq, 
                                           const float4* __restrict__ pair_b, const int* __restrict__ leaf_start,
                                           int depth, float size, int periodic, float* __restrict__ vout,
                                           float* __restrict__ gout, float4* A, float4* B, int2* s_imgw,
-                                          float4* s_shiftw, uint32_t bar, uint32_t& phase) {
+                                          float4* s_shiftw, unsigned char* s_imgof, uint32_t bar,
+                                          uint32_t& phase) {
   const int lane = threadIdx.x & 31;
   const int t0 = leaf_start[b], n = leaf_start[b + 1] - t0;
   if (n == 0) return;
@@ -228,7 +229,8 @@ __device__ __forceinline__ void p2p2_leaf(int b, const float4* __restrict__ xq, 
     const int nt = min(32, n - pb);
     int P = 1;
     while (P < 32 && nt * (2 * P) <= 32) P *= 2;
-    const int W = 32 / P, slot = lane & (W - 1), part = lane / W;
+    const int lp = __ffs(P) - 1;  // P = 2^lp: shifts, not integer divisions
+    const int W = 32 >> lp, slot = lane & (W - 1), part = lane >> (5 - lp);
     const bool act = slot < nt;
     const int ti = t0 + pb + (act ? slot : 0);
     const float4 me = xq[ti];
@@ -267,10 +269,17 @@ __device__ __forceinline__ void p2p2_leaf(int b, const float4* __restrict__ xq, 
         mbar_wait(bar, phase);
         phase ^= 1;
         if (nimg > 1) {
-          int im = 0;
-          for (int q = max(cb, hp) + lane; q < ce; q += 32) {
-            while (q >= s_imgw[im + 1].x) ++im;
-            const float4 sh = s_shiftw[im];
+          // each image lane marks its pairs of the chunk in a byte table,
+          // then every lane shifts its pairs (two dependent shared loads
+          // per pair instead of a per-lane search over the image table)
+          const int qlo = max(cb, hp);
+          if (lane >= 1 && lane < nimg) {
+            const int hi = min(i_off + i_np, ce);
+            for (int q = max(i_off, qlo); q < hi; ++q) s_imgof[q - cb] = (unsigned char)lane;
+          }
+          __syncwarp();
+          for (int q = qlo + lane; q < ce; q += 32) {
+            const float4 sh = s_shiftw[s_imgof[q - cb]];
             float4 av = A[q - cb];
             float4 bv = B[q - cb];
             av.x += sh.x;
@@ -289,7 +298,7 @@ __device__ __forceinline__ void p2p2_leaf(int b, const float4* __restrict__ xq, 
       {
         const int lo = cb, hi = max(lo, min(ce, hp));
         const int np = hi - lo;
-        const int k0 = lo + (np * part) / P, k1 = lo + (np * (part + 1)) / P;
+        const int k0 = lo + ((np * part) >> lp), k1 = lo + ((np * (part + 1)) >> lp);
         uint64_t p2 = 0;
         for (int k = k0; k < k1; ++k)
           p2p2_step<GRAD, true>(A - cb, B - cb, k, x2, y2, z2, self, p2, gx2, gy2, gz2);
@@ -299,7 +308,7 @@ __device__ __forceinline__ void p2p2_leaf(int b, const float4* __restrict__ xq, 
       {
         const int lo = max(cb, hp), hi = max(lo, ce);
         const int np = hi - lo;
-        const int k0 = lo + (np * part) / P, k1 = lo + (np * (part + 1)) / P;
+        const int k0 = lo + ((np * part) >> lp), k1 = lo + ((np * (part + 1)) >> lp);
         const float4* Ab = A - cb;
         const float4* Bb = B - cb;
         // two independent accumulator sets per step pair (ILP); potential
@@ -385,6 +394,7 @@ __global__ void __launch_bounds__(P2P2_WARPS * 32, LFMM_P2P2_MINB) k_p2p2(const 
   __shared__ __align__(8) uint64_t s_bar[P2P2_WARPS];
   __shared__ int2 s_img[P2P2_WARPS][28];  // {first staged pair, pair count}; sentinel at nimg
   __shared__ float4 s_shift[P2P2_WARPS][27];
+  __shared__ unsigned char s_imgof_all[P2P2_WARPS][P2P2_SMAX / 2];  // image of each staged pair (shift pass)
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   const int nleaf = 1 << (3 * depth);
   const int first = x0 << (2 * depth);  // the rank's first leaf plane
@@ -402,7 +412,7 @@ __global__ void __launch_bounds__(P2P2_WARPS * 32, LFMM_P2P2_MINB) k_p2p2(const 
     const int b = first + blockIdx.x * P2P2_WARPS + w;
     if (b >= nleaf || (b >> (2 * depth)) >= x1) return;
     p2p2_leaf<GRAD>(b, xq, pair_a, pair_b, leaf_start, depth, size, periodic, vout, gout, A, B, s_img[w],
-                    s_shift[w], bar, phase);
+                    s_shift[w], s_imgof_all[w], bar, phase);
     return;
   }
   for (;;) {
@@ -411,7 +421,7 @@ __global__ void __launch_bounds__(P2P2_WARPS * 32, LFMM_P2P2_MINB) k_p2p2(const 
     v = __shfl_sync(0xffffffffu, v, 0);
     if (v >= own) break;
     p2p2_leaf<GRAD>(first + v, xq, pair_a, pair_b, leaf_start, depth, size, periodic, vout, gout, A, B, s_img[w],
-                    s_shift[w], bar, phase);
+                    s_shift[w], s_imgof_all[w], bar, phase);
   }
 }
 
