@@ -462,6 +462,22 @@ def run_ours(args):
     ms_e2e = max_over_ranks(sum(t_e2e) / len(t_e2e))
     h2d = n * 3 * 8 + n * 8 + s * 4 * 8 + s * 4
     d2h = 8 + n * 3 * 8 + s * 4 * 8
+    # the PCIe rates of this box for the same pinned buffers (plain copies,
+    # CUDA events): device step + host->device + device->host bytes at
+    # these rates is the serial bound the e2e step is compared with
+    def copy_rate(dst, src, reps=10):
+        dst.copy_(src, non_blocking=True)
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for _ in range(reps):
+            dst.copy_(src, non_blocking=True)
+        e1.record()
+        e1.synchronize()
+        return src.numel() * src.element_size() * reps / (e0.elapsed_time(e1) * 1e-3) / 1e9
+    h2d_gbs = copy_rate(d_pos, h_pos)
+    d2h_gbs = copy_rate(h_f, d_f)
+    e2e_bound = ms_full + h2d / (h2d_gbs * 1e6) + d2h / (d2h_gbs * 1e6)
 
     # per-stage breakdown (separate profiled pass, CUDA events per launch)
     plan.profile(True)
@@ -572,7 +588,9 @@ def run_ours(args):
         "plain_fmm_ms_per_step": round(ms_plain, 4),
         "plan_reuse_ms_per_step": round(ms_reuse, 4),
         "e2e": {"value": round(world * 1000.0 / ms_e2e, 3), "unit": "steps/s", "h2d_bytes_per_step": h2d,
-                "d2h_bytes_per_step": d2h, "ms_per_step": round(ms_e2e, 4)},
+                "d2h_bytes_per_step": d2h, "ms_per_step": round(ms_e2e, 4),
+                "pcie_h2d_gbs": round(h2d_gbs, 1), "pcie_d2h_gbs": round(d2h_gbs, 1),
+                "serial_bound_ms": round(e2e_bound, 4)},
         "gpu_launches": launches,
         "clocks": clk.summary(),
         "roofline": roofline,

@@ -348,6 +348,20 @@ __global__ void __launch_bounds__(EXP_WARPS * 32) k_l2p_c(const vec4_t<T>* __res
 // staged as (2 Re, -2 Im) float2 so each term is one FFMA2 against the
 // (Re R, Im R) pair the recurrence produces (also in packed form); real
 // m = 0 terms stay scalar.  V = vs + acc.x + acc.y.
+// one (l, m > 0) term of k_l2p_f2: potential and, for l <= Q, the gradient
+template <bool GRAD>
+__device__ __forceinline__ void l2p_term(const float4* SC, int c, bool grad_term, uint64_t q, uint64_t& va,
+                                         uint64_t& gxa, uint64_t& gya, uint64_t& gza) {
+  const float4 a = SC[2 * c];
+  va = f2fma(f2pack(a.x, a.y), q, va);
+  if (GRAD && grad_term) {
+    const float4 b = SC[2 * c + 1];
+    gxa = f2fma(f2pack(a.z, a.w), q, gxa);
+    gya = f2fma(f2pack(b.x, b.y), q, gya);
+    gza = f2fma(f2pack(b.z, b.w), q, gza);
+  }
+}
+
 template <bool GRAD, int P>
 __global__ void __launch_bounds__(EXP_WARPS * 32) k_l2p_f2(const float4* __restrict__ xq,
                                                            const int* __restrict__ leaf_start, int depth,
@@ -355,8 +369,12 @@ __global__ void __launch_bounds__(EXP_WARPS * 32) k_l2p_f2(const float4* __restr
                                                            float* __restrict__ vout, float* __restrict__ gout, int x0, int x1) {
   constexpr int Q = P - 1;
   constexpr int NCC = P * (P + 1) / 2, NQC = Q * (Q + 1) / 2;  // complex coefficients (m > 0)
-  __shared__ float s0[EXP_WARPS][4][P + 1];                      // m = 0: L, Gx, Gy, Gz
-  __shared__ float2 sc[EXP_WARPS][NCC + 3 * NQC];                // m > 0: L | Gx | Gy | Gz
+  // coefficients interleaved per term so that one 16-B shared load feeds
+  // two packed FMAs (the term loop was bound by its 8-B loads):
+  //   m = 0, order l:  s0[l] = (L, Gx, Gy, Gz)
+  //   m > 0, term c:   sc[2c] = (L | Gx), sc[2c + 1] = (Gy | Gz) (complex)
+  __shared__ __align__(16) float4 s0[EXP_WARPS][P + 1];
+  __shared__ __align__(16) float4 sc[EXP_WARPS][2 * NCC];
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   const int b = (x0 << (2 * depth)) + blockIdx.x * (blockDim.x >> 5) + w;  // grid from the rank's first leaf plane
   const int nleaf = 1 << (3 * depth);
@@ -375,10 +393,11 @@ __global__ void __launch_bounds__(EXP_WARPS * 32) k_l2p_f2(const float4* __restr
   const float* Lh = sL[w];
   for (int e = lane; e < (P + 1) + NCC; e += 32) {
     if (e <= P) {
-      s0[w][0][e] = Lh[e];
+      s0[w][e].x = Lh[e];
     } else {
       const int a = (P + 1) + 2 * (e - (P + 1));
-      sc[w][e - (P + 1)] = make_float2(2.f * Lh[a], -2.f * Lh[a + 1]);
+      sc[w][2 * (e - (P + 1))].x = 2.f * Lh[a];
+      sc[w][2 * (e - (P + 1))].y = -2.f * Lh[a + 1];
     }
   }
   if (GRAD) {
@@ -403,20 +422,20 @@ __global__ void __launch_bounds__(EXP_WARPS * 32) k_l2p_f2(const float4* __restr
       const float gxr = 0.5f * (ar - br), gxi = 0.5f * (ai - bi);
       const float gyr = -0.5f * (ai + bi), gyi = 0.5f * (ar + br);
       if (e <= Q) {
-        s0[w][1][e] = gxr;
-        s0[w][2][e] = gyr;
-        s0[w][3][e] = cr;
+        s0[w][e].y = gxr;
+        s0[w][e].z = gyr;
+        s0[w][e].w = cr;
       } else {
-        const int c = e - (Q + 1);
-        sc[w][NCC + c] = make_float2(2.f * gxr, -2.f * gxi);
-        sc[w][NCC + NQC + c] = make_float2(2.f * gyr, -2.f * gyi);
-        sc[w][NCC + 2 * NQC + c] = make_float2(2.f * cr, -2.f * ci);
+        const int c = (k - 1) * (P + 1) - (k - 1) * k / 2 + (j - k);  // (j, k) in the order-P term order
+        sc[w][2 * c].z = 2.f * gxr;
+        sc[w][2 * c].w = -2.f * gxi;
+        sc[w][2 * c + 1] = make_float4(2.f * gyr, -2.f * gyi, 2.f * cr, -2.f * ci);
       }
     }
   }
   __syncwarp();
-  const float* S0 = &s0[w][0][0];
-  const uint64_t* SC = reinterpret_cast<const uint64_t*>(&sc[w][0]);
+  const float4* S0 = s0[w];
+  const float4* SC = sc[w];
   const float inv_s = 1.f / size;
   for (int tc = t0; tc < t1; tc += 32) {
     const int i = tc + lane;
@@ -430,17 +449,21 @@ __global__ void __launch_bounds__(EXP_WARPS * 32) k_l2p_f2(const float4* __restr
     // m = 0 column (real)
     {
       float p2 = 1.f, p1 = z;
-      vs = fmaf(S0[0], p2, vs);
-      if (GRAD) {
-        gxs = fmaf(S0[(P + 1) + 0], p2, gxs);
-        gys = fmaf(S0[2 * (P + 1) + 0], p2, gys);
-        gzs = fmaf(S0[3 * (P + 1) + 0], p2, gzs);
-      }
-      vs = fmaf(S0[1], p1, vs);
-      if (GRAD && 1 <= Q) {
-        gxs = fmaf(S0[(P + 1) + 1], p1, gxs);
-        gys = fmaf(S0[2 * (P + 1) + 1], p1, gys);
-        gzs = fmaf(S0[3 * (P + 1) + 1], p1, gzs);
+      {
+        const float4 c0 = S0[0];
+        vs = fmaf(c0.x, p2, vs);
+        if (GRAD) {
+          gxs = fmaf(c0.y, p2, gxs);
+          gys = fmaf(c0.z, p2, gys);
+          gzs = fmaf(c0.w, p2, gzs);
+        }
+        const float4 c1 = S0[1];
+        vs = fmaf(c1.x, p1, vs);
+        if (GRAD && 1 <= Q) {
+          gxs = fmaf(c1.y, p1, gxs);
+          gys = fmaf(c1.z, p1, gys);
+          gzs = fmaf(c1.w, p1, gzs);
+        }
       }
 #pragma unroll
       for (int l = 2; l <= P; ++l) {
@@ -448,17 +471,18 @@ __global__ void __launch_bounds__(EXP_WARPS * 32) k_l2p_f2(const float4* __restr
         const float nv = (float(2 * l - 1) * z * p1 - r2 * p2) * c;
         p2 = p1;
         p1 = nv;
-        vs = fmaf(S0[l], nv, vs);
+        const float4 cl = S0[l];
+        vs = fmaf(cl.x, nv, vs);
         if (GRAD && l <= Q) {
-          gxs = fmaf(S0[(P + 1) + l], nv, gxs);
-          gys = fmaf(S0[2 * (P + 1) + l], nv, gys);
-          gzs = fmaf(S0[3 * (P + 1) + l], nv, gzs);
+          gxs = fmaf(cl.y, nv, gxs);
+          gys = fmaf(cl.z, nv, gys);
+          gzs = fmaf(cl.w, nv, gzs);
         }
       }
     }
     // m > 0 columns (packed complex)
     float mr = 1.f, mi = 0.f;
-    int ci = 0, gi = 0;
+    int ci = 0;
 #pragma unroll
     for (int m = 1; m <= P; ++m) {
       const float c = 1.f / float(2 * m);
@@ -467,23 +491,11 @@ __global__ void __launch_bounds__(EXP_WARPS * 32) k_l2p_f2(const float4* __restr
       mi = ni;
       uint64_t q2 = f2pack(mr, mi);
       uint64_t q1 = f2mul(q2, f2pack(z, z));
-      va = f2fma(SC[ci], q2, va);
-      if (GRAD && m <= Q) {
-        gxa = f2fma(SC[NCC + gi], q2, gxa);
-        gya = f2fma(SC[NCC + NQC + gi], q2, gya);
-        gza = f2fma(SC[NCC + 2 * NQC + gi], q2, gza);
-      }
+      l2p_term<GRAD>(SC, ci, m <= Q, q2, va, gxa, gya, gza);
       ++ci;
-      if (m <= Q) ++gi;
       if (m + 1 <= P) {
-        va = f2fma(SC[ci], q1, va);
-        if (GRAD && m + 1 <= Q) {
-          gxa = f2fma(SC[NCC + gi], q1, gxa);
-          gya = f2fma(SC[NCC + NQC + gi], q1, gya);
-          gza = f2fma(SC[NCC + 2 * NQC + gi], q1, gza);
-        }
+        l2p_term<GRAD>(SC, ci, m + 1 <= Q, q1, va, gxa, gya, gza);
         ++ci;
-        if (m + 1 <= Q) ++gi;
       }
 #pragma unroll
       for (int l = m + 2; l <= P; ++l) {
@@ -492,14 +504,8 @@ __global__ void __launch_bounds__(EXP_WARPS * 32) k_l2p_f2(const float4* __restr
         const uint64_t nq = f2fma(q1, f2pack(a, a), f2mul(q2, f2pack(bcoef, bcoef)));
         q2 = q1;
         q1 = nq;
-        va = f2fma(SC[ci], nq, va);
-        if (GRAD && l <= Q) {
-          gxa = f2fma(SC[NCC + gi], nq, gxa);
-          gya = f2fma(SC[NCC + NQC + gi], nq, gya);
-          gza = f2fma(SC[NCC + 2 * NQC + gi], nq, gza);
-        }
+        l2p_term<GRAD>(SC, ci, l <= Q, nq, va, gxa, gya, gza);
         ++ci;
-        if (l <= Q) ++gi;
       }
     }
     if (act) {
