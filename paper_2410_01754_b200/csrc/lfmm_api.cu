@@ -645,7 +645,8 @@ struct lfmm_plan {
   int64_t stage_launch[ST_COUNT] = {0};
 
   // tree
-  DevBuf pos_in, pos_wrap, leaf_of, slot_of, counts, cursor, leaf_start, bucket, perm, inv_perm, pos_sorted, leaf_sorted, xq;
+  DevBuf scan_status;  // k_scan_lookback block states
+  DevBuf pos_in, key32, leaf_of, slot_of, counts, cursor, leaf_start, bucket, perm, inv_perm, pos_sorted, leaf_sorted, xq;
   // fp32 near-field source pairs (k_p2p2): [pair_cap] float4 x/y halves, then [pair_cap] z/q halves
   DevBuf pairs;
   int64_t pair_cap = 0;
@@ -784,9 +785,9 @@ struct lfmm_plan {
       cudaEventDestroy(e.b);
     }
     for (auto e : free_events) cudaEventDestroy(e);
-    DevBuf* hbufs[] = {&ops16, &hm_inv_r, &hm_inv_c, &hm_jobs, &hm_counter, &p2p_ctl, &hm_level_max, &mult16, &boxq, &site_pot, &ops_m2m_t, &ops_l2l_t, &ops_lat_t, &tr_cnt, &ops_m2l_t, &tt_m2m, &tt_l2l};
+    DevBuf* hbufs[] = {&ops16, &hm_inv_r, &hm_inv_c, &hm_jobs, &hm_counter, &p2p_ctl, &hm_level_max, &mult16, &boxq, &site_pot, &ops_m2m_t, &ops_l2l_t, &ops_lat_t, &tr_cnt, &ops_m2l_t, &tt_m2m, &tt_l2l, &scan_status};
     for (auto* b : hbufs) b->release();
-    DevBuf* bufs[] = {&pos_in, &pos_wrap, &leaf_of, &slot_of, &counts, &cursor, &leaf_start, &bucket, &perm,
+    DevBuf* bufs[] = {&pos_in, &key32, &leaf_of, &slot_of, &counts, &cursor, &leaf_start, &bucket, &perm,
                       &inv_perm, &pos_sorted, &leaf_sorted, &xq, &mult, &loc, &partial, &up_part, &up_cnt, &counters, &ops_m2l, &ops_m2m,
                       &ops_l2l, &ops_lat, &lat64t, &q_in, &qs, &vnear, &vfar, &gnear, &gfar, &part,
                       &scal, &epart, &roots, &out_pot, &out_near, &out_far, &out_dip, &out_forces, &energies,
@@ -1230,11 +1231,22 @@ struct lfmm_plan {
     if (N > 0) {
       launch(ST_TREE, [&] {
         k_wrap_cell<<<nblk(N, 256), 256, 0, stream>>>(on_device ? positions : pos_in.as<double>(), N, L, size, depth,
-                                                       pos_wrap.as<double>(), leaf_of.as<int>(), counts.as<int>(),
-                                                       slot_of.as<int>(), on_device ? pos_in.as<double>() : nullptr);
+                                                       leaf_of.as<int>(), counts.as<int>(),
+                                                       slot_of.as<int>(), on_device ? pos_in.as<double>() : nullptr,
+                                                       key32.as<float>());
       });
     }
-    launch(ST_TREE, [&] { k_scan_single<<<1, 1024, 0, stream>>>(counts.as<int>(), nleaf, leaf_start.as<int>()); });
+    if (nleaf >= SCAN_TILE) {
+      const int sb = (int)((nleaf + SCAN_TILE - 1) / SCAN_TILE);
+      scan_status.ensure(sizeof(unsigned long long) * sb);
+      LFMM_CUDA(cudaMemsetAsync(scan_status.p, 0, sizeof(unsigned long long) * sb, stream));
+      launch(ST_TREE, [&] {
+        k_scan_lookback<<<sb, SCAN_THREADS, 0, stream>>>(counts.as<int>(), nleaf, leaf_start.as<int>(),
+                                                         scan_status.as<unsigned long long>());
+      });
+    } else {
+      launch(ST_TREE, [&] { k_scan_single<<<1, 1024, 0, stream>>>(counts.as<int>(), nleaf, leaf_start.as<int>()); });
+    }
     if (N > 0) {
       launch(ST_TREE, [&] {
         k_scatter_leaf<<<nblk(N, 256), 256, 0, stream>>>(leaf_of.as<int>(), N, leaf_start.as<int>(),
@@ -1242,7 +1254,7 @@ struct lfmm_plan {
       });
       launch(ST_TREE, [&] {
         k_leaf_rank<T><<<nblk((int64_t)nleaf * 32, RANK_WARPS * 32), RANK_WARPS * 32, 0, stream>>>(
-            pos_wrap.as<double>(), leaf_start.as<int>(), bucket.as<int>(), nleaf, perm.as<int>(), inv_perm.as<int>(),
+            pos_in.as<double>(), L, key32.as<float>(), leaf_start.as<int>(), bucket.as<int>(), nleaf, perm.as<int>(), inv_perm.as<int>(),
             depth, size, pos_sorted.as<double>(), xq.as<vec4_t<T>>(), leaf_sorted.as<int>(), pair_a(), pair_b());
       });
     }
@@ -1986,7 +1998,7 @@ int lfmm_plan_create(const double* positions, int64_t n, double box_length, int 
     const size_t t = pl->tsz();
     const int64_t nn = std::max<int64_t>(n, 1);
     pl->pos_in.ensure(sizeof(double) * 3 * nn);
-    pl->pos_wrap.ensure(sizeof(double) * 3 * nn);
+    pl->key32.ensure(sizeof(float) * nn);
     pl->leaf_of.ensure(sizeof(int) * nn);
     pl->slot_of.ensure(sizeof(int) * nn);
     pl->counts.ensure(sizeof(int) * pl->nleaf);
@@ -2708,7 +2720,7 @@ int lfmm_plan_set_count(lfmm_plan* plan, int64_t n) {
     const int64_t nn = std::max<int64_t>(n, 1);
     const size_t t = plan->tsz();
     plan->pos_in.ensure(sizeof(double) * 3 * nn);
-    plan->pos_wrap.ensure(sizeof(double) * 3 * nn);
+    plan->key32.ensure(sizeof(float) * nn);
     plan->leaf_of.ensure(sizeof(int) * nn);
     plan->slot_of.ensure(sizeof(int) * nn);
     plan->bucket.ensure(sizeof(int) * nn);

@@ -25,11 +25,37 @@ __device__ __forceinline__ double np_mod(double a, double b) {
   return m;
 }
 
+// wrap_positions (system.py:103-108): np.mod(x, L), then x >= L -> 0.  The
+// common case 0 <= x < L is fmod's identity (and +0.0 for either zero).
+__device__ __forceinline__ double wrap_coord(double x, double box) {
+  const double w = (x >= 0.0 && x < box) ? x + 0.0 : np_mod(x, box);
+  return w >= box ? 0.0 : w;
+}
+// all three coordinates, the in-box case without any fmod code on its path
+__device__ __forceinline__ void wrap_xyz(const double* p, double box, double& x, double& y, double& z) {
+  x = p[0];
+  y = p[1];
+  z = p[2];
+  if (x >= 0.0 && x < box && y >= 0.0 && y < box && z >= 0.0 && z < box) {
+    x += 0.0;
+    y += 0.0;
+    z += 0.0;
+  } else {
+    x = wrap_coord(x, box);
+    y = wrap_coord(y, box);
+    z = wrap_coord(z, box);
+  }
+}
+
+// The wrapped coordinates are not stored (one 24 MB write less per
+// rebuild): k_leaf_rank recomputes them from the raw positions (wrap_coord);
+// only the wrapped x rounded to fp32, its fast-path sort key, is kept.
 // pos_copy (device-resident caller positions): also written to pos_copy,
 // the plan's copy of the raw positions (one pass instead of a memcpy first)
 __global__ void k_wrap_cell(const double* __restrict__ pos_in, int64_t n, double box, double size,
-                            int depth, double* __restrict__ pos_wrap, int* __restrict__ leaf_of,
-                            int* __restrict__ counts, int* __restrict__ slot_of, double* __restrict__ pos_copy) {
+                            int depth, int* __restrict__ leaf_of,
+                            int* __restrict__ counts, int* __restrict__ slot_of, double* __restrict__ pos_copy,
+                            float* __restrict__ key32) {
   const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   const bool ok = i < n;
   const int nside = 1 << depth;
@@ -40,9 +66,8 @@ __global__ void k_wrap_cell(const double* __restrict__ pos_in, int64_t n, double
     for (int a = 0; a < 3; ++a) {
       const double x = pos_in[3 * i + a];
       if (pos_copy) pos_copy[3 * i + a] = x;
-      double w = np_mod(x, box);
-      if (w >= box) w = 0.0;
-      pos_wrap[3 * i + a] = w;
+      const double w = wrap_coord(x, box);
+      if (a == 0) key32[i] = (float)w;  // k_leaf_rank's fast-path sort key
       double t = w / size;  // IEEE division, like positions / size
       long long c = (long long)t;  // astype(int64): truncation
       c = c < 0 ? 0 : (c > nside - 1 ? nside - 1 : c);
@@ -140,6 +165,65 @@ __global__ void __launch_bounds__(1024) k_scan_single(const int* __restrict__ co
   if (threadIdx.x == 0) start[n] = carry;
 }
 
+// Multi-block exclusive scan with decoupled look-back: block b scans 4096
+// counts (8 per thread, two int4), publishes its aggregate, then takes the
+// prefix of the blocks before it from their published aggregates / inclusive
+// prefixes (status zeroed before the launch; the grid is at most a few dozen
+// blocks, all resident, so the waits cannot starve).  Same result as
+// k_scan_single (integer sums), one launch of n / 4096 blocks.
+constexpr int SCAN_THREADS = 512, SCAN_TILE = 8 * SCAN_THREADS;
+__global__ void __launch_bounds__(SCAN_THREADS) k_scan_lookback(const int* __restrict__ counts, int n,
+                                                                int* __restrict__ start,
+                                                                unsigned long long* __restrict__ status) {
+  __shared__ int wt[32];
+  __shared__ int s_prefix;
+  const int b = blockIdx.x;
+  const int i0 = b * SCAN_TILE + 8 * threadIdx.x;
+  int4 a = make_int4(0, 0, 0, 0), c = make_int4(0, 0, 0, 0);
+  if (i0 < n) {
+    a = reinterpret_cast<const int4*>(counts + i0)[0];
+    c = reinterpret_cast<const int4*>(counts + i0)[1];
+  }
+  const int sum = a.x + a.y + a.z + a.w + c.x + c.y + c.z + c.w;
+  int total;
+  const int ex = block_scan_excl(sum, wt, total);
+  if (threadIdx.x == 0) {
+    volatile unsigned long long* st = status;
+    int prefix = 0;
+    if (b == 0) {
+      st[0] = (2ull << 32) | (unsigned)total;
+    } else {
+      st[b] = (1ull << 32) | (unsigned)total;
+      for (int j = b - 1; j >= 0; --j) {
+        unsigned long long v;
+        do {
+          v = st[j];
+        } while ((v >> 32) == 0);
+        prefix += (int)(unsigned)v;
+        if ((v >> 32) == 2) break;
+      }
+      __threadfence();
+      st[b] = (2ull << 32) | (unsigned)(prefix + total);
+    }
+    s_prefix = prefix;
+    if (b == gridDim.x - 1) start[n] = prefix + total;
+  }
+  __syncthreads();
+  if (i0 < n) {
+    int4 oa, ob;
+    oa.x = s_prefix + ex;
+    oa.y = oa.x + a.x;
+    oa.z = oa.y + a.y;
+    oa.w = oa.z + a.z;
+    ob.x = oa.w + a.w;
+    ob.y = ob.x + c.x;
+    ob.z = ob.y + c.y;
+    ob.w = ob.z + c.z;
+    reinterpret_cast<int4*>(start + i0)[0] = oa;
+    reinterpret_cast<int4*>(start + i0)[1] = ob;
+  }
+}
+
 __global__ void k_scatter_leaf(const int* __restrict__ leaf_of, int64_t n, const int* __restrict__ start,
                                const int* __restrict__ slot_of, int* __restrict__ bucket) {
   const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
@@ -166,7 +250,8 @@ __device__ __forceinline__ bool key_less(double ax, double ay, double az, int ai
 // size (octree.py:65-66) in T, leaf index), which it holds in registers.
 constexpr int RANK_WARPS = 4;
 template <class T>
-__global__ void __launch_bounds__(RANK_WARPS * 32) k_leaf_rank(const double* __restrict__ pos_wrap,
+__global__ void __launch_bounds__(RANK_WARPS * 32) k_leaf_rank(const double* __restrict__ pos, double box,
+                                                              const float* __restrict__ key32,
                                                               const int* __restrict__ start,
                                                               const int* __restrict__ bucket, int nleaf,
                                                               int* __restrict__ perm, int* __restrict__ inv_perm,
@@ -186,16 +271,14 @@ __global__ void __launch_bounds__(RANK_WARPS * 32) k_leaf_rank(const double* __r
     double x = 0, y = 0, z = 0;
     if (e < s1) {
       i = bucket[e];
-      x = pos_wrap[3 * i];
-      y = pos_wrap[3 * i + 1];
-      z = pos_wrap[3 * i + 2];
+      wrap_xyz(pos + 3 * (size_t)i, box, x, y, z);
     }
     const float x32 = (float)x;
     int rank = 0, eq = 0;
     for (int f0 = s0; f0 < s1; f0 += 32) {
       const int f = f0 + lane;
       __syncwarp();
-      kx[wl][lane] = f < s1 ? (float)pos_wrap[3 * bucket[f]] : 0.f;
+      kx[wl][lane] = f < s1 ? key32[bucket[f]] : 0.f;
       __syncwarp();
       const int cnt = min(32, s1 - f0);
       for (int k = 0; k < cnt; ++k) {
@@ -212,9 +295,7 @@ __global__ void __launch_bounds__(RANK_WARPS * 32) k_leaf_rank(const double* __r
         double xf = 0, yf = 0, zf = 0;
         if (f < s1) {
           jf = bucket[f];
-          xf = pos_wrap[3 * jf];
-          yf = pos_wrap[3 * jf + 1];
-          zf = pos_wrap[3 * jf + 2];
+          wrap_xyz(pos + 3 * (size_t)jf, box, xf, yf, zf);
         }
         const int cnt = min(32, s1 - f0);
         for (int k = 0; k < cnt; ++k) {
