@@ -1865,12 +1865,15 @@ void gather_site_positions(lfmm_plan* pl, const double* site_positions, int on_d
   }
 }
 
-void run_scale(lfmm_plan* pl, const double* q_dev, double* out_dev) {
-  pl->launch(ST_SCALE, [&] { k_scale_charges<<<nblk(pl->N, 256), 256, 0, pl->stream>>>(q_dev, pl->N, out_dev); });
+void blend_sites(lfmm_plan* pl, double* out_dev) {
   if (pl->n_sites == 0) return;
   HiArgs g{};
   hi_args(pl, g);
   pl->launch(ST_SCALE, [&] { k_blend_sites<<<(unsigned)pl->n_sites, 32, 0, pl->stream>>>(g, out_dev); });
+}
+void run_scale(lfmm_plan* pl, const double* q_dev, double* out_dev) {
+  pl->launch(ST_SCALE, [&] { k_scale_charges<<<nblk(pl->N, 256), 256, 0, pl->stream>>>(q_dev, pl->N, out_dev); });
+  blend_sites(pl, out_dev);
 }
 
 }  // namespace
@@ -2445,11 +2448,11 @@ void step_body(lfmm_plan* plan, const double* positions, const double* charges, 
   {
     const int64_t N = plan->N;
     LFMM_REQUIRE(mode == LFMM_MODE_HI || mode == LFMM_MODE_QI, "unknown mode");
-    // device-resident inputs: charges, scale_charges and the HI side work are
-    // issued before the tree build, so the HI kernels (site geometry, lambdas
-    // and blended site charges only) overlap the latency-bound tree kernels;
-    // host inputs keep the positions upload first (the charges upload hides
-    // the tree build)
+    // device-resident inputs: the lambdas and the HI side work are issued
+    // before the tree build, so the HI kernels (site geometry and lambdas
+    // only) overlap the latency-bound tree kernels, and the charges (copy +
+    // site blend) follow the tree; host inputs keep the positions upload
+    // first (the charges upload hides the tree build)
     const bool early = io_on_device && positions && !plain && plan->n_sites > 0 && !plan->profiling &&
                        potentials == nullptr;
     auto tree = [&] {
@@ -2460,7 +2463,6 @@ void step_body(lfmm_plan* plan, const double* positions, const double* charges, 
     };
     if (positions && !early) tree();
     plan->ensure_solve_buffers(1, true);
-    plan->q_tmp.ensure(sizeof(double) * std::max<int64_t>(N, 1));
     const auto kind = io_on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice;
     const bool overlap = !io_on_device;
     if (overlap && !plan->io_stream) {
@@ -2468,19 +2470,22 @@ void step_body(lfmm_plan* plan, const double* positions, const double* charges, 
       LFMM_CUDA(cudaEventCreateWithFlags(&plan->ev_q, cudaEventDisableTiming));
       LFMM_CUDA(cudaEventCreateWithFlags(&plan->ev_f, cudaEventDisableTiming));
     }
-    double* qdst = (plain || plan->n_sites == 0) ? plan->q_in.as<double>() : plan->q_tmp.as<double>();
-    if (overlap) {
-      // the charges upload overlaps the tree build
-      LFMM_CUDA(cudaMemcpyAsync(qdst, charges, sizeof(double) * N, kind, plan->io_stream));
-      LFMM_CUDA(cudaEventRecord(plan->ev_q, plan->io_stream));
-      LFMM_CUDA(cudaStreamWaitEvent(plan->stream, plan->ev_q, 0));
-    } else {
-      LFMM_CUDA(cudaMemcpyAsync(qdst, charges, sizeof(double) * N, kind, plan->stream));
-    }
-    if (!(plain || plan->n_sites == 0)) {
-      upload_lambdas(plan, lambdas, n_lambda, io_on_device);
-      run_scale(plan, plan->q_tmp.as<double>(), plan->q_in.as<double>());
-    }
+    const bool blend_q = !(plain || plan->n_sites == 0);
+    // scale_charges (system.py:179-197) = the charges copied into q_in, then
+    // the site atoms' entries blended over their forms (k_blend_sites)
+    auto charges_in = [&] {
+      if (overlap) {
+        // the charges upload overlaps the tree build
+        LFMM_CUDA(cudaMemcpyAsync(plan->q_in.p, charges, sizeof(double) * N, kind, plan->io_stream));
+        LFMM_CUDA(cudaEventRecord(plan->ev_q, plan->io_stream));
+        LFMM_CUDA(cudaStreamWaitEvent(plan->stream, plan->ev_q, 0));
+      } else {
+        LFMM_CUDA(cudaMemcpyAsync(plan->q_in.p, charges, sizeof(double) * N, kind, plan->stream));
+      }
+      if (blend_q) blend_sites(plan, plan->q_in.as<double>());
+    };
+    if (blend_q) upload_lambdas(plan, lambdas, n_lambda, io_on_device);
+    if (!early) charges_in();
     // HI corrections depend on the site geometry and lambdas only: they run
     // beside the solve (unless profiling, which wants serial stage times)
     const bool hi_side = !plain && plan->n_sites > 0 && !plan->profiling && potentials == nullptr;
@@ -2514,7 +2519,10 @@ void step_body(lfmm_plan* plan, const double* positions, const double* charges, 
       plan->stream = main;
       LFMM_CUDA(cudaEventRecord(plan->ev_hi_out, plan->hi_stream));
     }
-    if (early) tree();
+    if (early) {  // device inputs: the HI side stream is already running; charges after the tree
+      tree();
+      charges_in();
+    }
     plan->step_mode = potentials == nullptr;
     plan->near_after_hi = hi_side && !early;
     plan->run_solve(1, true);
