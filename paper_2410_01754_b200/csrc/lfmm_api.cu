@@ -624,6 +624,8 @@ struct lfmm_plan {
   // io_stream beside the tree build / HI work of `stream`
   cudaStream_t io_stream = nullptr;
   cudaEvent_t ev_q = nullptr, ev_f = nullptr;
+  static constexpr int kPosChunks = 4;          // host positions upload in chunks (build_tree)
+  cudaEvent_t ev_pos[kPosChunks + 1] = {};     // [0]: main stream ready, [1..]: chunk c landed
   // P2P runs on near_stream (lower priority) beside the far-field chain on
   // `stream`: the latency-bound translation / tree / HI kernels of the chain
   // leave SMs the near field fills.  Serialised when profiling.
@@ -804,6 +806,8 @@ struct lfmm_plan {
     if (ev_near_in) cudaEventDestroy(ev_near_in);
     if (ev_near_out) cudaEventDestroy(ev_near_out);
     if (ev_q) cudaEventDestroy(ev_q);
+    for (auto e : ev_pos)
+      if (e) cudaEventDestroy(e);
     if (ev_m2l_done) cudaEventDestroy(ev_m2l_done);
     if (step_graph.exec) cudaGraphExecDestroy(step_graph.exec);
     if (ev_f) cudaEventDestroy(ev_f);
@@ -1225,10 +1229,32 @@ struct lfmm_plan {
   // ----------------------------------------------------------- tree ----
   template <class T>
   void build_tree(const double* positions, bool on_device) {
-    if (!on_device)
+    // host positions of a large system: uploaded in kPosChunks pieces on the
+    // io stream, each piece wrapped and counted as soon as it lands (the
+    // counting pass hides behind the rest of the upload)
+    const bool chunked = !on_device && N >= (1 << 18) && !profiling;
+    if (!on_device && !chunked)
       LFMM_CUDA(cudaMemcpyAsync(pos_in.p, positions, sizeof(double) * 3 * N, cudaMemcpyHostToDevice, stream));
     LFMM_CUDA(cudaMemsetAsync(counts.p, 0, sizeof(int) * nleaf, stream));
-    if (N > 0) {
+    if (chunked) {
+      if (!io_stream) LFMM_CUDA(cudaStreamCreateWithFlags(&io_stream, cudaStreamNonBlocking));
+      for (auto& e : ev_pos)
+        if (!e) LFMM_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+      LFMM_CUDA(cudaEventRecord(ev_pos[0], stream));  // pos_in no longer read by earlier work
+      LFMM_CUDA(cudaStreamWaitEvent(io_stream, ev_pos[0], 0));
+      for (int c = 0; c < kPosChunks; ++c) {
+        const int64_t i0 = N * c / kPosChunks, i1 = N * (c + 1) / kPosChunks;
+        LFMM_CUDA(cudaMemcpyAsync(pos_in.as<double>() + 3 * i0, positions + 3 * i0, sizeof(double) * 3 * (i1 - i0),
+                                  cudaMemcpyHostToDevice, io_stream));
+        LFMM_CUDA(cudaEventRecord(ev_pos[c + 1], io_stream));
+        LFMM_CUDA(cudaStreamWaitEvent(stream, ev_pos[c + 1], 0));
+        launch(ST_TREE, [&] {
+          k_wrap_cell<<<nblk(i1 - i0, 256), 256, 0, stream>>>(pos_in.as<double>() + 3 * i0, i1 - i0, L, size, depth,
+                                                               leaf_of.as<int>() + i0, counts.as<int>(),
+                                                               slot_of.as<int>() + i0, nullptr, key32.as<float>() + i0);
+        });
+      }
+    } else if (N > 0) {
       launch(ST_TREE, [&] {
         k_wrap_cell<<<nblk(N, 256), 256, 0, stream>>>(on_device ? positions : pos_in.as<double>(), N, L, size, depth,
                                                        leaf_of.as<int>(), counts.as<int>(),
@@ -2465,10 +2491,10 @@ void step_body(lfmm_plan* plan, const double* positions, const double* charges, 
     plan->ensure_solve_buffers(1, true);
     const auto kind = io_on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice;
     const bool overlap = !io_on_device;
-    if (overlap && !plan->io_stream) {
-      LFMM_CUDA(cudaStreamCreateWithFlags(&plan->io_stream, cudaStreamNonBlocking));
-      LFMM_CUDA(cudaEventCreateWithFlags(&plan->ev_q, cudaEventDisableTiming));
-      LFMM_CUDA(cudaEventCreateWithFlags(&plan->ev_f, cudaEventDisableTiming));
+    if (overlap) {
+      if (!plan->io_stream) LFMM_CUDA(cudaStreamCreateWithFlags(&plan->io_stream, cudaStreamNonBlocking));
+      if (!plan->ev_q) LFMM_CUDA(cudaEventCreateWithFlags(&plan->ev_q, cudaEventDisableTiming));
+      if (!plan->ev_f) LFMM_CUDA(cudaEventCreateWithFlags(&plan->ev_f, cudaEventDisableTiming));
     }
     const bool blend_q = !(plain || plan->n_sites == 0);
     // scale_charges (system.py:179-197) = the charges copied into q_in, then
