@@ -166,6 +166,14 @@ inline void tt_launch(const TrArgs& ta, int ncols_total, const void* img, cudaSt
 // the SMs were configured for the whole shared-memory carveout by the kernels
 // running when the near field lands on them (a resident persistent CTA keeps
 // the SM from being reconfigured): P2M, charge staging, near field.
+// parent levels <= TT_CHAIN_TOP (<= 64 parents) in one k_translate_tc_chain
+// launch: 8 octants x 4 tiles of 16 columns
+constexpr int TT_CHAIN_TOP = 2;
+inline void tt_chain_launch(const TtChain& ch, const void* img, cudaStream_t st) {
+  LFMM_CUDA(cudaMemsetAsync(ch.bar, 0, sizeof(unsigned), st));
+  k_translate_tc_chain<16, 2><<<8 * 4, TT_THREADS, tt_smem_bytes<16, 2>(), st>>>(
+      ch, static_cast<const unsigned char*>(img));
+}
 inline void tt_set_attrs() {
   LFMM_CUDA(cudaFuncSetAttribute(k_translate_tc<64, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  (int)tt_smem_bytes<64, 2>()));
@@ -173,6 +181,9 @@ inline void tt_set_attrs() {
                                  (int)tt_smem_bytes<16, 2>()));
   LFMM_CUDA(cudaFuncSetAttribute(k_translate_tc<64, 2>, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
   LFMM_CUDA(cudaFuncSetAttribute(k_translate_tc<16, 2>, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
+  LFMM_CUDA(cudaFuncSetAttribute(k_translate_tc_chain<16, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)tt_smem_bytes<16, 2>()));
+  LFMM_CUDA(cudaFuncSetAttribute(k_translate_tc_chain<16, 2>, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
   LFMM_CUDA(cudaFuncSetAttribute(k_p2m_c<float, 10>, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
   LFMM_CUDA(cudaFuncSetAttribute(k_stage_q<float>, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
   LFMM_CUDA(cudaFuncSetAttribute(k_p2p2<true>, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
@@ -702,6 +713,7 @@ struct lfmm_plan {
   bool use_tt = false;                  // ... fp32 on k_translate_tc (tensor cores)
   bool tt_simt = false;                 // LFMM_TRANSLATE=simt: fp32 on k_translate
   DevBuf tt_m2m, tt_l2l;                // k_translate_tc operator images
+  DevBuf tt_bar;                        // k_translate_tc_chain grid-barrier counter
   DevBuf q_in, qs, vnear, vfar, gnear, gfar, part, scal, epart, roots;
   DevBuf out_pot, out_near, out_far, out_dip, out_forces, energies, dvec, qtot;
   int64_t last_k = 0;
@@ -787,7 +799,7 @@ struct lfmm_plan {
       cudaEventDestroy(e.b);
     }
     for (auto e : free_events) cudaEventDestroy(e);
-    DevBuf* hbufs[] = {&ops16, &hm_inv_r, &hm_inv_c, &hm_jobs, &hm_counter, &p2p_ctl, &hm_level_max, &mult16, &boxq, &site_pot, &ops_m2m_t, &ops_l2l_t, &ops_lat_t, &tr_cnt, &ops_m2l_t, &tt_m2m, &tt_l2l, &scan_status};
+    DevBuf* hbufs[] = {&ops16, &hm_inv_r, &hm_inv_c, &hm_jobs, &hm_counter, &p2p_ctl, &hm_level_max, &mult16, &boxq, &site_pot, &ops_m2m_t, &ops_l2l_t, &ops_lat_t, &tr_cnt, &ops_m2l_t, &tt_m2m, &tt_l2l, &scan_status, &tt_bar};
     for (auto* b : hbufs) b->release();
     DevBuf* bufs[] = {&pos_in, &key32, &leaf_of, &slot_of, &counts, &cursor, &leaf_start, &bucket, &perm,
                       &inv_perm, &pos_sorted, &leaf_sorted, &xq, &mult, &loc, &partial, &up_part, &up_cnt, &counters, &ops_m2l, &ops_m2m,
@@ -1022,6 +1034,7 @@ struct lfmm_plan {
         launch(ST_SETUP, [&] {
           k_tt_ops<<<nblk(8 * 128 * 128, 256), 256, 0, stream>>>(ops_l2l.as<float>(), tt_l2l.as<unsigned char>());
         });
+        tt_bar.ensure(sizeof(unsigned) * 4);
         tt_set_attrs();
       }
     }
@@ -1430,7 +1443,31 @@ struct lfmm_plan {
           own_x0);
     });
     {
-    for (int l = depth - 1; l >= (dist_phase == 1 ? dist_lg : 0); --l) m2m_level(l);
+    {
+      // single rank on the tensor cores: the small parent levels in one launch
+      const bool chain = use_tt && dist_phase == 0 && dist_lg == 0 && sizeof(T) == 4;
+      const int lo = dist_phase == 1 ? dist_lg : 0;
+      for (int l = depth - 1; l >= lo; --l) {
+        if (chain && l <= TT_CHAIN_TOP) {
+          TtChain ch{};
+          for (int k = l; k >= 0; --k) {
+            TrArgs& ta = ch.lev[ch.nlev++];
+            ta.mode = 0;
+            ta.level = k;
+            ta.ncp = ncp;
+            ta.src = M + level_off[k + 1] * ncp;
+            ta.dst = M + level_off[k] * ncp;
+            ta.slots = up_part.p;
+            ta.cnt = tr_cnt.as<int>();
+            owned_parents(k, ta.p0, ta.pend);
+          }
+          ch.bar = tt_bar.as<unsigned>();
+          launch(ST_M2M, [&] { tt_chain_launch(ch, tt_m2m.p, stream); });
+          break;
+        }
+        m2m_level(l);
+      }
+    }
     launch(ST_M2M, [&] {
       k_box_charges<T><<<nblk(nleaf, 256), 256, 0, stream>>>(qs.as<double>(), leaf_start.as<int>(), depth,
                                                              level_off[depth], ncp, M, boxq.as<double>(),
@@ -1556,7 +1593,26 @@ struct lfmm_plan {
           launch(ST_DOWN, [&] { k_gemm_gather<T><<<grid, G_THREADS, 0, stream>>>(ga); });
         }
       }
-      for (int l = 1; l <= depth; ++l) {
+      const bool chain_dn = use_tt && dist_phase == 0 && dist_lg == 0 && sizeof(T) == 4;
+      int l_first = 1;
+      if (chain_dn) {  // child levels 1 .. TT_CHAIN_TOP + 1 in one launch
+        TtChain ch{};
+        for (int l = 1; l <= std::min(depth, TT_CHAIN_TOP + 1); ++l) {
+          TrArgs& ta = ch.lev[ch.nlev++];
+          ta.mode = 1;
+          ta.level = l;
+          ta.ncp = ncp;
+          ta.src = Lc + level_off[l - 1] * ncp;
+          ta.dst = Lc + level_off[l] * ncp;
+          ta.partial = static_cast<const char*>(partial.p) + tsz() * (size_t)part_off[l] * ncp;
+          ta.nsplit = nsplit[l];
+          owned_parents(l - 1, ta.p0, ta.pend);
+          l_first = l + 1;
+        }
+        ch.bar = tt_bar.as<unsigned>();
+        launch(ST_L2L, [&] { tt_chain_launch(ch, tt_l2l.p, stream); });
+      }
+      for (int l = l_first; l <= depth; ++l) {
         if (use_tr) {
           TrArgs ta{};
           ta.mode = 1;

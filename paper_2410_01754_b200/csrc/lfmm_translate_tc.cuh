@@ -98,24 +98,66 @@ __global__ void k_tt_ops(const float* __restrict__ ops, unsigned char* __restric
   *reinterpret_cast<float*>(base + TT_APLANE + tt_off(r, k & 31)) = lo;
 }
 
+// Per-CTA state of the translation kernels (barriers, TMEM, tables).
 template <int TN, int NSTG>
-__global__ void __launch_bounds__(TT_THREADS) k_translate_tc(TrArgs g, const unsigned char* __restrict__ img) {
-  static_assert(TN % 16 == 0 && TN >= 16 && TN <= 64, "MMA N");
+struct TtCta {
+  uint64_t a_full[NSTG], mma_done[NSTG];
+  uint32_t tmem_sh;
+  int col_src[TN], col_dst[TN];
+  int last;
+};
+
+template <int TN, int NSTG>
+__device__ __forceinline__ uint32_t tt_cta_init(TtCta<TN, NSTG>& st) {
+  constexpr uint32_t TCOLS = TN < 32 ? 32 : TN;
+  const int tid = threadIdx.x, warp = tid >> 5;
+  if (tid == 0) {
+    for (int s = 0; s < NSTG; ++s) {
+      mbar_init(smem_u32(&st.a_full[s]), 2);
+      mbar_init(smem_u32(&st.mma_done[s]), 1);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(&st.tmem_sh)),
+                 "r"(TCOLS));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  return st.tmem_sh;
+}
+template <int TN, int NSTG>
+__device__ __forceinline__ void tt_cta_exit(uint32_t tmem) {
+  constexpr uint32_t TCOLS = TN < 32 ? 32 : TN;
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  if ((threadIdx.x >> 5) == 0)
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(TCOLS));
+}
+
+// One (column tile, octant) of one level.  Every call runs all TT_NCH
+// chunks, so each barrier completes an even number of phases per call and
+// the parity arithmetic below holds for any number of calls per CTA.
+template <int TN, int NSTG>
+__device__ __forceinline__ void tt_tile(const TrArgs& g, const unsigned char* __restrict__ img, int tile, int o,
+                                        unsigned char* sm, uint32_t sbase, uint32_t tmem, TtCta<TN, NSTG>& st) {
   constexpr int BPLANE = TN * TT_KC * 4;        // one B chunk, one plane
   constexpr int STAGE = TT_ACHUNK + 2 * BPLANE;  // A hi | A lo | B hi | B lo
   constexpr int PPT = TN * 8 / TT_THREADS;      // 16-B B pieces per thread per chunk
-  constexpr uint32_t TCOLS = TN < 32 ? 32 : TN;
-  extern __shared__ __align__(16) unsigned char tt_raw[];
-  __shared__ __align__(8) uint64_t a_full[NSTG], mma_done[NSTG];
-  __shared__ uint32_t tmem_sh;
-  __shared__ int col_src[TN], col_dst[TN];
-  __shared__ int last;
-  const uint32_t sbase = (smem_u32(tt_raw) + 1023u) & ~1023u;
-  unsigned char* sm = tt_raw + (sbase - smem_u32(tt_raw));
+  uint64_t* a_full = st.a_full;
+  uint64_t* mma_done = st.mma_done;
+  int* col_src = st.col_src;
+  int* col_dst = st.col_dst;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int o = blockIdx.y, tile = blockIdx.x;
+  (void)lane;
   const int pl = g.mode == 0 ? g.level : g.level - 1;  // parent level
   const int np = 1 << (3 * pl), pn = 1 << pl, cn = 2 * pn;
+  // the previous call's epilogue is done with the tables, the stages and
+  // (its TMEM loads ordered before this call's MMAs) the accumulator
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
   if (tid < TN) {
     const int p = g.p0 + tile * TN + tid;
     int s = -1, d = -1;
@@ -128,22 +170,7 @@ __global__ void __launch_bounds__(TT_THREADS) k_translate_tc(TrArgs g, const uns
     col_src[tid] = s;
     col_dst[tid] = d;
   }
-  if (tid == 0) {
-    for (int s = 0; s < NSTG; ++s) {
-      mbar_init(smem_u32(&a_full[s]), 2);
-      mbar_init(smem_u32(&mma_done[s]), 1);
-    }
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-  }
-  if (warp == 0) {
-    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(&tmem_sh)),
-                 "r"(TCOLS));
-    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
-  }
-  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
   __syncthreads();
-  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-  const uint32_t tmem = tmem_sh;
   const unsigned char* opimg = img + (size_t)o * TT_OPBYTES;
   auto load_a = [&](int c) {
     const int s = c % NSTG;
@@ -153,7 +180,8 @@ __global__ void __launch_bounds__(TT_THREADS) k_translate_tc(TrArgs g, const uns
   };
   if (tid == 0)
     for (int c = 0; c < NSTG && c < TT_NCH; ++c) load_a(c);
-  // every B piece of the tile in flight at once: piece e -> column
+  // every B piece of the tile in flight at once (L2 loads: in the chained
+  // small levels the sources were written earlier in the same launch): piece e -> column
   // n = 8 (e / 64) + e % 8, k quad (e / 8) % 8 (8 lanes fill one 128-B core
   // matrix row group: conflict-free stores)
   const float* src = reinterpret_cast<const float*>(g.src);
@@ -164,7 +192,7 @@ __global__ void __launch_bounds__(TT_THREADS) k_translate_tc(TrArgs g, const uns
     const int sb = col_src[n];
 #pragma unroll
     for (int c = 0; c < TT_NCH; ++c)
-      raw[c][i] = sb >= 0 ? __ldg(reinterpret_cast<const float4*>(src + (size_t)sb * 128 + c * TT_KC + kq * 4))
+      raw[c][i] = sb >= 0 ? __ldcg(reinterpret_cast<const float4*>(src + (size_t)sb * 128 + c * TT_KC + kq * 4))
                           : make_float4(0.f, 0.f, 0.f, 0.f);
   }
   const uint32_t idesc = (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(TN >> 3) << 17) | ((uint32_t)(128 >> 4) << 24);
@@ -275,9 +303,9 @@ __global__ void __launch_bounds__(TT_THREADS) k_translate_tc(TrArgs g, const uns
     }
     __threadfence();
     __syncthreads();
-    if (tid == 0) last = (atomicAdd(&g.cnt[tile], 1) == 7);
+    if (tid == 0) st.last = (atomicAdd(&g.cnt[tile], 1) == 7);
     __syncthreads();
-    if (last) {
+    if (st.last) {
       __threadfence();
       add_slots(nullptr, slots, (size_t)np * 128, 8, reinterpret_cast<float*>(g.dst));
       if (tid == 0) g.cnt[tile] = 0;
@@ -297,9 +325,57 @@ __global__ void __launch_bounds__(TT_THREADS) k_translate_tc(TrArgs g, const uns
       }
     }
   }
-  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
-  __syncthreads();
-  if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(TCOLS));
+}
+
+template <int TN, int NSTG>
+__global__ void __launch_bounds__(TT_THREADS) k_translate_tc(TrArgs g, const unsigned char* __restrict__ img) {
+  static_assert(TN % 16 == 0 && TN >= 16 && TN <= 64, "MMA N");
+  extern __shared__ __align__(16) unsigned char tt_raw[];
+  __shared__ __align__(8) TtCta<TN, NSTG> st;
+  const uint32_t sbase = (smem_u32(tt_raw) + 1023u) & ~1023u;
+  unsigned char* sm = tt_raw + (sbase - smem_u32(tt_raw));
+  const uint32_t tmem = tt_cta_init<TN, NSTG>(st);
+  tt_tile<TN, NSTG>(g, img, blockIdx.x, blockIdx.y, sm, sbase, tmem, st);
+  tt_cta_exit<TN, NSTG>(tmem);
+}
+
+// The small levels (at most TN * gridDim.x / 8 parents) in one launch: the
+// levels in order, a grid-wide barrier between them (every CTA of this small
+// grid is resident beside the near field; the counter is zeroed before the
+// launch).  Same tiles and arithmetic as one k_translate_tc launch per level.
+struct TtChain {
+  TrArgs lev[4];
+  int nlev;
+  unsigned* bar;
+};
+template <int TN, int NSTG>
+__global__ void __launch_bounds__(TT_THREADS) k_translate_tc_chain(TtChain ch, const unsigned char* __restrict__ img) {
+  extern __shared__ __align__(16) unsigned char tt_raw[];
+  __shared__ __align__(8) TtCta<TN, NSTG> st;
+  const uint32_t sbase = (smem_u32(tt_raw) + 1023u) & ~1023u;
+  unsigned char* sm = tt_raw + (sbase - smem_u32(tt_raw));
+  const uint32_t tmem = tt_cta_init<TN, NSTG>(st);
+  const int o = blockIdx.x & 7, tile = blockIdx.x >> 3;
+  const unsigned nblk = gridDim.x;
+  for (int l = 0; l < ch.nlev; ++l) {
+    const TrArgs& g = ch.lev[l];
+    const int pl = g.mode == 0 ? g.level : g.level - 1;
+    const int ntile = ((1 << (3 * pl)) + TN - 1) / TN;
+    if (tile < ntile) tt_tile<TN, NSTG>(g, img, tile, o, sm, sbase, tmem, st);
+    if (l + 1 < ch.nlev) {  // grid barrier: this level's outputs are the next level's inputs
+      __syncthreads();
+      if (threadIdx.x == 0) {
+        __threadfence();
+        atomicAdd(ch.bar, 1u);
+        const unsigned target = (unsigned)(l + 1) * nblk;
+        while (*reinterpret_cast<volatile unsigned*>(ch.bar) < target) {
+        }
+        __threadfence();
+      }
+      __syncthreads();
+    }
+  }
+  tt_cta_exit<TN, NSTG>(tmem);
 }
 
 }  // namespace lfmm
