@@ -5,11 +5,14 @@
 set -o pipefail
 mkdir -p gpurun_out
 timeout 1200 python -m pytest tests -m gpu -q 2>&1 | tail -3 > gpurun_out/r02f_gpu_tests.txt
+for tool in memcheck racecheck synccheck initcheck; do
+  timeout 900 compute-sanitizer --tool $tool --print-limit 20 python tools/sanitize_smoke.py > gpurun_out/r02f_sanitizer_$tool.txt 2>&1
+done
 timeout 900 python bench.py --steps 20 --warmup 5 > gpurun_out/r02f_bench.json 2> gpurun_out/r02f_bench.err
 timeout 1700 python bench.py --impl reference --steps 20 --warmup 5 > gpurun_out/r02f_reference.json 2> gpurun_out/r02f_reference.err
 timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-file gpurun_out/r02f_launches.csv \
   python bench.py --steps 2 --warmup 1 --no-cpu-baseline > /dev/null 2>&1
-timeout 900 ncu --set full --clock-control none --import-source on -k 'regex:k_m2l_halo|k_translate_tc|k_l2p_f2|k_p2m_c|k_step_tail|k_leaf_rank|k_wrap_cell|k_stage_q|k_finalize|k_hi_site' \
+timeout 900 ncu --set full --clock-control none --import-source on -k 'regex:k_m2l_halo|k_translate_tc|k_l2p_f2|k_p2m_c|k_step_tail|k_leaf_rank|k_wrap_cell|k_stage_q|k_finalize|k_hi_site|k_scan_lookback' \
   -c 40 -o gpurun_out/r02f_full python bench.py --steps 1 --warmup 1 --no-cpu-baseline > gpurun_out/r02f_ncu.log 2>&1
 LFMM_P2P=plain timeout 600 ncu --set full --clock-control none --import-source on -k regex:k_p2p2 -c 1 \
   -o gpurun_out/r02f_p2p python bench.py --steps 1 --warmup 1 --no-cpu-baseline > gpurun_out/r02f_ncu_p2p.log 2>&1
