@@ -239,8 +239,11 @@ __device__ __forceinline__ void tt_tile(const TrArgs& g, const unsigned char* __
       tt_commit_w(smem_u32(&mma_done[s]));
     }
   }
-  // the last commit tracks every MMA of the CTA
-  mbar_wait(smem_u32(&mma_done[(TT_NCH - 1) % NSTG]), ((TT_NCH - 1) / NSTG) & 1);
+  // the last commit tracks every MMA of the CTA; every stage's last phase
+  // is still waited on, so that each phase of each barrier has a waiter
+  // before its next arrival (a CTA of the chained kernel runs several tiles)
+#pragma unroll
+  for (int c = TT_NCH - NSTG; c < TT_NCH; ++c) mbar_wait(smem_u32(&mma_done[c % NSTG]), (c / NSTG) & 1);
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
   // drain D into shared memory as [column][128 rows] (the stages are free
   // now), then a vector epilogue: thread -> (column e / 32, rows 4 (e % 32)),
