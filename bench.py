@@ -516,12 +516,16 @@ def run_ours(args):
     achieved = fl / (m2l_ms * 1e-3) / 1e12 if m2l_ms > 0 else 0.0
     t_m2l = work["t_m2l"]
     issued = 3 * 2.0 * 128 * 128 * t_m2l
+    # ncu DRAM bytes of one M2L launch, captured on this workload (C3 fp32
+    # only: the profile is static)
     traffic = None
-    try:
-        with open(os.path.join(ROOT, "profiles", "r01_m2l_traffic.json")) as fh:
-            traffic = json.load(fh).get("dram_bytes_per_launch")
-    except OSError:
-        pass
+    if (args.atoms, args.sites, args.p, args.depth, args.precision) == (1_000_000, 512, 10, 5, "single"):
+        try:
+            with open(os.path.join(ROOT, "profiles", "r02_final_ncu_full.json")) as fh:
+                k = next(k for k in json.load(fh)["kernels"] if "k_m2l_halo" in k["kernel"])
+            traffic = int(round((float(k["dram__bytes_read.sum"]) + float(k["dram__bytes_write.sum"])) * 1e6))
+        except (OSError, StopIteration, KeyError, ValueError):
+            pass
     roofline = {
         "kernel": "k_m2l_halo (M2L, tcgen05 kind::f16 3-product split)", "bound": "tensor",
         "achieved": round(achieved, 3), "peak": peaks.get("bf16_tflops"), "unit": "TFLOP/s",
@@ -531,7 +535,7 @@ def run_ours(args):
                        f"({t_m2l} translations)",
         "issued_tflops": round(issued / (m2l_ms * 1e-3) / 1e12, 3) if m2l_ms > 0 else None,
         "traffic_source": "ncu --set full dram__bytes_read.sum + dram__bytes_write.sum of one launch "
-                          "(profiles/r01_m2l_traffic.json)",
+                          "(profiles/r02_final_ncu_full.json)",
     }
     p2p_ms = stage_rows.get("p2p", {}).get("ms", 0.0)
     fp32_pipe = 62.2  # TFLOP/s, FFMA microbenchmark on this pool (profiles/r01_pipe_peaks.txt)
