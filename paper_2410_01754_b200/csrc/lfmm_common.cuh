@@ -72,6 +72,27 @@ __host__ __device__ inline void pk_decode(int p, int a, int& l, int& m, int& par
   part = r & 1;
 }
 
+// pk_decode without the search over m: the m block starting at
+// pk_base(p, m) = (p+1) + 2((m-1)(p+1) - (m-1)m/2) inverted in closed form,
+// one fix-up step each way (checked against pk_decode for every index, p <= PMAX)
+__host__ __device__ inline void pk_decode_fast(int p, int a, int& l, int& m, int& part) {
+  if (a <= p) {
+    l = a;
+    m = 0;
+    part = 0;
+    return;
+  }
+  const int h = (a - (p + 1)) >> 1;  // complex slot index in the m-major order
+  const float b = 2.f * p + 1.f;
+  int mm = (int)((b - sqrtf(b * b - 8.f * (float)h)) * 0.5f);  // blocks before: (m-1)
+  if ((mm + 1) * (p + 1) - (mm + 1) * (mm + 2) / 2 <= h) ++mm;
+  if (mm * (p + 1) - mm * (mm + 1) / 2 > h) --mm;
+  m = mm + 1;
+  const int r = a - pk_base(p, m);
+  l = m + (r >> 1);
+  part = r & 1;
+}
+
 // recurrence constants, broadcast from constant memory
 __constant__ double c_inv_lm_d[(PMAX + 2) * (PMAX + 2)];  // 1/((l+m)(l-m)), l>m
 __constant__ float c_inv_lm_f[(PMAX + 2) * (PMAX + 2)];

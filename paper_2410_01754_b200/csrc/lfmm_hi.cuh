@@ -144,26 +144,34 @@ __device__ __noinline__ void hi_site_force(const HiArgs& g, int s, int a0, int n
   const bool dip = g.images_full && g.dipole;
   for (int i = wid; i < ns; i += blockDim.x / 32) {
     double gx = 0.0, gy = 0.0, gz = 0.0;
-    // near kernel: lanes over (partner, image)
-    const int nimg = g.images_full ? 27 : 1;
-    for (int e = lane; e < ns * nimg; e += 32) {
-      const int t = e / nimg, n = e - t * nimg;
-      if (t == i) continue;
-      double dx = pos[3 * i] - pos[3 * t], dy = pos[3 * i + 1] - pos[3 * t + 1], dz = pos[3 * i + 2] - pos[3 * t + 2];
-      if (g.images_full) {
-        dx += (n / 9 - 1) * L;
-        dy += ((n / 3) % 3 - 1) * L;
-        dz += (n % 3 - 1) * L;
-      } else {
+    // near kernel: full images, lane n < 27 takes image n of every partner
+    // (no integer division per term); minimum image, lanes over partners
+    if (g.images_full) {
+      const double ox = (lane / 9 - 1) * L, oy = ((lane / 3) % 3 - 1) * L, oz = (lane % 3 - 1) * L;
+      if (lane < 27)
+        for (int t = 0; t < ns; ++t) {
+          if (t == i) continue;
+          const double dx = pos[3 * i] - pos[3 * t] + ox, dy = pos[3 * i + 1] - pos[3 * t + 1] + oy,
+                       dz = pos[3 * i + 2] - pos[3 * t + 2] + oz;
+          const double ir = rsqrt(dx * dx + dy * dy + dz * dz);
+          const double c = -2.0 * Wm[i * ns + t] * ir * ir * ir;
+          gx = fma(c, dx, gx);
+          gy = fma(c, dy, gy);
+          gz = fma(c, dz, gz);
+        }
+    } else {
+      for (int t = lane; t < ns; t += 32) {
+        if (t == i) continue;
+        double dx = pos[3 * i] - pos[3 * t], dy = pos[3 * i + 1] - pos[3 * t + 1], dz = pos[3 * i + 2] - pos[3 * t + 2];
         dx -= L * rint(dx / L);
         dy -= L * rint(dy / L);
         dz -= L * rint(dz / L);
+        const double ir = rsqrt(dx * dx + dy * dy + dz * dz);
+        const double c = -2.0 * Wm[i * ns + t] * ir * ir * ir;
+        gx = fma(c, dx, gx);
+        gy = fma(c, dy, gy);
+        gz = fma(c, dz, gz);
       }
-      const double ir = 1.0 / sqrt(dx * dx + dy * dy + dz * dz);
-      const double c = -2.0 * Wm[i * ns + t] * ir * ir * ir;
-      gx = fma(c, dx, gx);
-      gy = fma(c, dy, gy);
-      gz = fma(c, dz, gz);
     }
     // lattice kernel: V = sum_t W_it U_t, contracted with grad_x R(x_i)
     if (lattice) {
@@ -173,7 +181,7 @@ __device__ __noinline__ void hi_site_force(const HiArgs& g, int s, int a0, int n
         double v = 0.0;
         for (int t = 0; t < ns; ++t) v = fma(Wm[i * ns + t], Us[(size_t)t * rs + c], v);
         int l, m, part;
-        pk_decode(p, c, l, m, part);
+        pk_decode_fast(p, c, l, m, part);
         if (l == 0) continue;
         const double2 A = pk_get(Ri, p, l - 1, m - 1), B = pk_get(Ri, p, l - 1, m + 1), C = pk_get(Ri, p, l - 1, m);
         double dxv, dyv, dzv;
