@@ -336,3 +336,28 @@ def test_overlapping_sites_rejected():
     solver = PeriodicSolver(bad.positions, bad.box_length, SolverConfig(p=6, depth=1))
     with pytest.raises(ValueError, match="overlap"):
         hi_energy_and_forces(bad, [lam.values[0], lam.values[0]], solver=solver)
+
+
+def test_host_input_step_matches_device_input_step():
+    """lfmm_step with host buffers (bench.py's e2e call: positions uploaded in
+    four pieces, each counted as it lands; charges on the io stream; forces
+    downloaded beside the HI tail) gives the device-input step's results bit
+    for bit, on a system large enough (>= 2^18 atoms) for the chunked upload,
+    and rebuilds the same tree."""
+    system, lam, _ = generate_water_box(300_000, 32, seed=5)
+    cfg = SolverConfig(p=10, depth=4, precision="single")
+    st = Stepper(system, lam.values, cfg)
+    e_dev, f_dev, lf_dev = st.step(system.positions)
+    h_dev = st.tree_hashes()[:2]
+    lt, nl = lambda_table(system, lam.values)
+    n, s = system.num_particles, len(system.sites)
+    e = np.empty(1)
+    f = np.empty((n, 3))
+    lf = np.empty((s, 4))
+    for _ in range(2):  # the second call reuses the plan's io stream and events
+        st.plan.step(np.ascontiguousarray(system.positions), np.ascontiguousarray(system.charges), lt, nl,
+                     mode=_native.MODE_HI, plain=False, on_device=False, energy=e, forces=f, lambda_forces=lf)
+        assert st.tree_hashes()[:2] == h_dev
+        assert e[0] == e_dev
+        np.testing.assert_array_equal(f, f_dev)
+        np.testing.assert_array_equal(lf, lf_dev)
