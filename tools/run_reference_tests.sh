@@ -9,5 +9,5 @@ PYTHONPATH=baseline/_ref:. timeout 1500 python -m pytest -p no:cacheprovider -p 
   baseline/_ref/lambdafmm_tests/test_fmm_engine.py baseline/_ref/lambdafmm_tests/test_corrections.py \
   baseline/_ref/lambdafmm_tests/test_lattice.py baseline/_ref/lambdafmm_tests/test_oracle.py \
   baseline/_ref/lambdafmm_tests/test_dynamics.py baseline/_ref/lambdafmm_tests/test_acceptance.py \
-  -m "not slow" 2>&1 | tail -40 > gpurun_out/r02_reference_tests_dropin.txt
-tail -15 gpurun_out/r02_reference_tests_dropin.txt
+  -m "not slow" 2>&1 | tail -40 > gpurun_out/r02_final_reference_tests_dropin.txt
+tail -15 gpurun_out/r02_final_reference_tests_dropin.txt
