@@ -10,6 +10,9 @@ computed exactly against emulated operand roundings:
   fp16x3    : same with fp16 hi/lo after scaling (subnormals kept)
   fp16x1    : one fp16 product (for scale)
 
+  far2b     : fp16x3, but two products (operator hi only) on the outer-shell
+              offsets (|o|inf = 3: 218 of the 316 operators)
+
 Error metric: max |dV| / max |V| of the potential the level-d locals produce
 at the particles (L2P), i.e. the reference's max-normalised metric applied to
 this stage's contribution alone (stricter than on the total far potential).
@@ -134,7 +137,14 @@ def main():
         gl = 2.0 ** (12 - np.ceil(np.log2(np.abs(Ms).max())))
         pairs = orc.m2l_pairs(level)
         variants = {"exact": None, "fp32": None, "tf32x3": None, "fp16x3": None, "fp16x2a": None,
-                    "fp16x2b": None, "fp16x1": None}
+                    "fp16x2b": None, "fp16x1": None, "far2b": None}
+        if len(sys.argv) > 3:
+            variants = {k: None for k in sys.argv[3].split(",")}
+        far = np.abs(orc.M2L_OFF).max(1) >= 3  # outer shell of the interaction list
+        r2min = float(sys.argv[4]) if len(sys.argv) > 4 else 0.0
+        if r2min > 0:  # far2b on the offsets with |o|^2 >= r2min only
+            far = (orc.M2L_OFF ** 2).sum(1) >= r2min
+        print("far2b offsets: %d of %d" % (far.sum(), len(far)))
         locs = {}
         for name in variants:
             Lh = np.zeros_like(Mh)
@@ -159,6 +169,11 @@ def main():
                     ah = np.asarray(Bs[row], np.float16).astype(np.float64)
                     bh, bl = split(Ms[:, s] * gl, "fp16")
                     Lh[:, t] += ((ah @ bh + ah @ bl) / r[:, None]) / gl
+                elif name == "far2b":  # operator one fp16 on the outer-shell offsets only
+                    ah, al = split(Bs[row], "fp16")
+                    bh, bl = split(Ms[:, s] * gl, "fp16")
+                    acc = ah @ bh + ah @ bl if far[row] else ah @ bh + ah @ bl + al @ bh
+                    Lh[:, t] += (acc / r[:, None]) / gl
                 elif name == "fp16x1":
                     ah = np.asarray(Bs[row], np.float16).astype(np.float64)
                     bh = np.asarray(Ms[:, s] * gl, np.float16).astype(np.float64)
