@@ -11,8 +11,10 @@
 // locals (DOWN).  Operands are split hi + lo, each rounded to tf32 (10-bit
 // mantissa, 8-bit exponent: no scaling), and the three products hi*hi +
 // hi*lo + lo*hi carry 22 operand bits, the fp32 SIMT kernel's precision at
-// the tensor rate.  One accumulation chain is 48 MMAs (4 K chunks x 3 products
-// x 4 K steps), inside the 78 the M2L keeps (tools/tc_probe.cu).
+// the tensor rate.  Each K chunk accumulates into its own TMEM columns (a
+// chain of 12 MMAs: 3 products x 4 K steps) and the chunks are added in fp32
+// registers: the tensor core's accumulation truncates, and one 48-MMA chain
+// per tile doubled the fp32 parity error.
 //
 // K is streamed in chunks of 32 (one 128-B row of fp32) through an NSTG-stage
 // ring: the operator chunk (hi | lo, 32 KB, pre-split in its shared-memory
@@ -109,7 +111,7 @@ struct TtCta {
 
 template <int TN, int NSTG>
 __device__ __forceinline__ uint32_t tt_cta_init(TtCta<TN, NSTG>& st) {
-  constexpr uint32_t TCOLS = TN < 32 ? 32 : TN;
+  constexpr uint32_t TCOLS = TT_NCH * TN < 32 ? 32 : TT_NCH * TN;  // one accumulator per K chunk
   const int tid = threadIdx.x, warp = tid >> 5;
   if (tid == 0) {
     for (int s = 0; s < NSTG; ++s) {
@@ -130,7 +132,7 @@ __device__ __forceinline__ uint32_t tt_cta_init(TtCta<TN, NSTG>& st) {
 }
 template <int TN, int NSTG>
 __device__ __forceinline__ void tt_cta_exit(uint32_t tmem) {
-  constexpr uint32_t TCOLS = TN < 32 ? 32 : TN;
+  constexpr uint32_t TCOLS = TT_NCH * TN < 32 ? 32 : TT_NCH * TN;  // one accumulator per K chunk
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
   __syncthreads();
   if ((threadIdx.x >> 5) == 0)
@@ -232,9 +234,12 @@ __device__ __forceinline__ void tt_tile(const TrArgs& g, const unsigned char* __
       for (int j = 0; j < TT_KC / 8; ++j) {
         const uint64_t ah = tt_desc(a0 + 256 * j), al = tt_desc(a0 + TT_APLANE + 256 * j);
         const uint64_t bh = tt_desc(b0 + 256 * j), bl = tt_desc(b0 + BPLANE + 256 * j);
-        tt_mma_w(tmem, ah, bh, idesc, (c > 0 || j > 0) ? 1u : 0u);
-        tt_mma_w(tmem, ah, bl, idesc, 1u);
-        tt_mma_w(tmem, al, bh, idesc, 1u);
+        // chunk c into its own accumulator: chains of 12 MMAs (the tensor
+        // core's fp32 accumulation truncates), chunks added in fp32 below
+        const uint32_t dacc = tmem + (uint32_t)(c * TN);
+        tt_mma_w(dacc, ah, bh, idesc, j > 0 ? 1u : 0u);
+        tt_mma_w(dacc, ah, bl, idesc, 1u);
+        tt_mma_w(dacc, al, bh, idesc, 1u);
       }
       tt_commit_w(smem_u32(&mma_done[s]));
     }
@@ -254,8 +259,14 @@ __device__ __forceinline__ void tt_tile(const TrArgs& g, const unsigned char* __
     const uint32_t trow = tmem + ((uint32_t)(32 * warp) << 16);
 #pragma unroll
     for (int cb = 0; cb < TN; cb += 16) {
-      float v[16];
+      float v[16], u[16];
       tt_ld16(trow + cb, v);
+#pragma unroll
+      for (int c = 1; c < TT_NCH; ++c) {
+        tt_ld16(trow + (uint32_t)(c * TN) + cb, u);
+#pragma unroll
+        for (int j = 0; j < 16; ++j) v[j] += u[j];
+      }
 #pragma unroll
       for (int j = 0; j < 16; ++j) dsm[(cb + j) * 128 + m] = v[j];
     }
